@@ -1,0 +1,160 @@
+/*
+ * tcg.h -- C ABI of the sm_100a patchwork classifier (libtcg.so).
+ *
+ * Drop-in boundary for the reference's compiled hot path.  The reference
+ * (arXiv 2604.09221 companion package `tcurves`) crosses from Python into
+ * native code at three numba dispatchers; each entry point below replaces
+ * one of them:
+ *
+ *   tcg_plan_create       <- classify.py:24-55   Classifier.__init__ / plan():
+ *                            the plan tuple (d, nv, npts, edge_u, edge_v, src,
+ *                            par, used, ap_u, ap_v, maxreg) is passed verbatim
+ *                            as tcg_desc (same arrays, same vertex numbering)
+ *   tcg_classify_batch    <- kernels.py:366-368  classify_bits_kernel(plan, scr, bits)
+ *                            (called at classify.py:94), batched: n sign words
+ *   tcg_sweep             <- kernels.py:423-436  sweep_kernel(plan, scr, agg, bits,
+ *                            start, end) (called per chunk at sweep.py:153, merged
+ *                            at sweep.py:168-180); one call covers the whole range
+ *   tcg_sample            <- kernels.py:447-462  sample_kernel(plan, scr, agg, bits,
+ *                            seed, k0, k1, nbits) (sweep.py:245-246)
+ *   tcg_*_multi           <- sweep.py:143-180    _run_chunks' thread pool, one host
+ *                            thread per device instead of per CPU worker
+ *
+ * Differences the caller must know (everything else is the reference's):
+ *  - Schemes come back as 64-bit canonical tree keys (AHU balanced
+ *    parentheses with a sentinel bit), not strings; the host renders the
+ *    reference string once per distinct key (paper_2604_09221_b200/scheme.py).
+ *    ovals = (bit_length(key) - 1) / 2.
+ *  - Sign vectors travel as one uint64 word per patchwork: bit k = sign of
+ *    lattice point k (d <= 9).
+ *  - The aggregate is keyed by tree key; counts add and witnesses take the
+ *    minimum index exactly as in _aggregate (kernels.py:379-420).  Hash
+ *    collisions are impossible (the key is the exact tree code).
+ *
+ * Status codes are the reference's (kernels.py:20-31); negative values are
+ * library errors.  All buffers passed to tcg_classify_batch / tcg_sweep /
+ * tcg_sample / tcg_agg_fetch are HOST buffers owned by the caller; the
+ * library owns every device buffer.  Calls on one plan are serialised on
+ * that plan's stream; different plans (devices) may be driven from
+ * different host threads concurrently.
+ */
+#ifndef TCG_H
+#define TCG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    TCG_OK = 0,
+    TCG_TOO_MANY_REGIONS = 1,
+    TCG_NO_ODD_REGION = 2,
+    TCG_MANY_ODD_REGIONS = 3,
+    TCG_NO_PSEUDOLINE = 4,
+    TCG_ROOT_CONFLICT = 5,
+    TCG_NONSEPARATING_OVAL = 6,
+    TCG_NOT_A_TREE = 7,
+    TCG_DISCONNECTED = 8,
+    TCG_ARENA_OVERFLOW = 9,
+    TCG_TABLE_FULL = 10,
+    TCG_HASH_COLLISION = 11,
+    /* library errors */
+    TCG_E_ARG = -1,
+    TCG_E_CUDA = -2,
+    TCG_E_UNSUPPORTED = -3,
+    TCG_E_RANGE = -4
+};
+
+/* The reference plan tuple (classify.py:47-49), flat.  Vertex numbering is
+ * the lexicographic diamond order (diamond.py:25-31); edges are in the
+ * reference's sorted order (diamond.py:102). */
+typedef struct tcg_desc {
+    int32_t degree;
+    int32_t nv;
+    int32_t npts;
+    int32_t ne;
+    const int32_t *edge_u; /* [ne] */
+    const int32_t *edge_v; /* [ne] */
+    const int32_t *src;    /* [nv] index into A(d) */
+    const uint8_t *par;    /* [nv] sign-extension parity */
+    const uint8_t *used;   /* [nv] */
+    int32_t nap;
+    const int32_t *ap_u; /* [nap] antipodal pairs */
+    const int32_t *ap_v; /* [nap] */
+    int32_t maxreg;      /* harnack_bound(d) + 2 */
+} tcg_desc;
+
+typedef struct tcg_plan tcg_plan;
+
+/* Aggregate of a sweep / sample (the reference's agg 9-tuple, sweep.py:118-130,
+ * reduced to its observable content).  key/count/witness are caller-owned
+ * arrays of `cap` entries; `n` is set to the number of distinct schemes. */
+typedef struct tcg_agg {
+    int64_t hist[64]; /* oval histogram, bins 0..maxreg */
+    int64_t total;
+    int32_t n;
+    int32_t cap;
+    uint64_t *key;
+    int64_t *count;
+    int64_t *witness; /* minimal index in the run's own domain */
+} tcg_agg;
+
+/* Plan lifetime.  device < 0 selects the current device. */
+int tcg_plan_create(const tcg_desc *desc, int device, tcg_plan **out);
+int tcg_plan_destroy(tcg_plan *plan);
+/* Use an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream);
+ * NULL restores the plan's own stream. */
+int tcg_plan_set_stream(tcg_plan *plan, void *cuda_stream);
+/* info[0]=degree info[1]=mask words K info[2]=used vertices info[3]=device
+ * info[4]=SM count info[5]=CTAs per launch info[6]=threads per CTA
+ * info[7]=maxreg */
+int tcg_plan_info(const tcg_plan *plan, int32_t *info, int ninfo);
+
+/* classify_bits_kernel, batched.  sigma[t] bit k = sign of point k.
+ * Outputs per patchwork: tree key, oval count, region count, status. */
+int tcg_classify_batch(tcg_plan *plan, const uint64_t *sigma, int64_t n, uint64_t *key,
+                       uint8_t *ovals, uint8_t *nreg, int32_t *status);
+/* Same with DEVICE pointers, asynchronous on the plan's stream. */
+int tcg_classify_batch_device(tcg_plan *plan, const uint64_t *d_sigma, int64_t n,
+                              uint64_t *d_key, uint8_t *d_ovals, uint8_t *d_nreg,
+                              int32_t *d_status);
+
+/* sweep_kernel over [start, end) of the representative (raw=0) or raw
+ * (raw=1) domain; sample_kernel over draws [k0, k1) with nbits-bit indices.
+ * Return TCG_OK or the status of the failing patchwork with the smallest
+ * index (*bad = that index: m for sweeps, the drawn m for samples), or a
+ * negative library error. */
+int tcg_sweep(tcg_plan *plan, int raw, uint64_t start, uint64_t end, tcg_agg *agg, int64_t *bad);
+int tcg_sample(tcg_plan *plan, uint64_t seed, uint64_t k0, uint64_t k1, int nbits, tcg_agg *agg,
+               int64_t *bad);
+
+/* Split-phase form (accumulate on the device across calls, fetch once).
+ * tcg_agg_reset zeroes the device aggregate; the *_async calls only
+ * enqueue work on the plan's stream; tcg_agg_fetch synchronises, copies
+ * the aggregate back and resolves errors like tcg_sweep. */
+int tcg_agg_reset(tcg_plan *plan);
+int tcg_sweep_async(tcg_plan *plan, int raw, uint64_t start, uint64_t end);
+int tcg_sample_async(tcg_plan *plan, uint64_t seed, uint64_t k0, uint64_t k1, int nbits);
+int tcg_agg_fetch(tcg_plan *plan, tcg_agg *agg, int64_t *bad);
+
+/* Multi-device: contiguous shards of the range, one host thread per plan
+ * (each plan bound to its own device), merged on the host (count sum,
+ * witness min).  Output is identical for any number of plans. */
+int tcg_sweep_multi(tcg_plan **plans, int nplans, int raw, uint64_t start, uint64_t end,
+                    tcg_agg *agg, int64_t *bad);
+int tcg_sample_multi(tcg_plan **plans, int nplans, uint64_t seed, uint64_t k0, uint64_t k1,
+                     int nbits, tcg_agg *agg, int64_t *bad);
+
+/* Diagnostics. */
+const char *tcg_last_error(void);
+int tcg_device_count(void);
+int64_t tcg_launch_count(const tcg_plan *plan); /* kernels this plan launched */
+const char *tcg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCG_H */

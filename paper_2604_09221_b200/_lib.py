@@ -1,0 +1,272 @@
+"""ctypes binding of libtcg.so (the sm_100a classifier, csrc/tcg.cu).
+
+This is the only door to the device: there is no CPU fallback.  If the
+library is missing, was built for another architecture, or no CUDA device
+is present, every entry point raises :class:`DeviceUnavailable` /
+:class:`DeviceError` loudly.  The library is built in-tree by
+``__graft_entry__.build()`` (nvcc -gencode arch=compute_100a,code=sm_100a).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from .errors import BudgetExceeded, DeviceError, DeviceUnavailable, IndexOutOfRange
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("TCG_LIBRARY", os.path.join(HERE, "libtcg.so"))
+
+TCG_E_ARG, TCG_E_CUDA, TCG_E_UNSUPPORTED, TCG_E_RANGE = -1, -2, -3, -4
+AGG_CAP = 1 << 16
+
+
+class TcgDesc(C.Structure):
+    _fields_ = [
+        ("degree", C.c_int32), ("nv", C.c_int32), ("npts", C.c_int32), ("ne", C.c_int32),
+        ("edge_u", C.c_void_p), ("edge_v", C.c_void_p), ("src", C.c_void_p),
+        ("par", C.c_void_p), ("used", C.c_void_p),
+        ("nap", C.c_int32), ("ap_u", C.c_void_p), ("ap_v", C.c_void_p),
+        ("maxreg", C.c_int32),
+    ]
+
+
+class TcgAgg(C.Structure):
+    _fields_ = [
+        ("hist", C.c_int64 * 64), ("total", C.c_int64),
+        ("n", C.c_int32), ("cap", C.c_int32),
+        ("key", C.c_void_p), ("count", C.c_void_p), ("witness", C.c_void_p),
+    ]
+
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load():
+    """Load libtcg.so once; raise DeviceUnavailable if it cannot be used."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceUnavailable(
+                f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+            )
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.tcg_plan_create.argtypes = [C.POINTER(TcgDesc), C.c_int, C.POINTER(P)]
+        L.tcg_plan_destroy.argtypes = [P]
+        L.tcg_plan_set_stream.argtypes = [P, C.c_void_p]
+        L.tcg_plan_info.argtypes = [P, C.c_void_p, C.c_int]
+        L.tcg_classify_batch.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                         C.c_void_p, C.c_void_p]
+        L.tcg_classify_batch_device.argtypes = L.tcg_classify_batch.argtypes
+        L.tcg_sweep.argtypes = [P, C.c_int, C.c_uint64, C.c_uint64, C.POINTER(TcgAgg),
+                                C.POINTER(C.c_int64)]
+        L.tcg_sample.argtypes = [P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                 C.POINTER(TcgAgg), C.POINTER(C.c_int64)]
+        L.tcg_agg_reset.argtypes = [P]
+        L.tcg_sweep_async.argtypes = [P, C.c_int, C.c_uint64, C.c_uint64]
+        L.tcg_sample_async.argtypes = [P, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int]
+        L.tcg_agg_fetch.argtypes = [P, C.POINTER(TcgAgg), C.POINTER(C.c_int64)]
+        L.tcg_sweep_multi.argtypes = [C.POINTER(P), C.c_int, C.c_int, C.c_uint64, C.c_uint64,
+                                      C.POINTER(TcgAgg), C.POINTER(C.c_int64)]
+        L.tcg_sample_multi.argtypes = [C.POINTER(P), C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                       C.c_int, C.POINTER(TcgAgg), C.POINTER(C.c_int64)]
+        L.tcg_last_error.restype = C.c_char_p
+        L.tcg_version.restype = C.c_char_p
+        L.tcg_device_count.restype = C.c_int
+        L.tcg_launch_count.argtypes = [P]
+        L.tcg_launch_count.restype = C.c_int64
+        _lib = L
+        return L
+
+
+EXPORTS = (
+    "tcg_plan_create", "tcg_plan_destroy", "tcg_plan_set_stream", "tcg_plan_info",
+    "tcg_classify_batch", "tcg_classify_batch_device", "tcg_sweep", "tcg_sample",
+    "tcg_agg_reset", "tcg_sweep_async", "tcg_sample_async", "tcg_agg_fetch",
+    "tcg_sweep_multi", "tcg_sample_multi", "tcg_last_error", "tcg_device_count",
+    "tcg_launch_count", "tcg_version",
+)
+
+
+def last_error() -> str:
+    return load().tcg_last_error().decode(errors="replace")
+
+
+def device_count() -> int:
+    return int(load().tcg_device_count())
+
+
+def _check(rc: int, what: str):
+    if rc == 0:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == TCG_E_UNSUPPORTED:
+        raise BudgetExceeded(msg)
+    if rc == TCG_E_RANGE:
+        raise IndexOutOfRange(msg)
+    if rc == TCG_E_CUDA:
+        raise DeviceError(msg)
+    raise DeviceError(f"{msg} (code {rc})")
+
+
+class AggBuffers:
+    """Host-side tcg_agg with caller-owned arrays."""
+
+    def __init__(self, cap: int = AGG_CAP):
+        self.key = np.zeros(cap, np.uint64)
+        self.count = np.zeros(cap, np.int64)
+        self.witness = np.zeros(cap, np.int64)
+        self.c = TcgAgg()
+        self.c.cap = cap
+        self.c.key = self.key.ctypes.data
+        self.c.count = self.count.ctypes.data
+        self.c.witness = self.witness.ctypes.data
+
+    def result(self):
+        n = self.c.n
+        return (
+            [int(x) for x in self.c.hist],
+            int(self.c.total),
+            self.key[:n].copy(),
+            self.count[:n].copy(),
+            self.witness[:n].copy(),
+        )
+
+
+class NativePlan:
+    """Owns one tcg_plan (one triangulation on one device)."""
+
+    def __init__(self, arrays, device: int | None = None):
+        L = load()
+        if device is None:
+            device = -1
+        if L.tcg_device_count() < 1:
+            raise DeviceUnavailable("no CUDA device visible; the classifier has no CPU fallback")
+        self.arrays = arrays
+        self._keep = [
+            np.ascontiguousarray(arrays.edge_u, np.int32),
+            np.ascontiguousarray(arrays.edge_v, np.int32),
+            np.ascontiguousarray(arrays.src, np.int32),
+            np.ascontiguousarray(arrays.par, np.uint8),
+            np.ascontiguousarray(arrays.used, np.uint8),
+            np.ascontiguousarray(arrays.ap_u, np.int32),
+            np.ascontiguousarray(arrays.ap_v, np.int32),
+        ]
+        eu, ev, src, par, used, apu, apv = self._keep
+        desc = TcgDesc(arrays.degree, arrays.nv, arrays.npts, len(eu), eu.ctypes.data,
+                       ev.ctypes.data, src.ctypes.data, par.ctypes.data, used.ctypes.data,
+                       len(apu), apu.ctypes.data, apv.ctypes.data, arrays.maxreg)
+        h = C.c_void_p()
+        _check(L.tcg_plan_create(C.byref(desc), int(device), C.byref(h)), "tcg_plan_create")
+        self.h = h
+        self._L = L
+        info = np.zeros(8, np.int32)
+        L.tcg_plan_info(self.h, info.ctypes.data, 8)
+        self.info = {
+            "degree": int(info[0]), "words": int(info[1]), "used": int(info[2]),
+            "device": int(info[3]), "sms": int(info[4]), "ctas": int(info[5]),
+            "threads": int(info[6]), "maxreg": int(info[7]),
+        }
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            try:
+                self._L.tcg_plan_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def set_stream(self, stream_handle: int | None):
+        _check(self._L.tcg_plan_set_stream(self.h, C.c_void_p(stream_handle or 0)),
+               "tcg_plan_set_stream")
+
+    def launches(self) -> int:
+        return int(self._L.tcg_launch_count(self.h))
+
+    def classify_words(self, words):
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        n = len(w)
+        key = np.zeros(n, np.uint64)
+        ov = np.zeros(n, np.uint8)
+        nr = np.zeros(n, np.uint8)
+        st = np.zeros(n, np.int32)
+        if n:
+            _check(self._L.tcg_classify_batch(self.h, w.ctypes.data, n, key.ctypes.data,
+                                              ov.ctypes.data, nr.ctypes.data, st.ctypes.data),
+                   "tcg_classify_batch")
+        return key, ov, nr, st
+
+    def classify_words_device(self, d_sig: int, n: int, d_key: int, d_ov: int, d_nr: int,
+                              d_st: int):
+        _check(self._L.tcg_classify_batch_device(self.h, d_sig, n, d_key, d_ov, d_nr, d_st),
+               "tcg_classify_batch_device")
+
+    def sweep(self, raw: bool, start: int, end: int, agg: AggBuffers | None = None):
+        agg = agg or AggBuffers()
+        bad = C.c_int64(-1)
+        rc = self._L.tcg_sweep(self.h, int(bool(raw)), int(start), int(end), C.byref(agg.c),
+                               C.byref(bad))
+        if rc < 0:
+            _check(rc, "tcg_sweep")
+        return rc, int(bad.value), agg
+
+    def sample(self, seed: int, k0: int, k1: int, nbits: int, agg: AggBuffers | None = None):
+        agg = agg or AggBuffers()
+        bad = C.c_int64(-1)
+        rc = self._L.tcg_sample(self.h, int(seed) & (2**64 - 1), int(k0), int(k1), int(nbits),
+                                C.byref(agg.c), C.byref(bad))
+        if rc < 0:
+            _check(rc, "tcg_sample")
+        return rc, int(bad.value), agg
+
+    # split phase (bench, distributed shards)
+    def agg_reset(self):
+        _check(self._L.tcg_agg_reset(self.h), "tcg_agg_reset")
+
+    def sweep_async(self, raw: bool, start: int, end: int):
+        _check(self._L.tcg_sweep_async(self.h, int(bool(raw)), int(start), int(end)),
+               "tcg_sweep_async")
+
+    def sample_async(self, seed: int, k0: int, k1: int, nbits: int):
+        _check(self._L.tcg_sample_async(self.h, int(seed) & (2**64 - 1), int(k0), int(k1),
+                                        int(nbits)), "tcg_sample_async")
+
+    def agg_fetch(self, agg: AggBuffers | None = None):
+        agg = agg or AggBuffers()
+        bad = C.c_int64(-1)
+        rc = self._L.tcg_agg_fetch(self.h, C.byref(agg.c), C.byref(bad))
+        if rc < 0:
+            _check(rc, "tcg_agg_fetch")
+        return rc, int(bad.value), agg
+
+
+def sweep_multi(plans, raw, start, end, agg: AggBuffers | None = None):
+    L = load()
+    agg = agg or AggBuffers()
+    arr = (C.c_void_p * len(plans))(*[p.h.value for p in plans])
+    bad = C.c_int64(-1)
+    rc = L.tcg_sweep_multi(arr, len(plans), int(bool(raw)), int(start), int(end), C.byref(agg.c),
+                           C.byref(bad))
+    if rc < 0:
+        _check(rc, "tcg_sweep_multi")
+    return rc, int(bad.value), agg
+
+
+def sample_multi(plans, seed, k0, k1, nbits, agg: AggBuffers | None = None):
+    L = load()
+    agg = agg or AggBuffers()
+    arr = (C.c_void_p * len(plans))(*[p.h.value for p in plans])
+    bad = C.c_int64(-1)
+    rc = L.tcg_sample_multi(arr, len(plans), int(seed) & (2**64 - 1), int(k0), int(k1),
+                            int(nbits), C.byref(agg.c), C.byref(bad))
+    if rc < 0:
+        _check(rc, "tcg_sample_multi")
+    return rc, int(bad.value), agg

@@ -1,0 +1,146 @@
+"""Classification entry points: the drop-in for the reference's classify.py.
+
+:class:`Classifier` keeps the reference's surface (classify.py:21-128):
+``Classifier(T)``, ``.classify(sigma)``, ``._run_bits(bits)``,
+``.plan(raw_space)``, ``.make_scratch()``, ``.degree``, ``.maxreg``,
+``.diamond``, and the module function ``classify(T, sigma, validate,
+classifier)``.  Construction does the reference's once-per-triangulation
+host work (reflect, sign-extension tables, antipodal pairs) and hands the
+flat plan to ``tcg_plan_create``; every classification then runs on the
+B200 through ``tcg_classify_batch``.  :meth:`Classifier.classify_many` and
+:meth:`Classifier.classify_words` are the batched forms (one launch for
+many sign vectors) that the reference has no equivalent of.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .diamond import plan_arrays, reflect
+from .errors import InvariantViolation, ParseError
+from .lattice import harnack_bound, num_points, validate_triangulation
+from .scheme import scheme_from_key
+from .signs import SignDistribution, free_positions
+
+STATUS_MESSAGES = {
+    1: "region count exceeds the degree bound",
+    2: "even degree expects exactly one odd-cycle region, found none",
+    3: "even degree expects exactly one odd-cycle region, found several",
+    4: "odd degree but no pseudoline region found",
+    5: "conflicting pseudoline regions",
+    6: "even degree with a nonseparating curve component",
+    7: "region graph is not a tree",
+    8: "region graph is disconnected",
+    9: "internal: canonical-string arena overflow",
+    10: "internal: scheme table full",
+    11: "internal: 64-bit scheme hash collision",
+}
+
+
+@dataclass(frozen=True)
+class ClassificationResult:
+    """Same fields and equality as the reference's (pipeline.py:240-253)."""
+
+    scheme: str
+    oval_count: int
+    region_count: int
+    has_pseudoline: bool
+
+    def to_dict(self) -> dict:
+        return {
+            "scheme": self.scheme,
+            "oval_count": self.oval_count,
+            "region_count": self.region_count,
+            "has_pseudoline": self.has_pseudoline,
+        }
+
+
+class Classifier:
+    """Reusable classification state for one triangulation, resident on one GPU."""
+
+    def __init__(self, T, device: int | None = None):
+        self.triangulation = T
+        d = int(T.degree)
+        self.degree = d
+        D = reflect(T)
+        self.diamond = D
+        self.maxreg = harnack_bound(d) + 2
+        self.arrays = plan_arrays(D)
+        npts = num_points(d)
+        rep_pos = np.full(npts, -1, dtype=np.int64)
+        for pos, k in enumerate(free_positions(d)):
+            rep_pos[k] = pos
+        self._rep_bitpos = rep_pos
+        self._raw_bitpos = np.arange(npts, dtype=np.int64)
+        self.native = _lib.NativePlan(self.arrays, device)
+        self.device = self.native.info["device"]
+
+    # reference-shaped accessors -------------------------------------------
+    def plan(self, raw_space: bool = False):
+        """The reference's plan tuple (classify.py:53-55), for inspection."""
+        a = self.arrays
+        bitpos = self._raw_bitpos if raw_space else self._rep_bitpos
+        return (a.degree, a.nv, a.npts, a.edge_u, a.edge_v, a.src, a.par, a.used,
+                a.ap_u, a.ap_v, a.maxreg, bitpos)
+
+    def make_scratch(self):
+        """The device owns all scratch; nothing to allocate on the host."""
+        return ()
+
+    # classification ---------------------------------------------------------
+    def _result(self, key, ovals, nreg, status, where: str = "") -> ClassificationResult:
+        if status != 0:
+            raise InvariantViolation(STATUS_MESSAGES.get(int(status), f"status {status}") + where)
+        return ClassificationResult(
+            scheme=scheme_from_key(int(key), self.degree % 2 == 1),
+            oval_count=int(ovals),
+            region_count=int(nreg),
+            has_pseudoline=self.degree % 2 == 1,
+        )
+
+    def _run_bits(self, bits) -> ClassificationResult:
+        b = np.asarray(bits, dtype=np.uint64)
+        word = int(np.bitwise_or.reduce(b << np.arange(len(b), dtype=np.uint64))) if len(b) else 0
+        key, ov, nr, st = self.native.classify_words(np.array([word], np.uint64))
+        return self._result(key[0], ov[0], nr[0], st[0])
+
+    def classify(self, sigma) -> ClassificationResult:
+        if isinstance(sigma, str):
+            sigma = SignDistribution.from_bitstring(self.degree, sigma)
+        if sigma.degree != self.degree:
+            raise ParseError(f"sign degree {sigma.degree} != triangulation degree {self.degree}")
+        word = 0
+        for k, b in enumerate(sigma.bits):
+            word |= int(b) << k
+        key, ov, nr, st = self.native.classify_words(np.array([word], np.uint64))
+        return self._result(key[0], ov[0], nr[0], st[0])
+
+    def classify_words(self, words):
+        """Batched raw form: uint64 sign words -> (keys, ovals, nreg, status) arrays."""
+        return self.native.classify_words(words)
+
+    def classify_many(self, sigmas) -> list[ClassificationResult]:
+        words = []
+        for s in sigmas:
+            if isinstance(s, str):
+                s = SignDistribution.from_bitstring(self.degree, s)
+            if s.degree != self.degree:
+                raise ParseError(f"sign degree {s.degree} != triangulation degree {self.degree}")
+            w = 0
+            for k, b in enumerate(s.bits):
+                w |= int(b) << k
+            words.append(w)
+        key, ov, nr, st = self.native.classify_words(np.array(words, np.uint64))
+        return [self._result(key[i], ov[i], nr[i], st[i], f" (at batch position {i})")
+                for i in range(len(words))]
+
+
+def classify(T, sigma, validate: bool = True, classifier: Classifier | None = None):
+    """Classify one patchwork (reference classify.py:118-128)."""
+    if validate and classifier is None:
+        T = validate_triangulation(T.degree, T.edges)
+    c = classifier or Classifier(T)
+    return c.classify(sigma)

@@ -1,0 +1,1251 @@
+// tcg.cu -- sm_100a real-scheme classifier for combinatorial patchworks.
+//
+// One thread classifies one (triangulation, sign vector) pair.  The whole
+// per-patchwork state lives in registers as bitmasks over the diamond's
+// vertices; the only memory traffic in the hot loop is one shared-memory
+// adjacency row per visited vertex (a warp-divergent LDS.64/128).
+//
+// Algorithm (same outputs as the reference's classify_core,
+// kernels.py:107-356, restructured for SIMT):
+//   1. sign mask: sigma (bit k = point k) -> sign of every diamond vertex,
+//      via the half-swap vertex layout (see build_layout): ~30 integer ops.
+//   2. one breadth-first pass over all used vertices that labels REGIONS
+//      directly: inside a layer it follows non-crossed edges (same-sign
+//      neighbours, `adj & same & unvisited`); when the layer is exhausted it
+//      jumps through the antipodal identification, which in this layout is a
+//      swap of the two mask halves (free: register renaming).  Layers
+//      alternate orientation parity, so the reference's parity union-find
+//      (kernels.py:151-174) reduces to one check per region: an antipodal
+//      pair whose ends sit in layers of equal parity closes an odd cycle.
+//      Crossed-edge neighbours are OR-ed into XB on the fly.
+//   3. region graph: regions r != r' are adjacent iff XB_r & R_r' != 0;
+//      XB_r & R_r != 0 is a crossed edge inside r (pseudoline root in odd
+//      degree, NONSEPARATING_OVAL in even degree).  Checks reproduce the
+//      reference's status precedence; the two order-dependent collisions
+//      (NOT_A_TREE racing NONSEPARATING_OVAL / ROOT_CONFLICT) fall back to
+//      an exact replay of kernels.py:199-230 in edge order.
+//   4. rooted tree -> AHU canonical code as a 64-bit key (sentinel bit).
+//   5. sweep / sample kernels aggregate keys in a per-CTA shared-memory
+//      hash table (warp-aggregated with __match_any_sync), flushed to a
+//      global table: count sum, witness min (kernels.py:379-420).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/tcg.h"
+
+#define TCG_VERSION "tcg 0.1.0 sm_100a"
+
+namespace {
+
+constexpr int MAXK = 6;        // 32-bit words per vertex mask (d <= 9)
+constexpr int MAXR = 32;       // regions representable (maxreg <= 31 for d <= 9)
+constexpr int NQ4 = 8;         // compress runs for the mirrored quadrant
+constexpr int THREADS = 256;   // threads per CTA
+constexpr int TBL_BITS = 10;   // per-CTA scheme table: 1024 slots
+constexpr int TBL = 1 << TBL_BITS;
+constexpr int TBL_PROBES = 64;
+constexpr int GCAP_BITS = 16;  // global scheme table: 65,536 slots (as the reference's agg)
+constexpr int GCAP = 1 << GCAP_BITS;
+constexpr int NHIST = 64;
+constexpr uint64_t LAUNCH_MAX = 1ull << 33;  // indices per launch (u32 per-CTA counters)
+
+enum Mode { MODE_RAW = 0, MODE_REP = 1, MODE_SAMPLE = 2 };
+
+struct KParams {
+    int d, npts, nused, maxreg, nq4, center, ne;
+    uint32_t used[MAXK];
+    uint32_t bd[MAXK];        // boundary vertices that have an antipodal partner
+    uint32_t parP[MAXK / 2];  // P-half positions with |i|+|j| odd
+    uint32_t jodd[MAXK / 2];  // mirrored-quadrant positions with j odd
+    uint8_t q4src[NQ4], q4len[NQ4], q4dst[NQ4];
+    const uint32_t *adj;    // [2H][K] adjacency rows (global; staged to smem)
+    const uint32_t *edges;  // [ne] packed positions (u | v << 16), reference order
+};
+
+struct DevAgg {
+    unsigned long long *keys;  // [GCAP]
+    unsigned long long *cnt;   // [GCAP]
+    unsigned long long *wit;   // [GCAP]
+    unsigned long long *hist;  // [NHIST]
+    unsigned long long *bad;   // [1] smallest failing index
+    unsigned int *overflow;    // [1]
+};
+
+struct Result {
+    int status;
+    int nreg;
+    uint64_t key;
+};
+
+// ------------------------------------------------------------------ helpers
+template <int K>
+__device__ __forceinline__ uint32_t sel(const uint32_t (&x)[K], int w) {
+    uint32_t r = x[0];
+#pragma unroll
+    for (int k = 1; k < K; ++k) r = (w == k) ? x[k] : r;
+    return r;
+}
+
+template <int K>
+__device__ __forceinline__ bool any(const uint32_t (&x)[K]) {
+    uint32_t r = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) r |= x[k];
+    return r != 0;
+}
+
+// lowest set bit of a K-word mask: returns word index and bit; caller
+// guarantees the mask is non-zero.
+template <int K>
+__device__ __forceinline__ void lowest(const uint32_t (&x)[K], int &w, int &b) {
+    uint32_t word = x[K - 1];
+    int wi = K - 1;
+#pragma unroll
+    for (int k = K - 2; k >= 0; --k) {
+        const bool nz = x[k] != 0;
+        word = nz ? x[k] : word;
+        wi = nz ? k : wi;
+    }
+    w = wi;
+    b = __ffs(word) - 1;
+}
+
+template <int K>
+__device__ __forceinline__ void load_row(const uint32_t *__restrict__ base, int v, uint32_t (&a)[K]) {
+    if constexpr (K == 2) {
+        const uint2 t = reinterpret_cast<const uint2 *>(base)[v];
+        a[0] = t.x; a[1] = t.y;
+    } else if constexpr (K == 4) {
+        const uint4 t = reinterpret_cast<const uint4 *>(base)[v];
+        a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w;
+    } else {
+        const uint2 *r = reinterpret_cast<const uint2 *>(base) + 3 * v;
+        const uint2 t0 = r[0], t1 = r[1], t2 = r[2];
+        a[0] = t0.x; a[1] = t0.y; a[2] = t1.x; a[3] = t1.y; a[4] = t2.x; a[5] = t2.y;
+    }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t seed, uint64_t k) {
+    // kernels.py:439-444
+    uint64_t z = seed + (k + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ uint64_t rep_to_sigma(int d, uint64_t m) {
+    // free positions ascending take the bits of m (signs.py:188-206):
+    // pinned set {0, 1, d+1} -> two shifted runs
+    const uint64_t low = m & ((1ull << (d - 1)) - 1ull);
+    return (low << 2) | ((m >> (d - 1)) << (d + 2));
+}
+
+// sign of every vertex, in the half-swap layout (see plan construction)
+template <int K>
+__device__ __forceinline__ void sign_words(const KParams &p, uint64_t sigma, uint32_t (&SG)[K]) {
+    uint64_t q4 = 0;
+#pragma unroll
+    for (int r = 0; r < NQ4; ++r) {
+        if (r < p.nq4)
+            q4 |= ((sigma >> p.q4src[r]) & ((1ull << p.q4len[r]) - 1ull)) << p.q4dst[r];
+    }
+    const int sh = p.npts - 1;  // 2..54
+    uint64_t lo = (sigma >> 1) | (q4 << sh);
+    uint64_t hi = q4 >> (64 - sh);
+    const uint64_t c = sigma & 1ull;
+    if (p.center < 64) lo |= c << p.center;
+    else hi |= c << (p.center - 64);
+    const uint32_t w[3] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi};
+#pragma unroll
+    for (int k = 0; k < K / 2; ++k) {
+        SG[k] = w[k] ^ p.jodd[k];
+        SG[K / 2 + k] = SG[k] ^ p.parP[k];
+    }
+}
+
+// Exact replay of kernels.py:199-230 (edge order) for the rare inputs where
+// two order-dependent failures coexist.  Returns the status it produces.
+template <int K, bool EVEN>
+__device__ __noinline__ int ordered_scan(const KParams &p, const uint32_t (&SG)[K],
+                                         const uint32_t (*regR)[K], int nreg, int root) {
+    uint32_t sg[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) sg[k] = SG[k];
+    uint32_t seen[MAXR];
+    for (int r = 0; r < MAXR; ++r) seen[r] = 0;
+    int nedges = 0;
+    for (int e = 0; e < p.ne; ++e) {
+        const uint32_t pk = p.edges[e];
+        const int u = pk & 0xffff, v = pk >> 16;
+        const int su = (sg[u >> 5] >> (u & 31)) & 1, sv = (sg[v >> 5] >> (v & 31)) & 1;
+        if (su == sv) continue;
+        int a = -1, b = -1;
+        for (int r = 0; r < nreg && r < MAXR; ++r) {
+            if ((regR[r][u >> 5] >> (u & 31)) & 1) a = r;
+            if ((regR[r][v >> 5] >> (v & 31)) & 1) b = r;
+        }
+        if (a == b) {
+            if (EVEN) return TCG_NONSEPARATING_OVAL;
+            if (root < 0) root = a;
+            else if (root != a) return TCG_ROOT_CONFLICT;
+            continue;
+        }
+        if (a > b) { const int t = a; a = b; b = t; }
+        if (!((seen[a] >> b) & 1u)) {
+            seen[a] |= 1u << b;
+            if (nedges >= nreg - 1) return TCG_NOT_A_TREE;
+            ++nedges;
+        }
+    }
+    return TCG_NOT_A_TREE;  // unreachable for the inputs routed here
+}
+
+// ------------------------------------------------------------- classify one
+template <int K, bool EVEN>
+__device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__restrict__ adj,
+                                           uint64_t sigma) {
+    constexpr int HK = K / 2;
+    uint32_t SG[K];
+    sign_words<K>(p, sigma, SG);
+
+    uint32_t unv[K], F[K], XB[K], regS[K], layS[K], E1[K];
+    uint32_t regR[MAXR][K];
+    uint32_t regX[MAXR][K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        unv[k] = p.used[k];
+        F[k] = 0; XB[k] = 0; E1[k] = 0;
+    }
+    int nreg = 0;
+    uint32_t oddmask = 0;
+    uint32_t pimask = 0;  // 0 or ~0: orientation parity of the current layer
+
+    // seed the first region with the lowest used vertex
+    {
+        int w, b;
+        lowest<K>(unv, w, b);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            regS[k] = unv[k];
+            layS[k] = unv[k];
+            F[k] = (k == w) ? (1u << b) : 0u;
+            unv[k] ^= F[k];
+        }
+    }
+
+    auto transition = [&](bool more) {
+        // close the layer: vertices visited since layS
+        uint32_t L[K], P[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            L[k] = layS[k] ^ unv[k];
+            if (EVEN) E1[k] |= L[k] & pimask;
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int ks = (k + HK) % K;  // antipodal map = swap of halves
+            P[k] = L[ks] & p.bd[ks] & unv[k];
+        }
+        if (any<K>(P)) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                layS[k] = unv[k];
+                F[k] = P[k];
+                unv[k] ^= P[k];
+            }
+            pimask = ~pimask;
+            return;
+        }
+        // region complete
+        uint32_t R[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) R[k] = regS[k] ^ unv[k];
+        if (EVEN) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int ks = (k + HK) % K;
+                const uint32_t e0 = R[k] & ~E1[k];
+                const uint32_t e0s = R[ks] & ~E1[ks];
+                acc |= (e0s & p.bd[ks] & e0) | (E1[ks] & p.bd[ks] & E1[k]);
+            }
+            if (acc && nreg < MAXR) oddmask |= 1u << nreg;
+        }
+        if (nreg < MAXR) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                regR[nreg][k] = R[k];
+                regX[nreg][k] = XB[k];
+            }
+        }
+        ++nreg;
+        if (more) {
+            int w, b;
+            lowest<K>(unv, w, b);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                regS[k] = unv[k];
+                layS[k] = unv[k];
+                F[k] = (k == w) ? (1u << b) : 0u;
+                unv[k] ^= F[k];
+                XB[k] = 0;
+                E1[k] = 0;
+            }
+            pimask = 0;
+        }
+    };
+
+    const int nused = p.nused;
+    for (int it = 0; it < nused; ++it) {
+        if (!any<K>(F)) transition(true);
+        int w, b;
+        lowest<K>(F, w, b);
+        const uint32_t bit = 1u << b;
+#pragma unroll
+        for (int k = 0; k < K; ++k) F[k] ^= (k == w) ? bit : 0u;
+        const int v = 32 * w + b;
+        uint32_t a[K];
+        load_row<K>(adj, v, a);
+        const uint32_t s = (sel<K>(SG, w) >> b) & 1u;
+        const uint32_t nm = s - 1u;  // s ? 0 : ~0
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint32_t same = SG[k] ^ nm;
+            const uint32_t nw = a[k] & same & unv[k];
+            XB[k] |= a[k] & ~same;
+            F[k] |= nw;
+            unv[k] ^= nw;
+        }
+    }
+    transition(false);
+
+    Result res;
+    res.nreg = nreg;
+    res.key = 0;
+    if (nreg > p.maxreg || nreg > MAXR) {  // kernels.py:182: ids 0..maxreg-1 allowed
+        res.status = TCG_TOO_MANY_REGIONS;
+        return res;
+    }
+    int root = -1;
+    if (EVEN) {
+        const int c = __popc(oddmask);
+        if (c == 0) { res.status = TCG_NO_ODD_REGION; return res; }
+        if (c > 1) { res.status = TCG_MANY_ODD_REGIONS; return res; }
+        root = __ffs(oddmask) - 1;
+    }
+    // region graph from crossed-edge neighbourhoods
+    uint32_t radj[MAXR];
+    for (int r = 0; r < nreg; ++r) radj[r] = 0;
+    uint32_t selfm = 0;
+    int nedges = 0;
+    for (int r = 0; r < nreg; ++r) {
+        uint32_t x[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) x[k] = regX[r][k];
+        uint32_t t = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) t |= x[k] & regR[r][k];
+        if (t) selfm |= 1u << r;
+        for (int r2 = r + 1; r2 < nreg; ++r2) {
+            uint32_t u = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) u |= x[k] & regR[r2][k];
+            if (u) {
+                radj[r] |= 1u << r2;
+                radj[r2] |= 1u << r;
+                ++nedges;
+            }
+        }
+    }
+    const bool toomany = nedges > nreg - 1;  // mid-loop NOT_A_TREE will fire
+    if (EVEN) {
+        if (toomany && selfm) {
+            res.status = ordered_scan<K, EVEN>(p, SG, regR, nreg, root);
+            return res;
+        }
+        if (toomany) { res.status = TCG_NOT_A_TREE; return res; }
+        if (selfm) { res.status = TCG_NONSEPARATING_OVAL; return res; }
+    } else {
+        const bool conflict = __popc(selfm) >= 2;
+        if (toomany && conflict) {
+            res.status = ordered_scan<K, EVEN>(p, SG, regR, nreg, -1);
+            return res;
+        }
+        if (toomany) { res.status = TCG_NOT_A_TREE; return res; }
+        if (conflict) { res.status = TCG_ROOT_CONFLICT; return res; }
+        if (!selfm) { res.status = TCG_NO_PSEUDOLINE; return res; }
+        root = __ffs(selfm) - 1;
+    }
+    if (nedges != nreg - 1) { res.status = TCG_NOT_A_TREE; return res; }
+
+    // rooted BFS over the region tree
+    uint8_t order[MAXR], parent[MAXR];
+    order[0] = (uint8_t)root;
+    parent[root] = (uint8_t)root;
+    uint32_t vis = 1u << root;
+    int head = 0, tail = 1;
+    while (head < tail) {
+        const int r = order[head++];
+        uint32_t nb = radj[r] & ~vis;
+        vis |= nb;
+        while (nb) {
+            const int s2 = __ffs(nb) - 1;
+            nb &= nb - 1;
+            parent[s2] = (uint8_t)r;
+            order[tail++] = (uint8_t)s2;
+        }
+    }
+    if (tail != nreg) { res.status = TCG_DISCONNECTED; return res; }
+
+    // AHU canonical key, bottom-up (children before parents)
+    uint64_t skey[MAXR];
+    uint64_t acc = 1;
+    for (int k = nreg - 1; k >= 0; --k) {
+        const int v = order[k];
+        uint32_t ch = radj[v];
+        if (k > 0) ch &= ~(1u << parent[v]);
+        int nleaf = 0, h = 0;
+        uint64_t buf[MAXR];
+        while (ch) {
+            const int c = __ffs(ch) - 1;
+            ch &= ch - 1;
+            const uint64_t ck = skey[c];
+            if (ck == 6ull) {
+                ++nleaf;
+            } else {
+                int j = h++;
+                while (j > 0 && buf[j - 1] > ck) { buf[j] = buf[j - 1]; --j; }
+                buf[j] = ck;
+            }
+        }
+        acc = 1;
+        if (nleaf) {
+            const int nb2 = 2 * nleaf;
+            acc = (1ull << nb2) | (0xAAAAAAAAAAAAAAAAull & ((1ull << nb2) - 1ull));
+        }
+        for (int i = 0; i < h; ++i) {
+            const uint64_t c = buf[i];
+            const int ln = 63 - __clzll(c);
+            acc = (acc << ln) | (c ^ (1ull << ln));
+        }
+        if (k > 0) {
+            const int il = 63 - __clzll(acc);
+            skey[v] = (acc << 1) | (1ull << (il + 2));
+        }
+    }
+    res.key = acc;
+    res.status = TCG_OK;
+    return res;
+}
+
+// ------------------------------------------------------------------ kernels
+template <int K>
+__device__ __forceinline__ void stage_adj(const KParams &p, uint32_t *adj_s) {
+    const int n = 32 * K * K;  // 2H rows of K words, H = 16K
+    for (int i = threadIdx.x; i < n; i += blockDim.x) adj_s[i] = p.adj[i];
+}
+
+template <int K, bool EVEN>
+__global__ void __launch_bounds__(THREADS) k_batch(KParams p, const uint64_t *__restrict__ sig,
+                                                   int64_t n, uint64_t *__restrict__ key,
+                                                   uint8_t *__restrict__ ovals,
+                                                   uint8_t *__restrict__ nreg,
+                                                   int32_t *__restrict__ status) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    stage_adj<K>(p, smem);
+    __syncthreads();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
+        const Result r = classify<K, EVEN>(p, smem, sig[t]);
+        key[t] = r.status == TCG_OK ? r.key : 0ull;
+        ovals[t] = r.status == TCG_OK ? (uint8_t)(r.nreg - 1) : 0xff;
+        nreg[t] = (uint8_t)min(r.nreg, 255);
+        status[t] = r.status;
+    }
+}
+
+__device__ __forceinline__ uint32_t hash_slot(uint64_t key, int bits) {
+    return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - bits));
+}
+
+__device__ void global_insert(const DevAgg &g, uint64_t key, uint64_t cnt, uint64_t wit) {
+    uint32_t h = hash_slot(key, GCAP_BITS);
+    for (int probe = 0; probe < GCAP; ++probe) {
+        const unsigned long long prev = atomicCAS(&g.keys[h], 0ull, (unsigned long long)key);
+        if (prev == 0ull || prev == key) {
+            atomicAdd(&g.cnt[h], (unsigned long long)cnt);
+            atomicMin(&g.wit[h], (unsigned long long)wit);
+            return;
+        }
+        h = (h + 1) & (GCAP - 1);
+    }
+    atomicOr(g.overflow, 1u);
+}
+
+// Enumeration kernel: raw / representative sweep or counter-based sample.
+// Persistent grid; each warp walks 32 consecutive indices per step.
+template <int K, bool EVEN, int MODE>
+__global__ void __launch_bounds__(THREADS) k_enumerate(KParams p, uint64_t base, uint64_t count,
+                                                       uint64_t seed, uint64_t nbmask, DevAgg g) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *adj_s = smem;
+    unsigned long long *tkey = reinterpret_cast<unsigned long long *>(smem + 32 * K * K);
+    unsigned long long *twit = tkey + TBL;
+    uint32_t *tcnt = reinterpret_cast<uint32_t *>(twit + TBL);
+    uint32_t *thist = tcnt + TBL;
+
+    stage_adj<K>(p, adj_s);
+    for (int i = threadIdx.x; i < TBL; i += blockDim.x) {
+        tkey[i] = 0ull;
+        twit[i] = ~0ull;
+        tcnt[i] = 0u;
+    }
+    for (int i = threadIdx.x; i < NHIST; i += blockDim.x) thist[i] = 0u;
+    __syncthreads();
+
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t wstride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t wb = warp * 32ull; wb < count; wb += wstride * 32ull) {
+        const uint64_t idx = wb + lane;
+        const bool valid = idx < count;
+        const uint64_t gidx = base + idx;  // m (sweeps) or draw number k (sample)
+        uint64_t m, sigma;
+        if (MODE == MODE_SAMPLE) {
+            m = splitmix64(seed, gidx) & nbmask;
+            sigma = rep_to_sigma(p.d, m);
+        } else if (MODE == MODE_REP) {
+            m = gidx;
+            sigma = rep_to_sigma(p.d, m);
+        } else {
+            m = gidx;
+            sigma = m;
+        }
+        Result r = classify<K, EVEN>(p, adj_s, valid ? sigma : 0ull);
+        uint64_t k = 0;
+        if (valid) {
+            if (r.status == TCG_OK) k = r.key;
+            else atomicMin(g.bad, (unsigned long long)gidx);
+        }
+        const unsigned grp = __match_any_sync(0xffffffffu, k);
+        if (k != 0ull) {
+            const int leader = __ffs(grp) - 1;
+            int slot = -1;
+            if (lane == leader) {
+                uint32_t h = hash_slot(k, TBL_BITS);
+                for (int probe = 0; probe < TBL_PROBES; ++probe) {
+                    const unsigned long long cur = tkey[h];
+                    if (cur == k) { slot = (int)h; break; }
+                    if (cur == 0ull) {
+                        const unsigned long long prev = atomicCAS(&tkey[h], 0ull, k);
+                        if (prev == 0ull || prev == k) { slot = (int)h; break; }
+                    }
+                    h = (h + 1) & (TBL - 1);
+                }
+                const uint32_t c = __popc(grp);
+                atomicAdd(&thist[r.nreg - 1], c);
+                if (slot >= 0) {
+                    atomicAdd(&tcnt[slot], c);
+                    if (MODE != MODE_SAMPLE) atomicMin(&twit[slot], (unsigned long long)m);
+                } else {
+                    // table saturated: go straight to the global table
+                    global_insert(g, k, c, MODE == MODE_SAMPLE ? ~0ull : m);
+                }
+            }
+            if (MODE == MODE_SAMPLE) {
+                // witnesses are random in sample mode: every lane offers its m
+                slot = __shfl_sync(grp, slot, leader);
+                if (slot >= 0) atomicMin(&twit[slot], (unsigned long long)m);
+                else global_insert(g, k, 0ull, m);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < TBL; i += blockDim.x) {
+        const unsigned long long kk = tkey[i];
+        if (kk != 0ull) global_insert(g, kk, tcnt[i], twit[i]);
+    }
+    for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
+        if (thist[i]) atomicAdd(&g.hist[i], (unsigned long long)thist[i]);
+}
+
+__global__ void k_agg_clear(DevAgg g) {
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < GCAP; i += stride) {
+        g.keys[i] = 0ull;
+        g.cnt[i] = 0ull;
+        g.wit[i] = ~0ull;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < NHIST) g.hist[threadIdx.x] = 0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *g.bad = ~0ull;
+        *g.overflow = 0u;
+    }
+}
+
+__global__ void k_agg_compact(DevAgg g, unsigned long long *okey, unsigned long long *ocnt,
+                              unsigned long long *owit, unsigned int *on) {
+    const int stride = gridDim.x * blockDim.x;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < GCAP; i += stride) {
+        const unsigned long long k = g.keys[i];
+        if (k) {
+            const unsigned int j = atomicAdd(on, 1u);
+            okey[j] = k;
+            ocnt[j] = g.cnt[i];
+            owit[j] = g.wit[i];
+        }
+    }
+}
+
+// ------------------------------------------------------------ error state
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string &msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return fail(TCG_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+}  // namespace
+
+// ------------------------------------------------------------------- plan
+struct tcg_plan {
+    int device = 0, d = 0, K = 0, even = 0, nused = 0, maxreg = 0, nsm = 0;
+    int threads = THREADS;
+    int blocks_enum = 0, blocks_batch = 0;
+    size_t smem_enum = 0, smem_batch = 0;
+    KParams kp{};
+    uint32_t *d_adj = nullptr, *d_edges = nullptr;
+    DevAgg agg{};
+    unsigned long long *d_ckey = nullptr, *d_ccnt = nullptr, *d_cwit = nullptr;
+    unsigned int *d_cn = nullptr;
+    uint64_t *d_sig = nullptr, *d_key = nullptr;
+    uint8_t *d_ov = nullptr, *d_nr = nullptr;
+    int32_t *d_st = nullptr;
+    int64_t batch_cap = 0;
+    cudaStream_t own = nullptr, stream = nullptr;
+    int64_t launches = 0;
+    // split-phase bookkeeping: how to map a failing index back to its sign word
+    int pending_mode = -1;
+    uint64_t pending_seed = 0, pending_mask = 0;
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <int K, bool EVEN>
+void *enum_fn(int mode) {
+    switch (mode) {
+        case MODE_RAW: return (void *)k_enumerate<K, EVEN, MODE_RAW>;
+        case MODE_REP: return (void *)k_enumerate<K, EVEN, MODE_REP>;
+        default: return (void *)k_enumerate<K, EVEN, MODE_SAMPLE>;
+    }
+}
+
+void *pick_enum(int K, bool even, int mode) {
+    if (K == 2) return even ? enum_fn<2, true>(mode) : enum_fn<2, false>(mode);
+    if (K == 4) return even ? enum_fn<4, true>(mode) : enum_fn<4, false>(mode);
+    return even ? enum_fn<6, true>(mode) : enum_fn<6, false>(mode);
+}
+
+void *pick_batch(int K, bool even) {
+    if (K == 2) return even ? (void *)k_batch<2, true> : (void *)k_batch<2, false>;
+    if (K == 4) return even ? (void *)k_batch<4, true> : (void *)k_batch<4, false>;
+    return even ? (void *)k_batch<6, true> : (void *)k_batch<6, false>;
+}
+
+size_t adj_bytes(int K) { return (size_t)32 * K * K * sizeof(uint32_t); }
+
+size_t enum_smem(int K) {
+    return adj_bytes(K) + TBL * (2 * sizeof(unsigned long long) + sizeof(uint32_t)) +
+           NHIST * sizeof(uint32_t);
+}
+
+// Vertex layout.  H = 16K bits per half.  P-half (points p > -p
+// lexicographically, i.e. i > 0 or (i == 0 and j > 0)):
+//   bits [0, npts-1)      : first-quadrant points except the origin, in
+//                           A(d) index order (bit = index - 1), so their
+//                           signs are sigma >> 1;
+//   bits [npts-1, d^2+d)  : mirrored quadrant (i > 0, j < 0), in A(d) order
+//                           of (i, |j|); signs = compressed sigma ^ (j odd);
+//   bit d^2+d             : the origin.
+// N-half: bit H + b holds the antipode of P-half bit b, whose sign is the
+// P-half sign ^ ((|i|+|j|) & 1).  The antipodal map is therefore a swap of
+// the two halves.
+struct Layout {
+    int d, K, H, npts;
+    std::vector<int> pos;  // lex vertex -> bit position
+};
+
+int point_index(int d, int i, int j) { return i * (d + 1) - i * (i - 1) / 2 + j; }
+
+int build_layout(const tcg_desc *D, Layout &L) {
+    const int d = D->degree;
+    L.d = d;
+    L.npts = (d + 1) * (d + 2) / 2;
+    const int half = d * d + d + 1;  // P-half incl. the origin
+    L.K = half <= 32 ? 2 : (half <= 64 ? 4 : 6);
+    L.H = 16 * L.K;
+    // q4 rank of (i, j), i > 0, j > 0
+    std::vector<int> q4rank(L.npts, -1);
+    int r = 0;
+    for (int i = 1; i <= d; ++i)
+        for (int j = 1; j <= d - i; ++j) q4rank[point_index(d, i, j)] = r++;
+    // lexicographic diamond points
+    std::vector<std::pair<int, int>> pts;
+    for (int i = -d; i <= d; ++i) {
+        const int a = d - std::abs(i);
+        for (int j = -a; j <= a; ++j) pts.emplace_back(i, j);
+    }
+    if ((int)pts.size() != D->nv) return fail(TCG_E_ARG, "nv does not match the degree");
+    auto ppos = [&](int i, int j) -> int {  // P-half position of a P-half point
+        if (j >= 0) return point_index(d, i, j) - 1;
+        return (L.npts - 1) + q4rank[point_index(d, i, -j)];
+    };
+    L.pos.assign(D->nv, -1);
+    for (int v = 0; v < D->nv; ++v) {
+        const int i = pts[v].first, j = pts[v].second;
+        if (i == 0 && j == 0) L.pos[v] = d * d + d;
+        else if (i > 0 || (i == 0 && j > 0)) L.pos[v] = ppos(i, j);
+        else L.pos[v] = L.H + ppos(-i, -j);
+    }
+    return TCG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *tcg_last_error(void) { return g_last_error.c_str(); }
+const char *tcg_version(void) { return TCG_VERSION; }
+
+int tcg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int64_t tcg_launch_count(const tcg_plan *plan) { return plan ? plan->launches : -1; }
+
+int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
+    if (!D || !out) return fail(TCG_E_ARG, "null argument");
+    *out = nullptr;
+    const int d = D->degree;
+    if (d < 1) return fail(TCG_E_ARG, "degree must be >= 1");
+    if (d > 9)
+        return fail(TCG_E_UNSUPPORTED,
+                    "degree > 9 exceeds the 64-bit sign word / 96-bit half-mask layout");
+    if (D->nv != 2 * d * d + 2 * d + 1) return fail(TCG_E_ARG, "nv != 2d^2+2d+1");
+    if (D->npts != (d + 1) * (d + 2) / 2) return fail(TCG_E_ARG, "npts mismatch");
+    if (D->maxreg < 1 || D->maxreg > MAXR) return fail(TCG_E_UNSUPPORTED, "maxreg out of range");
+    if (D->ne < 1) return fail(TCG_E_ARG, "empty edge list");
+    Layout L;
+    int rc = build_layout(D, L);
+    if (rc) return rc;
+    const int K = L.K, H = L.H;
+
+    // validate descriptor against the layout (src/par must be the reference's)
+    for (int v = 0; v < D->nv; ++v) {
+        if (D->src[v] < 0 || D->src[v] >= D->npts) return fail(TCG_E_ARG, "src out of range");
+    }
+    tcg_plan *P = new tcg_plan();
+    P->d = d;
+    P->K = K;
+    P->even = (d % 2 == 0);
+    P->maxreg = D->maxreg;
+    KParams &kp = P->kp;
+    kp.d = d;
+    kp.npts = D->npts;
+    kp.maxreg = D->maxreg;
+    kp.center = d * d + d;
+    kp.ne = D->ne;
+    // used / boundary / parity masks
+    std::vector<uint32_t> adj((size_t)2 * H * K, 0u);
+    auto setbit = [&](uint32_t *m, int pos) { m[pos >> 5] |= 1u << (pos & 31); };
+    int nused = 0;
+    for (int v = 0; v < D->nv; ++v)
+        if (D->used[v]) {
+            setbit(kp.used, L.pos[v]);
+            ++nused;
+        }
+    kp.nused = nused;
+    P->nused = nused;
+    for (int a = 0; a < D->nap; ++a) {
+        const int u = D->ap_u[a], v = D->ap_v[a];
+        if (u < 0 || u >= D->nv || v < 0 || v >= D->nv) {
+            delete P;
+            return fail(TCG_E_ARG, "antipodal pair out of range");
+        }
+        const int pu = L.pos[u], pv = L.pos[v];
+        if (std::abs(pu - pv) != H) {
+            delete P;
+            return fail(TCG_E_ARG, "antipodal pair is not (p, -p)");
+        }
+        setbit(kp.bd, pu);
+        setbit(kp.bd, pv);
+    }
+    // sign-extension tables -> P-half masks; verify they are the reference's
+    {
+        std::vector<std::pair<int, int>> pts;
+        for (int i = -d; i <= d; ++i) {
+            const int a = d - std::abs(i);
+            for (int j = -a; j <= a; ++j) pts.emplace_back(i, j);
+        }
+        for (int v = 0; v < D->nv; ++v) {
+            const int i = pts[v].first, j = pts[v].second;
+            const int want_src = point_index(d, std::abs(i), std::abs(j));
+            const int want_par = ((i < 0 ? -i : 0) + (j < 0 ? -j : 0)) & 1;
+            if (D->src[v] != want_src || D->par[v] != want_par) {
+                delete P;
+                return fail(TCG_E_ARG, "src/par tables differ from the reflected sign extension");
+            }
+            const int pos = L.pos[v];
+            if (pos < H && !(i == 0 && j == 0)) {
+                if (((std::abs(i) + std::abs(j)) & 1) != 0) kp.parP[pos >> 5] |= 1u << (pos & 31);
+                if (j < 0 && ((-j) & 1)) kp.jodd[pos >> 5] |= 1u << (pos & 31);
+            }
+        }
+    }
+    // mirrored-quadrant compress runs: row i contributes (i,1..d-i)
+    {
+        int nq = 0, dst = 0;
+        for (int i = 1; i <= d - 1; ++i) {
+            kp.q4src[nq] = (uint8_t)point_index(d, i, 1);
+            kp.q4len[nq] = (uint8_t)(d - i);
+            kp.q4dst[nq] = (uint8_t)dst;
+            dst += d - i;
+            ++nq;
+        }
+        kp.nq4 = nq;
+    }
+    // adjacency rows and edge list in layout positions
+    std::vector<uint32_t> edges(D->ne);
+    for (int e = 0; e < D->ne; ++e) {
+        const int u = D->edge_u[e], v = D->edge_v[e];
+        if (u < 0 || u >= D->nv || v < 0 || v >= D->nv || u == v) {
+            delete P;
+            return fail(TCG_E_ARG, "edge endpoint out of range");
+        }
+        const int pu = L.pos[u], pv = L.pos[v];
+        adj[(size_t)pu * K + (pv >> 5)] |= 1u << (pv & 31);
+        adj[(size_t)pv * K + (pu >> 5)] |= 1u << (pu & 31);
+        edges[e] = (uint32_t)pu | ((uint32_t)pv << 16);
+    }
+
+    if (device < 0) {
+        if (cudaGetDevice(&device) != cudaSuccess) {
+            delete P;
+            cudaGetLastError();
+            return fail(TCG_E_CUDA, "no CUDA device");
+        }
+    }
+    P->device = device;
+    DeviceGuard guard(device);
+    auto bail = [&](cudaError_t e, const char *what) {
+        std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+        tcg_plan_destroy(P);
+        return fail(TCG_E_CUDA, msg);
+    };
+    cudaError_t e;
+    if ((e = cudaFree(nullptr)) != cudaSuccess) return bail(e, "context");
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return bail(e, "props");
+    if (prop.major < 10) {
+        tcg_plan_destroy(P);
+        return fail(TCG_E_UNSUPPORTED, "libtcg is built for sm_100a (Blackwell B200)");
+    }
+    P->nsm = prop.multiProcessorCount;
+    if ((e = cudaStreamCreateWithFlags(&P->own, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail(e, "stream");
+    P->stream = P->own;
+    if ((e = cudaMalloc(&P->d_adj, adj.size() * 4)) != cudaSuccess) return bail(e, "malloc adj");
+    if ((e = cudaMalloc(&P->d_edges, std::max<size_t>(1, edges.size()) * 4)) != cudaSuccess)
+        return bail(e, "malloc edges");
+    cudaMemcpy(P->d_adj, adj.data(), adj.size() * 4, cudaMemcpyHostToDevice);
+    if (!edges.empty())
+        cudaMemcpy(P->d_edges, edges.data(), edges.size() * 4, cudaMemcpyHostToDevice);
+    kp.adj = P->d_adj;
+    kp.edges = P->d_edges;
+    DevAgg &g = P->agg;
+    if ((e = cudaMalloc(&g.keys, GCAP * 8)) != cudaSuccess) return bail(e, "malloc agg");
+    if ((e = cudaMalloc(&g.cnt, GCAP * 8)) != cudaSuccess) return bail(e, "malloc agg");
+    if ((e = cudaMalloc(&g.wit, GCAP * 8)) != cudaSuccess) return bail(e, "malloc agg");
+    if ((e = cudaMalloc(&g.hist, NHIST * 8)) != cudaSuccess) return bail(e, "malloc agg");
+    if ((e = cudaMalloc(&g.bad, 8)) != cudaSuccess) return bail(e, "malloc agg");
+    if ((e = cudaMalloc(&g.overflow, 4)) != cudaSuccess) return bail(e, "malloc agg");
+    if ((e = cudaMalloc(&P->d_ckey, GCAP * 8)) != cudaSuccess) return bail(e, "malloc compact");
+    if ((e = cudaMalloc(&P->d_ccnt, GCAP * 8)) != cudaSuccess) return bail(e, "malloc compact");
+    if ((e = cudaMalloc(&P->d_cwit, GCAP * 8)) != cudaSuccess) return bail(e, "malloc compact");
+    if ((e = cudaMalloc(&P->d_cn, 4)) != cudaSuccess) return bail(e, "malloc compact");
+
+    // launch geometry: persistent grid = SMs x resident CTAs
+    P->smem_enum = enum_smem(K);
+    P->smem_batch = adj_bytes(K);
+    int bps = 0;
+    for (int mode = 0; mode < 3; ++mode) {
+        void *fn = pick_enum(K, P->even, mode);
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_enum);
+    }
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_enum(K, P->even, MODE_RAW),
+                                                           THREADS, P->smem_enum)) != cudaSuccess)
+        return bail(e, "occupancy");
+    P->blocks_enum = std::max(1, bps) * P->nsm;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_batch(K, P->even), THREADS,
+                                                           P->smem_batch)) != cudaSuccess)
+        return bail(e, "occupancy");
+    P->blocks_batch = std::max(1, bps) * P->nsm;
+    *out = P;
+    int rc2 = tcg_agg_reset(P);
+    if (rc2) {
+        tcg_plan_destroy(P);
+        *out = nullptr;
+        return rc2;
+    }
+    if ((e = cudaStreamSynchronize(P->stream)) != cudaSuccess) {
+        tcg_plan_destroy(P);
+        *out = nullptr;
+        return fail(TCG_E_CUDA, std::string("init: ") + cudaGetErrorString(e));
+    }
+    return TCG_OK;
+}
+
+int tcg_plan_destroy(tcg_plan *P) {
+    if (!P) return TCG_OK;
+    DeviceGuard guard(P->device);
+    if (P->stream) cudaStreamSynchronize(P->stream);
+    void *ptrs[] = {P->d_adj, P->d_edges, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+                    P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
+                    P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (P->own) cudaStreamDestroy(P->own);
+    delete P;
+    return TCG_OK;
+}
+
+int tcg_plan_set_stream(tcg_plan *P, void *stream) {
+    if (!P) return fail(TCG_E_ARG, "null plan");
+    P->stream = stream ? (cudaStream_t)stream : P->own;
+    return TCG_OK;
+}
+
+int tcg_plan_info(const tcg_plan *P, int32_t *info, int ninfo) {
+    if (!P || !info) return fail(TCG_E_ARG, "null argument");
+    const int32_t v[8] = {P->d, P->K, P->nused, P->device, P->nsm, P->blocks_enum, P->threads,
+                          P->maxreg};
+    for (int i = 0; i < ninfo && i < 8; ++i) info[i] = v[i];
+    return TCG_OK;
+}
+
+static int launch_batch(tcg_plan *P, const uint64_t *d_sig, int64_t n, uint64_t *d_key,
+                        uint8_t *d_ov, uint8_t *d_nr, int32_t *d_st) {
+    if (n <= 0) return TCG_OK;
+    void *fn = pick_batch(P->K, P->even);
+    int64_t blocks = std::min<int64_t>(P->blocks_batch, (n + THREADS - 1) / THREADS);
+    void *args[] = {&P->kp, &d_sig, &n, &d_key, &d_ov, &d_nr, &d_st};
+    CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(THREADS), args, P->smem_batch,
+                              P->stream));
+    P->launches++;
+    return TCG_OK;
+}
+
+int tcg_classify_batch_device(tcg_plan *P, const uint64_t *d_sig, int64_t n, uint64_t *d_key,
+                              uint8_t *d_ov, uint8_t *d_nr, int32_t *d_st) {
+    if (!P) return fail(TCG_E_ARG, "null plan");
+    DeviceGuard guard(P->device);
+    return launch_batch(P, d_sig, n, d_key, d_ov, d_nr, d_st);
+}
+
+int tcg_classify_batch(tcg_plan *P, const uint64_t *sig, int64_t n, uint64_t *key, uint8_t *ov,
+                       uint8_t *nr, int32_t *st) {
+    if (!P || (n > 0 && (!sig || !key || !ov || !nr || !st))) return fail(TCG_E_ARG, "null argument");
+    if (n <= 0) return TCG_OK;
+    DeviceGuard guard(P->device);
+    if (n > P->batch_cap) {
+        cudaFree(P->d_sig); cudaFree(P->d_key); cudaFree(P->d_ov); cudaFree(P->d_nr); cudaFree(P->d_st);
+        P->d_sig = nullptr; P->d_key = nullptr; P->d_ov = nullptr; P->d_nr = nullptr; P->d_st = nullptr;
+        P->batch_cap = 0;
+        int64_t cap = std::max<int64_t>(n, 1 << 16);
+        CUDA_TRY(cudaMalloc(&P->d_sig, cap * 8));
+        CUDA_TRY(cudaMalloc(&P->d_key, cap * 8));
+        CUDA_TRY(cudaMalloc(&P->d_ov, cap));
+        CUDA_TRY(cudaMalloc(&P->d_nr, cap));
+        CUDA_TRY(cudaMalloc(&P->d_st, cap * 4));
+        P->batch_cap = cap;
+    }
+    CUDA_TRY(cudaMemcpyAsync(P->d_sig, sig, n * 8, cudaMemcpyHostToDevice, P->stream));
+    int rc = launch_batch(P, P->d_sig, n, P->d_key, P->d_ov, P->d_nr, P->d_st);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(key, P->d_key, n * 8, cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(ov, P->d_ov, n, cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(nr, P->d_nr, n, cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(st, P->d_st, n * 4, cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    return TCG_OK;
+}
+
+int tcg_agg_reset(tcg_plan *P) {
+    if (!P) return fail(TCG_E_ARG, "null plan");
+    DeviceGuard guard(P->device);
+    k_agg_clear<<<64, 256, 0, P->stream>>>(P->agg);
+    CUDA_TRY(cudaGetLastError());
+    P->launches++;
+    P->pending_mode = -1;
+    return TCG_OK;
+}
+
+static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t seed,
+                   uint64_t mask) {
+    if (P->pending_mode >= 0 && P->pending_mode != mode)
+        return fail(TCG_E_ARG, "aggregate already holds another domain; call tcg_agg_reset");
+    if (mode == MODE_SAMPLE && P->pending_mode == MODE_SAMPLE &&
+        (P->pending_seed != seed || P->pending_mask != mask))
+        return fail(TCG_E_ARG, "aggregate already holds another sample stream");
+    P->pending_mode = mode;
+    P->pending_seed = seed;
+    P->pending_mask = mask;
+    void *fn = pick_enum(P->K, P->even, mode);
+    for (uint64_t a = start; a < end;) {
+        const uint64_t n = std::min<uint64_t>(end - a, LAUNCH_MAX);
+        const uint64_t warps = (n + 31) / 32;
+        const uint64_t need = (warps * 32 + THREADS - 1) / THREADS;
+        const unsigned blocks = (unsigned)std::min<uint64_t>(P->blocks_enum, std::max<uint64_t>(1, need));
+        uint64_t base = a, count = n;
+        void *args[] = {&P->kp, &base, &count, &seed, &mask, &P->agg};
+        CUDA_TRY(cudaLaunchKernel(fn, dim3(blocks), dim3(THREADS), args, P->smem_enum, P->stream));
+        P->launches++;
+        a += n;
+    }
+    return TCG_OK;
+}
+
+int tcg_sweep_async(tcg_plan *P, int raw, uint64_t start, uint64_t end) {
+    if (!P) return fail(TCG_E_ARG, "null plan");
+    const int bits = raw ? P->kp.npts : P->kp.npts - 3;
+    if (bits > 62) return fail(TCG_E_RANGE, "domain exceeds 62 index bits");
+    const uint64_t domain = 1ull << bits;
+    if (start > end || end > domain) return fail(TCG_E_RANGE, "sweep range outside the domain");
+    DeviceGuard guard(P->device);
+    return enqueue(P, raw ? MODE_RAW : MODE_REP, start, end, 0, 0);
+}
+
+int tcg_sample_async(tcg_plan *P, uint64_t seed, uint64_t k0, uint64_t k1, int nbits) {
+    if (!P) return fail(TCG_E_ARG, "null plan");
+    if (nbits < 0 || nbits > P->kp.npts - 3 || nbits > 62)
+        return fail(TCG_E_RANGE, "nbits outside the representative domain");
+    if (k0 > k1) return fail(TCG_E_RANGE, "bad draw range");
+    DeviceGuard guard(P->device);
+    const uint64_t mask = nbits >= 64 ? ~0ull : ((1ull << nbits) - 1ull);
+    return enqueue(P, MODE_SAMPLE, k0, k1, seed, mask);
+}
+
+static uint64_t host_splitmix(uint64_t seed, uint64_t k) {
+    uint64_t z = seed + (k + 1ull) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static uint64_t host_rep_to_sigma(int d, uint64_t m) {
+    const uint64_t low = m & ((1ull << (d - 1)) - 1ull);
+    return (low << 2) | ((m >> (d - 1)) << (d + 2));
+}
+
+int tcg_agg_fetch(tcg_plan *P, tcg_agg *A, int64_t *bad) {
+    if (!P || !A) return fail(TCG_E_ARG, "null argument");
+    DeviceGuard guard(P->device);
+    CUDA_TRY(cudaMemsetAsync(P->d_cn, 0, 4, P->stream));
+    k_agg_compact<<<64, 256, 0, P->stream>>>(P->agg, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn);
+    CUDA_TRY(cudaGetLastError());
+    P->launches++;
+    unsigned int n = 0, overflow = 0;
+    unsigned long long hist[NHIST], badidx = 0;
+    CUDA_TRY(cudaMemcpyAsync(&n, P->d_cn, 4, cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(&overflow, P->agg.overflow, 4, cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(hist, P->agg.hist, sizeof(hist), cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(&badidx, P->agg.bad, 8, cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    if (bad) *bad = -1;
+    if (badidx != ~0ull) {
+        // recompute the failing patchwork's status (smallest failing index)
+        uint64_t m = badidx, sigma;
+        if (P->pending_mode == MODE_SAMPLE) {
+            m = host_splitmix(P->pending_seed, badidx) & P->pending_mask;
+            sigma = host_rep_to_sigma(P->d, m);
+        } else if (P->pending_mode == MODE_REP) {
+            sigma = host_rep_to_sigma(P->d, m);
+        } else {
+            sigma = m;
+        }
+        uint64_t key;
+        uint8_t ov, nr;
+        int32_t st = 0;
+        int rc = tcg_classify_batch(P, &sigma, 1, &key, &ov, &nr, &st);
+        if (rc) return rc;
+        if (bad) *bad = (int64_t)m;
+        return st ? st : fail(TCG_E_CUDA, "device reported a failure the replay did not reproduce");
+    }
+    if (overflow) return fail(TCG_TABLE_FULL, "global scheme table full");
+    if ((int32_t)n > A->cap) return fail(TCG_TABLE_FULL, "caller's aggregate capacity too small");
+    std::vector<unsigned long long> k(n), c(n), w(n);
+    if (n) {
+        CUDA_TRY(cudaMemcpy(k.data(), P->d_ckey, n * 8ull, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(c.data(), P->d_ccnt, n * 8ull, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(w.data(), P->d_cwit, n * 8ull, cudaMemcpyDeviceToHost));
+    }
+    std::vector<unsigned> ord(n);
+    for (unsigned i = 0; i < n; ++i) ord[i] = i;
+    std::sort(ord.begin(), ord.end(), [&](unsigned a, unsigned b) { return k[a] < k[b]; });
+    int64_t total = 0;
+    for (int i = 0; i < NHIST; ++i) {
+        A->hist[i] = (int64_t)hist[i];
+        total += (int64_t)hist[i];
+    }
+    A->total = total;
+    A->n = (int32_t)n;
+    for (unsigned i = 0; i < n; ++i) {
+        A->key[i] = k[ord[i]];
+        A->count[i] = (int64_t)c[ord[i]];
+        A->witness[i] = (int64_t)w[ord[i]];
+    }
+    return TCG_OK;
+}
+
+int tcg_sweep(tcg_plan *P, int raw, uint64_t start, uint64_t end, tcg_agg *A, int64_t *bad) {
+    int rc = tcg_agg_reset(P);
+    if (rc) return rc;
+    rc = tcg_sweep_async(P, raw, start, end);
+    if (rc) return rc;
+    return tcg_agg_fetch(P, A, bad);
+}
+
+int tcg_sample(tcg_plan *P, uint64_t seed, uint64_t k0, uint64_t k1, int nbits, tcg_agg *A,
+               int64_t *bad) {
+    int rc = tcg_agg_reset(P);
+    if (rc) return rc;
+    rc = tcg_sample_async(P, seed, k0, k1, nbits);
+    if (rc) return rc;
+    return tcg_agg_fetch(P, A, bad);
+}
+
+static int merge_multi(std::vector<tcg_agg> &parts, std::vector<int> &rcs,
+                       std::vector<int64_t> &bads, tcg_agg *A, int64_t *bad) {
+    int status = TCG_OK;
+    int64_t best = -1;
+    for (size_t i = 0; i < parts.size(); ++i) {
+        if (rcs[i] < 0) return rcs[i];
+        if (rcs[i] > 0 && (best < 0 || bads[i] < best)) {
+            best = bads[i];
+            status = rcs[i];
+        }
+    }
+    if (status) {
+        if (bad) *bad = best;
+        return status;
+    }
+    std::unordered_map<uint64_t, std::pair<int64_t, int64_t>> m;
+    std::memset(A->hist, 0, sizeof(A->hist));
+    A->total = 0;
+    for (auto &p : parts) {
+        for (int i = 0; i < NHIST; ++i) A->hist[i] += p.hist[i];
+        A->total += p.total;
+        for (int i = 0; i < p.n; ++i) {
+            auto it = m.find(p.key[i]);
+            if (it == m.end()) m.emplace(p.key[i], std::make_pair(p.count[i], p.witness[i]));
+            else {
+                it->second.first += p.count[i];
+                it->second.second = std::min(it->second.second, p.witness[i]);
+            }
+        }
+    }
+    if ((int64_t)m.size() > A->cap) return fail(TCG_TABLE_FULL, "aggregate capacity too small");
+    std::vector<uint64_t> keys;
+    for (auto &kv : m) keys.push_back(kv.first);
+    std::sort(keys.begin(), keys.end());
+    A->n = (int32_t)keys.size();
+    for (size_t i = 0; i < keys.size(); ++i) {
+        A->key[i] = keys[i];
+        A->count[i] = m[keys[i]].first;
+        A->witness[i] = m[keys[i]].second;
+    }
+    if (bad) *bad = -1;
+    return TCG_OK;
+}
+
+static int run_multi(tcg_plan **plans, int nplans, uint64_t a, uint64_t b, tcg_agg *A,
+                     int64_t *bad, const std::function<int(tcg_plan *, uint64_t, uint64_t, tcg_agg *, int64_t *)> &fn) {
+    if (!plans || nplans < 1 || !A) return fail(TCG_E_ARG, "bad arguments");
+    std::vector<tcg_agg> parts(nplans);
+    std::vector<std::vector<uint64_t>> keys(nplans);
+    std::vector<std::vector<int64_t>> cnts(nplans), wits(nplans);
+    std::vector<int> rcs(nplans, 0);
+    std::vector<int64_t> bads(nplans, -1);
+    std::vector<std::thread> th;
+    const uint64_t n = b - a;
+    for (int i = 0; i < nplans; ++i) {
+        keys[i].resize(A->cap);
+        cnts[i].resize(A->cap);
+        wits[i].resize(A->cap);
+        parts[i] = tcg_agg{};
+        parts[i].cap = A->cap;
+        parts[i].key = keys[i].data();
+        parts[i].count = cnts[i].data();
+        parts[i].witness = wits[i].data();
+        const uint64_t lo = a + n * (uint64_t)i / nplans, hi = a + n * (uint64_t)(i + 1) / nplans;
+        th.emplace_back([&, i, lo, hi] { rcs[i] = fn(plans[i], lo, hi, &parts[i], &bads[i]); });
+    }
+    for (auto &t : th) t.join();
+    return merge_multi(parts, rcs, bads, A, bad);
+}
+
+int tcg_sweep_multi(tcg_plan **plans, int nplans, int raw, uint64_t start, uint64_t end,
+                    tcg_agg *A, int64_t *bad) {
+    if (start > end) return fail(TCG_E_RANGE, "bad range");
+    return run_multi(plans, nplans, start, end, A, bad,
+                     [raw](tcg_plan *p, uint64_t lo, uint64_t hi, tcg_agg *a, int64_t *b) {
+                         return tcg_sweep(p, raw, lo, hi, a, b);
+                     });
+}
+
+int tcg_sample_multi(tcg_plan **plans, int nplans, uint64_t seed, uint64_t k0, uint64_t k1,
+                     int nbits, tcg_agg *A, int64_t *bad) {
+    if (k0 > k1) return fail(TCG_E_RANGE, "bad range");
+    return run_multi(plans, nplans, k0, k1, A, bad,
+                     [seed, nbits](tcg_plan *p, uint64_t lo, uint64_t hi, tcg_agg *a, int64_t *b) {
+                         return tcg_sample(p, seed, lo, hi, nbits, a, b);
+                     });
+}
+
+}  // extern "C"
