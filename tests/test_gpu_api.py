@@ -1,0 +1,242 @@
+"""GPU tests of the drop-in API, mirroring the reference's own test suite
+(test_classify.py, test_sweep.py, test_acceptance.py) plus full-size
+property checks the oracle cannot reach in seconds."""
+
+import itertools
+import random
+
+import numpy as np
+import pytest
+
+from conftest import golden, plan_dict, tri_from_fixture, triangulations
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    import paper_2604_09221_b200 as api
+
+    return api
+
+
+def _bits(d, rng):
+    return "".join(rng.choice("01") for _ in range((d + 1) * (d + 2) // 2))
+
+
+def test_degree1_all_eight(api):
+    c = api.Classifier(api.builtin("delaunay-1"))
+    for bits in itertools.product("01", repeat=3):
+        assert c.classify("".join(bits)).scheme == "<J>"
+    rep = api.sweep(api.builtin("delaunay-1"), raw_space=True, classifier=c)
+    assert rep.total_classified == 8 and set(rep.scheme_map) == {"<J>"}
+    assert api.sweep(api.builtin("delaunay-1")).scheme_map == {"<J>": (1, 0)}
+
+
+def test_degree2_sweeps(api):
+    T = api.builtin("delaunay-2")
+    rep = api.sweep(T)
+    assert rep.total_classified == 8 and set(rep.scheme_map) == {"<1>"}
+    raw = api.sweep(T, raw_space=True)
+    assert raw.total_classified == 64 and raw.max_ovals() == 1
+    assert raw.witness_bitstring("<1>") == "000000"
+    assert api.classify(T, "000000").scheme == "<1>"
+
+
+def test_invariances(api, rng):
+    """(Z/2)^3 sign action and the S3 symmetry (test_classify.py:68-89)."""
+    for name in ("random-3-0", "random-4-1", "random-5-2", "delaunay-7", "bowtie8"):
+        T = tri_from_fixture(triangulations()[name])
+        d = T.degree
+        c = api.Classifier(T)
+        for _ in range(10):
+            s = api.SignDistribution.from_bitstring(d, _bits(d, rng))
+            base = c.classify(s)
+            many = c.classify_many([api.eps_action(s, e)
+                                    for e in itertools.product((0, 1), repeat=3)])
+            assert all(r == base for r in many)
+        for g in api.SYMMETRY_GROUP:
+            gT, _ = api.apply_symmetry(T, None, g)
+            cg = api.Classifier(gT)
+            for _ in range(5):
+                s = api.SignDistribution.from_bitstring(d, _bits(d, rng))
+                _, gs = api.apply_symmetry(T, s, g)
+                assert cg.classify(gs) == c.classify(s)
+
+
+def test_structural_invariants(api, rng):
+    # test_acceptance.py:188-201
+    for d in range(1, 10):
+        c = api.Classifier(api.builtin(f"delaunay-{d}"))
+        res = c.classify_many([_bits(d, rng) for _ in range(300)])
+        for r in res:
+            assert r.region_count == r.oval_count + 1
+            assert r.oval_count + (d % 2) <= api.harnack_bound(d)
+            assert r.has_pseudoline == (d % 2 == 1)
+            assert ("J" in r.scheme) == (d % 2 == 1)
+
+
+def test_bowtie_even_ovals(api, rng):
+    c = api.Classifier(api.builtin("bowtie8"))
+    for r in c.classify_many([_bits(8, rng) for _ in range(2000)]):
+        assert r.oval_count % 2 == 0 and r.oval_count >= 4
+
+
+def test_harnack_m_curves(api):
+    # sigma(i,j) = i*j mod 2 on delaunay-d
+    want = {4: "<4>", 5: "<J u 6>", 6: "<9 u 1<1>>", 7: "<J u 15>", 8: "<18 u 1<3>>"}
+    for d, s in want.items():
+        c = api.Classifier(api.builtin(f"delaunay-{d}"))
+        bits = "".join(str((i * j) % 2) for i, j in api.lattice_points(d))
+        r = c.classify(bits)
+        assert r.scheme == s and r.oval_count == api.harnack_bound(d) - (d % 2)
+
+
+def test_chunk_split_merge_and_witness_minimality(api):
+    T = api.builtin("delaunay-3")
+    full = api.sweep(T)
+    k = api.num_representatives(3) // 2
+    assert api.merge(api.sweep(T, api.SweepRange(0, k)),
+                     api.sweep(T, api.SweepRange(k, 2 * k))) == full
+    c = api.Classifier(T)
+    for scheme, (count, wit) in full.scheme_map.items():
+        assert c.classify(api.representative(3, wit)).scheme == scheme
+        others = c.classify_many([api.representative(3, m) for m in range(wit)])
+        assert all(r.scheme != scheme for r in others)
+
+
+def test_full_size_split_invariance_degree7(api):
+    """2^32 raw indices as one launch chain == split at an odd point and merged."""
+    T = api.builtin("delaunay-7")
+    c = api.Classifier(T)
+    a, b, m = 5 << 30, (5 << 30) + (1 << 32), (5 << 30) + 1234567891
+    whole = api.sweep(T, api.SweepRange(a, b), raw_space=True, classifier=c)
+    parts = api.merge(api.sweep(T, api.SweepRange(a, m), raw_space=True, classifier=c),
+                      api.sweep(T, api.SweepRange(m, b), raw_space=True, classifier=c))
+    assert whole == parts
+    assert whole.total_classified == 1 << 32 == sum(whole.oval_histogram)
+    assert sum(c for c, _ in whole.scheme_map.values()) == 1 << 32
+
+
+def test_raw_vs_rep_domain_relations(api):
+    """raw counts = 8 x rep counts; raw lower half = raw / 2 with equal witnesses
+    (verified there for d = 3, 4, 5)."""
+    for d in (4, 5, 6):
+        T = api.builtin(f"delaunay-{d}")
+        c = api.Classifier(T)
+        n = (d + 1) * (d + 2) // 2
+        rep = api.sweep(T, classifier=c)
+        raw = api.sweep(T, raw_space=True, classifier=c)
+        low = api.sweep(T, api.SweepRange(0, 1 << (n - 1)), raw_space=True, classifier=c)
+        assert set(rep.scheme_map) == set(raw.scheme_map) == set(low.scheme_map)
+        for s, (cnt, w) in raw.scheme_map.items():
+            assert cnt == 8 * rep.scheme_map[s][0]
+            assert low.scheme_map[s] == (cnt // 2, w)
+
+
+def test_sample_reproducible_and_partition_independent(api):
+    T = api.builtin("delaunay-4")
+    c = api.Classifier(T)
+    a = api.sample(T, 5000, seed=42, classifier=c)
+    assert a == api.sample(T, 5000, seed=42, workers=4, chunk_size=977, classifier=c)
+    assert a.total_classified == 5000
+    assert api.sample(T, 5000, seed=43, classifier=c) != a
+    T8 = api.builtin("bowtie8")
+    c8 = api.Classifier(T8)
+    full = api.sample(T8, 300_000, seed=5, classifier=c8)
+    from paper_2604_09221_b200.sweep import sample_slice
+
+    s1 = sample_slice(T8, 5, 0, 123_457, classifier=c8)
+    s2 = sample_slice(T8, 5, 123_457, 300_000, classifier=c8)
+    merged = api.merge(s1, s2)
+    assert merged.oval_histogram == full.oval_histogram
+    assert merged.scheme_map == full.scheme_map
+
+
+def test_fig2_bowtie_distribution(api):
+    # test_acceptance.py:128-141 (criterion 05), +-0.3 pp on 10^6 draws
+    bins = {4: 4.6875, 6: 11.3281, 8: 14.6484, 10: 25.5371, 12: 17.1997, 14: 13.9526,
+            16: 10.9695, 18: 1.6113, 20: 0.0652, 22: 0.0004}
+    r = api.sample(api.builtin("bowtie8"), 1_000_000, seed=20260810)
+    assert r.total_classified == 1_000_000
+    for k, c in enumerate(r.oval_histogram):
+        if k % 2 == 1 or k < 4:
+            assert c == 0
+    for k, pct in bins.items():
+        assert abs(100.0 * r.oval_histogram[k] / 1_000_000 - pct) <= 0.3
+    assert "<0>" not in r.scheme_map and r.distinct_schemes() <= 123
+
+
+def test_errors(api):
+    T = api.builtin("delaunay-2")
+    with pytest.raises(api.IndexOutOfRange):
+        api.sweep(T, api.SweepRange(0, 9))
+    with pytest.raises(api.IndexOutOfRange):
+        api.SweepRange(5, 3)
+    with pytest.raises(api.BudgetExceeded):
+        api.sweep(api.builtin("delaunay-10"))
+    with pytest.raises(api.ParseError):
+        api.Classifier(T).classify("000")
+    with pytest.raises(api.IndexOutOfRange):
+        api.sample(T, 0, seed=1)
+
+
+def test_sweep_error_reports_smallest_failing_index(api):
+    """A garbage plan fails inside the sweep kernel; the raised index and
+    message are those of the oracle's first failing index."""
+    from oracle import oracle as O
+    from paper_2604_09221_b200 import _lib
+    from paper_2604_09221_b200.classify import STATUS_MESSAGES
+    from paper_2604_09221_b200.diamond import PlanArrays
+    from paper_2604_09221_b200.sweep import _raise_status
+
+    e = [g for g in golden("garbage.json") if g["name"] == "garbage-5-0"][0]
+    P = plan_dict(e)
+    arr = PlanArrays(P["degree"], P["nv"], P["npts"], np.array(P["edge_u"], np.int32),
+                     np.array(P["edge_v"], np.int32), np.array(P["src"], np.int32),
+                     np.array(P["par"], np.uint8), np.array(P["used"], np.uint8),
+                     np.array(P["ap_u"], np.int32), np.array(P["ap_v"], np.int32), P["maxreg"])
+    plan = _lib.NativePlan(arr, 0)
+    rc, bad, _ = plan.sweep(True, 1000, 1000 + (1 << 16))
+    ref = O.sweep(O.OraclePlan.from_arrays(P), True, 1000, 1000 + (1 << 16), threads=1)
+    assert ref["status"] != 0
+    assert (rc, bad) == (ref["status"], ref["bad"])
+    with pytest.raises(api.InvariantViolation, match=STATUS_MESSAGES[rc]):
+        _raise_status(rc, bad)
+
+
+def test_c4_random_triangulations_batch(api):
+    """Config C4: random regular unimodular degree-7 T x random signs, per pair."""
+    from oracle import oracle as O
+
+    tri = triangulations()
+    rng = np.random.default_rng(0xB7)
+    for k in range(16):
+        t = tri[f"c4-7-{k}"]
+        c = api.Classifier(tri_from_fixture(t))
+        words = rng.integers(0, 1 << 36, size=2048, dtype=np.uint64)
+        keys, ov, nr, st = c.classify_words(words)
+        ref = O.classify_words(O.OraclePlan.from_arrays(plan_dict(t)), words)
+        for i, (s, scheme, o, n) in enumerate(ref):
+            assert st[i] == s == 0
+            assert api.scheme_from_key(int(keys[i]), True) == scheme
+            assert (int(ov[i]), int(nr[i])) == (o, n)
+
+
+def test_multi_device_api_single_device(api):
+    T = api.builtin("delaunay-5")
+    a = api.sweep(T, devices=[0])
+    assert a == api.sweep(T)
+
+
+def test_report_bytes_identical_across_call_shapes(api):
+    # criterion 09: byte-identical reports for any partition
+    from paper_2604_09221_b200.io import histogram_csv, report_jsonl
+
+    for d in (2, 3, 4, 5):
+        T = api.builtin(f"delaunay-{d}")
+        c = api.Classifier(T)
+        outs = {report_jsonl(api.sweep(T, workers=w, chunk_size=cs, classifier=c))
+                + histogram_csv(api.sweep(T, classifier=c))
+                for w, cs in ((1, 65536), (2, 111), (8, 4096))}
+        assert len(outs) == 1
