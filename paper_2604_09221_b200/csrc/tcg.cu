@@ -34,6 +34,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -121,9 +122,17 @@ __device__ __forceinline__ void lowest(const uint32_t (&x)[K], int &w, int &b) {
     b = __ffs(word) - 1;
 }
 
-template <int K>
-__device__ __forceinline__ void load_row(const uint32_t *__restrict__ base, int v, uint32_t (&a)[K]) {
-    if constexpr (K == 2) {
+// Row v of a node table: K adjacency words (+ K partner words if ROWS, which
+// are OR-ed into PL).  Vectorised shared-memory loads.
+template <int K, bool ROWS>
+__device__ __forceinline__ void load_row(const uint32_t *__restrict__ base, int v, uint32_t (&a)[K],
+                                         uint32_t (&PL)[K]) {
+    if constexpr (ROWS) {
+        static_assert(K == 2, "contracted graphs use 64-node masks");
+        const uint4 t = reinterpret_cast<const uint4 *>(base)[v];
+        a[0] = t.x; a[1] = t.y;
+        PL[0] |= t.z; PL[1] |= t.w;
+    } else if constexpr (K == 2) {
         const uint2 t = reinterpret_cast<const uint2 *>(base)[v];
         a[0] = t.x; a[1] = t.y;
     } else if constexpr (K == 4) {
@@ -211,184 +220,12 @@ __device__ __noinline__ int ordered_scan(const KParams &p, const uint32_t (&SG)[
     return TCG_NOT_A_TREE;  // unreachable for the inputs routed here
 }
 
-// ------------------------------------------------------------- classify one
-template <int K, bool EVEN>
-__device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__restrict__ adj,
-                                           uint64_t sigma) {
-    constexpr int HK = K / 2;
-    uint32_t SG[K];
-    sign_words<K>(p, sigma, SG);
-
-    uint32_t unv[K], F[K], XB[K], regS[K], layS[K], E1[K];
-    uint32_t regR[MAXR][K];
-    uint32_t regX[MAXR][K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        unv[k] = p.used[k];
-        F[k] = 0; XB[k] = 0; E1[k] = 0;
-    }
-    int nreg = 0;
-    uint32_t oddmask = 0;
-    uint32_t pimask = 0;  // 0 or ~0: orientation parity of the current layer
-
-    // seed the first region with the lowest used vertex
-    {
-        int w, b;
-        lowest<K>(unv, w, b);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            regS[k] = unv[k];
-            layS[k] = unv[k];
-            F[k] = (k == w) ? (1u << b) : 0u;
-            unv[k] ^= F[k];
-        }
-    }
-
-    auto transition = [&](bool more) {
-        // close the layer: vertices visited since layS
-        uint32_t L[K], P[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            L[k] = layS[k] ^ unv[k];
-            if (EVEN) E1[k] |= L[k] & pimask;
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int ks = (k + HK) % K;  // antipodal map = swap of halves
-            P[k] = L[ks] & p.bd[ks] & unv[k];
-        }
-        if (any<K>(P)) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                layS[k] = unv[k];
-                F[k] = P[k];
-                unv[k] ^= P[k];
-            }
-            pimask = ~pimask;
-            return;
-        }
-        // region complete
-        uint32_t R[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) R[k] = regS[k] ^ unv[k];
-        if (EVEN) {
-            uint32_t acc = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int ks = (k + HK) % K;
-                const uint32_t e0 = R[k] & ~E1[k];
-                const uint32_t e0s = R[ks] & ~E1[ks];
-                acc |= (e0s & p.bd[ks] & e0) | (E1[ks] & p.bd[ks] & E1[k]);
-            }
-            if (acc && nreg < MAXR) oddmask |= 1u << nreg;
-        }
-        if (nreg < MAXR) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                regR[nreg][k] = R[k];
-                regX[nreg][k] = XB[k];
-            }
-        }
-        ++nreg;
-        if (more) {
-            int w, b;
-            lowest<K>(unv, w, b);
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                regS[k] = unv[k];
-                layS[k] = unv[k];
-                F[k] = (k == w) ? (1u << b) : 0u;
-                unv[k] ^= F[k];
-                XB[k] = 0;
-                E1[k] = 0;
-            }
-            pimask = 0;
-        }
-    };
-
-    const int nused = p.nused;
-    for (int it = 0; it < nused; ++it) {
-        if (!any<K>(F)) transition(true);
-        int w, b;
-        lowest<K>(F, w, b);
-        const uint32_t bit = 1u << b;
-#pragma unroll
-        for (int k = 0; k < K; ++k) F[k] ^= (k == w) ? bit : 0u;
-        const int v = 32 * w + b;
-        uint32_t a[K];
-        load_row<K>(adj, v, a);
-        const uint32_t s = (sel<K>(SG, w) >> b) & 1u;
-        const uint32_t nm = s - 1u;  // s ? 0 : ~0
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t same = SG[k] ^ nm;
-            const uint32_t nw = a[k] & same & unv[k];
-            XB[k] |= a[k] & ~same;
-            F[k] |= nw;
-            unv[k] ^= nw;
-        }
-    }
-    transition(false);
-
-    Result res;
-    res.nreg = nreg;
-    res.key = 0;
-    if (nreg > p.maxreg || nreg > MAXR) {  // kernels.py:182: ids 0..maxreg-1 allowed
-        res.status = TCG_TOO_MANY_REGIONS;
-        return res;
-    }
-    int root = -1;
-    if (EVEN) {
-        const int c = __popc(oddmask);
-        if (c == 0) { res.status = TCG_NO_ODD_REGION; return res; }
-        if (c > 1) { res.status = TCG_MANY_ODD_REGIONS; return res; }
-        root = __ffs(oddmask) - 1;
-    }
-    // region graph from crossed-edge neighbourhoods
-    uint32_t radj[MAXR];
-    for (int r = 0; r < nreg; ++r) radj[r] = 0;
-    uint32_t selfm = 0;
-    int nedges = 0;
-    for (int r = 0; r < nreg; ++r) {
-        uint32_t x[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) x[k] = regX[r][k];
-        uint32_t t = 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) t |= x[k] & regR[r][k];
-        if (t) selfm |= 1u << r;
-        for (int r2 = r + 1; r2 < nreg; ++r2) {
-            uint32_t u = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) u |= x[k] & regR[r2][k];
-            if (u) {
-                radj[r] |= 1u << r2;
-                radj[r2] |= 1u << r;
-                ++nedges;
-            }
-        }
-    }
-    const bool toomany = nedges > nreg - 1;  // mid-loop NOT_A_TREE will fire
-    if (EVEN) {
-        if (toomany && selfm) {
-            res.status = ordered_scan<K, EVEN>(p, SG, regR, nreg, root);
-            return res;
-        }
-        if (toomany) { res.status = TCG_NOT_A_TREE; return res; }
-        if (selfm) { res.status = TCG_NONSEPARATING_OVAL; return res; }
-    } else {
-        const bool conflict = __popc(selfm) >= 2;
-        if (toomany && conflict) {
-            res.status = ordered_scan<K, EVEN>(p, SG, regR, nreg, -1);
-            return res;
-        }
-        if (toomany) { res.status = TCG_NOT_A_TREE; return res; }
-        if (conflict) { res.status = TCG_ROOT_CONFLICT; return res; }
-        if (!selfm) { res.status = TCG_NO_PSEUDOLINE; return res; }
-        root = __ffs(selfm) - 1;
-    }
-    if (nedges != nreg - 1) { res.status = TCG_NOT_A_TREE; return res; }
-
+// Rooted BFS over the region tree, then the AHU canonical key bottom-up:
+// code(v) = 1 . sorted child codes . 0, children ordered by sentinel key
+// (length first), leaves (key 0b110) emitted as one run; the root contributes
+// only its child sequence.  Sets status (OK or DISCONNECTED).
+__device__ __forceinline__ uint64_t tree_key(const uint32_t (&radj)[MAXR], int nreg, int root,
+                                             int &status) {
     // rooted BFS over the region tree
     uint8_t order[MAXR], parent[MAXR];
     order[0] = (uint8_t)root;
@@ -406,7 +243,7 @@ __device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__r
             order[tail++] = (uint8_t)s2;
         }
     }
-    if (tail != nreg) { res.status = TCG_DISCONNECTED; return res; }
+    if (tail != nreg) { status = TCG_DISCONNECTED; return 0ull; }
 
     // AHU canonical key, bottom-up (children before parents)
     uint64_t skey[MAXR];
@@ -444,9 +281,244 @@ __device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__r
             skey[v] = (acc << 1) | (1ull << (il + 2));
         }
     }
-    res.key = acc;
-    res.status = TCG_OK;
+    status = TCG_OK;
+    return acc;
+}
+
+// ------------------------------------------------------------- classify one
+// Regions of one patchwork as vertex (or node) masks.
+template <int K, int CAP = MAXR>
+struct Regions {
+    uint32_t R[CAP][K];  // region vertex sets
+    uint32_t X[CAP][K];  // crossed-edge neighbourhoods (COMPS mode: all neighbours)
+    uint32_t oddmask;     // regions closing an orientation-reversing cycle
+    int nreg;
+};
+
+// One breadth-first pass over the used vertices that labels regions.
+//  * inside a layer all vertices share one sign (non-crossed edges join equal
+//    signs), so `same` is a per-layer mask and a visited vertex costs
+//    new = adj & unvS; unvS ^= new; F |= new; NB |= adj   (4 ops per word);
+//  * a layer ends when its frontier empties; the next layer is seeded by the
+//    antipodal partners of the layer (ROWS=false: swap of mask halves;
+//    ROWS=true: per-node partner rows, for contracted graphs).  Partners have
+//    the same sign in even degree and the opposite sign in odd degree;
+//  * layers alternate orientation parity: a partner link between two nodes of
+//    equal layer parity closes an odd cycle (the reference's parity
+//    union-find, kernels.py:151-174).
+// rows: per node K words of adjacency (+ K words of partner links if ROWS).
+// COMPS: no antipodal jumps, so every "region" is one same-sign component and
+// X collects all of its neighbours (used to contract a tile's fixed part).
+template <int K, bool EVEN, bool ROWS, bool COMPS = false, int CAP = MAXR>
+__device__ __forceinline__ void region_pass(const uint32_t *__restrict__ rows,
+                                            const uint32_t (&SG)[K], const uint32_t (&USED)[K],
+                                            const uint32_t (&BD)[K], int nused,
+                                            Regions<K, CAP> &out) {
+    constexpr int HK = K / 2;
+    uint32_t unvS[K], unvO[K], F[K], NB[K], XB[K], regS[K], LS[K], SAME[K], PL[K];
+    uint32_t Ec[EVEN ? K : 1], Eo[EVEN ? K : 1];
+    int nreg = 0;
+    uint32_t oddmask = 0;
+    bool odd = false;
+
+    auto seed = [&](const uint32_t (&unv)[K]) {
+        int w, b;
+        lowest<K>(unv, w, b);
+        const uint32_t nm = ((sel<K>(SG, w) >> b) & 1u) - 1u;  // seed sign s: s ? 0 : ~0
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            SAME[k] = SG[k] ^ nm;
+            unvS[k] = unv[k] & SAME[k];
+            unvO[k] = unv[k] & ~SAME[k];
+            regS[k] = unv[k];
+            LS[k] = unvS[k];
+            F[k] = (k == w) ? (1u << b) : 0u;
+            unvS[k] ^= F[k];
+            XB[k] = 0u;
+            NB[k] = 0u;
+            PL[k] = 0u;
+            if (EVEN) { Ec[k] = 0u; Eo[k] = 0u; }
+        }
+        odd = false;
+    };
+
+    auto layer_end = [&](bool more) {
+        uint32_t L[K], unv[K], P[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            XB[k] |= COMPS ? NB[k] : (NB[k] & ~SAME[k]);
+            NB[k] = 0u;
+            L[k] = LS[k] ^ unvS[k];
+            unv[k] = unvS[k] | unvO[k];
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (COMPS) {
+                P[k] = 0u;
+            } else if (ROWS) {
+                P[k] = PL[k];
+                PL[k] = 0u;
+            } else {
+                const int ks = (k + HK) % K;  // antipodal map = swap of halves
+                P[k] = L[ks] & BD[ks];
+            }
+        }
+        if (EVEN) {
+            uint32_t hit = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                Ec[k] |= L[k];
+                hit |= P[k] & Ec[k];
+            }
+            odd |= hit != 0u;
+        }
+        uint32_t anyp = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            P[k] &= unv[k];
+            anyp |= P[k];
+        }
+        if (anyp) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                if (!EVEN) {  // partners carry the opposite sign in odd degree
+                    SAME[k] = ~SAME[k];
+                    unvS[k] = unv[k] & SAME[k];
+                    unvO[k] = unv[k] & ~SAME[k];
+                }
+                LS[k] = unvS[k];
+                F[k] = P[k];
+                unvS[k] ^= P[k];
+                if (EVEN) {
+                    const uint32_t t = Ec[k];
+                    Ec[k] = Eo[k];
+                    Eo[k] = t;
+                }
+            }
+            return;
+        }
+        // region complete
+        if (nreg < CAP) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                out.R[nreg][k] = regS[k] ^ unv[k];
+                out.X[nreg][k] = XB[k];
+            }
+            if (EVEN && odd) oddmask |= 1u << nreg;
+        }
+        ++nreg;
+        if (more) seed(unv);
+    };
+
+    seed(USED);
+    for (int it = 0; it < nused; ++it) {
+        if (!any<K>(F)) layer_end(true);
+        int w, b;
+        lowest<K>(F, w, b);
+        const int v = 32 * w + b;
+        const uint32_t bit = 1u << b;
+        uint32_t a[K];
+        load_row<K, ROWS>(rows, v, a, PL);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint32_t nw = a[k] & unvS[k];
+            unvS[k] ^= nw;
+            F[k] = (F[k] ^ ((k == w) ? bit : 0u)) | nw;
+            NB[k] |= a[k];
+        }
+    }
+    layer_end(false);
+    out.nreg = nreg;
+    out.oddmask = oddmask;
+}
+
+// Region graph -> status (reference precedence) -> rooted tree -> AHU key.
+// EXACT: replay the two order-dependent status collisions in edge order
+// (only meaningful for the flat diamond layout); otherwise report a failure
+// and let the host recompute the exact status through the flat kernel.
+template <int K, bool EVEN, bool EXACT>
+__device__ __forceinline__ Result finish(const KParams &p, const uint32_t (&SG)[K],
+                                         const Regions<K> &rg, int maxreg) {
+    Result res;
+    const int nreg = rg.nreg;
+    res.nreg = nreg;
+    res.key = 0;
+    if (nreg > maxreg || nreg > MAXR) {  // kernels.py:182: ids 0..maxreg-1 allowed
+        res.status = TCG_TOO_MANY_REGIONS;
+        return res;
+    }
+    int root = -1;
+    if (EVEN) {
+        const int c = __popc(rg.oddmask);
+        if (c == 0) { res.status = TCG_NO_ODD_REGION; return res; }
+        if (c > 1) { res.status = TCG_MANY_ODD_REGIONS; return res; }
+        root = __ffs(rg.oddmask) - 1;
+    }
+    // region graph from crossed-edge neighbourhoods
+    uint32_t radj[MAXR];
+    uint32_t selfm = 0;
+    int nedges = 0;
+    for (int r = 0; r < nreg; ++r) radj[r] = 0u;
+    for (int r = 0; r < nreg; ++r) {
+        uint32_t x[K];
+        uint32_t t = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            x[k] = rg.X[r][k];
+            t |= x[k] & rg.R[r][k];
+        }
+        if (t) selfm |= 1u << r;
+        for (int r2 = r + 1; r2 < nreg; ++r2) {
+            uint32_t u = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) u |= x[k] & rg.R[r2][k];
+            if (u) {
+                radj[r] |= 1u << r2;
+                radj[r2] |= 1u << r;
+                ++nedges;
+            }
+        }
+    }
+    const bool toomany = nedges > nreg - 1;  // mid-loop NOT_A_TREE will fire
+    if (EVEN) {
+        if (toomany && selfm) {
+            if constexpr (EXACT) res.status = ordered_scan<K, EVEN>(p, SG, rg.R, nreg, root);
+            else res.status = TCG_NOT_A_TREE;
+            return res;
+        }
+        if (toomany) { res.status = TCG_NOT_A_TREE; return res; }
+        if (selfm) { res.status = TCG_NONSEPARATING_OVAL; return res; }
+    } else {
+        const bool conflict = __popc(selfm) >= 2;
+        if (toomany && conflict) {
+            if constexpr (EXACT) res.status = ordered_scan<K, EVEN>(p, SG, rg.R, nreg, -1);
+            else res.status = TCG_NOT_A_TREE;
+            return res;
+        }
+        if (toomany) { res.status = TCG_NOT_A_TREE; return res; }
+        if (conflict) { res.status = TCG_ROOT_CONFLICT; return res; }
+        if (!selfm) { res.status = TCG_NO_PSEUDOLINE; return res; }
+        root = __ffs(selfm) - 1;
+    }
+    if (nedges != nreg - 1) { res.status = TCG_NOT_A_TREE; return res; }
+    res.key = tree_key(radj, nreg, root, res.status);
     return res;
+}
+
+template <int K, bool EVEN>
+__device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__restrict__ adj,
+                                           uint64_t sigma) {
+    uint32_t SG[K];
+    sign_words<K>(p, sigma, SG);
+    uint32_t used[K], bd[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        used[k] = p.used[k];
+        bd[k] = p.bd[k];
+    }
+    Regions<K> rg;
+    region_pass<K, EVEN, false>(adj, SG, used, bd, p.nused, rg);
+    return finish<K, EVEN, true>(p, SG, rg, p.maxreg);
 }
 
 // ------------------------------------------------------------------ kernels
@@ -493,6 +565,80 @@ __device__ void global_insert(const DevAgg &g, uint64_t key, uint64_t cnt, uint6
     atomicOr(g.overflow, 1u);
 }
 
+// Per-CTA scheme table in shared memory (flushed to the global table).
+struct CtaTable {
+    unsigned long long *key, *wit;
+    uint32_t *cnt, *hist;
+
+    __device__ void init() {
+        for (int i = threadIdx.x; i < TBL; i += blockDim.x) {
+            key[i] = 0ull;
+            wit[i] = ~0ull;
+            cnt[i] = 0u;
+        }
+        for (int i = threadIdx.x; i < NHIST; i += blockDim.x) hist[i] = 0u;
+    }
+
+    // Warp-aggregated insert of one result per lane (all 32 lanes call).
+    // WITNESS_BY_LEADER: lanes are in increasing index order, so the group
+    // leader holds the group's minimal index (sweeps); otherwise every lane
+    // offers its own index (random draws).
+    template <bool WITNESS_BY_LEADER>
+    __device__ __forceinline__ void add(const DevAgg &g, uint64_t k, int nreg, uint64_t m) {
+        const int lane = threadIdx.x & 31;
+        const unsigned grp = __match_any_sync(0xffffffffu, k);
+        if (k == 0ull) return;
+        const int leader = __ffs(grp) - 1;
+        int slot = -1;
+        if (lane == leader) {
+            uint32_t h = hash_slot(k, TBL_BITS);
+            for (int probe = 0; probe < TBL_PROBES; ++probe) {
+                const unsigned long long cur = key[h];
+                if (cur == k) { slot = (int)h; break; }
+                if (cur == 0ull) {
+                    const unsigned long long prev = atomicCAS(&key[h], 0ull, k);
+                    if (prev == 0ull || prev == k) { slot = (int)h; break; }
+                }
+                h = (h + 1) & (TBL - 1);
+            }
+            const uint32_t c = __popc(grp);
+            atomicAdd(&hist[nreg - 1], c);
+            if (slot >= 0) {
+                atomicAdd(&cnt[slot], c);
+                if (WITNESS_BY_LEADER) atomicMin(&wit[slot], (unsigned long long)m);
+            } else {  // table saturated: straight to the global table
+                global_insert(g, k, c, WITNESS_BY_LEADER ? m : ~0ull);
+            }
+        }
+        if (!WITNESS_BY_LEADER) {
+            slot = __shfl_sync(grp, slot, leader);
+            if (slot >= 0) atomicMin(&wit[slot], (unsigned long long)m);
+            else global_insert(g, k, 0ull, m);
+        }
+    }
+
+    __device__ void flush(const DevAgg &g) {
+        for (int i = threadIdx.x; i < TBL; i += blockDim.x) {
+            const unsigned long long kk = key[i];
+            if (kk != 0ull) global_insert(g, kk, cnt[i], wit[i]);
+        }
+        for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
+            if (hist[i]) atomicAdd(&g.hist[i], (unsigned long long)hist[i]);
+    }
+};
+
+constexpr size_t TABLE_SMEM = TBL * (2 * sizeof(unsigned long long) + sizeof(uint32_t)) +
+                              NHIST * sizeof(uint32_t);
+
+__device__ __forceinline__ CtaTable carve_table(void *at) {
+    CtaTable t;
+    t.key = reinterpret_cast<unsigned long long *>(at);
+    t.wit = t.key + TBL;
+    t.cnt = reinterpret_cast<uint32_t *>(t.wit + TBL);
+    t.hist = t.cnt + TBL;
+    return t;
+}
+
 // Enumeration kernel: raw / representative sweep or counter-based sample.
 // Persistent grid; each warp walks 32 consecutive indices per step.
 template <int K, bool EVEN, int MODE>
@@ -500,18 +646,9 @@ __global__ void __launch_bounds__(THREADS) k_enumerate(KParams p, uint64_t base,
                                                        uint64_t seed, uint64_t nbmask, DevAgg g) {
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t *adj_s = smem;
-    unsigned long long *tkey = reinterpret_cast<unsigned long long *>(smem + 32 * K * K);
-    unsigned long long *twit = tkey + TBL;
-    uint32_t *tcnt = reinterpret_cast<uint32_t *>(twit + TBL);
-    uint32_t *thist = tcnt + TBL;
-
+    CtaTable tab = carve_table(smem + 32 * K * K);
     stage_adj<K>(p, adj_s);
-    for (int i = threadIdx.x; i < TBL; i += blockDim.x) {
-        tkey[i] = 0ull;
-        twit[i] = ~0ull;
-        tcnt[i] = 0u;
-    }
-    for (int i = threadIdx.x; i < NHIST; i += blockDim.x) thist[i] = 0u;
+    tab.init();
     __syncthreads();
 
     const int lane = threadIdx.x & 31;
@@ -532,52 +669,194 @@ __global__ void __launch_bounds__(THREADS) k_enumerate(KParams p, uint64_t base,
             m = gidx;
             sigma = m;
         }
-        Result r = classify<K, EVEN>(p, adj_s, valid ? sigma : 0ull);
+        const Result r = classify<K, EVEN>(p, adj_s, valid ? sigma : 0ull);
         uint64_t k = 0;
         if (valid) {
             if (r.status == TCG_OK) k = r.key;
             else atomicMin(g.bad, (unsigned long long)gidx);
         }
-        const unsigned grp = __match_any_sync(0xffffffffu, k);
-        if (k != 0ull) {
-            const int leader = __ffs(grp) - 1;
-            int slot = -1;
-            if (lane == leader) {
-                uint32_t h = hash_slot(k, TBL_BITS);
-                for (int probe = 0; probe < TBL_PROBES; ++probe) {
-                    const unsigned long long cur = tkey[h];
-                    if (cur == k) { slot = (int)h; break; }
-                    if (cur == 0ull) {
-                        const unsigned long long prev = atomicCAS(&tkey[h], 0ull, k);
-                        if (prev == 0ull || prev == k) { slot = (int)h; break; }
-                    }
-                    h = (h + 1) & (TBL - 1);
-                }
-                const uint32_t c = __popc(grp);
-                atomicAdd(&thist[r.nreg - 1], c);
-                if (slot >= 0) {
-                    atomicAdd(&tcnt[slot], c);
-                    if (MODE != MODE_SAMPLE) atomicMin(&twit[slot], (unsigned long long)m);
-                } else {
-                    // table saturated: go straight to the global table
-                    global_insert(g, k, c, MODE == MODE_SAMPLE ? ~0ull : m);
-                }
-            }
-            if (MODE == MODE_SAMPLE) {
-                // witnesses are random in sample mode: every lane offers its m
-                slot = __shfl_sync(grp, slot, leader);
-                if (slot >= 0) atomicMin(&twit[slot], (unsigned long long)m);
-                else global_insert(g, k, 0ull, m);
-            }
-        }
+        tab.add<MODE != MODE_SAMPLE>(g, k, r.nreg, m);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < TBL; i += blockDim.x) {
-        const unsigned long long kk = tkey[i];
-        if (kk != 0ull) global_insert(g, kk, tcnt[i], twit[i]);
+    tab.flush(g);
+}
+
+// ---------------------------------------------------------- tile contraction
+// A sweep tile is 2^TILE_BITS consecutive indices aligned to its size: every
+// index in it shares all sign bits except those of a few "free" lattice
+// points (raw: points 0..9, i.e. the j-axis and two more; representative:
+// the first 10 free positions).  Their diamond copies are the free vertices.
+// Once per tile, warp 0 labels the same-sign components of the remaining
+// (fixed) vertices and contracts each to one node; every lane then
+// classifies its patchwork on the contracted graph -- at most 64 nodes
+// (components + free vertices), one 64-bit mask per set -- with the same
+// region pass (ROWS mode: per-node adjacency and antipodal-link rows).
+// Any tile whose contraction does not fit falls back to the flat kernel.
+constexpr int TILE_BITS = 10;
+constexpr int TILE = 1 << TILE_BITS;
+constexpr int MAXC = 48;  // fixed components per tile
+constexpr int MAXF = 32;  // free vertices
+
+struct TileTables {  // per plan and domain (raw / representative), device memory
+    int nf, nfixed, pad0, pad1;
+    uint32_t fixed[MAXK];                  // used and not free (layout mask)
+    uint32_t fword[MAXF], fbit[MAXF];      // layout word / bit of free node f
+    unsigned long long fadj[MAXF];         // free-free adjacency (bit g = free node g)
+    unsigned long long fpl[MAXF];          // free-free antipodal links
+    unsigned long long fcopy[TILE_BITS];   // free nodes whose sign is index bit i
+    unsigned long long fpar;               // sign-extension parity of the free nodes
+};
+
+template <int K>
+struct TileShared {
+    Regions<K, MAXC> comps;
+    uint4 rows[64];  // per node: adjacency (x, y), antipodal links (z, w)
+    unsigned long long sgn_fixed;
+    int n, nnodes, fallback;
+};
+
+template <int K, int MODE>
+__device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base,
+                           const uint32_t *__restrict__ adj_s, TileShared<K> &ts) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, base) : base;
+    uint32_t SG[K], fixed[K], zero[K];
+    sign_words<K>(p, sigma, SG);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        fixed[k] = tt.fixed[k];
+        zero[k] = 0u;
     }
-    for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
-        if (thist[i]) atomicAdd(&g.hist[i], (unsigned long long)thist[i]);
+    // identical in all 32 lanes: the shared-memory writes are benign
+    region_pass<K, false, false, true, MAXC>(adj_s, SG, fixed, zero, tt.nfixed, ts.comps);
+    __syncwarp();
+    const int n = ts.comps.nreg;
+    const int nn = n + tt.nf;
+    const bool fits = n <= MAXC && nn <= 64;
+    unsigned long long sbits = 0;
+    if (fits) {
+        for (int node = lane; node < nn; node += 32) {
+            unsigned long long adj = 0, pl = 0;
+            if (node < n) {
+                uint32_t X[K], R[K], P[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    X[k] = ts.comps.X[node][k];
+                    R[k] = ts.comps.R[node][k];
+                }
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int ks = (k + K / 2) % K;
+                    P[k] = R[ks] & p.bd[ks];
+                }
+                for (int c = 0; c < n; ++c) {
+                    uint32_t a = 0, q = 0;
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        a |= X[k] & ts.comps.R[c][k];
+                        q |= P[k] & ts.comps.R[c][k];
+                    }
+                    if (a && c != node) adj |= 1ull << c;
+                    if (q) pl |= 1ull << c;  // includes a self link (pair inside one component)
+                }
+                for (int f = 0; f < tt.nf; ++f)
+                    if (sel<K>(X, tt.fword[f]) & tt.fbit[f]) adj |= 1ull << (n + f);
+                uint32_t sg = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) sg |= R[k] & SG[k];
+                if (sg) sbits |= 1ull << node;
+            } else {
+                const int f = node - n;
+                adj = tt.fadj[f] << n;
+                pl = tt.fpl[f] << n;
+                const uint32_t w = tt.fword[f], b = tt.fbit[f];
+                for (int c = 0; c < n; ++c) {
+                    uint32_t x[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) x[k] = ts.comps.X[c][k];
+                    if (sel<K>(x, w) & b) adj |= 1ull << c;
+                }
+            }
+            ts.rows[node] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
+                                       (uint32_t)(pl >> 32));
+        }
+    }
+    // OR the sign bits of all component nodes across lanes
+    unsigned long long s = sbits;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s |= __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        ts.sgn_fixed = s;
+        ts.n = n;
+        ts.nnodes = nn;
+        ts.fallback = fits ? 0 : 1;
+    }
+}
+
+template <bool EVEN>
+__device__ __forceinline__ Result classify_tile(const KParams &p, const TileTables &tt,
+                                                const uint4 *rows,
+                                                unsigned long long sgn_fixed, int n, int nn,
+                                                uint32_t low) {
+    unsigned long long fs = tt.fpar;
+#pragma unroll
+    for (int i = 0; i < TILE_BITS; ++i)
+        if ((low >> i) & 1u) fs ^= tt.fcopy[i];
+    const unsigned long long sg = sgn_fixed | (fs << n);
+    const unsigned long long used = nn >= 64 ? ~0ull : ((1ull << nn) - 1ull);
+    const uint32_t SG[2] = {(uint32_t)sg, (uint32_t)(sg >> 32)};
+    const uint32_t USED[2] = {(uint32_t)used, (uint32_t)(used >> 32)};
+    const uint32_t BD[2] = {0u, 0u};
+    Regions<2> rg;
+    region_pass<2, EVEN, true>(reinterpret_cast<const uint32_t *>(rows), SG, USED, BD, nn, rg);
+    return finish<2, EVEN, false>(p, SG, rg, p.maxreg);
+}
+
+// Sweep over [start, end) by tiles.  MODE: raw or representative.
+template <int K, bool EVEN, int MODE>
+__global__ void __launch_bounds__(THREADS) k_tiles(KParams p, const TileTables *__restrict__ tt_g,
+                                                   uint64_t start, uint64_t end, DevAgg g) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *adj_s = smem;
+    CtaTable tab = carve_table(smem + 32 * K * K);
+    TileTables *tt = reinterpret_cast<TileTables *>(
+        reinterpret_cast<char *>(smem) + 32 * K * K * 4 + TABLE_SMEM);
+    TileShared<K> *ts = reinterpret_cast<TileShared<K> *>(tt + 1);
+    stage_adj<K>(p, adj_s);
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    tab.init();
+    __syncthreads();
+
+    const uint64_t t0 = start >> TILE_BITS, t1 = (end + TILE - 1) >> TILE_BITS;
+    for (uint64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
+        const uint64_t base = t << TILE_BITS;
+        if (threadIdx.x < 32) build_tile<K, MODE>(p, *tt, base, adj_s, *ts);
+        __syncthreads();
+        const int n = ts->n, nn = ts->nnodes;
+        const bool fb = ts->fallback != 0;
+        const unsigned long long sgf = ts->sgn_fixed;
+        for (int q = 0; q < TILE / THREADS; ++q) {
+            const uint32_t low = (uint32_t)(q * THREADS + threadIdx.x);
+            const uint64_t m = base + low;
+            const bool valid = m >= start && m < end;
+            Result r;
+            if (fb) {
+                const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, m) : m;
+                r = classify<K, EVEN>(p, adj_s, valid ? sigma : 0ull);
+            } else {
+                r = classify_tile<EVEN>(p, *tt, ts->rows, sgf, n, nn, low);
+            }
+            uint64_t k = 0;
+            if (valid) {
+                if (r.status == TCG_OK) k = r.key;
+                else atomicMin(g.bad, (unsigned long long)m);
+            }
+            tab.add<true>(g, k, r.nreg, m);
+        }
+        __syncthreads();
+    }
+    tab.flush(g);
 }
 
 __global__ void k_agg_clear(DevAgg g) {
@@ -642,6 +921,11 @@ struct tcg_plan {
     int64_t batch_cap = 0;
     cudaStream_t own = nullptr, stream = nullptr;
     int64_t launches = 0;
+    // tile contraction (sweeps): per domain (raw, representative)
+    TileTables *d_tiles = nullptr;   // [2]
+    int tiles_ok[2] = {0, 0};
+    int blocks_tiles = 0;
+    size_t smem_tiles = 0;
     // split-phase bookkeeping: how to map a failing index back to its sign word
     int pending_mode = -1;
     uint64_t pending_seed = 0, pending_mask = 0;
@@ -675,6 +959,23 @@ void *pick_enum(int K, bool even, int mode) {
     if (K == 2) return even ? enum_fn<2, true>(mode) : enum_fn<2, false>(mode);
     if (K == 4) return even ? enum_fn<4, true>(mode) : enum_fn<4, false>(mode);
     return even ? enum_fn<6, true>(mode) : enum_fn<6, false>(mode);
+}
+
+template <int K, bool EVEN>
+void *tiles_fn(int mode) {
+    return mode == MODE_RAW ? (void *)k_tiles<K, EVEN, MODE_RAW> : (void *)k_tiles<K, EVEN, MODE_REP>;
+}
+
+void *pick_tiles(int K, bool even, int mode) {
+    if (K == 2) return even ? tiles_fn<2, true>(mode) : tiles_fn<2, false>(mode);
+    if (K == 4) return even ? tiles_fn<4, true>(mode) : tiles_fn<4, false>(mode);
+    return even ? tiles_fn<6, true>(mode) : tiles_fn<6, false>(mode);
+}
+
+size_t tiles_smem(int K) {
+    const size_t ts = K == 2 ? sizeof(TileShared<2>) : (K == 4 ? sizeof(TileShared<4>)
+                                                               : sizeof(TileShared<6>));
+    return (size_t)32 * K * K * 4 + TABLE_SMEM + sizeof(TileTables) + ts;
 }
 
 void *pick_batch(int K, bool even) {
@@ -739,6 +1040,57 @@ int build_layout(const tcg_desc *D, Layout &L) {
         else L.pos[v] = L.H + ppos(-i, -j);
     }
     return TCG_OK;
+}
+
+
+// Free vertices of a tile (index bits 0..TILE_BITS-1) and the fixed mask.
+bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
+    const int d = D->degree;
+    const int npts = D->npts;
+    const int dom_bits = mode == MODE_RAW ? npts : npts - 3;
+    if (d < 5 || dom_bits < TILE_BITS + 2) return false;
+    std::memset(&T, 0, sizeof(T));
+    int sbit[TILE_BITS];
+    for (int i = 0; i < TILE_BITS; ++i)
+        sbit[i] = mode == MODE_RAW ? i : (i < d - 1 ? i + 2 : i - (d - 1) + d + 2);
+    std::vector<int> fnode(D->nv, -1);
+    int nf = 0;
+    for (int v = 0; v < D->nv; ++v) {
+        if (!D->used[v]) continue;
+        int bit = -1;
+        for (int i = 0; i < TILE_BITS; ++i)
+            if (sbit[i] == D->src[v]) bit = i;
+        const int pos = L.pos[v];
+        if (bit < 0) {
+            T.fixed[pos >> 5] |= 1u << (pos & 31);
+            ++T.nfixed;
+            continue;
+        }
+        if (nf >= MAXF) return false;
+        fnode[v] = nf;
+        T.fword[nf] = (uint32_t)(pos >> 5);
+        T.fbit[nf] = 1u << (pos & 31);
+        T.fpar |= (unsigned long long)(D->par[v] & 1) << nf;
+        T.fcopy[bit] |= 1ull << nf;
+        ++nf;
+    }
+    T.nf = nf;
+    for (int e = 0; e < D->ne; ++e) {
+        const int fu = fnode[D->edge_u[e]], fv = fnode[D->edge_v[e]];
+        if (fu >= 0 && fv >= 0) {
+            T.fadj[fu] |= 1ull << fv;
+            T.fadj[fv] |= 1ull << fu;
+        }
+    }
+    for (int a = 0; a < D->nap; ++a) {
+        const int fu = fnode[D->ap_u[a]], fv = fnode[D->ap_v[a]];
+        if ((fu >= 0) != (fv >= 0)) return false;  // cannot happen: p and -p share src
+        if (fu >= 0) {
+            T.fpl[fu] |= 1ull << fv;
+            T.fpl[fv] |= 1ull << fu;
+        }
+    }
+    return T.nfixed > 0 && nf > 0;
 }
 
 }  // namespace
@@ -898,6 +1250,15 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
         cudaMemcpy(P->d_edges, edges.data(), edges.size() * 4, cudaMemcpyHostToDevice);
     kp.adj = P->d_adj;
     kp.edges = P->d_edges;
+    {
+        TileTables tt[2];
+        const char *no_tiles = std::getenv("TCG_NO_TILES");
+        for (int mode = 0; mode < 2; ++mode)
+            P->tiles_ok[mode] = (!no_tiles || !*no_tiles || no_tiles[0] == '0') &&
+                                build_tiles(D, L, mode, tt[mode]);
+        if ((e = cudaMalloc(&P->d_tiles, sizeof(tt))) != cudaSuccess) return bail(e, "malloc tiles");
+        cudaMemcpy(P->d_tiles, tt, sizeof(tt), cudaMemcpyHostToDevice);
+    }
     DevAgg &g = P->agg;
     if ((e = cudaMalloc(&g.keys, GCAP * 8)) != cudaSuccess) return bail(e, "malloc agg");
     if ((e = cudaMalloc(&g.cnt, GCAP * 8)) != cudaSuccess) return bail(e, "malloc agg");
@@ -926,6 +1287,14 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
                                                            P->smem_batch)) != cudaSuccess)
         return bail(e, "occupancy");
     P->blocks_batch = std::max(1, bps) * P->nsm;
+    P->smem_tiles = tiles_smem(K);
+    for (int mode = 0; mode < 2; ++mode)
+        cudaFuncSetAttribute(pick_tiles(K, P->even, mode),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_tiles);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_tiles(K, P->even, MODE_RAW),
+                                                           THREADS, P->smem_tiles)) != cudaSuccess)
+        return bail(e, "occupancy");
+    P->blocks_tiles = std::max(1, bps) * P->nsm;
     *out = P;
     int rc2 = tcg_agg_reset(P);
     if (rc2) {
@@ -945,7 +1314,7 @@ int tcg_plan_destroy(tcg_plan *P) {
     if (!P) return TCG_OK;
     DeviceGuard guard(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
-    void *ptrs[] = {P->d_adj, P->d_edges, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
@@ -1036,6 +1405,22 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
     P->pending_mode = mode;
     P->pending_seed = seed;
     P->pending_mask = mask;
+    if (mode != MODE_SAMPLE && P->tiles_ok[mode] && end > start) {
+        void *fn = pick_tiles(P->K, P->even, mode);
+        const TileTables *tt = P->d_tiles + mode;
+        for (uint64_t a = start; a < end;) {
+            const uint64_t b = std::min<uint64_t>(end, (a / LAUNCH_MAX + 1) * LAUNCH_MAX);
+            const uint64_t ntiles = ((b + TILE - 1) >> TILE_BITS) - (a >> TILE_BITS);
+            const unsigned blocks = (unsigned)std::min<uint64_t>(P->blocks_tiles, ntiles);
+            uint64_t lo = a, hi = b;
+            void *args[] = {&P->kp, &tt, &lo, &hi, &P->agg};
+            CUDA_TRY(cudaLaunchKernel(fn, dim3(blocks), dim3(THREADS), args, P->smem_tiles,
+                                      P->stream));
+            P->launches++;
+            a = b;
+        }
+        return TCG_OK;
+    }
     void *fn = pick_enum(P->K, P->even, mode);
     for (uint64_t a = start; a < end;) {
         const uint64_t n = std::min<uint64_t>(end - a, LAUNCH_MAX);
