@@ -66,6 +66,8 @@ class ClockSampler:
     def __enter__(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
+        if os.environ.get("BENCH_NO_CLOCKS"):
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={CLOCK_FIELDS}", "--format=csv,noheader,nounits",
@@ -199,7 +201,8 @@ def run_ours(args, rank, world, local_rank):
     sl = 1 << args.slice_log2
 
     def rng_of(step):
-        a = ((step * world + rank) * sl) % DOMAIN
+        a = (args.offset + (step * world + rank) * sl) % DOMAIN
+        a -= a % sl
         return a, a + sl
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -208,8 +211,9 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
-    # ---- warm-up (untimed)
+    # ---- warm-up (untimed): same launches as a timed step, L2 flush included
     for s in range(args.warmup):
+        flush.zero_()
         a, b = rng_of(args.steps + s)
         c.native.agg_reset()
         c.native.sweep_async(True, a, b)
@@ -228,13 +232,18 @@ def run_ours(args, rank, world, local_rank):
     tables = []
     k_ms = []
     launches0 = c.native.launches()
+    c.native.kernel_times()  # clear
+    c.native.set_timing(True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(gpu_index) as clocks:
         barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
+        step_ev = []
         for s in range(args.steps):
+            sa = torch.cuda.Event(enable_timing=True)
+            sa.record(stream)
             flush.zero_()  # L2 flush between steps (256 MiB > 126 MB L2)
             a, b = rng_of(s)
             ka = torch.cuda.Event(enable_timing=True)
@@ -250,6 +259,9 @@ def run_ours(args, rank, world, local_rank):
             hist_acc += np.asarray(h, np.int64)
             tables.append((keys, counts, wits))
             k_ms.append((ka, kb))
+            sb = torch.cuda.Event(enable_timing=True)
+            sb.record(stream)
+            step_ev.append((sa, sb))
         from paper_2604_09221_b200.distributed import merge_tables
 
         keys, counts, wits = merge_tables(tables)
@@ -260,12 +272,19 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         barrier()
     ms = ev0.elapsed_time(ev1)
+    c.native.set_timing(False)
+    ktimes = c.native.kernel_times()
     kern = [x.elapsed_time(y) for x, y in k_ms]
+    log("step ms:", [round(x.elapsed_time(y), 2) for x, y in step_ev], "kernel ms:",
+        [round(k, 2) for k in kern], "total ms:", round(ms, 2))
     launches = c.native.launches() - launches0
-    t = torch.tensor([ms, statistics.mean(kern)], dtype=torch.float64, device=dev)
+    # dominant kernel: tile classification (tiled sweeps) or flat enumeration
+    dom = "tile_classify" if ktimes["tile_classify"][1] else "enumerate"
+    dom_ms, dom_n = ktimes[dom]
+    t = torch.tensor([ms, dom_ms, statistics.mean(kern)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, kern_ms = float(t[0]), float(t[1])
+    ms_max, dom_ms_max, sweep_ms = float(t[0]), float(t[1]), float(t[2])
     units = args.steps * sl * world
     value = units / (ms_max / 1e3)
     report = report_from_agg(T, True, hist, total, keys, counts, wits, {})
@@ -316,8 +335,11 @@ def run_ours(args, rank, world, local_rank):
     mhz, peak_src = peaks()
     nsm = c.native.info["sms"]
     peak = nsm * 128 * mhz * 1e6  # thread-instruction issue slots / s / GPU
-    per_gpu_kernel_pps = sl / (kern_ms / 1e3)
+    per_gpu_kernel_pps = args.steps * sl / (dom_ms_max / 1e3)
     achieved = per_gpu_kernel_pps * W_D[DEGREE]
+    kernel_names = {"tile_classify": "k_tile_classify<K=4,odd,raw>",
+                    "enumerate": "k_enumerate<K=4,odd,raw>"}
+    total_kernel_ms = sum(v[0] for v in ktimes.values())
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -344,10 +366,15 @@ def run_ours(args, rank, world, local_rank):
             "bound": "issue", "achieved": achieved, "peak": peak, "unit": "elem-visits/s",
             "frac": achieved / peak, "traffic": None,
             "note": f"integer-issue roofline (no tensor/HBM work): algorithmic element "
-                    f"visits W(7)=2|E|+|V|=729 per patchwork x k_enumerate rate "
-                    f"{per_gpu_kernel_pps:.3e}/s, over {nsm} SMs x 128 lanes x {mhz:.0f} MHz "
+                    f"visits W(7)=2|E|+|V|=729 per patchwork x {dom} rate "
+                    f"{per_gpu_kernel_pps:.3e}/s (all timed patchworks / summed CUDA-event "
+                    f"time of its {dom_n} launches), over {nsm} SMs x 128 lanes x {mhz:.0f} MHz "
                     f"({peak_src}); dram traffic per launch: see profiles/",
-            "kernel": "k_enumerate<4,false,0>", "kernel_ms": kern_ms,
+            "kernel": kernel_names[dom], "kernel_ms": dom_ms_max / max(1, dom_n),
+            "launches": dom_n,
+            "share_of_device_time": dom_ms / total_kernel_ms if total_kernel_ms else None,
+            "kernels_ms": {k: round(v[0], 3) for k, v in ktimes.items()},
+            "sweep_ms_per_step": sweep_ms,
         },
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "patchworks/s", "h2d_bytes_per_step": 16,
@@ -372,6 +399,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--slice-log2", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--offset", type=lambda x: int(x, 0), default=0,
+                    help="first index of the timed slices (profiling away from the easy low prefix)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: the contract asks for >= 3 warm-up steps")

@@ -109,8 +109,15 @@ int tcg_plan_destroy(tcg_plan *plan);
 int tcg_plan_set_stream(tcg_plan *plan, void *cuda_stream);
 /* info[0]=degree info[1]=mask words K info[2]=used vertices info[3]=device
  * info[4]=SM count info[5]=CTAs per launch info[6]=threads per CTA
- * info[7]=maxreg */
+ * info[7]=maxreg info[8]/info[9]=tile bits for raw/representative sweeps
+ * (0 = sweeps of that domain use the flat kernel) */
 int tcg_plan_info(const tcg_plan *plan, int32_t *info, int ninfo);
+/* Per-kernel device time (CUDA events on the plan's stream around every
+ * launch) while enabled.  tcg_kernel_times returns and clears the totals:
+ * ms[0..3] / counts[0..3] = tile contraction, tile classification, flat
+ * enumeration, batch classification. */
+int tcg_plan_set_timing(tcg_plan *plan, int enable);
+int tcg_kernel_times(tcg_plan *plan, double *ms, int64_t *counts);
 
 /* classify_bits_kernel, batched.  sigma[t] bit k = sign of point k.
  * Outputs per patchwork: tree key, oval count, region count, status. */

@@ -62,6 +62,8 @@ def load():
         L.tcg_plan_destroy.argtypes = [P]
         L.tcg_plan_set_stream.argtypes = [P, C.c_void_p]
         L.tcg_plan_info.argtypes = [P, C.c_void_p, C.c_int]
+        L.tcg_plan_set_timing.argtypes = [P, C.c_int]
+        L.tcg_kernel_times.argtypes = [P, C.c_void_p, C.c_void_p]
         L.tcg_classify_batch.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p]
         L.tcg_classify_batch_device.argtypes = L.tcg_classify_batch.argtypes
@@ -88,6 +90,7 @@ def load():
 
 EXPORTS = (
     "tcg_plan_create", "tcg_plan_destroy", "tcg_plan_set_stream", "tcg_plan_info",
+    "tcg_plan_set_timing", "tcg_kernel_times",
     "tcg_classify_batch", "tcg_classify_batch_device", "tcg_sweep", "tcg_sample",
     "tcg_agg_reset", "tcg_sweep_async", "tcg_sample_async", "tcg_agg_fetch",
     "tcg_sweep_multi", "tcg_sample_multi", "tcg_last_error", "tcg_device_count",
@@ -167,12 +170,13 @@ class NativePlan:
         _check(L.tcg_plan_create(C.byref(desc), int(device), C.byref(h)), "tcg_plan_create")
         self.h = h
         self._L = L
-        info = np.zeros(8, np.int32)
-        L.tcg_plan_info(self.h, info.ctypes.data, 8)
+        info = np.zeros(10, np.int32)
+        L.tcg_plan_info(self.h, info.ctypes.data, 10)
         self.info = {
             "degree": int(info[0]), "words": int(info[1]), "used": int(info[2]),
             "device": int(info[3]), "sms": int(info[4]), "ctas": int(info[5]),
-            "threads": int(info[6]), "maxreg": int(info[7]),
+            "threads": int(info[6]), "maxreg": int(info[7]), "tile_bits_raw": int(info[8]),
+            "tile_bits_rep": int(info[9]),
         }
 
     def __del__(self):
@@ -190,6 +194,17 @@ class NativePlan:
 
     def launches(self) -> int:
         return int(self._L.tcg_launch_count(self.h))
+
+    def set_timing(self, enable: bool):
+        _check(self._L.tcg_plan_set_timing(self.h, int(bool(enable))), "tcg_plan_set_timing")
+
+    def kernel_times(self):
+        """{kind: (ms, launches)} since the last call; kinds as in tcg.h."""
+        ms = np.zeros(4, np.float64)
+        n = np.zeros(4, np.int64)
+        _check(self._L.tcg_kernel_times(self.h, ms.ctypes.data, n.ctypes.data), "tcg_kernel_times")
+        names = ("tile_build", "tile_classify", "enumerate", "batch")
+        return {names[i]: (float(ms[i]), int(n[i])) for i in range(4)}
 
     def classify_words(self, words):
         w = np.ascontiguousarray(words, dtype=np.uint64)

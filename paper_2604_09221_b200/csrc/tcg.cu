@@ -692,32 +692,35 @@ __global__ void __launch_bounds__(THREADS) k_enumerate(KParams p, uint64_t base,
 // (components + free vertices), one 64-bit mask per set -- with the same
 // region pass (ROWS mode: per-node adjacency and antipodal-link rows).
 // Any tile whose contraction does not fit falls back to the flat kernel.
-constexpr int TILE_BITS = 10;
-constexpr int TILE = 1 << TILE_BITS;
+constexpr int TILE_BITS_MAX = 12;
 constexpr int MAXC = 48;  // fixed components per tile
 constexpr int MAXF = 32;  // free vertices
 
 struct TileTables {  // per plan and domain (raw / representative), device memory
-    int nf, nfixed, pad0, pad1;
+    int nf, nfixed, bits, pad1;
     uint32_t fixed[MAXK];                  // used and not free (layout mask)
     uint32_t fword[MAXF], fbit[MAXF];      // layout word / bit of free node f
     unsigned long long fadj[MAXF];         // free-free adjacency (bit g = free node g)
     unsigned long long fpl[MAXF];          // free-free antipodal links
-    unsigned long long fcopy[TILE_BITS];   // free nodes whose sign is index bit i
+    unsigned long long fcopy[TILE_BITS_MAX];  // free nodes whose sign is index bit i
     unsigned long long fpar;               // sign-extension parity of the free nodes
 };
 
-template <int K>
-struct TileShared {
-    Regions<K, MAXC> comps;
+// Contracted tile, written by k_tile_build and staged into shared memory by
+// k_tile_classify.
+struct TileRec {
     uint4 rows[64];  // per node: adjacency (x, y), antipodal links (z, w)
     unsigned long long sgn_fixed;
-    int n, nnodes, fallback;
+    int n, nnodes, fallback, pad;
 };
 
+// One warp contracts one tile: same-sign components of the fixed vertices
+// (region_pass in COMPS mode, identical in all lanes), then lane-parallel
+// node rows.  comps: per-warp shared scratch; rec: global output.
 template <int K, int MODE>
 __device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base,
-                           const uint32_t *__restrict__ adj_s, TileShared<K> &ts) {
+                           const uint32_t *__restrict__ adj_s, Regions<K, MAXC> &comps,
+                           TileRec *__restrict__ rec) {
     const int lane = threadIdx.x & 31;
     const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, base) : base;
     uint32_t SG[K], fixed[K], zero[K];
@@ -728,9 +731,9 @@ __device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base
         zero[k] = 0u;
     }
     // identical in all 32 lanes: the shared-memory writes are benign
-    region_pass<K, false, false, true, MAXC>(adj_s, SG, fixed, zero, tt.nfixed, ts.comps);
+    region_pass<K, false, false, true, MAXC>(adj_s, SG, fixed, zero, tt.nfixed, comps);
     __syncwarp();
-    const int n = ts.comps.nreg;
+    const int n = comps.nreg;
     const int nn = n + tt.nf;
     const bool fits = n <= MAXC && nn <= 64;
     unsigned long long sbits = 0;
@@ -741,8 +744,8 @@ __device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base
                 uint32_t X[K], R[K], P[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    X[k] = ts.comps.X[node][k];
-                    R[k] = ts.comps.R[node][k];
+                    X[k] = comps.X[node][k];
+                    R[k] = comps.R[node][k];
                 }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
@@ -753,8 +756,8 @@ __device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base
                     uint32_t a = 0, q = 0;
 #pragma unroll
                     for (int k = 0; k < K; ++k) {
-                        a |= X[k] & ts.comps.R[c][k];
-                        q |= P[k] & ts.comps.R[c][k];
+                        a |= X[k] & comps.R[c][k];
+                        q |= P[k] & comps.R[c][k];
                     }
                     if (a && c != node) adj |= 1ull << c;
                     if (q) pl |= 1ull << c;  // includes a self link (pair inside one component)
@@ -773,24 +776,92 @@ __device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base
                 for (int c = 0; c < n; ++c) {
                     uint32_t x[K];
 #pragma unroll
-                    for (int k = 0; k < K; ++k) x[k] = ts.comps.X[c][k];
+                    for (int k = 0; k < K; ++k) x[k] = comps.X[c][k];
                     if (sel<K>(x, w) & b) adj |= 1ull << c;
                 }
             }
-            ts.rows[node] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
-                                       (uint32_t)(pl >> 32));
+            rec->rows[node] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
+                                         (uint32_t)(pl >> 32));
         }
     }
-    // OR the sign bits of all component nodes across lanes
-    unsigned long long s = sbits;
+    unsigned long long sg = sbits;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s |= __shfl_xor_sync(0xffffffffu, s, o);
+    for (int o = 16; o > 0; o >>= 1) sg |= __shfl_xor_sync(0xffffffffu, sg, o);
     if (lane == 0) {
-        ts.sgn_fixed = s;
-        ts.n = n;
-        ts.nnodes = nn;
-        ts.fallback = fits ? 0 : 1;
+        rec->sgn_fixed = sg;
+        rec->n = n;
+        rec->nnodes = nn;
+        rec->fallback = fits ? 0 : 1;
     }
+}
+
+// Region pass over a contracted graph (<= 64 nodes, one u64 per set) without
+// layers: antipodal links are followed in the same step as edges, so a lane
+// only branches when a region ends.  Each popped node v uses its own sign:
+//   new = unvisited & ((adj & same_v) | links_v);   XB |= adj & ~same_v.
+// Even degree: orientation parity is tracked per node (edges keep it, links
+// flip it); any edge or link whose ends violate the 2-colouring closes an odd
+// cycle (the reference's parity union-find, kernels.py:151-174).
+template <bool EVEN>
+__device__ __forceinline__ void node_pass(const uint4 *__restrict__ rows, uint64_t SG,
+                                          uint64_t USED, int nn, Regions<2> &out) {
+    uint64_t unv = USED, F = 0, XB = 0, PI = 0, regS = 0;
+    bool odd = false;
+    int nreg = 0;
+    uint32_t oddmask = 0;
+    auto seed = [&]() {
+        const uint64_t low = unv & (0ull - unv);
+        F = low;
+        regS = unv;
+        unv ^= low;
+        XB = 0;
+        PI = 0;
+        odd = false;
+    };
+    auto close = [&]() {
+        if (nreg < MAXR) {
+            const uint64_t R = regS ^ unv;
+            out.R[nreg][0] = (uint32_t)R;
+            out.R[nreg][1] = (uint32_t)(R >> 32);
+            out.X[nreg][0] = (uint32_t)XB;
+            out.X[nreg][1] = (uint32_t)(XB >> 32);
+            if (EVEN && odd) oddmask |= 1u << nreg;
+        }
+        ++nreg;
+    };
+    seed();
+    for (int it = 0; it < nn; ++it) {
+        if (F == 0ull) {
+            close();
+            seed();
+        }
+        const int v = __ffsll((long long)F) - 1;
+        F &= F - 1ull;
+        const uint4 row = rows[v];
+        const uint64_t a = ((uint64_t)row.y << 32) | row.x;
+        const uint64_t pl = ((uint64_t)row.w << 32) | row.z;
+        const uint64_t same = SG ^ ((((SG >> v) & 1ull)) - 1ull);  // s_v ? SG : ~SG
+        XB |= a & ~same;
+        if (EVEN) {
+            const uint64_t pv = ((PI >> v) & 1ull) ? ~0ull : 0ull;
+            const uint64_t te = a & same, nT = te & unv, nP = pl & unv;
+            // nodes with parity equal to v's: PI if pv else ~PI
+            const uint64_t eq = ~(PI ^ pv);
+            const uint64_t bad = (nT & nP) | (te & ~unv & ~eq) | (pl & ~unv & eq);
+            odd |= bad != 0ull;
+            PI |= (nT & pv) | (nP & ~pv);
+            const uint64_t nw = nT | nP;
+            unv ^= nw;
+            F |= nw;
+        } else {
+            const uint64_t nw = ((a & same) | pl) & unv;
+            unv ^= nw;
+            F |= nw;
+        }
+    }
+    close();
+    out.nreg = nreg;
+    out.oddmask = oddmask;
 }
 
 template <bool EVEN>
@@ -799,45 +870,74 @@ __device__ __forceinline__ Result classify_tile(const KParams &p, const TileTabl
                                                 unsigned long long sgn_fixed, int n, int nn,
                                                 uint32_t low) {
     unsigned long long fs = tt.fpar;
-#pragma unroll
-    for (int i = 0; i < TILE_BITS; ++i)
+    for (int i = 0; i < tt.bits; ++i)
         if ((low >> i) & 1u) fs ^= tt.fcopy[i];
     const unsigned long long sg = sgn_fixed | (fs << n);
     const unsigned long long used = nn >= 64 ? ~0ull : ((1ull << nn) - 1ull);
     const uint32_t SG[2] = {(uint32_t)sg, (uint32_t)(sg >> 32)};
-    const uint32_t USED[2] = {(uint32_t)used, (uint32_t)(used >> 32)};
-    const uint32_t BD[2] = {0u, 0u};
     Regions<2> rg;
-    region_pass<2, EVEN, true>(reinterpret_cast<const uint32_t *>(rows), SG, USED, BD, nn, rg);
+    node_pass<EVEN>(rows, sg, used, nn, rg);
     return finish<2, EVEN, false>(p, SG, rg, p.maxreg);
 }
 
-// Sweep over [start, end) by tiles.  MODE: raw or representative.
+constexpr int BUILD_WARPS = 8;  // warps (= tiles in flight) per build CTA
+
+// Contract tiles tile0 .. tile0+ntiles-1 (one warp per tile).
+template <int K, int MODE>
+__global__ void __launch_bounds__(32 * BUILD_WARPS) k_tile_build(KParams p,
+                                                                 const TileTables *__restrict__ tt_g,
+                                                                 uint64_t tile0, uint32_t ntiles,
+                                                                 TileRec *__restrict__ recs) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *adj_s = smem;
+    TileTables *tt = reinterpret_cast<TileTables *>(smem + 32 * K * K);
+    Regions<K, MAXC> *comps = reinterpret_cast<Regions<K, MAXC> *>(tt + 1);
+    stage_adj<K>(p, adj_s);
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    __syncthreads();
+    const int w = threadIdx.x >> 5;
+    for (uint32_t t = blockIdx.x * BUILD_WARPS + w; t < ntiles; t += gridDim.x * BUILD_WARPS)
+        build_tile<K, MODE>(p, *tt, (tile0 + t) << tt->bits, adj_s, comps[w], recs + t);
+}
+
+// Classify every index of [start, end) that falls in tiles tile0 .. tile0+ntiles-1.
 template <int K, bool EVEN, int MODE>
-__global__ void __launch_bounds__(THREADS) k_tiles(KParams p, const TileTables *__restrict__ tt_g,
-                                                   uint64_t start, uint64_t end, DevAgg g) {
+__global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
+                                                           const TileTables *__restrict__ tt_g,
+                                                           const TileRec *__restrict__ recs,
+                                                           uint64_t tile0, uint32_t ntiles,
+                                                           uint64_t start, uint64_t end,
+                                                           DevAgg g) {
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t *adj_s = smem;
     CtaTable tab = carve_table(smem + 32 * K * K);
     TileTables *tt = reinterpret_cast<TileTables *>(
         reinterpret_cast<char *>(smem) + 32 * K * K * 4 + TABLE_SMEM);
-    TileShared<K> *ts = reinterpret_cast<TileShared<K> *>(tt + 1);
+    TileRec *rec = reinterpret_cast<TileRec *>(tt + 1);
     stage_adj<K>(p, adj_s);
     for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
         reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
     tab.init();
     __syncthreads();
-
-    const uint64_t t0 = start >> TILE_BITS, t1 = (end + TILE - 1) >> TILE_BITS;
-    for (uint64_t t = t0 + blockIdx.x; t < t1; t += gridDim.x) {
-        const uint64_t base = t << TILE_BITS;
-        if (threadIdx.x < 32) build_tile<K, MODE>(p, *tt, base, adj_s, *ts);
+    const int bits = tt->bits;
+    const uint32_t tsize = 1u << bits;
+    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const TileRec *src = recs + t;
+        const int nn_g = src->nnodes;
+        if (threadIdx.x < 64 && (int)threadIdx.x < nn_g) rec->rows[threadIdx.x] = src->rows[threadIdx.x];
+        if (threadIdx.x == 64) {
+            rec->sgn_fixed = src->sgn_fixed;
+            rec->n = src->n;
+            rec->nnodes = nn_g;
+            rec->fallback = src->fallback;
+        }
         __syncthreads();
-        const int n = ts->n, nn = ts->nnodes;
-        const bool fb = ts->fallback != 0;
-        const unsigned long long sgf = ts->sgn_fixed;
-        for (int q = 0; q < TILE / THREADS; ++q) {
-            const uint32_t low = (uint32_t)(q * THREADS + threadIdx.x);
+        const uint64_t base = (tile0 + t) << bits;
+        const int n = rec->n, nn = rec->nnodes;
+        const bool fb = rec->fallback != 0;
+        const unsigned long long sgf = rec->sgn_fixed;
+        for (uint32_t low = threadIdx.x; low < tsize; low += THREADS) {
             const uint64_t m = base + low;
             const bool valid = m >= start && m < end;
             Result r;
@@ -845,7 +945,7 @@ __global__ void __launch_bounds__(THREADS) k_tiles(KParams p, const TileTables *
                 const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, m) : m;
                 r = classify<K, EVEN>(p, adj_s, valid ? sigma : 0ull);
             } else {
-                r = classify_tile<EVEN>(p, *tt, ts->rows, sgf, n, nn, low);
+                r = classify_tile<EVEN>(p, *tt, rec->rows, sgf, n, nn, low);
             }
             uint64_t k = 0;
             if (valid) {
@@ -923,9 +1023,16 @@ struct tcg_plan {
     int64_t launches = 0;
     // tile contraction (sweeps): per domain (raw, representative)
     TileTables *d_tiles = nullptr;   // [2]
+    TileRec *d_recs = nullptr;       // [CHUNK_TILES]
     int tiles_ok[2] = {0, 0};
-    int blocks_tiles = 0;
-    size_t smem_tiles = 0;
+    int tile_bits[2] = {0, 0};
+    int blocks_build = 0, blocks_cls = 0;
+    size_t smem_build = 0, smem_cls = 0;
+    // optional per-kernel timing (CUDA events on the launching stream)
+    int timing = 0;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;  // kind, start, stop
+    double t_ms[4] = {0, 0, 0, 0};   // build, classify (tiles), enumerate, batch
+    int64_t t_n[4] = {0, 0, 0, 0};
     // split-phase bookkeeping: how to map a failing index back to its sign word
     int pending_mode = -1;
     uint64_t pending_seed = 0, pending_mask = 0;
@@ -946,6 +1053,37 @@ struct DeviceGuard {
     }
 };
 
+// Per-kernel timing: events bracket each launch on the plan's stream and are
+// resolved after the next synchronisation (tcg_agg_fetch / tcg_kernel_times).
+cudaEvent_t timing_begin(tcg_plan *P) {
+    if (!P->timing) return nullptr;
+    cudaEvent_t a;
+    cudaEventCreate(&a);
+    cudaEventRecord(a, P->stream);
+    return a;
+}
+
+void timing_end(tcg_plan *P, int kind, cudaEvent_t a) {
+    if (!P->timing || !a) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, P->stream);
+    P->tev.push_back({kind, {a, b}});
+}
+
+void timing_resolve(tcg_plan *P) {
+    for (auto &t : P->tev) {
+        float ms = 0.f;
+        cudaEventSynchronize(t.second.second);
+        cudaEventElapsedTime(&ms, t.second.first, t.second.second);
+        P->t_ms[t.first] += ms;
+        P->t_n[t.first] += 1;
+        cudaEventDestroy(t.second.first);
+        cudaEventDestroy(t.second.second);
+    }
+    P->tev.clear();
+}
+
 template <int K, bool EVEN>
 void *enum_fn(int mode) {
     switch (mode) {
@@ -961,22 +1099,40 @@ void *pick_enum(int K, bool even, int mode) {
     return even ? enum_fn<6, true>(mode) : enum_fn<6, false>(mode);
 }
 
+template <int K>
+void *build_fn(int mode) {
+    return mode == MODE_RAW ? (void *)k_tile_build<K, MODE_RAW> : (void *)k_tile_build<K, MODE_REP>;
+}
+
+void *pick_build(int K, int mode) {
+    if (K == 2) return build_fn<2>(mode);
+    if (K == 4) return build_fn<4>(mode);
+    return build_fn<6>(mode);
+}
+
 template <int K, bool EVEN>
-void *tiles_fn(int mode) {
-    return mode == MODE_RAW ? (void *)k_tiles<K, EVEN, MODE_RAW> : (void *)k_tiles<K, EVEN, MODE_REP>;
+void *cls_fn(int mode) {
+    return mode == MODE_RAW ? (void *)k_tile_classify<K, EVEN, MODE_RAW>
+                            : (void *)k_tile_classify<K, EVEN, MODE_REP>;
 }
 
-void *pick_tiles(int K, bool even, int mode) {
-    if (K == 2) return even ? tiles_fn<2, true>(mode) : tiles_fn<2, false>(mode);
-    if (K == 4) return even ? tiles_fn<4, true>(mode) : tiles_fn<4, false>(mode);
-    return even ? tiles_fn<6, true>(mode) : tiles_fn<6, false>(mode);
+void *pick_cls(int K, bool even, int mode) {
+    if (K == 2) return even ? cls_fn<2, true>(mode) : cls_fn<2, false>(mode);
+    if (K == 4) return even ? cls_fn<4, true>(mode) : cls_fn<4, false>(mode);
+    return even ? cls_fn<6, true>(mode) : cls_fn<6, false>(mode);
 }
 
-size_t tiles_smem(int K) {
-    const size_t ts = K == 2 ? sizeof(TileShared<2>) : (K == 4 ? sizeof(TileShared<4>)
-                                                               : sizeof(TileShared<6>));
-    return (size_t)32 * K * K * 4 + TABLE_SMEM + sizeof(TileTables) + ts;
+size_t build_smem(int K) {
+    const size_t rg = K == 2 ? sizeof(Regions<2, MAXC>)
+                             : (K == 4 ? sizeof(Regions<4, MAXC>) : sizeof(Regions<6, MAXC>));
+    return (size_t)32 * K * K * 4 + sizeof(TileTables) + BUILD_WARPS * rg;
 }
+
+size_t cls_smem(int K) {
+    return (size_t)32 * K * K * 4 + TABLE_SMEM + sizeof(TileTables) + sizeof(TileRec);
+}
+
+constexpr uint32_t CHUNK_TILES = 1u << 16;
 
 void *pick_batch(int K, bool even) {
     if (K == 2) return even ? (void *)k_batch<2, true> : (void *)k_batch<2, false>;
@@ -1043,22 +1199,23 @@ int build_layout(const tcg_desc *D, Layout &L) {
 }
 
 
-// Free vertices of a tile (index bits 0..TILE_BITS-1) and the fixed mask.
-bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
+// Free vertices of a tile (index bits 0..bits-1) and the fixed mask.
+bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, TileTables &T) {
     const int d = D->degree;
     const int npts = D->npts;
     const int dom_bits = mode == MODE_RAW ? npts : npts - 3;
-    if (d < 5 || dom_bits < TILE_BITS + 2) return false;
+    if (d < 5 || bits > TILE_BITS_MAX || dom_bits < bits + 2) return false;
     std::memset(&T, 0, sizeof(T));
-    int sbit[TILE_BITS];
-    for (int i = 0; i < TILE_BITS; ++i)
+    T.bits = bits;
+    int sbit[TILE_BITS_MAX];
+    for (int i = 0; i < bits; ++i)
         sbit[i] = mode == MODE_RAW ? i : (i < d - 1 ? i + 2 : i - (d - 1) + d + 2);
     std::vector<int> fnode(D->nv, -1);
     int nf = 0;
     for (int v = 0; v < D->nv; ++v) {
         if (!D->used[v]) continue;
         int bit = -1;
-        for (int i = 0; i < TILE_BITS; ++i)
+        for (int i = 0; i < bits; ++i)
             if (sbit[i] == D->src[v]) bit = i;
         const int pos = L.pos[v];
         if (bit < 0) {
@@ -1091,6 +1248,17 @@ bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
         }
     }
     return T.nfixed > 0 && nf > 0;
+}
+
+// Tile size: 2^bits indices.  Larger tiles amortise the contraction but add
+// free vertices (lane work); default 2^10, capped so at least 36 of the 64
+// node slots stay for components.  TCG_TILE_BITS overrides.
+bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
+    int want = 10;
+    if (const char *e = std::getenv("TCG_TILE_BITS")) want = std::atoi(e);
+    for (int bits = std::min(want, TILE_BITS_MAX); bits >= 6; --bits)
+        if (build_tiles_bits(D, L, mode, bits, T) && T.nf <= 28) return true;
+    return false;
 }
 
 }  // namespace
@@ -1253,11 +1421,17 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
     {
         TileTables tt[2];
         const char *no_tiles = std::getenv("TCG_NO_TILES");
-        for (int mode = 0; mode < 2; ++mode)
+        for (int mode = 0; mode < 2; ++mode) {
             P->tiles_ok[mode] = (!no_tiles || !*no_tiles || no_tiles[0] == '0') &&
                                 build_tiles(D, L, mode, tt[mode]);
+            P->tile_bits[mode] = P->tiles_ok[mode] ? tt[mode].bits : 0;
+        }
         if ((e = cudaMalloc(&P->d_tiles, sizeof(tt))) != cudaSuccess) return bail(e, "malloc tiles");
         cudaMemcpy(P->d_tiles, tt, sizeof(tt), cudaMemcpyHostToDevice);
+        if (P->tiles_ok[0] || P->tiles_ok[1]) {
+            if ((e = cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)CHUNK_TILES)) != cudaSuccess)
+                return bail(e, "malloc tile records");
+        }
     }
     DevAgg &g = P->agg;
     if ((e = cudaMalloc(&g.keys, GCAP * 8)) != cudaSuccess) return bail(e, "malloc agg");
@@ -1287,14 +1461,22 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
                                                            P->smem_batch)) != cudaSuccess)
         return bail(e, "occupancy");
     P->blocks_batch = std::max(1, bps) * P->nsm;
-    P->smem_tiles = tiles_smem(K);
-    for (int mode = 0; mode < 2; ++mode)
-        cudaFuncSetAttribute(pick_tiles(K, P->even, mode),
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_tiles);
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_tiles(K, P->even, MODE_RAW),
-                                                           THREADS, P->smem_tiles)) != cudaSuccess)
+    P->smem_build = build_smem(K);
+    P->smem_cls = cls_smem(K);
+    for (int mode = 0; mode < 2; ++mode) {
+        cudaFuncSetAttribute(pick_build(K, mode), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)P->smem_build);
+        cudaFuncSetAttribute(pick_cls(K, P->even, mode),
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_cls);
+    }
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_cls(K, P->even, MODE_RAW),
+                                                           THREADS, P->smem_cls)) != cudaSuccess)
         return bail(e, "occupancy");
-    P->blocks_tiles = std::max(1, bps) * P->nsm;
+    P->blocks_cls = std::max(1, bps) * P->nsm;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_build(K, MODE_RAW),
+                                                           32 * BUILD_WARPS, P->smem_build)) != cudaSuccess)
+        return bail(e, "occupancy");
+    P->blocks_build = std::max(1, bps) * P->nsm;
     *out = P;
     int rc2 = tcg_agg_reset(P);
     if (rc2) {
@@ -1314,7 +1496,8 @@ int tcg_plan_destroy(tcg_plan *P) {
     if (!P) return TCG_OK;
     DeviceGuard guard(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
-    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+    timing_resolve(P);
+    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
@@ -1330,11 +1513,32 @@ int tcg_plan_set_stream(tcg_plan *P, void *stream) {
     return TCG_OK;
 }
 
+int tcg_plan_set_timing(tcg_plan *P, int enable) {
+    if (!P) return fail(TCG_E_ARG, "null plan");
+    DeviceGuard guard(P->device);
+    timing_resolve(P);
+    P->timing = enable ? 1 : 0;
+    return TCG_OK;
+}
+
+int tcg_kernel_times(tcg_plan *P, double *ms, int64_t *counts) {
+    if (!P || !ms || !counts) return fail(TCG_E_ARG, "null argument");
+    DeviceGuard guard(P->device);
+    timing_resolve(P);
+    for (int i = 0; i < 4; ++i) {
+        ms[i] = P->t_ms[i];
+        counts[i] = P->t_n[i];
+        P->t_ms[i] = 0;
+        P->t_n[i] = 0;
+    }
+    return TCG_OK;
+}
+
 int tcg_plan_info(const tcg_plan *P, int32_t *info, int ninfo) {
     if (!P || !info) return fail(TCG_E_ARG, "null argument");
-    const int32_t v[8] = {P->d, P->K, P->nused, P->device, P->nsm, P->blocks_enum, P->threads,
-                          P->maxreg};
-    for (int i = 0; i < ninfo && i < 8; ++i) info[i] = v[i];
+    const int32_t v[10] = {P->d, P->K, P->nused, P->device, P->nsm, P->blocks_enum, P->threads,
+                           P->maxreg, P->tile_bits[0], P->tile_bits[1]};
+    for (int i = 0; i < ninfo && i < 10; ++i) info[i] = v[i];
     return TCG_OK;
 }
 
@@ -1344,8 +1548,10 @@ static int launch_batch(tcg_plan *P, const uint64_t *d_sig, int64_t n, uint64_t 
     void *fn = pick_batch(P->K, P->even);
     int64_t blocks = std::min<int64_t>(P->blocks_batch, (n + THREADS - 1) / THREADS);
     void *args[] = {&P->kp, &d_sig, &n, &d_key, &d_ov, &d_nr, &d_st};
+    cudaEvent_t e3 = timing_begin(P);
     CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(THREADS), args, P->smem_batch,
                               P->stream));
+    timing_end(P, 3, e3);
     P->launches++;
     return TCG_OK;
 }
@@ -1406,18 +1612,31 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
     P->pending_seed = seed;
     P->pending_mask = mask;
     if (mode != MODE_SAMPLE && P->tiles_ok[mode] && end > start) {
-        void *fn = pick_tiles(P->K, P->even, mode);
+        // chunks of CHUNK_TILES tiles: contract (one warp per tile), then classify
+        void *fb = pick_build(P->K, mode);
+        void *fc = pick_cls(P->K, P->even, mode);
         const TileTables *tt = P->d_tiles + mode;
-        for (uint64_t a = start; a < end;) {
-            const uint64_t b = std::min<uint64_t>(end, (a / LAUNCH_MAX + 1) * LAUNCH_MAX);
-            const uint64_t ntiles = ((b + TILE - 1) >> TILE_BITS) - (a >> TILE_BITS);
-            const unsigned blocks = (unsigned)std::min<uint64_t>(P->blocks_tiles, ntiles);
-            uint64_t lo = a, hi = b;
-            void *args[] = {&P->kp, &tt, &lo, &hi, &P->agg};
-            CUDA_TRY(cudaLaunchKernel(fn, dim3(blocks), dim3(THREADS), args, P->smem_tiles,
+        const int bits = P->tile_bits[mode];
+        const uint64_t t_end = ((end - 1) >> bits) + 1;
+        for (uint64_t t0 = start >> bits; t0 < t_end; t0 += CHUNK_TILES) {
+            uint32_t nt = (uint32_t)std::min<uint64_t>(CHUNK_TILES, t_end - t0);
+            uint64_t tile0 = t0;
+            TileRec *recs = P->d_recs;
+            const unsigned gb = (unsigned)std::min<uint64_t>(
+                P->blocks_build, (nt + BUILD_WARPS - 1) / BUILD_WARPS);
+            void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs};
+            cudaEvent_t e0 = timing_begin(P);
+            CUDA_TRY(cudaLaunchKernel(fb, dim3(gb), dim3(32 * BUILD_WARPS), ab, P->smem_build,
                                       P->stream));
-            P->launches++;
-            a = b;
+            timing_end(P, 0, e0);
+            const unsigned gc = (unsigned)std::min<uint64_t>(P->blocks_cls, nt);
+            uint64_t lo = start, hi = end;
+            const TileRec *crecs = recs;
+            void *ac[] = {&P->kp, &tt, &crecs, &tile0, &nt, &lo, &hi, &P->agg};
+            cudaEvent_t e1 = timing_begin(P);
+            CUDA_TRY(cudaLaunchKernel(fc, dim3(gc), dim3(THREADS), ac, P->smem_cls, P->stream));
+            timing_end(P, 1, e1);
+            P->launches += 2;
         }
         return TCG_OK;
     }
@@ -1429,7 +1648,9 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
         const unsigned blocks = (unsigned)std::min<uint64_t>(P->blocks_enum, std::max<uint64_t>(1, need));
         uint64_t base = a, count = n;
         void *args[] = {&P->kp, &base, &count, &seed, &mask, &P->agg};
+        cudaEvent_t e2 = timing_begin(P);
         CUDA_TRY(cudaLaunchKernel(fn, dim3(blocks), dim3(THREADS), args, P->smem_enum, P->stream));
+        timing_end(P, 2, e2);
         P->launches++;
         a += n;
     }

@@ -11,10 +11,24 @@ def main(path, min_pct=0.5):
     raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr = rows[1]
+    sections, cur = [], None
+    for r in rows:
+        if r and r[0] == "Kernel Name":
+            cur = [r[1], None, []]
+            sections.append(cur)
+        elif cur is not None and cur[1] is None:
+            cur[1] = r
+        elif cur is not None:
+            cur[2].append(r)
+    for name, hdr, body in sections:
+        print("==", name[:100])
+        report(hdr, body, min_pct)
+
+
+def report(hdr, body, min_pct):
     ix = {h: i for i, h in enumerate(hdr)}
     data = []
-    for r in rows[2:]:
+    for r in body:
         if len(r) != len(hdr):
             continue
         try:
