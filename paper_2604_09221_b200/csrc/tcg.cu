@@ -501,6 +501,14 @@ __device__ __forceinline__ Result finish(const KParams &p, const uint32_t (&SG)[
         root = __ffs(selfm) - 1;
     }
     if (nedges != nreg - 1) { res.status = TCG_NOT_A_TREE; return res; }
+    // a tree on nreg <= 3 nodes is connected; its key is closed-form:
+    // 1 = <no oval>, 0b110 = one oval, 0b11010 = two leaves under the root,
+    // 0b11100 = a chain (one oval inside another)
+    if (nreg <= 3) {
+        res.status = TCG_OK;
+        res.key = nreg == 1 ? 1ull : (nreg == 2 ? 6ull : (__popc(radj[root]) == 2 ? 26ull : 28ull));
+        return res;
+    }
     res.key = tree_key(radj, nreg, root, res.status);
     return res;
 }
@@ -704,6 +712,9 @@ struct TileTables {  // per plan and domain (raw / representative), device memor
     unsigned long long fpl[MAXF];          // free-free antipodal links
     unsigned long long fcopy[TILE_BITS_MAX];  // free nodes whose sign is index bit i
     unsigned long long fpar;               // sign-extension parity of the free nodes
+    // free-node sign words for the tile-local index: fsign[0][low & 63] ^
+    // fsign[1][(low >> 6) & 63] (parity folded into fsign[0])
+    unsigned long long fsign[2][64];
 };
 
 // Contracted tile, written by k_tile_build and staged into shared memory by
@@ -803,60 +814,81 @@ __device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base
 // flip it); any edge or link whose ends violate the 2-colouring closes an odd
 // cycle (the reference's parity union-find, kernels.py:151-174).
 template <bool EVEN>
-__device__ __forceinline__ void node_pass(const uint4 *__restrict__ rows, uint64_t SG,
-                                          uint64_t USED, int nn, Regions<2> &out) {
-    uint64_t unv = USED, F = 0, XB = 0, PI = 0, regS = 0;
+__device__ __forceinline__ void node_pass(const uint4 *__restrict__ rows, uint32_t sg0,
+                                          uint32_t sg1, uint32_t u0, uint32_t u1, int nn,
+                                          Regions<2> &out) {
+    // two 32-bit halves per node set: lo = nodes 0..31, hi = nodes 32..63
+    uint32_t un0 = u0, un1 = u1, f0 = 0, f1 = 0, x0 = 0, x1 = 0, q0 = 0, q1 = 0, r0 = 0, r1 = 0;
     bool odd = false;
     int nreg = 0;
     uint32_t oddmask = 0;
     auto seed = [&]() {
-        const uint64_t low = unv & (0ull - unv);
-        F = low;
-        regS = unv;
-        unv ^= low;
-        XB = 0;
-        PI = 0;
+        const bool lo = un0 != 0u;
+        const uint32_t w = lo ? un0 : un1;
+        const uint32_t low = w & (0u - w);
+        r0 = un0;
+        r1 = un1;
+        f0 = lo ? low : 0u;
+        f1 = lo ? 0u : low;
+        un0 ^= f0;
+        un1 ^= f1;
+        x0 = x1 = 0u;
+        if (EVEN) q0 = q1 = 0u;
         odd = false;
     };
     auto close = [&]() {
         if (nreg < MAXR) {
-            const uint64_t R = regS ^ unv;
-            out.R[nreg][0] = (uint32_t)R;
-            out.R[nreg][1] = (uint32_t)(R >> 32);
-            out.X[nreg][0] = (uint32_t)XB;
-            out.X[nreg][1] = (uint32_t)(XB >> 32);
+            out.R[nreg][0] = r0 ^ un0;
+            out.R[nreg][1] = r1 ^ un1;
+            out.X[nreg][0] = x0;
+            out.X[nreg][1] = x1;
             if (EVEN && odd) oddmask |= 1u << nreg;
         }
         ++nreg;
     };
     seed();
     for (int it = 0; it < nn; ++it) {
-        if (F == 0ull) {
+        if ((f0 | f1) == 0u) {
             close();
             seed();
         }
-        const int v = __ffsll((long long)F) - 1;
-        F &= F - 1ull;
+        const bool lo = f0 != 0u;
+        const uint32_t w = lo ? f0 : f1;
+        const int b = __ffs(w) - 1;
+        const uint32_t rest = w & (w - 1u);
+        f0 = lo ? rest : f0;
+        f1 = lo ? f1 : rest;
+        const int v = lo ? b : b + 32;
         const uint4 row = rows[v];
-        const uint64_t a = ((uint64_t)row.y << 32) | row.x;
-        const uint64_t pl = ((uint64_t)row.w << 32) | row.z;
-        const uint64_t same = SG ^ ((((SG >> v) & 1ull)) - 1ull);  // s_v ? SG : ~SG
-        XB |= a & ~same;
+        // opp = nodes whose sign differs from v's: SG ^ (s_v ? ~0 : 0)
+        const uint32_t sv = (uint32_t)((int32_t)((lo ? sg0 : sg1) << (31 - b)) >> 31);
+        const uint32_t o0 = sg0 ^ sv, o1 = sg1 ^ sv;
+        x0 |= row.x & o0;
+        x1 |= row.y & o1;
         if (EVEN) {
-            const uint64_t pv = ((PI >> v) & 1ull) ? ~0ull : 0ull;
-            const uint64_t te = a & same, nT = te & unv, nP = pl & unv;
-            // nodes with parity equal to v's: PI if pv else ~PI
-            const uint64_t eq = ~(PI ^ pv);
-            const uint64_t bad = (nT & nP) | (te & ~unv & ~eq) | (pl & ~unv & eq);
-            odd |= bad != 0ull;
-            PI |= (nT & pv) | (nP & ~pv);
-            const uint64_t nw = nT | nP;
-            unv ^= nw;
-            F |= nw;
+            // parity of v (equal-parity mask pv): edges keep it, links flip it
+            const uint32_t pv = (uint32_t)((int32_t)((lo ? q0 : q1) << (31 - b)) >> 31);
+            const uint32_t te0 = row.x & ~o0, te1 = row.y & ~o1;
+            const uint32_t nt0 = te0 & un0, nt1 = te1 & un1;
+            const uint32_t np0 = row.z & un0, np1 = row.w & un1;
+            const uint32_t eq0 = ~(q0 ^ pv), eq1 = ~(q1 ^ pv);
+            const uint32_t bad = (nt0 & np0) | (nt1 & np1) | (te0 & ~un0 & ~eq0) |
+                                 (te1 & ~un1 & ~eq1) | (row.z & ~un0 & eq0) | (row.w & ~un1 & eq1);
+            odd |= bad != 0u;
+            q0 |= (nt0 & pv) | (np0 & ~pv);
+            q1 |= (nt1 & pv) | (np1 & ~pv);
+            const uint32_t n0 = nt0 | np0, n1 = nt1 | np1;
+            un0 ^= n0;
+            un1 ^= n1;
+            f0 |= n0;
+            f1 |= n1;
         } else {
-            const uint64_t nw = ((a & same) | pl) & unv;
-            unv ^= nw;
-            F |= nw;
+            const uint32_t n0 = ((row.x & ~o0) | row.z) & un0;
+            const uint32_t n1 = ((row.y & ~o1) | row.w) & un1;
+            un0 ^= n0;
+            un1 ^= n1;
+            f0 |= n0;
+            f1 |= n1;
         }
     }
     close();
@@ -869,14 +901,14 @@ __device__ __forceinline__ Result classify_tile(const KParams &p, const TileTabl
                                                 const uint4 *rows,
                                                 unsigned long long sgn_fixed, int n, int nn,
                                                 uint32_t low) {
-    unsigned long long fs = tt.fpar;
-    for (int i = 0; i < tt.bits; ++i)
-        if ((low >> i) & 1u) fs ^= tt.fcopy[i];
+    // signs of the free nodes: two table lookups on the tile-local index
+    const unsigned long long fs = tt.fsign[0][low & 63u] ^ tt.fsign[1][(low >> 6) & 63u];
     const unsigned long long sg = sgn_fixed | (fs << n);
     const unsigned long long used = nn >= 64 ? ~0ull : ((1ull << nn) - 1ull);
-    const uint32_t SG[2] = {(uint32_t)sg, (uint32_t)(sg >> 32)};
     Regions<2> rg;
-    node_pass<EVEN>(rows, sg, used, nn, rg);
+    node_pass<EVEN>(rows, (uint32_t)sg, (uint32_t)(sg >> 32), (uint32_t)used,
+                    (uint32_t)(used >> 32), nn, rg);
+    const uint32_t SG[2] = {(uint32_t)sg, (uint32_t)(sg >> 32)};
     return finish<2, EVEN, false>(p, SG, rg, p.maxreg);
 }
 
@@ -902,6 +934,10 @@ __global__ void __launch_bounds__(32 * BUILD_WARPS) k_tile_build(KParams p,
 }
 
 // Classify every index of [start, end) that falls in tiles tile0 .. tile0+ntiles-1.
+// One warp owns a whole tile at a time (its contracted graph staged in a
+// per-warp shared-memory slot), so warps never wait on each other.
+constexpr int CLS_WARPS = THREADS / 32;
+
 template <int K, bool EVEN, int MODE>
 __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
                                                            const TileTables *__restrict__ tt_g,
@@ -914,7 +950,8 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
     CtaTable tab = carve_table(smem + 32 * K * K);
     TileTables *tt = reinterpret_cast<TileTables *>(
         reinterpret_cast<char *>(smem) + 32 * K * K * 4 + TABLE_SMEM);
-    TileRec *rec = reinterpret_cast<TileRec *>(tt + 1);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    TileRec *rec = reinterpret_cast<TileRec *>(tt + 1) + w;
     stage_adj<K>(p, adj_s);
     for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
         reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
@@ -922,22 +959,17 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
     __syncthreads();
     const int bits = tt->bits;
     const uint32_t tsize = 1u << bits;
-    for (uint32_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (uint32_t t = blockIdx.x * CLS_WARPS + w; t < ntiles; t += gridDim.x * CLS_WARPS) {
         const TileRec *src = recs + t;
-        const int nn_g = src->nnodes;
-        if (threadIdx.x < 64 && (int)threadIdx.x < nn_g) rec->rows[threadIdx.x] = src->rows[threadIdx.x];
-        if (threadIdx.x == 64) {
-            rec->sgn_fixed = src->sgn_fixed;
-            rec->n = src->n;
-            rec->nnodes = nn_g;
-            rec->fallback = src->fallback;
-        }
-        __syncthreads();
+        const int nn = src->nnodes;
+        if (lane < nn) rec->rows[lane] = src->rows[lane];
+        if (lane + 32 < nn) rec->rows[lane + 32] = src->rows[lane + 32];
+        const int n = src->n;
+        const bool fb = src->fallback != 0;
+        const unsigned long long sgf = src->sgn_fixed;
+        __syncwarp();
         const uint64_t base = (tile0 + t) << bits;
-        const int n = rec->n, nn = rec->nnodes;
-        const bool fb = rec->fallback != 0;
-        const unsigned long long sgf = rec->sgn_fixed;
-        for (uint32_t low = threadIdx.x; low < tsize; low += THREADS) {
+        for (uint32_t low = lane; low < tsize; low += 32) {
             const uint64_t m = base + low;
             const bool valid = m >= start && m < end;
             Result r;
@@ -954,8 +986,9 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
             }
             tab.add<true>(g, k, r.nreg, m);
         }
-        __syncthreads();
+        __syncwarp();
     }
+    __syncthreads();
     tab.flush(g);
 }
 
@@ -1129,10 +1162,10 @@ size_t build_smem(int K) {
 }
 
 size_t cls_smem(int K) {
-    return (size_t)32 * K * K * 4 + TABLE_SMEM + sizeof(TileTables) + sizeof(TileRec);
+    return (size_t)32 * K * K * 4 + TABLE_SMEM + sizeof(TileTables) + CLS_WARPS * sizeof(TileRec);
 }
 
-constexpr uint32_t CHUNK_TILES = 1u << 16;
+constexpr uint32_t CHUNK_TILES = 1u << 18;
 
 void *pick_batch(int K, bool even) {
     if (K == 2) return even ? (void *)k_batch<2, true> : (void *)k_batch<2, false>;
@@ -1232,6 +1265,13 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
         ++nf;
     }
     T.nf = nf;
+    for (int h = 0; h < 2; ++h)
+        for (int x = 0; x < 64; ++x) {
+            unsigned long long w = h == 0 ? T.fpar : 0ull;
+            for (int i = 0; i < 6; ++i)
+                if (((x >> i) & 1) && 6 * h + i < bits) w ^= T.fcopy[6 * h + i];
+            T.fsign[h][x] = w;
+        }
     for (int e = 0; e < D->ne; ++e) {
         const int fu = fnode[D->edge_u[e]], fv = fnode[D->edge_v[e]];
         if (fu >= 0 && fv >= 0) {
@@ -1629,7 +1669,8 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             CUDA_TRY(cudaLaunchKernel(fb, dim3(gb), dim3(32 * BUILD_WARPS), ab, P->smem_build,
                                       P->stream));
             timing_end(P, 0, e0);
-            const unsigned gc = (unsigned)std::min<uint64_t>(P->blocks_cls, nt);
+            const unsigned gc = (unsigned)std::min<uint64_t>(P->blocks_cls,
+                                                             (nt + CLS_WARPS - 1) / CLS_WARPS);
             uint64_t lo = start, hi = end;
             const TileRec *crecs = recs;
             void *ac[] = {&P->kp, &tt, &crecs, &tile0, &nt, &lo, &hi, &P->agg};
