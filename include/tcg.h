@@ -154,6 +154,18 @@ int tcg_sweep_multi(tcg_plan **plans, int nplans, int raw, uint64_t start, uint6
 int tcg_sample_multi(tcg_plan **plans, int nplans, uint64_t seed, uint64_t k0, uint64_t k1,
                      int nbits, tcg_agg *agg, int64_t *bad);
 
+/* Many triangulations of one degree on one device (config C4, SURVEY
+ * section 8f row 2): pairs (tri[t], sigma[t]) are grouped by triangulation
+ * and every CTA classifies one group on its own topology.  Host buffers;
+ * outputs in the input order.  tcg_multi_last_ms = device time of the last
+ * classification kernel (CUDA events). */
+typedef struct tcg_multi tcg_multi;
+int tcg_multi_create(const tcg_desc *descs, int32_t ntri, int device, tcg_multi **out);
+int tcg_multi_destroy(tcg_multi *m);
+int tcg_multi_classify(tcg_multi *m, const int32_t *tri, const uint64_t *sigma, int64_t n,
+                       uint64_t *key, uint8_t *ovals, uint8_t *nreg, int32_t *status);
+double tcg_multi_last_ms(const tcg_multi *m);
+
 /* Diagnostics. */
 const char *tcg_last_error(void);
 int tcg_device_count(void);

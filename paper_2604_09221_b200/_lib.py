@@ -84,6 +84,12 @@ def load():
         L.tcg_device_count.restype = C.c_int
         L.tcg_launch_count.argtypes = [P]
         L.tcg_launch_count.restype = C.c_int64
+        L.tcg_multi_create.argtypes = [C.POINTER(TcgDesc), C.c_int32, C.c_int, C.POINTER(P)]
+        L.tcg_multi_destroy.argtypes = [P]
+        L.tcg_multi_classify.argtypes = [P, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                         C.c_void_p, C.c_void_p, C.c_void_p]
+        L.tcg_multi_last_ms.argtypes = [P]
+        L.tcg_multi_last_ms.restype = C.c_double
         _lib = L
         return L
 
@@ -94,7 +100,8 @@ EXPORTS = (
     "tcg_classify_batch", "tcg_classify_batch_device", "tcg_sweep", "tcg_sample",
     "tcg_agg_reset", "tcg_sweep_async", "tcg_sample_async", "tcg_agg_fetch",
     "tcg_sweep_multi", "tcg_sample_multi", "tcg_last_error", "tcg_device_count",
-    "tcg_launch_count", "tcg_version",
+    "tcg_launch_count", "tcg_version", "tcg_multi_create", "tcg_multi_destroy",
+    "tcg_multi_classify", "tcg_multi_last_ms",
 )
 
 
@@ -141,6 +148,68 @@ class AggBuffers:
             self.count[:n].copy(),
             self.witness[:n].copy(),
         )
+
+
+def _desc(arrays, keep):
+    arrs = [
+        np.ascontiguousarray(arrays.edge_u, np.int32),
+        np.ascontiguousarray(arrays.edge_v, np.int32),
+        np.ascontiguousarray(arrays.src, np.int32),
+        np.ascontiguousarray(arrays.par, np.uint8),
+        np.ascontiguousarray(arrays.used, np.uint8),
+        np.ascontiguousarray(arrays.ap_u, np.int32),
+        np.ascontiguousarray(arrays.ap_v, np.int32),
+    ]
+    keep.extend(arrs)
+    eu, ev, src, par, used, apu, apv = arrs
+    return TcgDesc(arrays.degree, arrays.nv, arrays.npts, len(eu), eu.ctypes.data,
+                   ev.ctypes.data, src.ctypes.data, par.ctypes.data, used.ctypes.data,
+                   len(apu), apu.ctypes.data, apv.ctypes.data, arrays.maxreg)
+
+
+class NativeMulti:
+    """Owns one tcg_multi (many triangulations of one degree on one device)."""
+
+    def __init__(self, arrays_list, device: int | None = None):
+        L = load()
+        if L.tcg_device_count() < 1:
+            raise DeviceUnavailable("no CUDA device visible; the classifier has no CPU fallback")
+        self._keep = []
+        descs = (TcgDesc * len(arrays_list))(*[_desc(a, self._keep) for a in arrays_list])
+        h = C.c_void_p()
+        _check(L.tcg_multi_create(descs, len(arrays_list), -1 if device is None else int(device),
+                                  C.byref(h)), "tcg_multi_create")
+        self.h = h
+        self._L = L
+        self.ntri = len(arrays_list)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            try:
+                self._L.tcg_multi_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def classify_words(self, tri, words):
+        t = np.ascontiguousarray(tri, dtype=np.int32)
+        w = np.ascontiguousarray(words, dtype=np.uint64)
+        n = len(w)
+        if len(t) != n:
+            raise ValueError("tri and words must have the same length")
+        key = np.zeros(n, np.uint64)
+        ov = np.zeros(n, np.uint8)
+        nr = np.zeros(n, np.uint8)
+        st = np.zeros(n, np.int32)
+        if n:
+            _check(self._L.tcg_multi_classify(self.h, t.ctypes.data, w.ctypes.data, n,
+                                              key.ctypes.data, ov.ctypes.data, nr.ctypes.data,
+                                              st.ctypes.data), "tcg_multi_classify")
+        return key, ov, nr, st
+
+    def last_ms(self) -> float:
+        return float(self._L.tcg_multi_last_ms(self.h))
 
 
 class NativePlan:

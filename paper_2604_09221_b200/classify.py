@@ -144,3 +144,49 @@ def classify(T, sigma, validate: bool = True, classifier: Classifier | None = No
         T = validate_triangulation(T.degree, T.edges)
     c = classifier or Classifier(T)
     return c.classify(sigma)
+
+
+class MultiClassifier:
+    """Many triangulations of one degree resident on one GPU (config C4).
+
+    The reference has no multi-triangulation API; its
+    equivalent is one ``Classifier(T).classify(sigma)`` per pair.  Here all
+    triangulations are uploaded once and a batch of (triangulation index,
+    sign vector) pairs is classified in one launch, one topology per CTA.
+    """
+
+    def __init__(self, triangulations, device: int | None = None):
+        self.triangulations = list(triangulations)
+        if not self.triangulations:
+            raise ParseError("need at least one triangulation")
+        degs = {int(T.degree) for T in self.triangulations}
+        if len(degs) != 1:
+            raise ParseError(f"all triangulations must share one degree, got {sorted(degs)}")
+        self.degree = degs.pop()
+        self.native = _lib.NativeMulti([plan_arrays(reflect(T)) for T in self.triangulations],
+                                       device)
+
+    def classify_words(self, tri, words):
+        return self.native.classify_words(tri, words)
+
+    def classify_pairs(self, pairs) -> list[ClassificationResult]:
+        tri, words = [], []
+        for t, s in pairs:
+            if isinstance(s, str):
+                s = SignDistribution.from_bitstring(self.degree, s)
+            w = 0
+            for k, b in enumerate(s.bits):
+                w |= int(b) << k
+            tri.append(int(t))
+            words.append(w)
+        key, ov, nr, st = self.native.classify_words(np.array(tri, np.int32),
+                                                     np.array(words, np.uint64))
+        odd = self.degree % 2 == 1
+        out = []
+        for i in range(len(words)):
+            if st[i] != 0:
+                raise InvariantViolation(STATUS_MESSAGES.get(int(st[i]), f"status {st[i]}")
+                                         + f" (at pair {i})")
+            out.append(ClassificationResult(scheme_from_key(int(key[i]), odd), int(ov[i]),
+                                            int(nr[i]), odd))
+        return out

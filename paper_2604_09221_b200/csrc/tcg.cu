@@ -555,6 +555,35 @@ __global__ void __launch_bounds__(THREADS) k_batch(KParams p, const uint64_t *__
     }
 }
 
+// Many triangulations of one degree (config C4): a work item is
+// (triangulation, first pair, pair count) over pairs sorted by triangulation;
+// each CTA stages its item's descriptor and adjacency rows in shared memory,
+// so consecutive CTAs classify on different topologies.
+template <int K, bool EVEN>
+__global__ void __launch_bounds__(THREADS) k_multi(const KParams *__restrict__ kps,
+                                                   const int4 *__restrict__ items,
+                                                   const uint64_t *__restrict__ sig,
+                                                   uint64_t *__restrict__ key,
+                                                   uint8_t *__restrict__ ovals,
+                                                   uint8_t *__restrict__ nreg,
+                                                   int32_t *__restrict__ status) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    __shared__ KParams kp_s;
+    const int4 it = items[blockIdx.x];  // x = triangulation, y = first, z = count
+    if (threadIdx.x == 0) kp_s = kps[it.x];
+    __syncthreads();
+    stage_adj<K>(kp_s, smem);
+    __syncthreads();
+    for (int t = threadIdx.x; t < it.z; t += blockDim.x) {
+        const int64_t i = (int64_t)it.y + t;
+        const Result r = classify<K, EVEN>(kp_s, smem, sig[i]);
+        key[i] = r.status == TCG_OK ? r.key : 0ull;
+        ovals[i] = r.status == TCG_OK ? (uint8_t)(r.nreg - 1) : 0xff;
+        nreg[i] = (uint8_t)min(r.nreg, 255);
+        status[i] = r.status;
+    }
+}
+
 __device__ __forceinline__ uint32_t hash_slot(uint64_t key, int bits) {
     return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - bits));
 }
@@ -1301,6 +1330,105 @@ bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
     return false;
 }
 
+// Host-side plan: layout, masks, adjacency rows and edge list of one
+// triangulation, validated against the reference's sign-extension tables.
+struct HostPlan {
+    int d = 0, K = 0, even = 0, nused = 0;
+    KParams kp{};
+    Layout L;
+    std::vector<uint32_t> adj, edges;
+};
+
+int build_host_plan(const tcg_desc *D, HostPlan &HP) {
+    if (!D) return fail(TCG_E_ARG, "null descriptor");
+    const int d = D->degree;
+    if (d < 1) return fail(TCG_E_ARG, "degree must be >= 1");
+    if (d > 9)
+        return fail(TCG_E_UNSUPPORTED,
+                    "degree > 9 exceeds the 64-bit sign word / 96-bit half-mask layout");
+    if (D->nv != 2 * d * d + 2 * d + 1) return fail(TCG_E_ARG, "nv != 2d^2+2d+1");
+    if (D->npts != (d + 1) * (d + 2) / 2) return fail(TCG_E_ARG, "npts mismatch");
+    if (D->maxreg < 1 || D->maxreg > MAXR) return fail(TCG_E_UNSUPPORTED, "maxreg out of range");
+    if (D->ne < 1) return fail(TCG_E_ARG, "empty edge list");
+    Layout &L = HP.L;
+    int rc = build_layout(D, L);
+    if (rc) return rc;
+    const int K = L.K, H = L.H;
+    HP.d = d;
+    HP.K = K;
+    HP.even = (d % 2 == 0);
+    KParams &kp = HP.kp;
+    kp = KParams{};
+    kp.d = d;
+    kp.npts = D->npts;
+    kp.maxreg = D->maxreg;
+    kp.center = d * d + d;
+    kp.ne = D->ne;
+    std::vector<std::pair<int, int>> pts;
+    for (int i = -d; i <= d; ++i) {
+        const int a = d - std::abs(i);
+        for (int j = -a; j <= a; ++j) pts.emplace_back(i, j);
+    }
+    auto setbit = [&](uint32_t *m, int pos) { m[pos >> 5] |= 1u << (pos & 31); };
+    int nused = 0;
+    for (int v = 0; v < D->nv; ++v)
+        if (D->used[v]) {
+            setbit(kp.used, L.pos[v]);
+            ++nused;
+        }
+    kp.nused = nused;
+    HP.nused = nused;
+    for (int a = 0; a < D->nap; ++a) {
+        const int u = D->ap_u[a], v = D->ap_v[a];
+        if (u < 0 || u >= D->nv || v < 0 || v >= D->nv)
+            return fail(TCG_E_ARG, "antipodal pair out of range");
+        const int pu = L.pos[u], pv = L.pos[v];
+        if (std::abs(pu - pv) != H) return fail(TCG_E_ARG, "antipodal pair is not (p, -p)");
+        if (std::abs(pts[u].first) + std::abs(pts[u].second) != d)
+            return fail(TCG_E_ARG, "antipodal pair off the diamond boundary");
+        setbit(kp.bd, pu);
+        setbit(kp.bd, pv);
+    }
+    // sign-extension tables -> P-half masks; verify they are the reference's
+    for (int v = 0; v < D->nv; ++v) {
+        const int i = pts[v].first, j = pts[v].second;
+        const int want_src = point_index(d, std::abs(i), std::abs(j));
+        const int want_par = ((i < 0 ? -i : 0) + (j < 0 ? -j : 0)) & 1;
+        if (D->src[v] != want_src || D->par[v] != want_par)
+            return fail(TCG_E_ARG, "src/par tables differ from the reflected sign extension");
+        const int pos = L.pos[v];
+        if (pos < H && !(i == 0 && j == 0)) {
+            if (((std::abs(i) + std::abs(j)) & 1) != 0) kp.parP[pos >> 5] |= 1u << (pos & 31);
+            if (j < 0 && ((-j) & 1)) kp.jodd[pos >> 5] |= 1u << (pos & 31);
+        }
+    }
+    // mirrored-quadrant compress runs: row i contributes (i,1..d-i)
+    {
+        int nq = 0, dst = 0;
+        for (int i = 1; i <= d - 1; ++i) {
+            kp.q4src[nq] = (uint8_t)point_index(d, i, 1);
+            kp.q4len[nq] = (uint8_t)(d - i);
+            kp.q4dst[nq] = (uint8_t)dst;
+            dst += d - i;
+            ++nq;
+        }
+        kp.nq4 = nq;
+    }
+    // adjacency rows and edge list in layout positions
+    HP.adj.assign((size_t)2 * H * K, 0u);
+    HP.edges.assign(D->ne, 0u);
+    for (int e = 0; e < D->ne; ++e) {
+        const int u = D->edge_u[e], v = D->edge_v[e];
+        if (u < 0 || u >= D->nv || v < 0 || v >= D->nv || u == v)
+            return fail(TCG_E_ARG, "edge endpoint out of range");
+        const int pu = L.pos[u], pv = L.pos[v];
+        HP.adj[(size_t)pu * K + (pv >> 5)] |= 1u << (pv & 31);
+        HP.adj[(size_t)pv * K + (pu >> 5)] |= 1u << (pu & 31);
+        HP.edges[e] = (uint32_t)pu | ((uint32_t)pv << 16);
+    }
+    return TCG_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1322,108 +1450,21 @@ int64_t tcg_launch_count(const tcg_plan *plan) { return plan ? plan->launches : 
 int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
     if (!D || !out) return fail(TCG_E_ARG, "null argument");
     *out = nullptr;
-    const int d = D->degree;
-    if (d < 1) return fail(TCG_E_ARG, "degree must be >= 1");
-    if (d > 9)
-        return fail(TCG_E_UNSUPPORTED,
-                    "degree > 9 exceeds the 64-bit sign word / 96-bit half-mask layout");
-    if (D->nv != 2 * d * d + 2 * d + 1) return fail(TCG_E_ARG, "nv != 2d^2+2d+1");
-    if (D->npts != (d + 1) * (d + 2) / 2) return fail(TCG_E_ARG, "npts mismatch");
-    if (D->maxreg < 1 || D->maxreg > MAXR) return fail(TCG_E_UNSUPPORTED, "maxreg out of range");
-    if (D->ne < 1) return fail(TCG_E_ARG, "empty edge list");
-    Layout L;
-    int rc = build_layout(D, L);
+    HostPlan HP;
+    int rc = build_host_plan(D, HP);
     if (rc) return rc;
-    const int K = L.K, H = L.H;
-
-    // validate descriptor against the layout (src/par must be the reference's)
-    for (int v = 0; v < D->nv; ++v) {
-        if (D->src[v] < 0 || D->src[v] >= D->npts) return fail(TCG_E_ARG, "src out of range");
-    }
+    const Layout &L = HP.L;
+    const int K = HP.K;
     tcg_plan *P = new tcg_plan();
-    P->d = d;
+    P->d = HP.d;
     P->K = K;
-    P->even = (d % 2 == 0);
+    P->even = HP.even;
     P->maxreg = D->maxreg;
+    P->nused = HP.nused;
     KParams &kp = P->kp;
-    kp.d = d;
-    kp.npts = D->npts;
-    kp.maxreg = D->maxreg;
-    kp.center = d * d + d;
-    kp.ne = D->ne;
-    // used / boundary / parity masks
-    std::vector<uint32_t> adj((size_t)2 * H * K, 0u);
-    auto setbit = [&](uint32_t *m, int pos) { m[pos >> 5] |= 1u << (pos & 31); };
-    int nused = 0;
-    for (int v = 0; v < D->nv; ++v)
-        if (D->used[v]) {
-            setbit(kp.used, L.pos[v]);
-            ++nused;
-        }
-    kp.nused = nused;
-    P->nused = nused;
-    for (int a = 0; a < D->nap; ++a) {
-        const int u = D->ap_u[a], v = D->ap_v[a];
-        if (u < 0 || u >= D->nv || v < 0 || v >= D->nv) {
-            delete P;
-            return fail(TCG_E_ARG, "antipodal pair out of range");
-        }
-        const int pu = L.pos[u], pv = L.pos[v];
-        if (std::abs(pu - pv) != H) {
-            delete P;
-            return fail(TCG_E_ARG, "antipodal pair is not (p, -p)");
-        }
-        setbit(kp.bd, pu);
-        setbit(kp.bd, pv);
-    }
-    // sign-extension tables -> P-half masks; verify they are the reference's
-    {
-        std::vector<std::pair<int, int>> pts;
-        for (int i = -d; i <= d; ++i) {
-            const int a = d - std::abs(i);
-            for (int j = -a; j <= a; ++j) pts.emplace_back(i, j);
-        }
-        for (int v = 0; v < D->nv; ++v) {
-            const int i = pts[v].first, j = pts[v].second;
-            const int want_src = point_index(d, std::abs(i), std::abs(j));
-            const int want_par = ((i < 0 ? -i : 0) + (j < 0 ? -j : 0)) & 1;
-            if (D->src[v] != want_src || D->par[v] != want_par) {
-                delete P;
-                return fail(TCG_E_ARG, "src/par tables differ from the reflected sign extension");
-            }
-            const int pos = L.pos[v];
-            if (pos < H && !(i == 0 && j == 0)) {
-                if (((std::abs(i) + std::abs(j)) & 1) != 0) kp.parP[pos >> 5] |= 1u << (pos & 31);
-                if (j < 0 && ((-j) & 1)) kp.jodd[pos >> 5] |= 1u << (pos & 31);
-            }
-        }
-    }
-    // mirrored-quadrant compress runs: row i contributes (i,1..d-i)
-    {
-        int nq = 0, dst = 0;
-        for (int i = 1; i <= d - 1; ++i) {
-            kp.q4src[nq] = (uint8_t)point_index(d, i, 1);
-            kp.q4len[nq] = (uint8_t)(d - i);
-            kp.q4dst[nq] = (uint8_t)dst;
-            dst += d - i;
-            ++nq;
-        }
-        kp.nq4 = nq;
-    }
-    // adjacency rows and edge list in layout positions
-    std::vector<uint32_t> edges(D->ne);
-    for (int e = 0; e < D->ne; ++e) {
-        const int u = D->edge_u[e], v = D->edge_v[e];
-        if (u < 0 || u >= D->nv || v < 0 || v >= D->nv || u == v) {
-            delete P;
-            return fail(TCG_E_ARG, "edge endpoint out of range");
-        }
-        const int pu = L.pos[u], pv = L.pos[v];
-        adj[(size_t)pu * K + (pv >> 5)] |= 1u << (pv & 31);
-        adj[(size_t)pv * K + (pu >> 5)] |= 1u << (pu & 31);
-        edges[e] = (uint32_t)pu | ((uint32_t)pv << 16);
-    }
-
+    kp = HP.kp;
+    std::vector<uint32_t> &adj = HP.adj;
+    std::vector<uint32_t> &edges = HP.edges;
     if (device < 0) {
         if (cudaGetDevice(&device) != cudaSuccess) {
             delete P;
@@ -1894,5 +1935,188 @@ int tcg_sample_multi(tcg_plan **plans, int nplans, uint64_t seed, uint64_t k0, u
                          return tcg_sample(p, seed, lo, hi, nbits, a, b);
                      });
 }
+
+
+// ------------------------------------------------------------ many triangulations
+struct tcg_multi {
+    int device = 0, d = 0, K = 0, even = 0, ntri = 0;
+    KParams *d_kp = nullptr;
+    uint32_t *d_adj = nullptr, *d_edges = nullptr;
+    size_t smem = 0;
+    cudaStream_t stream = nullptr;
+    int64_t cap = 0;
+    uint64_t *d_sig = nullptr, *d_key = nullptr;
+    uint8_t *d_ov = nullptr, *d_nr = nullptr;
+    int32_t *d_st = nullptr;
+    int4 *d_items = nullptr;
+    int64_t items_cap = 0;
+    float last_ms = 0.f;
+    int64_t launches = 0;
+};
+
+static void *pick_multi(int K, bool even) {
+    if (K == 2) return even ? (void *)k_multi<2, true> : (void *)k_multi<2, false>;
+    if (K == 4) return even ? (void *)k_multi<4, true> : (void *)k_multi<4, false>;
+    return even ? (void *)k_multi<6, true> : (void *)k_multi<6, false>;
+}
+
+int tcg_multi_destroy(tcg_multi *M) {
+    if (!M) return TCG_OK;
+    DeviceGuard guard(M->device);
+    if (M->stream) cudaStreamSynchronize(M->stream);
+    void *ptrs[] = {M->d_kp, M->d_adj, M->d_edges, M->d_sig, M->d_key, M->d_ov, M->d_nr,
+                    M->d_st, M->d_items};
+    for (void *q : ptrs)
+        if (q) cudaFree(q);
+    if (M->stream) cudaStreamDestroy(M->stream);
+    delete M;
+    return TCG_OK;
+}
+
+int tcg_multi_create(const tcg_desc *descs, int32_t ntri, int device, tcg_multi **out) {
+    if (!descs || !out || ntri < 1) return fail(TCG_E_ARG, "bad arguments");
+    *out = nullptr;
+    std::vector<HostPlan> hps(ntri);
+    for (int t = 0; t < ntri; ++t) {
+        int rc = build_host_plan(descs + t, hps[t]);
+        if (rc) return rc;
+        if (hps[t].d != hps[0].d) return fail(TCG_E_ARG, "all triangulations must share one degree");
+    }
+    const int K = hps[0].K;
+    const size_t arow = (size_t)32 * K * K;
+    size_t ne_tot = 0;
+    for (auto &h : hps) ne_tot += h.edges.size();
+    if (device < 0 && cudaGetDevice(&device) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(TCG_E_CUDA, "no CUDA device");
+    }
+    tcg_multi *M = new tcg_multi();
+    M->device = device;
+    M->d = hps[0].d;
+    M->K = K;
+    M->even = hps[0].even;
+    M->ntri = ntri;
+    DeviceGuard guard(device);
+    auto bail = [&](cudaError_t e, const char *what) {
+        std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+        tcg_multi_destroy(M);
+        return fail(TCG_E_CUDA, msg);
+    };
+    cudaError_t e;
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return bail(e, "props");
+    if (prop.major < 10) {
+        tcg_multi_destroy(M);
+        return fail(TCG_E_UNSUPPORTED, "libtcg is built for sm_100a (Blackwell B200)");
+    }
+    if ((e = cudaStreamCreateWithFlags(&M->stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail(e, "stream");
+    if ((e = cudaMalloc(&M->d_kp, sizeof(KParams) * ntri)) != cudaSuccess) return bail(e, "malloc");
+    if ((e = cudaMalloc(&M->d_adj, 4 * arow * ntri)) != cudaSuccess) return bail(e, "malloc");
+    if ((e = cudaMalloc(&M->d_edges, 4 * std::max<size_t>(1, ne_tot))) != cudaSuccess)
+        return bail(e, "malloc");
+    std::vector<KParams> kps(ntri);
+    std::vector<uint32_t> adj(arow * ntri), edges(std::max<size_t>(1, ne_tot));
+    size_t eo = 0;
+    for (int t = 0; t < ntri; ++t) {
+        kps[t] = hps[t].kp;
+        kps[t].adj = M->d_adj + arow * t;
+        kps[t].edges = M->d_edges + eo;
+        std::copy(hps[t].adj.begin(), hps[t].adj.end(), adj.begin() + arow * t);
+        std::copy(hps[t].edges.begin(), hps[t].edges.end(), edges.begin() + eo);
+        eo += hps[t].edges.size();
+    }
+    cudaMemcpy(M->d_kp, kps.data(), sizeof(KParams) * ntri, cudaMemcpyHostToDevice);
+    cudaMemcpy(M->d_adj, adj.data(), 4 * adj.size(), cudaMemcpyHostToDevice);
+    if ((e = cudaMemcpy(M->d_edges, edges.data(), 4 * edges.size(), cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+        return bail(e, "upload");
+    M->smem = 4 * arow;
+    *out = M;
+    return TCG_OK;
+}
+
+int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, int64_t n,
+                       uint64_t *key, uint8_t *ov, uint8_t *nr, int32_t *st) {
+    if (!M || (n > 0 && (!tri || !sig || !key || !ov || !nr || !st)))
+        return fail(TCG_E_ARG, "null argument");
+    if (n <= 0) return TCG_OK;
+    if (n > INT32_MAX) return fail(TCG_E_RANGE, "at most 2^31-1 pairs per call");
+    DeviceGuard guard(M->device);
+    // counting sort of the pairs by triangulation; items of <= 2048 pairs
+    constexpr int ITEM = 2048;
+    std::vector<int64_t> cnt(M->ntri + 1, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        if (tri[i] < 0 || tri[i] >= M->ntri) return fail(TCG_E_ARG, "triangulation index out of range");
+        cnt[tri[i] + 1]++;
+    }
+    for (int t = 0; t < M->ntri; ++t) cnt[t + 1] += cnt[t];
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1), order(n);
+    std::vector<uint64_t> ssig(n);
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t j = pos[tri[i]]++;
+        order[j] = i;
+        ssig[j] = sig[i];
+    }
+    std::vector<int4> items;
+    for (int t = 0; t < M->ntri; ++t)
+        for (int64_t a = cnt[t]; a < cnt[t + 1]; a += ITEM)
+            items.push_back(make_int4(t, (int)a, (int)std::min<int64_t>(ITEM, cnt[t + 1] - a), 0));
+    if (n > M->cap) {
+        void *ptrs[] = {M->d_sig, M->d_key, M->d_ov, M->d_nr, M->d_st};
+        for (void *q : ptrs)
+            if (q) cudaFree(q);
+        M->cap = 0;
+        const int64_t cap = std::max<int64_t>(n, 1 << 16);
+        CUDA_TRY(cudaMalloc(&M->d_sig, cap * 8));
+        CUDA_TRY(cudaMalloc(&M->d_key, cap * 8));
+        CUDA_TRY(cudaMalloc(&M->d_ov, cap));
+        CUDA_TRY(cudaMalloc(&M->d_nr, cap));
+        CUDA_TRY(cudaMalloc(&M->d_st, cap * 4));
+        M->cap = cap;
+    }
+    if ((int64_t)items.size() > M->items_cap) {
+        if (M->d_items) cudaFree(M->d_items);
+        M->d_items = nullptr;
+        M->items_cap = 0;
+        CUDA_TRY(cudaMalloc(&M->d_items, sizeof(int4) * items.size()));
+        M->items_cap = (int64_t)items.size();
+    }
+    CUDA_TRY(cudaMemcpyAsync(M->d_sig, ssig.data(), n * 8, cudaMemcpyHostToDevice, M->stream));
+    CUDA_TRY(cudaMemcpyAsync(M->d_items, items.data(), sizeof(int4) * items.size(),
+                             cudaMemcpyHostToDevice, M->stream));
+    void *fn = pick_multi(M->K, M->even);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M->smem);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, M->stream);
+    void *args[] = {&M->d_kp, &M->d_items, &M->d_sig, &M->d_key, &M->d_ov, &M->d_nr, &M->d_st};
+    CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)items.size()), dim3(THREADS), args, M->smem,
+                              M->stream));
+    cudaEventRecord(e1, M->stream);
+    M->launches++;
+    std::vector<uint64_t> k(n);
+    std::vector<uint8_t> o(n), r(n);
+    std::vector<int32_t> s(n);
+    CUDA_TRY(cudaMemcpyAsync(k.data(), M->d_key, n * 8, cudaMemcpyDeviceToHost, M->stream));
+    CUDA_TRY(cudaMemcpyAsync(o.data(), M->d_ov, n, cudaMemcpyDeviceToHost, M->stream));
+    CUDA_TRY(cudaMemcpyAsync(r.data(), M->d_nr, n, cudaMemcpyDeviceToHost, M->stream));
+    CUDA_TRY(cudaMemcpyAsync(s.data(), M->d_st, n * 4, cudaMemcpyDeviceToHost, M->stream));
+    CUDA_TRY(cudaStreamSynchronize(M->stream));
+    cudaEventElapsedTime(&M->last_ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (int64_t j = 0; j < n; ++j) {
+        const int64_t i = order[j];
+        key[i] = k[j];
+        ov[i] = o[j];
+        nr[i] = r[j];
+        st[i] = s[j];
+    }
+    return TCG_OK;
+}
+
+double tcg_multi_last_ms(const tcg_multi *M) { return M ? (double)M->last_ms : -1.0; }
 
 }  // extern "C"

@@ -15,7 +15,7 @@ from conftest import ROOT
 def _declared():
     with open(os.path.join(ROOT, "include", "tcg.h")) as fh:
         text = fh.read()
-    decl = r"^(?:int|int64_t|const char \*)\s*\*?\s*(tcg_[a-z_0-9]+)\s*\("
+    decl = r"^(?:int|int64_t|double|const char \*)\s*\*?\s*(tcg_[a-z_0-9]+)\s*\("
     return sorted(set(re.findall(decl, text, flags=re.M)))
 
 

@@ -240,3 +240,52 @@ def test_report_bytes_identical_across_call_shapes(api):
                 + histogram_csv(api.sweep(T, classifier=c))
                 for w, cs in ((1, 65536), (2, 111), (8, 4096))}
         assert len(outs) == 1
+
+
+def test_multi_triangulation_batch_matches_oracle(api):
+    """Config C4 through MultiClassifier: one launch, one topology per CTA."""
+    import random as _random
+
+    from oracle import oracle as O
+    from paper_2604_09221_b200.diamond import plan_arrays, reflect
+    from paper_2604_09221_b200.lifting import random_unimodular
+
+    rng = _random.Random(0xB7)
+    Ts = [random_unimodular(7, rng) for _ in range(48)]
+    Ts += [tri_from_fixture(triangulations()[f"c4-7-{k}"]) for k in range(16)]
+    mc = api.MultiClassifier(Ts)
+    g = np.random.default_rng(4)
+    n = 1 << 16
+    tri = g.integers(0, len(Ts), size=n).astype(np.int32)
+    words = g.integers(0, 1 << 36, size=n, dtype=np.uint64)
+    keys, ov, nr, st = mc.classify_words(tri, words)
+    assert (st == 0).all()
+    for t in range(len(Ts)):
+        sel = np.nonzero(tri == t)[0][:64]
+        ref = O.classify_words(O.OraclePlan.from_arrays(plan_arrays(reflect(Ts[t]))), words[sel])
+        for i, (s, scheme, o, r) in zip(sel, ref):
+            assert api.scheme_from_key(int(keys[i]), True) == scheme
+            assert (int(ov[i]), int(nr[i])) == (o, r)
+    pairs = [(int(tri[i]), "".join(str((int(words[i]) >> k) & 1) for k in range(36)))
+             for i in range(200)]
+    res = mc.classify_pairs(pairs)
+    assert [r.scheme for r in res] == [api.scheme_from_key(int(keys[i]), True)
+                                       for i in range(200)]
+
+
+def test_cli_reports_byte_identical_to_reference(api, tmp_path, capsys):
+    from paper_2604_09221_b200.cli import main
+
+    g = golden("reports.json")["sweep-delaunay-4-raw"]
+    out, hist = tmp_path / "r.jsonl", tmp_path / "h.csv"
+    code = main(["sweep", "--builtin", "delaunay-4", "--raw-sign-space", "--output", str(out),
+                 "--histogram", str(hist)])
+    assert code == 0
+    assert out.read_text() == g["jsonl"] and hist.read_text() == g["csv"]
+    code = main(["classify", "--builtin", "delaunay-2", "000000", "--json"])
+    assert code == 0
+    assert '"scheme": "<1>"' in capsys.readouterr().out
+    s = golden("reports.json")["sample-delaunay-4-5000-42"]
+    code = main(["sample", "--builtin", "delaunay-4", "-n", "5000", "--seed", "42",
+                 "--output", str(out), "--histogram", str(hist)])
+    assert code == 0 and out.read_text() == s["jsonl"] and hist.read_text() == s["csv"]
