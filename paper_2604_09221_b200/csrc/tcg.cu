@@ -609,10 +609,10 @@ __device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__r
         bd[k] = p.bd[k];
     }
     Regions<K> rg;
-#ifdef TCG_FLAT_LAYERS
-    region_pass<K, EVEN, false>(adj, SG, used, bd, p.nused, rg);
-#else
+#ifdef TCG_FLAT_NODES  // layer-free variant: faster on bowtie8, slower on delaunay-8
     flat_node_pass<K, EVEN>(adj, SG, used, bd, p.nused, rg);
+#else
+    region_pass<K, EVEN, false>(adj, SG, used, bd, p.nused, rg);
 #endif
     return finish<K, EVEN, true>(p, SG, rg, p.maxreg);
 }
