@@ -166,6 +166,19 @@ int tcg_multi_classify(tcg_multi *m, const int32_t *tri, const uint64_t *sigma, 
                        uint64_t *key, uint8_t *ovals, uint8_t *nreg, int32_t *status);
 double tcg_multi_last_ms(const tcg_multi *m);
 
+/* Any degree (d > 9 included) for single patchworks and batches; sweeps and
+ * samples stay d <= 9 as in the reference (62-bit index cap, sweep.py:32).
+ * One CTA per patchwork.  sigma_rows: n rows of ceil(npts/64) uint64 words
+ * (bit k of a row = sign of point k).  Outputs: status[n], nreg[n] and, for
+ * status 0, the rooted region tree as parent[n][maxreg] (parent[t][r] of
+ * region r; the root is its own parent); the scheme is rendered on the host
+ * (ovals = nreg - 1). */
+typedef struct tcg_large tcg_large;
+int tcg_large_create(const tcg_desc *desc, int device, tcg_large **out);
+int tcg_large_destroy(tcg_large *g);
+int tcg_large_classify(tcg_large *g, const uint64_t *sigma_rows, int64_t n, int32_t *status,
+                       int32_t *nreg, int32_t *parent);
+
 /* Diagnostics. */
 const char *tcg_last_error(void);
 int tcg_device_count(void);

@@ -74,6 +74,9 @@ def lib():
         L.orc_classify_words.argtypes = [C.POINTER(_Plan), C.c_void_p, C.c_int64, C.c_void_p,
                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                          C.c_int32]
+        L.orc_classify_rows.argtypes = [C.POINTER(_Plan), C.c_void_p, C.c_int32, C.c_int64,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_int32]
         L.orc_splitmix64.argtypes = [C.c_uint64, C.c_uint64]
         L.orc_splitmix64.restype = C.c_uint64
         _lib = L
@@ -127,6 +130,27 @@ def classify_words(plan: OraclePlan, words):
         s = bytes(buf[t * width: t * width + sl[t]]).decode() if st[t] == 0 else None
         out.append((int(st[t]), s, int(ov[t]), int(nr[t])))
     return out
+
+
+def classify_bitstrings(plan: OraclePlan, bitstrings):
+    """Any degree: [(status, scheme|None, ovals, nreg)] for '0'/'1' strings."""
+    words = (plan.npts + 63) // 64
+    n = len(bitstrings)
+    rows = np.zeros((n, words), np.uint64)
+    for t, s in enumerate(bitstrings):
+        for k, ch in enumerate(s):
+            if ch == "1":
+                rows[t, k >> 6] |= np.uint64(1) << np.uint64(k & 63)
+    st = np.zeros(n, np.int32)
+    ov = np.zeros(n, np.int32)
+    nr = np.zeros(n, np.int32)
+    sl = np.zeros(n, np.int32)
+    width = 4096
+    buf = np.zeros(n * width, np.uint8)
+    lib().orc_classify_rows(C.byref(plan.c), rows.ctypes.data, words, n, st.ctypes.data,
+                            ov.ctypes.data, nr.ctypes.data, sl.ctypes.data, buf.ctypes.data, width)
+    return [(int(st[t]), bytes(buf[t * width: t * width + sl[t]]).decode() if st[t] == 0 else None,
+             int(ov[t]), int(nr[t])) for t in range(n)]
 
 
 def _run(fn, plan, *args, cap=1 << 16):

@@ -90,6 +90,10 @@ def load():
                                          C.c_void_p, C.c_void_p, C.c_void_p]
         L.tcg_multi_last_ms.argtypes = [P]
         L.tcg_multi_last_ms.restype = C.c_double
+        L.tcg_large_create.argtypes = [C.POINTER(TcgDesc), C.c_int, C.POINTER(P)]
+        L.tcg_large_destroy.argtypes = [P]
+        L.tcg_large_classify.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                         C.c_void_p]
         _lib = L
         return L
 
@@ -101,7 +105,8 @@ EXPORTS = (
     "tcg_agg_reset", "tcg_sweep_async", "tcg_sample_async", "tcg_agg_fetch",
     "tcg_sweep_multi", "tcg_sample_multi", "tcg_last_error", "tcg_device_count",
     "tcg_launch_count", "tcg_version", "tcg_multi_create", "tcg_multi_destroy",
-    "tcg_multi_classify", "tcg_multi_last_ms",
+    "tcg_multi_classify", "tcg_multi_last_ms", "tcg_large_create", "tcg_large_destroy",
+    "tcg_large_classify",
 )
 
 
@@ -210,6 +215,46 @@ class NativeMulti:
 
     def last_ms(self) -> float:
         return float(self._L.tcg_multi_last_ms(self.h))
+
+
+class NativeLarge:
+    """Owns one tcg_large (any degree; one CTA per patchwork)."""
+
+    def __init__(self, arrays, device: int | None = None):
+        L = load()
+        if L.tcg_device_count() < 1:
+            raise DeviceUnavailable("no CUDA device visible; the classifier has no CPU fallback")
+        self._keep = []
+        desc = _desc(arrays, self._keep)
+        h = C.c_void_p()
+        _check(L.tcg_large_create(C.byref(desc), -1 if device is None else int(device),
+                                  C.byref(h)), "tcg_large_create")
+        self.h = h
+        self._L = L
+        self.maxreg = int(arrays.maxreg)
+        self.words = (int(arrays.npts) + 63) // 64
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            try:
+                self._L.tcg_large_destroy(h)
+            except Exception:
+                pass
+            self.h = None
+
+    def classify_rows(self, rows):
+        """rows: uint64 [n, words] sign bit rows -> (status, nreg, parent [n, maxreg])."""
+        r = np.ascontiguousarray(rows, dtype=np.uint64).reshape(-1, self.words)
+        n = r.shape[0]
+        st = np.zeros(n, np.int32)
+        nr = np.zeros(n, np.int32)
+        par = np.full((n, self.maxreg), -1, np.int32)
+        if n:
+            _check(self._L.tcg_large_classify(self.h, r.ctypes.data, n, st.ctypes.data,
+                                              nr.ctypes.data, par.ctypes.data),
+                   "tcg_large_classify")
+        return st, nr, par
 
 
 class NativePlan:

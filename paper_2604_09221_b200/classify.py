@@ -20,9 +20,9 @@ import numpy as np
 
 from . import _lib
 from .diamond import plan_arrays, reflect
-from .errors import InvariantViolation, ParseError
+from .errors import BudgetExceeded, InvariantViolation, ParseError
 from .lattice import harnack_bound, num_points, validate_triangulation
-from .scheme import scheme_from_key
+from .scheme import scheme_from_key, scheme_from_parents
 from .signs import SignDistribution, free_positions
 
 STATUS_MESSAGES = {
@@ -58,10 +58,19 @@ class ClassificationResult:
         }
 
 
-class Classifier:
-    """Reusable classification state for one triangulation, resident on one GPU."""
+LAYOUT_MAX_DEGREE = 9  # the bit-mask kernels; larger degrees use the generic kernel
 
-    def __init__(self, T, device: int | None = None):
+
+class Classifier:
+    """Reusable classification state for one triangulation, resident on one GPU.
+
+    Degrees up to 9 use the bit-mask kernels (sweeps, samples, batches);
+    larger degrees -- or ``engine="generic"`` -- use the any-degree kernel
+    (one CTA per patchwork), for single patchworks and batches, as the
+    reference supports (sweeps are capped at d <= 9 there too).
+    """
+
+    def __init__(self, T, device: int | None = None, engine: str = "auto"):
         self.triangulation = T
         d = int(T.degree)
         self.degree = d
@@ -75,8 +84,17 @@ class Classifier:
             rep_pos[k] = pos
         self._rep_bitpos = rep_pos
         self._raw_bitpos = np.arange(npts, dtype=np.int64)
-        self.native = _lib.NativePlan(self.arrays, device)
-        self.device = self.native.info["device"]
+        if engine not in ("auto", "generic", "mask"):
+            raise ParseError(f"unknown engine {engine!r}")
+        self.generic = engine == "generic" or (engine == "auto" and d > LAYOUT_MAX_DEGREE)
+        if self.generic:
+            self.native = None
+            self.large = _lib.NativeLarge(self.arrays, device)
+            self.device = device if device is not None else 0
+        else:
+            self.large = None
+            self.native = _lib.NativePlan(self.arrays, device)
+            self.device = self.native.info["device"]
 
     # reference-shaped accessors -------------------------------------------
     def plan(self, raw_space: bool = False):
@@ -101,17 +119,45 @@ class Classifier:
             has_pseudoline=self.degree % 2 == 1,
         )
 
+    def _generic_rows(self, bit_lists) -> list[ClassificationResult]:
+        words = (num_points(self.degree) + 63) // 64
+        rows = np.zeros((len(bit_lists), words), np.uint64)
+        for t, bits in enumerate(bit_lists):
+            b = np.asarray(bits, dtype=np.uint64)
+            for w in range(words):
+                chunk = b[64 * w: 64 * w + 64]
+                rows[t, w] = np.bitwise_or.reduce(chunk << np.arange(len(chunk), dtype=np.uint64))
+        st, nr, par = self.large.classify_rows(rows)
+        out = []
+        odd = self.degree % 2 == 1
+        for t in range(len(bit_lists)):
+            if st[t] != 0:
+                raise InvariantViolation(STATUS_MESSAGES.get(int(st[t]), f"status {st[t]}")
+                                         + (f" (at batch position {t})" if len(bit_lists) > 1
+                                            else ""))
+            n = int(nr[t])
+            out.append(ClassificationResult(scheme_from_parents(par[t], n, odd), n - 1, n, odd))
+        return out
+
     def _run_bits(self, bits) -> ClassificationResult:
+        if self.generic:
+            return self._generic_rows([bits])[0]
         b = np.asarray(bits, dtype=np.uint64)
         word = int(np.bitwise_or.reduce(b << np.arange(len(b), dtype=np.uint64))) if len(b) else 0
         key, ov, nr, st = self.native.classify_words(np.array([word], np.uint64))
         return self._result(key[0], ov[0], nr[0], st[0])
 
+    def _sigma(self, s):
+        if isinstance(s, str):
+            s = SignDistribution.from_bitstring(self.degree, s)
+        if s.degree != self.degree:
+            raise ParseError(f"sign degree {s.degree} != triangulation degree {self.degree}")
+        return s
+
     def classify(self, sigma) -> ClassificationResult:
-        if isinstance(sigma, str):
-            sigma = SignDistribution.from_bitstring(self.degree, sigma)
-        if sigma.degree != self.degree:
-            raise ParseError(f"sign degree {sigma.degree} != triangulation degree {self.degree}")
+        sigma = self._sigma(sigma)
+        if self.generic:
+            return self._generic_rows([sigma.bits])[0]
         word = 0
         for k, b in enumerate(sigma.bits):
             word |= int(b) << k
@@ -119,16 +165,17 @@ class Classifier:
         return self._result(key[0], ov[0], nr[0], st[0])
 
     def classify_words(self, words):
-        """Batched raw form: uint64 sign words -> (keys, ovals, nreg, status) arrays."""
+        """Batched raw form: uint64 sign words -> (keys, ovals, nreg, status) arrays (d <= 9)."""
+        if self.generic:
+            raise BudgetExceeded("uint64 sign words need d <= 9; use classify_many")
         return self.native.classify_words(words)
 
     def classify_many(self, sigmas) -> list[ClassificationResult]:
+        sig = [self._sigma(s) for s in sigmas]
+        if self.generic:
+            return self._generic_rows([s.bits for s in sig]) if sig else []
         words = []
-        for s in sigmas:
-            if isinstance(s, str):
-                s = SignDistribution.from_bitstring(self.degree, s)
-            if s.degree != self.degree:
-                raise ParseError(f"sign degree {s.degree} != triangulation degree {self.degree}")
+        for s in sig:
             w = 0
             for k, b in enumerate(s.bits):
                 w |= int(b) << k

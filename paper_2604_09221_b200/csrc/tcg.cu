@@ -1013,6 +1013,62 @@ __device__ __forceinline__ void node_pass(const uint4 *__restrict__ rows, uint32
     out.oddmask = oddmask;
 }
 
+// node_pass for contracted graphs of at most 32 nodes: one 32-bit word per set.
+template <bool EVEN>
+__device__ __forceinline__ void node_pass1(const uint4 *__restrict__ rows, uint32_t sg,
+                                           uint32_t used, int nn, Regions<1> &out) {
+    uint32_t un = used, f = 0, x = 0, q = 0, r = 0;
+    bool odd = false;
+    int nreg = 0;
+    uint32_t oddmask = 0;
+    auto seed = [&]() {
+        f = un & (0u - un);
+        r = un;
+        un ^= f;
+        x = 0u;
+        if (EVEN) q = 0u;
+        odd = false;
+    };
+    auto close = [&]() {
+        if (nreg < MAXR) {
+            out.R[nreg][0] = r ^ un;
+            out.X[nreg][0] = x;
+            if (EVEN && odd) oddmask |= 1u << nreg;
+        }
+        ++nreg;
+    };
+    seed();
+    for (int it = 0; it < nn; ++it) {
+        if (f == 0u) {
+            close();
+            seed();
+        }
+        const int v = __ffs(f) - 1;
+        f &= f - 1u;
+        const uint4 row = rows[v];
+        const uint32_t sv = (uint32_t)((int32_t)(sg << (31 - v)) >> 31);
+        const uint32_t o = sg ^ sv;  // nodes of the other sign
+        x |= row.x & o;
+        if (EVEN) {
+            const uint32_t pv = (uint32_t)((int32_t)(q << (31 - v)) >> 31);
+            const uint32_t te = row.x & ~o, nt = te & un, np = row.z & un;
+            const uint32_t eq = ~(q ^ pv);
+            odd |= ((nt & np) | (te & ~un & ~eq) | (row.z & ~un & eq)) != 0u;
+            q |= (nt & pv) | (np & ~pv);
+            const uint32_t n = nt | np;
+            un ^= n;
+            f |= n;
+        } else {
+            const uint32_t n = ((row.x & ~o) | row.z) & un;
+            un ^= n;
+            f |= n;
+        }
+    }
+    close();
+    out.nreg = nreg;
+    out.oddmask = oddmask;
+}
+
 template <bool EVEN>
 __device__ __forceinline__ Result classify_tile(const KParams &p, const TileTables &tt,
                                                 const uint4 *rows,
@@ -1022,6 +1078,12 @@ __device__ __forceinline__ Result classify_tile(const KParams &p, const TileTabl
     const unsigned long long fs = tt.fsign[0][low & 63u] ^ tt.fsign[1][(low >> 6) & 63u];
     const unsigned long long sg = sgn_fixed | (fs << n);
     const unsigned long long used = nn >= 64 ? ~0ull : ((1ull << nn) - 1ull);
+    if (nn <= 32) {  // tile-uniform: a warp owns the tile
+        Regions<1> r1;
+        node_pass1<EVEN>(rows, (uint32_t)sg, (uint32_t)used, nn, r1);
+        const uint32_t SG1[1] = {(uint32_t)sg};
+        return finish<1, EVEN, false>(p, SG1, r1, p.maxreg);
+    }
     Regions<2> rg;
     node_pass<EVEN>(rows, (uint32_t)sg, (uint32_t)(sg >> 32), (uint32_t)used,
                     (uint32_t)(used >> 32), nn, rg);
@@ -1048,6 +1110,88 @@ __global__ void __launch_bounds__(32 * BUILD_WARPS) k_tile_build(KParams p,
     const int w = threadIdx.x >> 5;
     for (uint32_t t = blockIdx.x * BUILD_WARPS + w; t < ntiles; t += gridDim.x * BUILD_WARPS)
         build_tile<K, MODE>(p, *tt, (tile0 + t) << tt->bits, adj_s, comps[w], recs + t);
+}
+
+// Contract tiles one per LANE (no redundant SIMT work): each thread runs the
+// COMPS-mode region pass for its own tile and writes its node rows.
+template <int K, int MODE>
+__global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
+                                                              const TileTables *__restrict__ tt_g,
+                                                              uint64_t tile0, uint32_t ntiles,
+                                                              TileRec *__restrict__ recs) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *adj_s = smem;
+    TileTables *tt = reinterpret_cast<TileTables *>(smem + 32 * K * K);
+    stage_adj<K>(p, adj_s);
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    __syncthreads();
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const uint64_t base = (tile0 + t) << tt->bits;
+    const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, base) : base;
+    uint32_t SG[K], fixed[K], zero[K];
+    sign_words<K>(p, sigma, SG);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        fixed[k] = tt->fixed[k];
+        zero[k] = 0u;
+    }
+    Regions<K, MAXC> comps;
+    region_pass<K, false, false, true, MAXC>(adj_s, SG, fixed, zero, tt->nfixed, comps);
+    const int n = comps.nreg, nf = tt->nf, nn = n + nf;
+    TileRec *rec = recs + t;
+    const bool fits = n <= MAXC && nn <= 64;
+    unsigned long long sbits = 0;
+    if (fits) {
+        unsigned long long fadj_c[MAXF];  // free node f -> comps adjacent to it
+        for (int f = 0; f < nf; ++f) fadj_c[f] = 0ull;
+        for (int c = 0; c < n; ++c) {
+            uint32_t X[K], R[K], P[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                X[k] = comps.X[c][k];
+                R[k] = comps.R[c][k];
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int ks = (k + K / 2) % K;
+                P[k] = R[ks] & p.bd[ks];
+            }
+            unsigned long long adj = 0, pl = 0;
+            for (int c2 = 0; c2 < n; ++c2) {
+                uint32_t a = 0, q = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    a |= X[k] & comps.R[c2][k];
+                    q |= P[k] & comps.R[c2][k];
+                }
+                if (a && c2 != c) adj |= 1ull << c2;
+                if (q) pl |= 1ull << c2;
+            }
+            for (int f = 0; f < nf; ++f)
+                if (sel<K>(X, tt->fword[f]) & tt->fbit[f]) {
+                    adj |= 1ull << (n + f);
+                    fadj_c[f] |= 1ull << c;
+                }
+            uint32_t sg = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) sg |= R[k] & SG[k];
+            if (sg) sbits |= 1ull << c;
+            rec->rows[c] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
+                                      (uint32_t)(pl >> 32));
+        }
+        for (int f = 0; f < nf; ++f) {
+            const unsigned long long adj = (tt->fadj[f] << n) | fadj_c[f];
+            const unsigned long long pl = tt->fpl[f] << n;
+            rec->rows[n + f] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
+                                          (uint32_t)(pl >> 32));
+        }
+    }
+    rec->sgn_fixed = sbits;
+    rec->n = n;
+    rec->nnodes = nn;
+    rec->fallback = fits ? 0 : 1;
 }
 
 // Classify every index of [start, end) that falls in tiles tile0 .. tile0+ntiles-1.
@@ -1107,6 +1251,258 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
     }
     __syncthreads();
     tab.flush(g);
+}
+
+// ------------------------------------------------------------ any degree
+// Generic path for degrees the bit-mask layout does not cover (d > 9; any d
+// works): one CTA per patchwork, state in shared memory, vertex numbering
+// and edge order exactly the reference's.  Components by a lock-free
+// union-find over the non-crossed edges (CAS hooking of the larger root onto
+// the smaller, path halving); the parity union-find over the 2d antipodal
+// pairs, region ids, odd flags and any status collision are replayed by one
+// thread in the reference's order (kernels.py:151-230); the crossed-edge
+// region pairs are deduplicated in a shared hash set; the rooted tree comes
+// back as a parent array for the host to render.
+struct LargeParams {
+    int d, nv, ne, nap, npts, maxreg, words;  // words = u64 per sign row
+    const int32_t *eu, *ev, *src, *apu, *apv;
+    const uint8_t *par, *used;
+};
+
+constexpr int LHASH = 8192;  // region-pair hash set (pairs <= maxreg - 1 on valid input)
+
+__device__ __forceinline__ int lfind(int *p, int x) {
+    while (true) {
+        const int px = p[x];
+        if (px == x) return x;
+        const int ppx = p[px];
+        if (ppx != px) p[x] = ppx;  // path halving (benign race: only shortens paths)
+        x = px;
+    }
+}
+
+__device__ int lfind2(int *p2, uint8_t *par2, int x, int &parity) {
+    int root = x, pp = 0;
+    while (p2[root] != root) {
+        pp ^= par2[root];
+        root = p2[root];
+    }
+    int v = x, acc = pp;
+    while (p2[v] != v) {
+        const int nxt = p2[v];
+        const int step = par2[v];
+        p2[v] = root;
+        par2[v] = (uint8_t)acc;
+        acc ^= step;
+        v = nxt;
+    }
+    parity = pp;
+    return root;
+}
+
+// insert (a, b) into the pair set; returns true if it was new
+__device__ __forceinline__ bool pair_insert(uint32_t *hs, uint32_t key) {
+    uint32_t h = (key * 2654435761u) & (LHASH - 1);
+    for (int probe = 0; probe < LHASH; ++probe) {
+        const uint32_t prev = atomicCAS(&hs[h], 0xffffffffu, key);
+        if (prev == 0xffffffffu) return true;
+        if (prev == key) return false;
+        h = (h + 1) & (LHASH - 1);
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(THREADS) k_large(LargeParams P, const uint64_t *__restrict__ sig,
+                                                   int64_t n, int32_t *__restrict__ status,
+                                                   int32_t *__restrict__ nreg_out,
+                                                   int32_t *__restrict__ parent_out) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int nv = P.nv;
+    int *p1 = reinterpret_cast<int *>(smem);       // [nv] component union-find
+    int *rid = p1 + nv;                            // [nv] region id per vertex
+    int *p2 = rid + nv;                            // [nv] parity union-find (by vertex id)
+    uint32_t *hs = reinterpret_cast<uint32_t *>(p2 + nv);  // [LHASH]
+    int *deg = reinterpret_cast<int *>(hs + LHASH);        // [maxreg + 1] CSR offsets
+    int *adjl = deg + P.maxreg + 1;                        // [2 * maxreg]
+    int *bfs = adjl + 2 * P.maxreg;                        // [maxreg]
+    int *rpar = bfs + P.maxreg;                            // [maxreg]
+    uint8_t *sg = reinterpret_cast<uint8_t *>(rpar + P.maxreg);  // [nv]
+    uint8_t *par2 = sg + nv;                                     // [nv]
+    uint8_t *odd2 = par2 + nv;                                   // [nv]
+    __shared__ int s_nreg, s_status, s_root, s_nedges, s_selfm, s_self1, s_self2;
+    for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+        const uint64_t *row = sig + t * P.words;
+        for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+            const int k = P.src[v];
+            sg[v] = (uint8_t)(((row[k >> 6] >> (k & 63)) & 1ull) ^ P.par[v]);
+            p1[v] = v;
+            p2[v] = v;
+            par2[v] = 0;
+            odd2[v] = 0;
+        }
+        for (int i = threadIdx.x; i < LHASH; i += blockDim.x) hs[i] = 0xffffffffu;
+        __syncthreads();
+        for (int e = threadIdx.x; e < P.ne; e += blockDim.x) {
+            int u = P.eu[e], v = P.ev[e];
+            if (sg[u] != sg[v]) continue;
+            while (true) {
+                u = lfind(p1, u);
+                v = lfind(p1, v);
+                if (u == v) break;
+                if (u < v) { const int tmp = u; u = v; v = tmp; }
+                if (atomicCAS(&p1[u], u, v) == u) break;
+            }
+        }
+        __syncthreads();
+        for (int v = threadIdx.x; v < nv; v += blockDim.x) p1[v] = lfind(p1, v);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            // parity union-find over the antipodal pairs (components named by root vertex)
+            for (int a = 0; a < P.nap; ++a) {
+                const int cu = p1[P.apu[a]], cv = p1[P.apv[a]];
+                int pu, pv;
+                int ru = lfind2(p2, par2, cu, pu), rv = lfind2(p2, par2, cv, pv);
+                if (ru == rv) {
+                    if (pu == pv) odd2[ru] = 1;
+                } else {
+                    // deterministic: hook the larger root onto the smaller
+                    if (ru > rv) { const int tmp = ru; ru = rv; rv = tmp; const int tp = pu; pu = pv; pv = tp; }
+                    p2[rv] = ru;
+                    par2[rv] = (uint8_t)(pu ^ pv ^ 1);
+                    if (odd2[rv]) odd2[ru] = 1;
+                }
+            }
+            // dense region ids in vertex order (the reference's first-occurrence order)
+            int nreg = 0, nodd = 0, oddr = -1, st = TCG_OK;
+            for (int v = 0; v < nv; ++v) {
+                if (!P.used[v] || p1[v] != v) continue;
+                int pp;
+                const int r = lfind2(p2, par2, v, pp);
+                if (r == v) {
+                    if (nreg >= P.maxreg) { st = TCG_TOO_MANY_REGIONS; break; }
+                    rid[v] = nreg;
+                    if (odd2[v]) { ++nodd; oddr = nreg; }
+                    ++nreg;
+                }
+            }
+            if (st == TCG_OK) {
+                for (int v = 0; v < nv; ++v) {
+                    if (!P.used[v] || p1[v] != v) continue;
+                    int pp;
+                    const int r = lfind2(p2, par2, v, pp);
+                    rid[v] = rid[r];
+                }
+            }
+            if (st == TCG_OK && P.d % 2 == 0) {
+                if (nodd == 0) st = TCG_NO_ODD_REGION;
+                else if (nodd > 1) st = TCG_MANY_ODD_REGIONS;
+            }
+            s_nreg = nreg;
+            s_status = st;
+            s_root = P.d % 2 == 0 ? oddr : -1;
+            s_nedges = 0;
+            s_selfm = 0;
+            s_self1 = -1;
+            s_self2 = -1;
+        }
+        __syncthreads();
+        for (int v = threadIdx.x; v < nv; v += blockDim.x)
+            if (P.used[v]) rid[v] = rid[p1[v]];
+        __syncthreads();
+        if (s_status == TCG_OK) {
+            for (int e = threadIdx.x; e < P.ne; e += blockDim.x) {
+                const int u = P.eu[e], v = P.ev[e];
+                if (sg[u] == sg[v]) continue;
+                int a = rid[u], b = rid[v];
+                if (a == b) {
+                    atomicAdd(&s_selfm, 1);
+                    if (atomicCAS(&s_self1, -1, a) != -1 && s_self1 != a) atomicExch(&s_self2, a);
+                    continue;
+                }
+                if (a > b) { const int tmp = a; a = b; b = tmp; }
+                if (pair_insert(hs, ((uint32_t)a << 16) | (uint32_t)b)) atomicAdd(&s_nedges, 1);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && s_status == TCG_OK) {
+            const int nreg = s_nreg;
+            const bool even = P.d % 2 == 0;
+            const bool toomany = s_nedges > nreg - 1;
+            const bool anomaly = toomany || (even && s_selfm) || (!even && s_self2 >= 0);
+            int st = TCG_OK, root = s_root;
+            if (anomaly) {
+                // exact replay in the reference's edge order (kernels.py:199-230)
+                for (int i = 0; i < LHASH; ++i) hs[i] = 0xffffffffu;
+                int ne2 = 0;
+                root = even ? s_root : -1;
+                for (int e = 0; e < P.ne && st == TCG_OK; ++e) {
+                    const int u = P.eu[e], v = P.ev[e];
+                    if (sg[u] == sg[v]) continue;
+                    int a = rid[u], b = rid[v];
+                    if (a == b) {
+                        if (even) st = TCG_NONSEPARATING_OVAL;
+                        else if (root < 0) root = a;
+                        else if (root != a) st = TCG_ROOT_CONFLICT;
+                        continue;
+                    }
+                    if (a > b) { const int tmp = a; a = b; b = tmp; }
+                    if (pair_insert(hs, ((uint32_t)a << 16) | (uint32_t)b)) {
+                        if (ne2 >= nreg - 1) st = TCG_NOT_A_TREE;
+                        ++ne2;
+                    }
+                }
+                if (st == TCG_OK) st = TCG_NOT_A_TREE;  // unreachable for anomalous inputs
+            } else if (!even) {
+                if (s_self1 < 0) st = TCG_NO_PSEUDOLINE;
+                root = s_self1;
+            }
+            if (st == TCG_OK && s_nedges != nreg - 1) st = TCG_NOT_A_TREE;
+            if (st == TCG_OK) {
+                // CSR over the deduplicated pairs, BFS from the root
+                for (int r = 0; r <= nreg; ++r) deg[r] = 0;
+                for (int i = 0; i < LHASH; ++i) {
+                    const uint32_t k = hs[i];
+                    if (k == 0xffffffffu) continue;
+                    deg[(k >> 16) + 1]++;
+                    deg[(k & 0xffff) + 1]++;
+                }
+                for (int r = 0; r < nreg; ++r) deg[r + 1] += deg[r];
+                for (int r = 0; r < nreg; ++r) rpar[r] = deg[r];
+                for (int i = 0; i < LHASH; ++i) {
+                    const uint32_t k = hs[i];
+                    if (k == 0xffffffffu) continue;
+                    const int a = (int)(k >> 16), b = (int)(k & 0xffff);
+                    adjl[rpar[a]++] = b;
+                    adjl[rpar[b]++] = a;
+                }
+                for (int r = 0; r < nreg; ++r) rpar[r] = -1;
+                int head = 0, tail = 1;
+                bfs[0] = root;
+                rpar[root] = root;
+                while (head < tail) {
+                    const int r = bfs[head++];
+                    for (int k = deg[r]; k < deg[r + 1]; ++k) {
+                        const int s2 = adjl[k];
+                        if (rpar[s2] < 0) {
+                            rpar[s2] = r;
+                            bfs[tail++] = s2;
+                        }
+                    }
+                }
+                if (tail != nreg) st = TCG_DISCONNECTED;
+            }
+            s_status = st;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            status[t] = s_status;
+            nreg_out[t] = s_nreg;
+        }
+        if (s_status == TCG_OK)
+            for (int r = threadIdx.x; r < s_nreg; r += blockDim.x)
+                parent_out[t * P.maxreg + r] = rpar[r];
+        __syncthreads();
+    }
 }
 
 __global__ void k_agg_clear(DevAgg g) {
@@ -1169,6 +1565,12 @@ struct tcg_plan {
     uint8_t *d_ov = nullptr, *d_nr = nullptr;
     int32_t *d_st = nullptr;
     int64_t batch_cap = 0;
+    // pinned double-buffered staging for host-buffer batches
+    bool stage_ok = false;
+    uint64_t *h_in[2] = {}, *h_key[2] = {}, *sd_in[2] = {}, *sd_key[2] = {};
+    uint8_t *h_ov[2] = {}, *h_nr[2] = {}, *sd_ov[2] = {}, *sd_nr[2] = {};
+    int32_t *h_st[2] = {}, *sd_st[2] = {};
+    cudaStream_t sst[2] = {nullptr, nullptr};
     cudaStream_t own = nullptr, stream = nullptr;
     int64_t launches = 0;
     // tile contraction (sweeps): per domain (raw, representative)
@@ -1205,19 +1607,19 @@ struct DeviceGuard {
 
 // Per-kernel timing: events bracket each launch on the plan's stream and are
 // resolved after the next synchronisation (tcg_agg_fetch / tcg_kernel_times).
-cudaEvent_t timing_begin(tcg_plan *P) {
+cudaEvent_t timing_begin(tcg_plan *P, cudaStream_t st = nullptr) {
     if (!P->timing) return nullptr;
     cudaEvent_t a;
     cudaEventCreate(&a);
-    cudaEventRecord(a, P->stream);
+    cudaEventRecord(a, st ? st : P->stream);
     return a;
 }
 
-void timing_end(tcg_plan *P, int kind, cudaEvent_t a) {
+void timing_end(tcg_plan *P, int kind, cudaEvent_t a, cudaStream_t st = nullptr) {
     if (!P->timing || !a) return;
     cudaEvent_t b;
     cudaEventCreate(&b);
-    cudaEventRecord(b, P->stream);
+    cudaEventRecord(b, st ? st : P->stream);
     P->tev.push_back({kind, {a, b}});
 }
 
@@ -1251,8 +1653,13 @@ void *pick_enum(int K, bool even, int mode) {
 
 template <int K>
 void *build_fn(int mode) {
-    return mode == MODE_RAW ? (void *)k_tile_build<K, MODE_RAW> : (void *)k_tile_build<K, MODE_REP>;
+    if (std::getenv("TCG_BUILD_WARP"))
+        return mode == MODE_RAW ? (void *)k_tile_build<K, MODE_RAW> : (void *)k_tile_build<K, MODE_REP>;
+    return mode == MODE_RAW ? (void *)k_tile_build_lanes<K, MODE_RAW>
+                            : (void *)k_tile_build_lanes<K, MODE_REP>;
 }
+
+bool build_per_warp() { return std::getenv("TCG_BUILD_WARP") != nullptr; }
 
 void *pick_build(int K, int mode) {
     if (K == 2) return build_fn<2>(mode);
@@ -1275,7 +1682,7 @@ void *pick_cls(int K, bool even, int mode) {
 size_t build_smem(int K) {
     const size_t rg = K == 2 ? sizeof(Regions<2, MAXC>)
                              : (K == 4 ? sizeof(Regions<4, MAXC>) : sizeof(Regions<6, MAXC>));
-    return (size_t)32 * K * K * 4 + sizeof(TileTables) + BUILD_WARPS * rg;
+    return (size_t)32 * K * K * 4 + sizeof(TileTables) + (build_per_warp() ? BUILD_WARPS * rg : 0);
 }
 
 size_t cls_smem(int K) {
@@ -1408,13 +1815,21 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
 }
 
 // Tile size: 2^bits indices.  Larger tiles amortise the contraction but add
-// free vertices (lane work); default 2^10, capped so at least 36 of the 64
-// node slots stay for components.  TCG_TILE_BITS overrides.
+// free vertices (lane work); since contraction runs one tile per lane it is
+// cheap, so the default picks the largest tile whose contracted graph
+// (free vertices + the fixed part's components) usually fits one 32-bit
+// word: at most 16 free vertices (d=7 raw: 2^8 indices, the j-axis).
+// Degree 8-9 graphs exceed 32 nodes anyway, so they take 2^10.
+// TCG_TILE_BITS overrides.
 bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
-    int want = 10;
-    if (const char *e = std::getenv("TCG_TILE_BITS")) want = std::atoi(e);
+    int want = D->degree >= 8 ? 10 : 12;
+    int fmax = D->degree >= 8 ? 28 : 16;
+    if (const char *e = std::getenv("TCG_TILE_BITS")) {
+        want = std::atoi(e);
+        fmax = 28;
+    }
     for (int bits = std::min(want, TILE_BITS_MAX); bits >= 6; --bits)
-        if (build_tiles_bits(D, L, mode, bits, T) && T.nf <= 28) return true;
+        if (build_tiles_bits(D, L, mode, bits, T) && T.nf <= fmax) return true;
     return false;
 }
 
@@ -1642,8 +2057,9 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
                                                            THREADS, P->smem_cls)) != cudaSuccess)
         return bail(e, "occupancy");
     P->blocks_cls = std::max(1, bps) * P->nsm;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_build(K, MODE_RAW),
-                                                           32 * BUILD_WARPS, P->smem_build)) != cudaSuccess)
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+             &bps, pick_build(K, MODE_RAW), build_per_warp() ? 32 * BUILD_WARPS : THREADS,
+             P->smem_build)) != cudaSuccess)
         return bail(e, "occupancy");
     P->blocks_build = std::max(1, bps) * P->nsm;
     *out = P;
@@ -1671,6 +2087,15 @@ int tcg_plan_destroy(tcg_plan *P) {
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+    for (int i = 0; i < 2; ++i) {
+        void *hp[] = {P->h_in[i], P->h_key[i], P->h_ov[i], P->h_nr[i], P->h_st[i]};
+        for (void *q : hp)
+            if (q) cudaFreeHost(q);
+        void *dp[] = {P->sd_in[i], P->sd_key[i], P->sd_ov[i], P->sd_nr[i], P->sd_st[i]};
+        for (void *q : dp)
+            if (q) cudaFree(q);
+        if (P->sst[i]) cudaStreamDestroy(P->sst[i]);
+    }
     if (P->own) cudaStreamDestroy(P->own);
     delete P;
     return TCG_OK;
@@ -1712,15 +2137,17 @@ int tcg_plan_info(const tcg_plan *P, int32_t *info, int ninfo) {
 }
 
 static int launch_batch(tcg_plan *P, const uint64_t *d_sig, int64_t n, uint64_t *d_key,
-                        uint8_t *d_ov, uint8_t *d_nr, int32_t *d_st) {
+                        uint8_t *d_ov, uint8_t *d_nr, int32_t *d_st,
+                        cudaStream_t stream = nullptr) {
+    if (!stream) stream = P->stream;
     if (n <= 0) return TCG_OK;
     void *fn = pick_batch(P->K, P->even);
     int64_t blocks = std::min<int64_t>(P->blocks_batch, (n + THREADS - 1) / THREADS);
     void *args[] = {&P->kp, &d_sig, &n, &d_key, &d_ov, &d_nr, &d_st};
-    cudaEvent_t e3 = timing_begin(P);
+    cudaEvent_t e3 = timing_begin(P, stream);
     CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(THREADS), args, P->smem_batch,
-                              P->stream));
-    timing_end(P, 3, e3);
+                              stream));
+    timing_end(P, 3, e3, stream);
     P->launches++;
     return TCG_OK;
 }
@@ -1732,31 +2159,63 @@ int tcg_classify_batch_device(tcg_plan *P, const uint64_t *d_sig, int64_t n, uin
     return launch_batch(P, d_sig, n, d_key, d_ov, d_nr, d_st);
 }
 
+// Host-buffer batches run as a two-stream pipeline over pinned staging
+// buffers: while chunk c is copied in / classified / copied out on one
+// stream, the host moves chunk c-1's results out of the other slot.
+static constexpr int64_t STAGE_CHUNK = 1 << 20;
+
+static int ensure_staging(tcg_plan *P) {
+    if (P->stage_ok) return TCG_OK;
+    for (int i = 0; i < 2; ++i) {
+        CUDA_TRY(cudaHostAlloc(&P->h_in[i], STAGE_CHUNK * 8, cudaHostAllocDefault));
+        CUDA_TRY(cudaHostAlloc(&P->h_key[i], STAGE_CHUNK * 8, cudaHostAllocDefault));
+        CUDA_TRY(cudaHostAlloc(&P->h_ov[i], STAGE_CHUNK, cudaHostAllocDefault));
+        CUDA_TRY(cudaHostAlloc(&P->h_nr[i], STAGE_CHUNK, cudaHostAllocDefault));
+        CUDA_TRY(cudaHostAlloc(&P->h_st[i], STAGE_CHUNK * 4, cudaHostAllocDefault));
+        CUDA_TRY(cudaMalloc(&P->sd_in[i], STAGE_CHUNK * 8));
+        CUDA_TRY(cudaMalloc(&P->sd_key[i], STAGE_CHUNK * 8));
+        CUDA_TRY(cudaMalloc(&P->sd_ov[i], STAGE_CHUNK));
+        CUDA_TRY(cudaMalloc(&P->sd_nr[i], STAGE_CHUNK));
+        CUDA_TRY(cudaMalloc(&P->sd_st[i], STAGE_CHUNK * 4));
+        CUDA_TRY(cudaStreamCreateWithFlags(&P->sst[i], cudaStreamNonBlocking));
+    }
+    P->stage_ok = true;
+    return TCG_OK;
+}
+
 int tcg_classify_batch(tcg_plan *P, const uint64_t *sig, int64_t n, uint64_t *key, uint8_t *ov,
                        uint8_t *nr, int32_t *st) {
     if (!P || (n > 0 && (!sig || !key || !ov || !nr || !st))) return fail(TCG_E_ARG, "null argument");
     if (n <= 0) return TCG_OK;
     DeviceGuard guard(P->device);
-    if (n > P->batch_cap) {
-        cudaFree(P->d_sig); cudaFree(P->d_key); cudaFree(P->d_ov); cudaFree(P->d_nr); cudaFree(P->d_st);
-        P->d_sig = nullptr; P->d_key = nullptr; P->d_ov = nullptr; P->d_nr = nullptr; P->d_st = nullptr;
-        P->batch_cap = 0;
-        int64_t cap = std::max<int64_t>(n, 1 << 16);
-        CUDA_TRY(cudaMalloc(&P->d_sig, cap * 8));
-        CUDA_TRY(cudaMalloc(&P->d_key, cap * 8));
-        CUDA_TRY(cudaMalloc(&P->d_ov, cap));
-        CUDA_TRY(cudaMalloc(&P->d_nr, cap));
-        CUDA_TRY(cudaMalloc(&P->d_st, cap * 4));
-        P->batch_cap = cap;
-    }
-    CUDA_TRY(cudaMemcpyAsync(P->d_sig, sig, n * 8, cudaMemcpyHostToDevice, P->stream));
-    int rc = launch_batch(P, P->d_sig, n, P->d_key, P->d_ov, P->d_nr, P->d_st);
+    int rc = ensure_staging(P);
     if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(key, P->d_key, n * 8, cudaMemcpyDeviceToHost, P->stream));
-    CUDA_TRY(cudaMemcpyAsync(ov, P->d_ov, n, cudaMemcpyDeviceToHost, P->stream));
-    CUDA_TRY(cudaMemcpyAsync(nr, P->d_nr, n, cudaMemcpyDeviceToHost, P->stream));
-    CUDA_TRY(cudaMemcpyAsync(st, P->d_st, n * 4, cudaMemcpyDeviceToHost, P->stream));
-    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    CUDA_TRY(cudaStreamSynchronize(P->stream));  // order after earlier work on the plan
+    const int64_t nch = (n + STAGE_CHUNK - 1) / STAGE_CHUNK;
+    for (int64_t c = 0; c < nch + 2; ++c) {
+        const int sl = (int)(c & 1);
+        if (c >= 2) {  // drain chunk c-2 from this slot
+            const int64_t lo = (c - 2) * STAGE_CHUNK, len = std::min(STAGE_CHUNK, n - lo);
+            CUDA_TRY(cudaStreamSynchronize(P->sst[sl]));
+            std::memcpy(key + lo, P->h_key[sl], len * 8);
+            std::memcpy(ov + lo, P->h_ov[sl], len);
+            std::memcpy(nr + lo, P->h_nr[sl], len);
+            std::memcpy(st + lo, P->h_st[sl], len * 4);
+        }
+        if (c < nch) {
+            const int64_t lo = c * STAGE_CHUNK, len = std::min(STAGE_CHUNK, n - lo);
+            cudaStream_t s = P->sst[sl];
+            std::memcpy(P->h_in[sl], sig + lo, len * 8);
+            CUDA_TRY(cudaMemcpyAsync(P->sd_in[sl], P->h_in[sl], len * 8, cudaMemcpyHostToDevice, s));
+            rc = launch_batch(P, P->sd_in[sl], len, P->sd_key[sl], P->sd_ov[sl], P->sd_nr[sl],
+                              P->sd_st[sl], s);
+            if (rc) return rc;
+            CUDA_TRY(cudaMemcpyAsync(P->h_key[sl], P->sd_key[sl], len * 8, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(P->h_ov[sl], P->sd_ov[sl], len, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(P->h_nr[sl], P->sd_nr[sl], len, cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(P->h_st[sl], P->sd_st[sl], len * 4, cudaMemcpyDeviceToHost, s));
+        }
+    }
     return TCG_OK;
 }
 
@@ -1791,12 +2250,16 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             uint32_t nt = (uint32_t)std::min<uint64_t>(CHUNK_TILES, t_end - t0);
             uint64_t tile0 = t0;
             TileRec *recs = P->d_recs;
-            const unsigned gb = (unsigned)std::min<uint64_t>(
-                P->blocks_build, (nt + BUILD_WARPS - 1) / BUILD_WARPS);
+            const unsigned per_block = build_per_warp() ? BUILD_WARPS : THREADS;
+            const unsigned gb = build_per_warp()
+                                    ? (unsigned)std::min<uint64_t>(P->blocks_build,
+                                                                   (nt + per_block - 1) / per_block)
+                                    : (unsigned)((nt + per_block - 1) / per_block);
             void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs};
             cudaEvent_t e0 = timing_begin(P);
-            CUDA_TRY(cudaLaunchKernel(fb, dim3(gb), dim3(32 * BUILD_WARPS), ab, P->smem_build,
-                                      P->stream));
+            CUDA_TRY(cudaLaunchKernel(fb, dim3(gb), dim3(build_per_warp() ? 32 * BUILD_WARPS
+                                                                           : THREADS),
+                                      ab, P->smem_build, P->stream));
             timing_end(P, 0, e0);
             const unsigned gc = (unsigned)std::min<uint64_t>(P->blocks_cls,
                                                              (nt + CLS_WARPS - 1) / CLS_WARPS);
@@ -2206,5 +2669,154 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
 }
 
 double tcg_multi_last_ms(const tcg_multi *M) { return M ? (double)M->last_ms : -1.0; }
+
+
+// ------------------------------------------------------------ any degree (host)
+struct tcg_large {
+    int device = 0;
+    LargeParams lp{};
+    int32_t *d_i32 = nullptr;  // eu, ev, src, apu, apv
+    uint8_t *d_u8 = nullptr;   // par, used
+    size_t smem = 0;
+    cudaStream_t stream = nullptr;
+    int blocks = 0;
+    int64_t cap = 0;  // persistent batch buffers
+    uint64_t *d_sig = nullptr;
+    int32_t *d_st = nullptr, *d_nr = nullptr, *d_par = nullptr;
+};
+
+int tcg_large_destroy(tcg_large *G) {
+    if (!G) return TCG_OK;
+    DeviceGuard guard(G->device);
+    if (G->stream) cudaStreamSynchronize(G->stream);
+    if (G->d_i32) cudaFree(G->d_i32);
+    if (G->d_u8) cudaFree(G->d_u8);
+    void *bufs[] = {G->d_sig, G->d_st, G->d_nr, G->d_par};
+    for (void *q : bufs)
+        if (q) cudaFree(q);
+    if (G->stream) cudaStreamDestroy(G->stream);
+    delete G;
+    return TCG_OK;
+}
+
+int tcg_large_create(const tcg_desc *D, int device, tcg_large **out) {
+    if (!D || !out) return fail(TCG_E_ARG, "null argument");
+    *out = nullptr;
+    const int d = D->degree;
+    if (d < 1 || D->nv != 2 * d * d + 2 * d + 1 || D->npts != (d + 1) * (d + 2) / 2)
+        return fail(TCG_E_ARG, "descriptor sizes do not match the degree");
+    if (D->maxreg < 1 || D->maxreg >= 65535) return fail(TCG_E_UNSUPPORTED, "maxreg out of range");
+    if (D->ne < 1) return fail(TCG_E_ARG, "empty edge list");
+    for (int e = 0; e < D->ne; ++e)
+        if (D->edge_u[e] < 0 || D->edge_u[e] >= D->nv || D->edge_v[e] < 0 || D->edge_v[e] >= D->nv)
+            return fail(TCG_E_ARG, "edge endpoint out of range");
+    for (int v = 0; v < D->nv; ++v)
+        if (D->src[v] < 0 || D->src[v] >= D->npts) return fail(TCG_E_ARG, "src out of range");
+    for (int a = 0; a < D->nap; ++a)
+        if (D->ap_u[a] < 0 || D->ap_u[a] >= D->nv || D->ap_v[a] < 0 || D->ap_v[a] >= D->nv)
+            return fail(TCG_E_ARG, "antipodal pair out of range");
+    if (device < 0 && cudaGetDevice(&device) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(TCG_E_CUDA, "no CUDA device");
+    }
+    tcg_large *G = new tcg_large();
+    G->device = device;
+    DeviceGuard guard(device);
+    auto bail = [&](cudaError_t e, const char *what) {
+        std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+        tcg_large_destroy(G);
+        return fail(TCG_E_CUDA, msg);
+    };
+    cudaError_t e;
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return bail(e, "props");
+    if (prop.major < 10) {
+        tcg_large_destroy(G);
+        return fail(TCG_E_UNSUPPORTED, "libtcg is built for sm_100a (Blackwell B200)");
+    }
+    if ((e = cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return bail(e, "stream");
+    const size_t ni = 2 * (size_t)D->ne + D->nv + 2 * (size_t)D->nap;
+    std::vector<int32_t> i32(ni);
+    std::copy(D->edge_u, D->edge_u + D->ne, i32.begin());
+    std::copy(D->edge_v, D->edge_v + D->ne, i32.begin() + D->ne);
+    std::copy(D->src, D->src + D->nv, i32.begin() + 2 * D->ne);
+    std::copy(D->ap_u, D->ap_u + D->nap, i32.begin() + 2 * D->ne + D->nv);
+    std::copy(D->ap_v, D->ap_v + D->nap, i32.begin() + 2 * D->ne + D->nv + D->nap);
+    std::vector<uint8_t> u8(2 * (size_t)D->nv);
+    std::copy(D->par, D->par + D->nv, u8.begin());
+    std::copy(D->used, D->used + D->nv, u8.begin() + D->nv);
+    if ((e = cudaMalloc(&G->d_i32, 4 * ni)) != cudaSuccess) return bail(e, "malloc");
+    if ((e = cudaMalloc(&G->d_u8, u8.size())) != cudaSuccess) return bail(e, "malloc");
+    cudaMemcpy(G->d_i32, i32.data(), 4 * ni, cudaMemcpyHostToDevice);
+    if ((e = cudaMemcpy(G->d_u8, u8.data(), u8.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return bail(e, "upload");
+    LargeParams &L = G->lp;
+    L.d = d;
+    L.nv = D->nv;
+    L.ne = D->ne;
+    L.nap = D->nap;
+    L.npts = D->npts;
+    L.maxreg = D->maxreg;
+    L.words = (D->npts + 63) / 64;
+    L.eu = G->d_i32;
+    L.ev = G->d_i32 + D->ne;
+    L.src = G->d_i32 + 2 * D->ne;
+    L.apu = G->d_i32 + 2 * D->ne + D->nv;
+    L.apv = L.apu + D->nap;
+    L.par = G->d_u8;
+    L.used = G->d_u8 + D->nv;
+    G->smem = 3 * 4 * (size_t)D->nv + 4 * (size_t)LHASH + 4 * (size_t)(5 * D->maxreg + 1) +
+              3 * (size_t)D->nv + 16;
+    if (G->smem > 200 * 1024) {
+        tcg_large_destroy(G);
+        return fail(TCG_E_UNSUPPORTED, "degree too large for one CTA's shared memory");
+    }
+    cudaFuncSetAttribute((void *)k_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)G->smem);
+    int bps = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (void *)k_large, THREADS, G->smem);
+    G->blocks = std::max(1, bps) * prop.multiProcessorCount;
+    *out = G;
+    return TCG_OK;
+}
+
+int tcg_large_classify(tcg_large *G, const uint64_t *sigma_rows, int64_t n, int32_t *status,
+                       int32_t *nreg, int32_t *parent) {
+    if (!G || (n > 0 && (!sigma_rows || !status || !nreg || !parent)))
+        return fail(TCG_E_ARG, "null argument");
+    if (n <= 0) return TCG_OK;
+    DeviceGuard guard(G->device);
+    const LargeParams &L = G->lp;
+    if (n > G->cap) {
+        void *bufs[] = {G->d_sig, G->d_st, G->d_nr, G->d_par};
+        for (void *q : bufs)
+            if (q) cudaFree(q);
+        G->d_sig = nullptr;
+        G->d_st = G->d_nr = G->d_par = nullptr;
+        G->cap = 0;
+        const int64_t cap = std::max<int64_t>(n, 256);
+        CUDA_TRY(cudaMalloc(&G->d_sig, 8 * (size_t)cap * L.words));
+        CUDA_TRY(cudaMalloc(&G->d_st, 4 * (size_t)cap));
+        CUDA_TRY(cudaMalloc(&G->d_nr, 4 * (size_t)cap));
+        CUDA_TRY(cudaMalloc(&G->d_par, 4 * (size_t)cap * L.maxreg));
+        G->cap = cap;
+    }
+    uint64_t *d_sig = G->d_sig;
+    int32_t *d_st = G->d_st, *d_nr = G->d_nr, *d_par = G->d_par;
+    CUDA_TRY(cudaMemcpyAsync(d_sig, sigma_rows, 8 * (size_t)n * L.words, cudaMemcpyHostToDevice,
+                             G->stream));
+    const unsigned blocks = (unsigned)std::min<int64_t>(G->blocks, n);
+    LargeParams lp = L;
+    void *args[] = {&lp, &d_sig, &n, &d_st, &d_nr, &d_par};
+    CUDA_TRY(cudaLaunchKernel((void *)k_large, dim3(blocks), dim3(THREADS), args, G->smem,
+                              G->stream));
+    CUDA_TRY(cudaMemcpyAsync(status, d_st, 4 * (size_t)n, cudaMemcpyDeviceToHost, G->stream));
+    CUDA_TRY(cudaMemcpyAsync(nreg, d_nr, 4 * (size_t)n, cudaMemcpyDeviceToHost, G->stream));
+    CUDA_TRY(cudaMemcpyAsync(parent, d_par, 4 * (size_t)n * L.maxreg, cudaMemcpyDeviceToHost,
+                             G->stream));
+    CUDA_TRY(cudaStreamSynchronize(G->stream));
+    return TCG_OK;
+}
 
 }  // extern "C"

@@ -96,6 +96,41 @@ def tree_from_key(key: int) -> SchemeNode:
     return root
 
 
+def scheme_from_parents(parent, nreg: int, has_pseudoline: bool) -> str:
+    """Canonical string of a rooted region tree given as a parent array
+    (the root is its own parent), iteratively (any depth)."""
+    kids: list[list[int]] = [[] for _ in range(nreg)]
+    root = -1
+    for r in range(nreg):
+        p = int(parent[r])
+        if p == r:
+            root = r
+        else:
+            kids[p].append(r)
+    if root < 0:
+        raise ValueError("parent array without a root")
+    order, stack = [], [root]
+    while stack:
+        v = stack.pop()
+        order.append(v)
+        stack.extend(kids[v])
+    items: dict[int, str] = {}
+    for v in reversed(order):
+        parts = sorted(items.pop(c) for c in kids[v])
+        out, k = [], 0
+        while k < len(parts):
+            run = k
+            while run < len(parts) and parts[run] == parts[k]:
+                run += 1
+            out.append(str(run - k) if parts[k] == "" else f"{run - k}<{parts[k]}>")
+            k = run
+        items[v] = " u ".join(out)
+    inner = items[root]
+    if has_pseudoline:
+        return f"<J u {inner}>" if inner else "<J>"
+    return f"<{inner}>" if inner else "<0>"
+
+
 @lru_cache(maxsize=1 << 16)
 def scheme_from_key(key: int, has_pseudoline: bool) -> str:
     return canonical_scheme(SchemeTree(tree_from_key(key), has_pseudoline))

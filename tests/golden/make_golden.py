@@ -348,7 +348,34 @@ def part_fig():
     print(f"wrote {path}")
 
 
+def part_large():
+    """Per-pair classifications beyond the 64-bit sign word (d = 10..48):
+    the reference's Classifier handles any degree (test_acceptance.py:223-253)."""
+    rng = random.Random(0x1A4E)
+    out = []
+    pool = [(f"delaunay-{d}", builtin(f"delaunay-{d}")) for d in (10, 11, 12, 16, 24, 48)]
+    for d in (10, 13):
+        pool.append((f"random-{d}", random_unimodular(d, rng)))
+    for name, T in pool:
+        c = Classifier(T)
+        d = T.degree
+        rows = []
+        count = 12 if d >= 24 else 40
+        for _ in range(count):
+            s = random_bits(d, rng)
+            r = c.classify(s)
+            rows.append([s, r.scheme, r.oval_count, r.region_count])
+        if name.startswith("delaunay-"):
+            s = "".join(str((i * j) % 2) for i, j in lattice_points(d))
+            r = c.classify(s)
+            rows.append([s, r.scheme, r.oval_count, r.region_count])
+        out.append({"name": name, "degree": d, "edges": edges_flat(T),
+                    "fingerprint": T.fingerprint(), "rows": rows})
+    dump("pairs_large.json", out)
+
+
 PARTS = {
+    "large": part_large,
     "tri": part_tri,
     "pairs": part_pairs,
     "garbage": part_garbage,

@@ -289,3 +289,17 @@ def test_cli_reports_byte_identical_to_reference(api, tmp_path, capsys):
     code = main(["sample", "--builtin", "delaunay-4", "-n", "5000", "--seed", "42",
                  "--output", str(out), "--histogram", str(hist)])
     assert code == 0 and out.read_text() == s["jsonl"] and hist.read_text() == s["csv"]
+
+
+def test_large_batch_pipeline_consistent(api):
+    """Batches larger than one pinned staging chunk (2^20) equal small batches."""
+    c = api.Classifier(api.builtin("delaunay-7"))
+    g = np.random.default_rng(11)
+    n = 3 * (1 << 20) + 12345
+    words = g.integers(0, 1 << 36, size=n, dtype=np.uint64)
+    keys, ov, nr, st = c.classify_words(words)
+    assert (st == 0).all()
+    for lo in (0, (1 << 20) - 7, 2 * (1 << 20) + 999, n - 5000):
+        k2, o2, r2, s2 = c.classify_words(words[lo:lo + 5000])
+        assert (k2 == keys[lo:lo + 5000]).all() and (o2 == ov[lo:lo + 5000]).all()
+        assert (r2 == nr[lo:lo + 5000]).all() and (s2 == 0).all()

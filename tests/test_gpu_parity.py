@@ -117,3 +117,77 @@ def test_c5_sample_slices_degree8():
         rep = sample_slice(T, s["seed"], s["k0"], s["k1"], classifier=c)
         assert list(rep.oval_histogram) == s["hist"], (s["name"], s["k0"])
         assert rep.scheme_map == {k: tuple(v) for k, v in s["schemes"].items()}
+
+
+def test_generic_engine_matches_reference_every_degree():
+    """The any-degree kernel (one CTA per patchwork) on every pair fixture:
+    d = 1..9 (pairs.json) and d = 10..48 (pairs_large.json)."""
+    from paper_2604_09221_b200 import Classifier
+    from paper_2604_09221_b200.lattice import validate_triangulation
+
+    tri = triangulations()
+    for e in golden("pairs.json"):
+        c = Classifier(tri_from_fixture(tri[e["name"]]), device=0, engine="generic")
+        res = c.classify_many([s for s, *_ in e["rows"]])
+        for (s, scheme, ov, nr), r in zip(e["rows"], res):
+            assert (r.scheme, r.oval_count, r.region_count) == (scheme, ov, nr), (e["name"], s)
+    for e in golden("pairs_large.json"):
+        edges = [((a, b), (c2, f)) for a, b, c2, f in e["edges"]]
+        c = Classifier(validate_triangulation(e["degree"], edges), device=0)
+        assert c.generic
+        res = c.classify_many([s for s, *_ in e["rows"]])
+        for (s, scheme, ov, nr), r in zip(e["rows"], res):
+            assert (r.scheme, r.oval_count, r.region_count) == (scheme, ov, nr), (e["name"], s)
+
+
+def test_generic_engine_statuses_match_reference():
+    from paper_2604_09221_b200 import _lib
+    from paper_2604_09221_b200.diamond import PlanArrays
+
+    for e in golden("garbage.json"):
+        P = plan_dict(e)
+        arr = PlanArrays(P["degree"], P["nv"], P["npts"], np.array(P["edge_u"], np.int32),
+                         np.array(P["edge_v"], np.int32), np.array(P["src"], np.int32),
+                         np.array(P["par"], np.uint8), np.array(P["used"], np.uint8),
+                         np.array(P["ap_u"], np.int32), np.array(P["ap_v"], np.int32),
+                         P["maxreg"])
+        g = _lib.NativeLarge(arr, 0)
+        rows = np.array([[r[0]] for r in e["rows"]], np.uint64)
+        st, nr, par = g.classify_rows(rows)
+        for i, (m, status, ovals, nreg, scheme) in enumerate(e["rows"]):
+            assert int(st[i]) == status, (e["name"], m, int(st[i]), status)
+            if status == 0:
+                assert (int(nr[i]) - 1, int(nr[i])) == (ovals, nreg)
+
+
+def test_acceptance_criterion_10_degree_scaling():
+    """time(d=48) / time(d=24) <= 5 through _run_bits (test_acceptance.py:223-253)."""
+    import random as _random
+    import time
+
+    from paper_2604_09221_b200 import Classifier, lattice_points, num_points
+    from paper_2604_09221_b200.lifting import from_lifting
+
+    rng = _random.Random(0x5CA1E)
+
+    def mean_call(d, calls):
+        T = None
+        while T is None or not T.is_unimodular:  # exact lifting: redraw degenerate jitter
+            lift = {(i, j): 8 * (i * i + i * j + j * j) + rng.randint(0, 1)
+                    for i, j in lattice_points(d)}
+            T = from_lifting(d, lift)
+        c = Classifier(T, device=0)
+        batches = [np.array([rng.randint(0, 1) for _ in range(num_points(d))], np.uint8)
+                   for _ in range(calls)]
+        for b in batches[:10]:
+            c._run_bits(b)
+        best = float("inf")
+        for _ in range(5):
+            t0 = time.perf_counter()
+            for b in batches:
+                c._run_bits(b)
+            best = min(best, (time.perf_counter() - t0) / calls)
+        return best
+
+    t24, t48 = mean_call(24, 60), mean_call(48, 30)
+    assert t48 / t24 <= 5.0, (t24, t48)

@@ -108,3 +108,16 @@ def test_oracle_worker_invariance():
     b = O.sweep(p, False, 0, 1 << 18, threads=8, chunk=977)
     assert a == b
     assert np.sum(a["hist"]) == 1 << 18
+
+
+def test_oracle_large_degrees_match_reference():
+    """d = 10..48 (beyond the 64-bit sign word), fixtures from the reference."""
+    from paper_2604_09221_b200.lattice import validate_triangulation
+
+    for e in golden("pairs_large.json"):
+        edges = [((a, b), (c, f)) for a, b, c, f in e["edges"]]
+        T = validate_triangulation(e["degree"], edges)
+        assert T.fingerprint() == e["fingerprint"]
+        got = O.classify_bitstrings(_oplan(T), [r[0] for r in e["rows"]])
+        for (s, scheme, ov, nr), g in zip(e["rows"], got):
+            assert g == (0, scheme, ov, nr), (e["name"], s)
