@@ -767,7 +767,10 @@ __device__ __forceinline__ CtaTable carve_table(void *at) {
 // Enumeration kernel: raw / representative sweep or counter-based sample.
 // Persistent grid; each warp walks 32 consecutive indices per step.
 template <int K, bool EVEN, int MODE>
-__global__ void __launch_bounds__(THREADS) k_enumerate(KParams p, uint64_t base, uint64_t count,
+#ifndef TCG_ENUM_MINB6
+#define TCG_ENUM_MINB6 1
+#endif
+__global__ void __launch_bounds__(THREADS, K == 6 ? TCG_ENUM_MINB6 : 1) k_enumerate(KParams p, uint64_t base, uint64_t count,
                                                        uint64_t seed, uint64_t nbmask, DevAgg g) {
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t *adj_s = smem;
@@ -822,7 +825,7 @@ constexpr int MAXC = 48;  // fixed components per tile
 constexpr int MAXF = 32;  // free vertices
 
 struct TileTables {  // per plan and domain (raw / representative), device memory
-    int nf, nfixed, bits, pad1;
+    int nf, nfixed, bits, maxnodes;  // maxnodes: contraction size limit (64; lower only in tests)
     uint32_t fixed[MAXK];                  // used and not free (layout mask)
     uint32_t fword[MAXF], fbit[MAXF];      // layout word / bit of free node f
     unsigned long long fadj[MAXF];         // free-free adjacency (bit g = free node g)
@@ -863,7 +866,7 @@ __device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base
     __syncwarp();
     const int n = comps.nreg;
     const int nn = n + tt.nf;
-    const bool fits = n <= MAXC && nn <= 64;
+    const bool fits = n <= MAXC && nn <= tt.maxnodes;
     unsigned long long sbits = 0;
     if (fits) {
         for (int node = lane; node < nn; node += 32) {
@@ -1141,7 +1144,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
     region_pass<K, false, false, true, MAXC>(adj_s, SG, fixed, zero, tt->nfixed, comps);
     const int n = comps.nreg, nf = tt->nf, nn = n + nf;
     TileRec *rec = recs + t;
-    const bool fits = n <= MAXC && nn <= 64;
+    const bool fits = n <= MAXC && nn <= tt->maxnodes;
     unsigned long long sbits = 0;
     if (fits) {
         unsigned long long fadj_c[MAXF];  // free node f -> comps adjacent to it
@@ -1764,6 +1767,8 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
     if (d < 5 || bits > TILE_BITS_MAX || dom_bits < bits + 2) return false;
     std::memset(&T, 0, sizeof(T));
     T.bits = bits;
+    T.maxnodes = 64;
+    if (const char *e = std::getenv("TCG_TILE_MAXNODES")) T.maxnodes = std::max(0, std::min(64, std::atoi(e)));
     int sbit[TILE_BITS_MAX];
     for (int i = 0; i < bits; ++i)
         sbit[i] = mode == MODE_RAW ? i : (i < d - 1 ? i + 2 : i - (d - 1) + d + 2);
@@ -2012,10 +2017,6 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
         }
         if ((e = cudaMalloc(&P->d_tiles, sizeof(tt))) != cudaSuccess) return bail(e, "malloc tiles");
         cudaMemcpy(P->d_tiles, tt, sizeof(tt), cudaMemcpyHostToDevice);
-        if (P->tiles_ok[0] || P->tiles_ok[1]) {
-            if ((e = cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)CHUNK_TILES)) != cudaSuccess)
-                return bail(e, "malloc tile records");
-        }
     }
     DevAgg &g = P->agg;
     if ((e = cudaMalloc(&g.keys, GCAP * 8)) != cudaSuccess) return bail(e, "malloc agg");
@@ -2241,6 +2242,8 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
     P->pending_mask = mask;
     if (mode != MODE_SAMPLE && P->tiles_ok[mode] && end > start) {
         // chunks of CHUNK_TILES tiles: contract (one warp per tile), then classify
+        if (!P->d_recs)  // contraction records: allocated on the first tiled sweep
+            CUDA_TRY(cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)CHUNK_TILES));
         void *fb = pick_build(P->K, mode);
         void *fc = pick_cls(P->K, P->even, mode);
         const TileTables *tt = P->d_tiles + mode;

@@ -303,3 +303,29 @@ def test_large_batch_pipeline_consistent(api):
         k2, o2, r2, s2 = c.classify_words(words[lo:lo + 5000])
         assert (k2 == keys[lo:lo + 5000]).all() and (o2 == ov[lo:lo + 5000]).all()
         assert (r2 == nr[lo:lo + 5000]).all() and (s2 == 0).all()
+
+
+def test_tile_fallback_path_is_exact():
+    """Force every tile through the full-diamond fallback (contraction limit
+    lowered in a subprocess) and compare with the contracted path."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json,sys; sys.path.insert(0, %r)\n"
+        "from paper_2604_09221_b200 import builtin, sweep, SweepRange\n"
+        "out = {}\n"
+        "for name, raw, a in (('delaunay-7', True, 12345678), ('delaunay-6', False, 777),"
+        " ('bowtie8', False, 1 << 38)):\n"
+        "    r = sweep(builtin(name), SweepRange(a, a + (1 << 18) + 77), raw_space=raw)\n"
+        "    out[name] = [list(r.oval_histogram), sorted(r.scheme_map.items())]\n"
+        "print(json.dumps(out))\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    res = {}
+    for limit in ("64", "8"):
+        env = dict(os.environ, TCG_TILE_MAXNODES=limit)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        assert p.returncode == 0, p.stderr
+        res[limit] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["64"] == res["8"]
