@@ -53,7 +53,10 @@ constexpr int MAXK = 6;        // 32-bit words per vertex mask (d <= 9)
 constexpr int MAXR = 32;       // regions representable (maxreg <= 31 for d <= 9)
 constexpr int NQ4 = 8;         // compress runs for the mirrored quadrant
 constexpr int THREADS = 256;   // threads per CTA
-constexpr int TBL_BITS = 10;   // per-CTA scheme table: 1024 slots
+#ifndef TCG_TBL_BITS
+#define TCG_TBL_BITS 9
+#endif
+constexpr int TBL_BITS = TCG_TBL_BITS;  // per-CTA scheme table slots (overflow goes to the global table)
 constexpr int TBL = 1 << TBL_BITS;
 constexpr int TBL_PROBES = 64;
 constexpr int GCAP_BITS = 16;  // global scheme table: 65,536 slots (as the reference's agg)
@@ -768,7 +771,7 @@ __device__ __forceinline__ CtaTable carve_table(void *at) {
 // Persistent grid; each warp walks 32 consecutive indices per step.
 template <int K, bool EVEN, int MODE>
 #ifndef TCG_ENUM_MINB6
-#define TCG_ENUM_MINB6 1
+#define TCG_ENUM_MINB6 3  // d = 8, 9: cap registers for 3 resident CTAs (measured +14 % on bowtie8)
 #endif
 __global__ void __launch_bounds__(THREADS, K == 6 ? TCG_ENUM_MINB6 : 1) k_enumerate(KParams p, uint64_t base, uint64_t count,
                                                        uint64_t seed, uint64_t nbmask, DevAgg g) {
@@ -2053,6 +2056,13 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
                              (int)P->smem_build);
         cudaFuncSetAttribute(pick_cls(K, P->even, mode),
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_cls);
+        // 38 % of the unified L1/shared array as shared memory (the 100 KB config:
+        // 4 resident CTAs), the rest stays L1
+        // for the per-thread region arrays (measured: the driver's default
+        // choice halves throughput with the 512-slot table)
+        const char *c = std::getenv("TCG_CARVEOUT");
+        cudaFuncSetAttribute(pick_cls(K, P->even, mode),
+                             cudaFuncAttributePreferredSharedMemoryCarveout, c ? std::atoi(c) : 38);
     }
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_cls(K, P->even, MODE_RAW),
                                                            THREADS, P->smem_cls)) != cudaSuccess)
