@@ -456,6 +456,48 @@ __device__ __forceinline__ Result finish(const KParams &p, const uint32_t (&SG)[
         if (c == 0) { res.status = TCG_NO_ODD_REGION; return res; }
         if (c > 1) { res.status = TCG_MANY_ODD_REGIONS; return res; }
         root = __ffs(rg.oddmask) - 1;
+    } else {
+        // the pseudoline region: the first region with a crossed edge inside
+        for (int r = 0; r < nreg; ++r) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) t |= rg.X[r][k] & rg.R[r][k];
+            if (t) { root = r; break; }
+        }
+    }
+    // Fast path, flat trees (92 % of degree-7 patchworks): every other
+    // region touches only the root across crossed edges.  Then the region
+    // graph is the star at the root -- nreg-1 edges, connected, no crossed
+    // edge inside a non-root region -- so no status can fire and the key is
+    // the root with nreg-1 leaf children.  Anything else takes the general
+    // path below (which also settles every status exactly).
+    if (root >= 0) {
+        bool flat = true;
+        uint32_t rroot[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) rroot[k] = rg.R[root][k];
+        if (EVEN) {
+            uint32_t t = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) t |= rg.X[root][k] & rroot[k];
+            flat = t == 0u;
+        }
+        for (int r = 0; r < nreg && flat; ++r) {
+            if (r == root) continue;
+            uint32_t out = 0, in = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                out |= rg.X[r][k] & ~rroot[k];
+                in |= rg.X[r][k];
+            }
+            flat = out == 0u && in != 0u;
+        }
+        if (flat) {
+            const int nb2 = 2 * (nreg - 1);
+            res.status = TCG_OK;
+            res.key = (1ull << nb2) | (0xAAAAAAAAAAAAAAAAull & ((1ull << nb2) - 1ull));
+            return res;
+        }
     }
     // region graph from crossed-edge neighbourhoods
     uint32_t radj[MAXR];
