@@ -33,6 +33,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "patchworks classified/sec, degree-7 full sign enumeration, 1/2/4/8 B200"
+BACKEND = os.environ.get("BENCH_BACKEND", "nccl")
 DEGREE = 7
 DOMAIN = 1 << 35  # raw lower half: one index per global-flip orbit
 W_D = {4: 249, 5: 381, 6: 541, 7: 729, 8: 945, 9: 1189}  # 2|E_diamond| + |V_diamond|
@@ -189,10 +190,15 @@ def run_ours(args, rank, world, local_rank):
     from paper_2604_09221_b200.distributed import allreduce_aggregate
     from paper_2604_09221_b200.sweep import report_from_agg
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    # one process per GPU; BENCH_BACKEND=gloo lets a 2-rank run share one GPU
+    # (used to exercise the N>1 path on a single-GPU box; ranks never wait
+    # on each other inside a kernel)
+    gpu = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    coll_dev = dev if BACKEND == "nccl" else torch.device("cpu")
     T = builtin(f"delaunay-{DEGREE}")
-    c = Classifier(T, device=local_rank)
+    c = Classifier(T, device=gpu)
     # a dedicated stream: the library and the timing events must share it
     # (handle 0 would mean "the plan's own stream" to tcg_plan_set_stream)
     stream = torch.cuda.Stream(device=dev)
@@ -221,7 +227,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
 
     # ---- timed: K steps, device events, max over ranks
-    gpu_index = local_rank
+    gpu_index = gpu
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
         try:
@@ -267,7 +273,7 @@ def run_ours(args, rank, world, local_rank):
         keys, counts, wits = merge_tables(tables)
         hist, total, keys, counts, wits = allreduce_aggregate(
             hist_acc.tolist(), int(hist_acc.sum()), keys, counts, wits,
-            device=dev if world > 1 else None)
+            device=coll_dev if world > 1 else None)
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -281,7 +287,7 @@ def run_ours(args, rank, world, local_rank):
     # dominant kernel: tile classification (tiled sweeps) or flat enumeration
     dom = "tile_classify" if ktimes["tile_classify"][1] else "enumerate"
     dom_ms, dom_n = ktimes[dom]
-    t = torch.tensor([ms, dom_ms, statistics.mean(kern)], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms, dom_ms, statistics.mean(kern)], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max, dom_ms_max, sweep_ms = float(t[0]), float(t[1]), float(t[2])
@@ -310,7 +316,7 @@ def run_ours(args, rank, world, local_rank):
                                           rep.total_classified))
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    te = torch.tensor([e2e_s], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = units / float(te[0])
@@ -414,8 +420,12 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        gpu = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(gpu)
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", gpu))
+        else:
+            dist.init_process_group(BACKEND)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

@@ -329,3 +329,24 @@ def test_tile_fallback_path_is_exact():
         assert p.returncode == 0, p.stderr
         res[limit] = json.loads(p.stdout.strip().splitlines()[-1])
     assert res["64"] == res["8"]
+
+
+def test_two_rank_sharded_sweep_equals_single_process():
+    """distributed.sweep_sharded with 2 ranks (gloo collectives, both ranks on
+    cuda:0) merges to exactly the single-process report."""
+    import os
+    import socket
+    import subprocess
+    import sys
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), os.path.join(root, "scripts", "sharded_check.py")],
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-2000:]
+    assert "sharded == single: True" in p.stdout
