@@ -46,6 +46,16 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)[kernel]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -370,12 +380,13 @@ def run_ours(args, rank, world, local_rank):
         },
         "roofline": {
             "bound": "issue", "achieved": achieved, "peak": peak, "unit": "elem-visits/s",
-            "frac": achieved / peak, "traffic": None,
+            "frac": achieved / peak, "traffic": ncu_traffic(kernel_names[dom]),
             "note": f"integer-issue roofline (no tensor/HBM work): algorithmic element "
                     f"visits W(7)=2|E|+|V|=729 per patchwork x {dom} rate "
                     f"{per_gpu_kernel_pps:.3e}/s (all timed patchworks / summed CUDA-event "
                     f"time of its {dom_n} launches), over {nsm} SMs x 128 lanes x {mhz:.0f} MHz "
-                    f"({peak_src}); dram traffic per launch: see profiles/",
+                    f"({peak_src}); traffic = dram bytes per launch from the committed ncu "
+                    "capture profiles/ncu_traffic.json",
             "kernel": kernel_names[dom], "kernel_ms": dom_ms_max / max(1, dom_n),
             "launches": dom_n,
             "share_of_device_time": dom_ms / total_kernel_ms if total_kernel_ms else None,
