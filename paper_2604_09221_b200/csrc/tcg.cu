@@ -1117,6 +1117,89 @@ __device__ __forceinline__ void node_pass1(const uint4 *__restrict__ rows, uint3
     out.oddmask = oddmask;
 }
 
+// Two independent patchworks of one tile per thread, stepped in lock-step:
+// the region opens/closes stay branches, but both shared-memory row loads
+// and both expansions sit in one basic block, so their latencies overlap.
+template <bool EVEN>
+struct NP1 {
+    uint32_t un, f, x, q, r, oddmask;
+    bool odd;
+    int nreg;
+    __device__ __forceinline__ void start(uint32_t used) {
+        un = used;
+        nreg = 0;
+        oddmask = 0u;
+        seed();
+    }
+    __device__ __forceinline__ void seed() {
+        f = un & (0u - un);
+        r = un;
+        un ^= f;
+        x = 0u;
+        if (EVEN) q = 0u;
+        odd = false;
+    }
+    __device__ __forceinline__ void close(Regions<1> &out) {
+        if (nreg < MAXR) {
+            out.R[nreg][0] = r ^ un;
+            out.X[nreg][0] = x;
+            if (EVEN && odd) oddmask |= 1u << nreg;
+        }
+        ++nreg;
+    }
+    __device__ __forceinline__ void expand(const uint4 row, int v, uint32_t sg) {
+        const uint32_t sv = (uint32_t)((int32_t)(sg << (31 - v)) >> 31);
+        const uint32_t o = sg ^ sv;
+        x |= row.x & o;
+        if (EVEN) {
+            const uint32_t pv = (uint32_t)((int32_t)(q << (31 - v)) >> 31);
+            const uint32_t te = row.x & ~o, nt = te & un, np = row.z & un;
+            const uint32_t eq = ~(q ^ pv);
+            odd |= ((nt & np) | (te & ~un & ~eq) | (row.z & ~un & eq)) != 0u;
+            q |= (nt & pv) | (np & ~pv);
+            const uint32_t n = nt | np;
+            un ^= n;
+            f |= n;
+        } else {
+            const uint32_t n = ((row.x & ~o) | row.z) & un;
+            un ^= n;
+            f |= n;
+        }
+    }
+    __device__ __forceinline__ void finish(Regions<1> &out) {
+        close(out);
+        out.nreg = nreg;
+        out.oddmask = oddmask;
+    }
+};
+
+template <bool EVEN>
+__device__ __forceinline__ void node_pass1x2(const uint4 *__restrict__ rows, uint32_t sga,
+                                             uint32_t sgb, uint32_t used, int nn,
+                                             Regions<1> &oa, Regions<1> &ob) {
+    NP1<EVEN> a, b;
+    a.start(used);
+    b.start(used);
+    for (int it = 0; it < nn; ++it) {
+        if (a.f == 0u) {
+            a.close(oa);
+            a.seed();
+        }
+        if (b.f == 0u) {
+            b.close(ob);
+            b.seed();
+        }
+        const int va = __ffs(a.f) - 1, vb = __ffs(b.f) - 1;
+        a.f &= a.f - 1u;
+        b.f &= b.f - 1u;
+        const uint4 ra = rows[va], rb = rows[vb];
+        a.expand(ra, va, sga);
+        b.expand(rb, vb, sgb);
+    }
+    a.finish(oa);
+    b.finish(ob);
+}
+
 template <bool EVEN>
 __device__ __forceinline__ Result classify_tile(const KParams &p, const TileTables &tt,
                                                 const uint4 *rows,
@@ -1247,6 +1330,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
 // per-warp shared-memory slot), so warps never wait on each other.
 constexpr int CLS_WARPS = THREADS / 32;
 
+
 template <int K, bool EVEN, int MODE>
 __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
                                                            const TileTables *__restrict__ tt_g,
@@ -1278,6 +1362,36 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
         const unsigned long long sgf = src->sgn_fixed;
         __syncwarp();
         const uint64_t base = (tile0 + t) << bits;
+#ifndef TCG_NO_PAIRS
+        if (!fb && nn <= 32) {  // two patchworks per thread (tile sizes are >= 64)
+            const uint32_t used = nn >= 32 ? ~0u : ((1u << nn) - 1u);
+            for (uint32_t low = lane; low < tsize; low += 64) {
+                const unsigned long long fa =
+                    tt->fsign[0][low & 63u] ^ tt->fsign[1][(low >> 6) & 63u];
+                const unsigned long long fb2 =
+                    tt->fsign[0][(low + 32) & 63u] ^ tt->fsign[1][((low + 32) >> 6) & 63u];
+                const uint32_t sga = (uint32_t)(sgf | (fa << n));
+                const uint32_t sgb = (uint32_t)(sgf | (fb2 << n));
+                Regions<1> ra, rb;
+                node_pass1x2<EVEN>(rec->rows, sga, sgb, used, nn, ra, rb);
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    const uint64_t m = base + low + 32u * h;
+                    const bool valid = m >= start && m < end;
+                    const uint32_t SG1[1] = {h ? sgb : sga};
+                    const Result r = finish<1, EVEN, false>(p, SG1, h ? rb : ra, p.maxreg);
+                    uint64_t k = 0;
+                    if (valid) {
+                        if (r.status == TCG_OK) k = r.key;
+                        else atomicMin(g.bad, (unsigned long long)m);
+                    }
+                    tab.add<true>(g, k, r.nreg, m);
+                }
+            }
+            __syncwarp();
+            continue;
+        }
+#endif
         for (uint32_t low = lane; low < tsize; low += 32) {
             const uint64_t m = base + low;
             const bool valid = m >= start && m < end;
