@@ -1147,21 +1147,22 @@ struct NP1 {
         }
         ++nreg;
     }
-    __device__ __forceinline__ void expand(const uint4 row, int v, uint32_t sg) {
+    __device__ __forceinline__ void expand(const uint32_t rx, const uint32_t rz, int v,
+                                           uint32_t sg) {
         const uint32_t sv = (uint32_t)((int32_t)(sg << (31 - v)) >> 31);
         const uint32_t o = sg ^ sv;
-        x |= row.x & o;
+        x |= rx & o;
         if (EVEN) {
             const uint32_t pv = (uint32_t)((int32_t)(q << (31 - v)) >> 31);
-            const uint32_t te = row.x & ~o, nt = te & un, np = row.z & un;
+            const uint32_t te = rx & ~o, nt = te & un, np = rz & un;
             const uint32_t eq = ~(q ^ pv);
-            odd |= ((nt & np) | (te & ~un & ~eq) | (row.z & ~un & eq)) != 0u;
+            odd |= ((nt & np) | (te & ~un & ~eq) | (rz & ~un & eq)) != 0u;
             q |= (nt & pv) | (np & ~pv);
             const uint32_t n = nt | np;
             un ^= n;
             f |= n;
         } else {
-            const uint32_t n = ((row.x & ~o) | row.z) & un;
+            const uint32_t n = ((rx & ~o) | rz) & un;
             un ^= n;
             f |= n;
         }
@@ -1174,7 +1175,8 @@ struct NP1 {
 };
 
 template <bool EVEN>
-__device__ __forceinline__ void node_pass1x2(const uint4 *__restrict__ rows, uint32_t sga,
+__device__ __forceinline__ void node_pass1x2(const uint32_t *__restrict__ ax,
+                                             const uint32_t *__restrict__ az, uint32_t sga,
                                              uint32_t sgb, uint32_t used, int nn,
                                              Regions<1> &oa, Regions<1> &ob) {
     NP1<EVEN> a, b;
@@ -1192,9 +1194,9 @@ __device__ __forceinline__ void node_pass1x2(const uint4 *__restrict__ rows, uin
         const int va = __ffs(a.f) - 1, vb = __ffs(b.f) - 1;
         a.f &= a.f - 1u;
         b.f &= b.f - 1u;
-        const uint4 ra = rows[va], rb = rows[vb];
-        a.expand(ra, va, sga);
-        b.expand(rb, vb, sgb);
+        const uint32_t xa = ax[va], xb = ax[vb], za = az[va], zb = az[vb];
+        a.expand(xa, za, va, sga);
+        b.expand(xb, zb, vb, sgb);
     }
     a.finish(oa);
     b.finish(ob);
@@ -1355,14 +1357,24 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
     for (uint32_t t = blockIdx.x * CLS_WARPS + w; t < ntiles; t += gridDim.x * CLS_WARPS) {
         const TileRec *src = recs + t;
         const int nn = src->nnodes;
-        if (lane < nn) rec->rows[lane] = src->rows[lane];
-        if (lane + 32 < nn) rec->rows[lane + 32] = src->rows[lane + 32];
-        const int n = src->n;
         const bool fb = src->fallback != 0;
+        // nn <= 32: the node pass reads only the low adjacency and link words;
+        // stage them as two 32-word arrays (one bank per node: no conflicts)
+        uint32_t *ax = reinterpret_cast<uint32_t *>(rec->rows), *az = ax + 32;
+        if (!fb && nn <= 32) {
+            if (lane < nn) {
+                const uint4 row = src->rows[lane];
+                ax[lane] = row.x;
+                az[lane] = row.z;
+            }
+        } else {
+            if (lane < nn) rec->rows[lane] = src->rows[lane];
+            if (lane + 32 < nn) rec->rows[lane + 32] = src->rows[lane + 32];
+        }
+        const int n = src->n;
         const unsigned long long sgf = src->sgn_fixed;
         __syncwarp();
         const uint64_t base = (tile0 + t) << bits;
-#ifndef TCG_NO_PAIRS
         if (!fb && nn <= 32) {  // two patchworks per thread (tile sizes are >= 64)
             const uint32_t used = nn >= 32 ? ~0u : ((1u << nn) - 1u);
             for (uint32_t low = lane; low < tsize; low += 64) {
@@ -1373,7 +1385,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
                 const uint32_t sga = (uint32_t)(sgf | (fa << n));
                 const uint32_t sgb = (uint32_t)(sgf | (fb2 << n));
                 Regions<1> ra, rb;
-                node_pass1x2<EVEN>(rec->rows, sga, sgb, used, nn, ra, rb);
+                node_pass1x2<EVEN>(ax, az, sga, sgb, used, nn, ra, rb);
 #pragma unroll 1
                 for (int h = 0; h < 2; ++h) {
                     const uint64_t m = base + low + 32u * h;
@@ -1391,7 +1403,6 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
             __syncwarp();
             continue;
         }
-#endif
         for (uint32_t low = lane; low < tsize; low += 32) {
             const uint64_t m = base + low;
             const bool valid = m >= start && m < end;
