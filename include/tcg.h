@@ -118,6 +118,15 @@ int tcg_plan_info(const tcg_plan *plan, int32_t *info, int ninfo);
  * enumeration, batch classification. */
 int tcg_plan_set_timing(tcg_plan *plan, int enable);
 int tcg_kernel_times(tcg_plan *plan, double *ms, int64_t *counts);
+/* Tile deduplication (exhaustive sweeps): tiles whose contracted records are
+ * identical are classified once and counted with their multiplicity (the
+ * witness is taken from the group's smallest tile, so reports are unchanged).
+ * enable: 1 on, 0 off, -1 default (on unless TCG_NO_DEDUP=1). */
+int tcg_plan_set_dedup(tcg_plan *plan, int enable);
+/* out[0] = tiles contracted, out[1] = tiles classified (= out[0] without
+ * deduplication) since the last call
+ * (synchronises the plan's stream); resets both. */
+int tcg_tile_stats(tcg_plan *plan, int64_t *out);
 
 /* classify_bits_kernel, batched.  sigma[t] bit k = sign of point k.
  * Outputs per patchwork: tree key, oval count, region count, status. */

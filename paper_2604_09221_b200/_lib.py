@@ -64,6 +64,8 @@ def load():
         L.tcg_plan_info.argtypes = [P, C.c_void_p, C.c_int]
         L.tcg_plan_set_timing.argtypes = [P, C.c_int]
         L.tcg_kernel_times.argtypes = [P, C.c_void_p, C.c_void_p]
+        L.tcg_plan_set_dedup.argtypes = [P, C.c_int]
+        L.tcg_tile_stats.argtypes = [P, C.c_void_p]
         L.tcg_classify_batch.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p]
         L.tcg_classify_batch_device.argtypes = L.tcg_classify_batch.argtypes
@@ -100,7 +102,7 @@ def load():
 
 EXPORTS = (
     "tcg_plan_create", "tcg_plan_destroy", "tcg_plan_set_stream", "tcg_plan_info",
-    "tcg_plan_set_timing", "tcg_kernel_times",
+    "tcg_plan_set_timing", "tcg_kernel_times", "tcg_plan_set_dedup", "tcg_tile_stats",
     "tcg_classify_batch", "tcg_classify_batch_device", "tcg_sweep", "tcg_sample",
     "tcg_agg_reset", "tcg_sweep_async", "tcg_sample_async", "tcg_agg_fetch",
     "tcg_sweep_multi", "tcg_sample_multi", "tcg_last_error", "tcg_device_count",
@@ -319,6 +321,17 @@ class NativePlan:
         _check(self._L.tcg_kernel_times(self.h, ms.ctypes.data, n.ctypes.data), "tcg_kernel_times")
         names = ("tile_build", "tile_classify", "enumerate", "batch")
         return {names[i]: (float(ms[i]), int(n[i])) for i in range(4)}
+
+    def set_dedup(self, enable: bool | None):
+        """Tile deduplication on / off / None = default (see tcg.h)."""
+        flag = -1 if enable is None else int(bool(enable))
+        _check(self._L.tcg_plan_set_dedup(self.h, flag), "tcg_plan_set_dedup")
+
+    def tile_stats(self):
+        """(tiles contracted, tiles classified) since the last call."""
+        out = np.zeros(2, np.int64)
+        _check(self._L.tcg_tile_stats(self.h, out.ctypes.data), "tcg_tile_stats")
+        return int(out[0]), int(out[1])
 
     def classify_words(self, words):
         w = np.ascontiguousarray(words, dtype=np.uint64)

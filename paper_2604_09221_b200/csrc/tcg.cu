@@ -754,7 +754,8 @@ struct CtaTable {
     // leader holds the group's minimal index (sweeps); otherwise every lane
     // offers its own index (random draws).
     template <bool WITNESS_BY_LEADER>
-    __device__ __forceinline__ void add(const DevAgg &g, uint64_t k, int nreg, uint64_t m) {
+    __device__ __forceinline__ void add(const DevAgg &g, uint64_t k, int nreg, uint64_t m,
+                                        uint32_t weight = 1u) {
         const int lane = threadIdx.x & 31;
         const unsigned grp = __match_any_sync(0xffffffffu, k);
         if (k == 0ull) return;
@@ -771,7 +772,7 @@ struct CtaTable {
                 }
                 h = (h + 1) & (TBL - 1);
             }
-            const uint32_t c = __popc(grp);
+            const uint32_t c = __popc(grp) * weight;
             atomicAdd(&hist[nreg - 1], c);
             if (slot >= 0) {
                 atomicAdd(&cnt[slot], c);
@@ -890,6 +891,22 @@ struct TileRec {
     int n, nnodes, fallback, pad;
 };
 
+// Graphs of <= 32 nodes (all of d = 6, 99 % of d = 7) store only the low
+// adjacency and link words, packed as uint2 at the start of rows[]: a quarter
+// of the bytes to write, deduplicate and stage.
+__device__ __forceinline__ const uint2 *rows2(const TileRec *r) {
+    return reinterpret_cast<const uint2 *>(r->rows);
+}
+
+__device__ __forceinline__ void store_row(TileRec *rec, int node, int nn, unsigned long long adj,
+                                          unsigned long long pl) {
+    if (nn <= 32)
+        reinterpret_cast<uint2 *>(rec->rows)[node] = make_uint2((uint32_t)adj, (uint32_t)pl);
+    else
+        rec->rows[node] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
+                                     (uint32_t)(pl >> 32));
+}
+
 // One warp contracts one tile: same-sign components of the fixed vertices
 // (region_pass in COMPS mode, identical in all lanes), then lane-parallel
 // node rows.  comps: per-warp shared scratch; rec: global output.
@@ -956,8 +973,7 @@ __device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base
                     if (sel<K>(x, w) & b) adj |= 1ull << c;
                 }
             }
-            rec->rows[node] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
-                                         (uint32_t)(pl >> 32));
+            store_row(rec, node, nn, adj, pl);
         }
     }
     unsigned long long sg = sbits;
@@ -1311,20 +1327,115 @@ __global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
 #pragma unroll
             for (int k = 0; k < K; ++k) sg |= R[k] & SG[k];
             if (sg) sbits |= 1ull << c;
-            rec->rows[c] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
-                                      (uint32_t)(pl >> 32));
+            store_row(rec, c, nn, adj, pl);
         }
         for (int f = 0; f < nf; ++f) {
             const unsigned long long adj = (tt->fadj[f] << n) | fadj_c[f];
             const unsigned long long pl = tt->fpl[f] << n;
-            rec->rows[n + f] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
-                                          (uint32_t)(pl >> 32));
+            store_row(rec, n + f, nn, adj, pl);
         }
     }
     rec->sgn_fixed = sbits;
     rec->n = n;
     rec->nnodes = nn;
     rec->fallback = fits ? 0 : 1;
+}
+
+// Tile deduplication.  A tile's classification depends only on its contracted
+// record (rows, fixed signs, sizes) and the tile-local index, so tiles with
+// byte-identical records produce identical results index by index.  One warp
+// per tile hashes the record and inserts it into an open-addressing table of
+// tile ids; an equal record already present (compared word by word, never by
+// hash alone) takes the tile as a duplicate: dup[rep] += 1, mint[rep] = min
+// tile id (the witness of every scheme in the group is the smallest index,
+// which lies in the group's smallest tile).  Representatives are appended to
+// list[]; partial tiles (range ends) and fallback tiles are never merged.
+constexpr uint32_t DEDUP_EMPTY = 0xffffffffu;
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restrict__ recs,
+                                                        uint32_t ntiles, uint64_t tile0, int bits,
+                                                        uint64_t start, uint64_t end,
+                                                        uint32_t *__restrict__ slots,
+                                                        uint32_t smask, uint32_t *__restrict__ dup,
+                                                        uint32_t *__restrict__ mint,
+                                                        uint32_t *__restrict__ list,
+                                                        uint32_t *__restrict__ count) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t t = warp; t < ntiles; t += nwarps) {
+        const TileRec *r = recs + t;
+        const int nn = r->nnodes, n = r->n;
+        const unsigned long long sg = r->sgn_fixed;
+        const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
+        if (r->fallback || b0 < start || b1 > end) {
+            if (lane == 0) list[atomicAdd(count, 1u)] = t;
+            continue;
+        }
+        const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+        auto load = [&](const TileRec *q, uint4 &a, uint4 &b) {
+            a = z4;
+            b = z4;
+            if (nn <= 32) {
+                if (lane < nn) {
+                    const uint2 w = rows2(q)[lane];
+                    a.x = w.x;
+                    a.z = w.y;
+                }
+            } else {
+                if (lane < nn) a = q->rows[lane];
+                if (lane + 32 < nn) b = q->rows[lane + 32];
+            }
+        };
+        uint4 ra, rb;
+        load(r, ra, rb);
+        unsigned long long h =
+            mix64(((unsigned long long)ra.y << 32 | ra.x) + 0x9E3779B97F4A7C15ull * (lane + 1)) ^
+            mix64(((unsigned long long)ra.w << 32 | ra.z) + 0xD1B54A32D192ED03ull * (lane + 1)) ^
+            mix64(((unsigned long long)rb.y << 32 | rb.x) + 0x8CB92BA72F3D8DD7ull * (lane + 1)) ^
+            mix64(((unsigned long long)rb.w << 32 | rb.z) + 0xABC98388FB8FAC03ull * (lane + 1));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+        h ^= mix64(sg ^ ((unsigned long long)nn << 56) ^ ((unsigned long long)n << 48));
+        uint32_t at = (uint32_t)(h >> 20) & smask;
+        while (true) {
+            uint32_t cur = 0;
+            if (lane == 0) {
+                cur = slots[at];
+                if (cur == DEDUP_EMPTY) {
+                    const uint32_t prev = atomicCAS(&slots[at], DEDUP_EMPTY, t);
+                    cur = prev == DEDUP_EMPTY ? t : prev;
+                }
+            }
+            cur = __shfl_sync(0xffffffffu, cur, 0);
+            if (cur == t) {  // new representative
+                if (lane == 0) list[atomicAdd(count, 1u)] = t;
+                break;
+            }
+            const TileRec *o = recs + cur;
+            bool eq = o->nnodes == nn && o->n == n && o->sgn_fixed == sg;
+            if (eq) {
+                uint4 oa, ob;
+                load(o, oa, ob);
+                eq = oa.x == ra.x && oa.y == ra.y && oa.z == ra.z && oa.w == ra.w &&
+                     ob.x == rb.x && ob.y == rb.y && ob.z == rb.z && ob.w == rb.w;
+            }
+            if (__all_sync(0xffffffffu, eq)) {
+                if (lane == 0) {
+                    atomicAdd(&dup[cur], 1u);
+                    atomicMin(&mint[cur], t);
+                }
+                break;
+            }
+            at = (at + 1) & smask;
+        }
+    }
 }
 
 // Classify every index of [start, end) that falls in tiles tile0 .. tile0+ntiles-1.
@@ -1339,7 +1450,11 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
                                                            const TileRec *__restrict__ recs,
                                                            uint64_t tile0, uint32_t ntiles,
                                                            uint64_t start, uint64_t end,
-                                                           DevAgg g) {
+                                                           DevAgg g, const uint32_t *__restrict__ list,
+                                                           const uint32_t *__restrict__ count,
+                                                           const uint32_t *__restrict__ dup,
+                                                           const uint32_t *__restrict__ mint,
+                                                           unsigned long long *__restrict__ tstats) {
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t *adj_s = smem;
     CtaTable tab = carve_table(smem + 32 * K * K);
@@ -1354,7 +1469,14 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
     __syncthreads();
     const int bits = tt->bits;
     const uint32_t tsize = 1u << bits;
-    for (uint32_t t = blockIdx.x * CLS_WARPS + w; t < ntiles; t += gridDim.x * CLS_WARPS) {
+    // list != nullptr: classify only the representatives, each with the weight
+    // of its duplicate group and the group's smallest tile as the witness base
+    const uint32_t nwork = list ? *count : ntiles;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(tstats, (unsigned long long)nwork);
+    for (uint32_t i = blockIdx.x * CLS_WARPS + w; i < nwork; i += gridDim.x * CLS_WARPS) {
+        const uint32_t t = list ? list[i] : i;
+        const uint32_t weight = list ? 1u + dup[t] : 1u;
+        const uint32_t tw = list ? min(t, mint[t]) : t;
         const TileRec *src = recs + t;
         const int nn = src->nnodes;
         const bool fb = src->fallback != 0;
@@ -1363,9 +1485,9 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
         uint32_t *ax = reinterpret_cast<uint32_t *>(rec->rows), *az = ax + 32;
         if (!fb && nn <= 32) {
             if (lane < nn) {
-                const uint4 row = src->rows[lane];
+                const uint2 row = rows2(src)[lane];
                 ax[lane] = row.x;
-                az[lane] = row.z;
+                az[lane] = row.y;
             }
         } else {
             if (lane < nn) rec->rows[lane] = src->rows[lane];
@@ -1374,7 +1496,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
         const int n = src->n;
         const unsigned long long sgf = src->sgn_fixed;
         __syncwarp();
-        const uint64_t base = (tile0 + t) << bits;
+        const uint64_t base = (tile0 + tw) << bits;
         if (!fb && nn <= 32) {  // two patchworks per thread (tile sizes are >= 64)
             const uint32_t used = nn >= 32 ? ~0u : ((1u << nn) - 1u);
             for (uint32_t low = lane; low < tsize; low += 64) {
@@ -1397,7 +1519,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
                         if (r.status == TCG_OK) k = r.key;
                         else atomicMin(g.bad, (unsigned long long)m);
                     }
-                    tab.add<true>(g, k, r.nreg, m);
+                    tab.add<true>(g, k, r.nreg, m, weight);
                 }
             }
             __syncwarp();
@@ -1418,7 +1540,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
                 if (r.status == TCG_OK) k = r.key;
                 else atomicMin(g.bad, (unsigned long long)m);
             }
-            tab.add<true>(g, k, r.nreg, m);
+            tab.add<true>(g, k, r.nreg, m, weight);
         }
         __syncwarp();
     }
@@ -1748,7 +1870,11 @@ struct tcg_plan {
     int64_t launches = 0;
     // tile contraction (sweeps): per domain (raw, representative)
     TileTables *d_tiles = nullptr;   // [2]
-    TileRec *d_recs = nullptr;       // [CHUNK_TILES]
+    TileRec *d_recs = nullptr;       // [chunk_tiles()]
+    uint32_t *d_dedup = nullptr;     // slots[2C] | mint[C] | dup[C] | count[1] | list[C]
+    unsigned long long *d_tstats = nullptr;  // [1] tiles classified after deduplication
+    int dedup = -1;                  // -1: TCG_NO_DEDUP decides
+    int64_t tiles_built = 0;
     int tiles_ok[2] = {0, 0};
     int tile_bits[2] = {0, 0};
     int blocks_build = 0, blocks_cls = 0;
@@ -1862,7 +1988,16 @@ size_t cls_smem(int K) {
     return (size_t)32 * K * K * 4 + TABLE_SMEM + sizeof(TileTables) + CLS_WARPS * sizeof(TileRec);
 }
 
-constexpr uint32_t CHUNK_TILES = 1u << 18;
+// Tiles per contraction chunk (records: 1 KiB each).  Larger chunks find more
+// duplicate tiles; TCG_CHUNK_LOG2 (14..21) overrides the default.
+static uint32_t chunk_tiles() {
+    static const uint32_t c = [] {
+        int lg = 20;
+        if (const char *e = std::getenv("TCG_CHUNK_LOG2")) lg = std::max(14, std::min(21, std::atoi(e)));
+        return 1u << lg;
+    }();
+    return c;
+}
 
 void *pick_batch(int K, bool even) {
     if (K == 2) return even ? (void *)k_batch<2, true> : (void *)k_batch<2, false>;
@@ -2260,7 +2395,7 @@ int tcg_plan_destroy(tcg_plan *P) {
     DeviceGuard guard(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     timing_resolve(P);
-    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
@@ -2290,6 +2425,27 @@ int tcg_plan_set_timing(tcg_plan *P, int enable) {
     DeviceGuard guard(P->device);
     timing_resolve(P);
     P->timing = enable ? 1 : 0;
+    return TCG_OK;
+}
+
+int tcg_plan_set_dedup(tcg_plan *P, int enable) {
+    if (!P) return fail(TCG_E_ARG, "null plan");
+    P->dedup = enable < 0 ? -1 : (enable ? 1 : 0);
+    return TCG_OK;
+}
+
+int tcg_tile_stats(tcg_plan *P, int64_t *out) {
+    if (!P || !out) return fail(TCG_E_ARG, "null argument");
+    DeviceGuard guard(P->device);
+    unsigned long long c = 0;
+    if (P->d_tstats) {
+        CUDA_TRY(cudaStreamSynchronize(P->stream));
+        CUDA_TRY(cudaMemcpy(&c, P->d_tstats, sizeof(c), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemset(P->d_tstats, 0, sizeof(c)));
+    }
+    out[0] = P->tiles_built;
+    out[1] = (int64_t)c;
+    P->tiles_built = 0;
     return TCG_OK;
 }
 
@@ -2407,6 +2563,15 @@ int tcg_agg_reset(tcg_plan *P) {
     return TCG_OK;
 }
 
+// TCG_NO_DEDUP=1 classifies every tile (A/B and debugging); results are identical.
+static bool dedup_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("TCG_NO_DEDUP");
+        return !(e && e[0] && e[0] != '0');
+    }();
+    return on;
+}
+
 static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t seed,
                    uint64_t mask) {
     if (P->pending_mode >= 0 && P->pending_mode != mode)
@@ -2418,16 +2583,21 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
     P->pending_seed = seed;
     P->pending_mask = mask;
     if (mode != MODE_SAMPLE && P->tiles_ok[mode] && end > start) {
-        // chunks of CHUNK_TILES tiles: contract (one warp per tile), then classify
-        if (!P->d_recs)  // contraction records: allocated on the first tiled sweep
-            CUDA_TRY(cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)CHUNK_TILES));
+        // chunks of chunk_tiles() tiles: contract, deduplicate, classify
+        if (!P->d_recs) {  // contraction records: allocated on the first tiled sweep
+            CUDA_TRY(cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)chunk_tiles()));
+            CUDA_TRY(cudaMalloc(&P->d_tstats, sizeof(unsigned long long)));
+            CUDA_TRY(cudaMemsetAsync(P->d_tstats, 0, sizeof(unsigned long long), P->stream));
+        }
         void *fb = pick_build(P->K, mode);
         void *fc = pick_cls(P->K, P->even, mode);
         const TileTables *tt = P->d_tiles + mode;
         const int bits = P->tile_bits[mode];
         const uint64_t t_end = ((end - 1) >> bits) + 1;
-        for (uint64_t t0 = start >> bits; t0 < t_end; t0 += CHUNK_TILES) {
-            uint32_t nt = (uint32_t)std::min<uint64_t>(CHUNK_TILES, t_end - t0);
+        // per-CTA scheme counters are 32-bit: keep a launch below 2^31 patchworks
+        const uint32_t chunk = std::min<uint32_t>(chunk_tiles(), 1u << (31 - bits));
+        for (uint64_t t0 = start >> bits; t0 < t_end; t0 += chunk) {
+            uint32_t nt = (uint32_t)std::min<uint64_t>(chunk, t_end - t0);
             uint64_t tile0 = t0;
             TileRec *recs = P->d_recs;
             const unsigned per_block = build_per_warp() ? BUILD_WARPS : THREADS;
@@ -2440,12 +2610,35 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             CUDA_TRY(cudaLaunchKernel(fb, dim3(gb), dim3(build_per_warp() ? 32 * BUILD_WARPS
                                                                            : THREADS),
                                       ab, P->smem_build, P->stream));
+            uint64_t lo = start, hi = end;
+            const TileRec *crecs = recs;
+            const uint32_t *list = nullptr, *cnt = nullptr, *dup = nullptr, *mint = nullptr;
+            if (P->dedup < 0 ? dedup_enabled() : P->dedup != 0) {
+                const size_t C = chunk_tiles();
+                if (!P->d_dedup) CUDA_TRY(cudaMalloc(&P->d_dedup, sizeof(uint32_t) * (5 * C + 1)));
+                uint32_t *slots = P->d_dedup, *mnt = slots + 2 * C, *dp = mnt + C, *ct = dp + C,
+                         *ls = ct + 1;
+                CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(uint32_t) * 3 * C, P->stream));
+                CUDA_TRY(cudaMemsetAsync(dp, 0, sizeof(uint32_t) * (C + 1), P->stream));
+                uint32_t smask = (uint32_t)(2 * C - 1);
+                int ibits = bits;
+                void *ad[] = {&crecs, &nt, &tile0, &ibits, &lo, &hi, &slots, &smask, &dp, &mnt, &ls, &ct};
+                const unsigned gd = (unsigned)std::min<uint64_t>(
+                    (uint64_t)P->nsm * 8, (nt + CLS_WARPS - 1) / CLS_WARPS);
+                CUDA_TRY(cudaLaunchKernel((void *)k_tile_dedup, dim3(gd), dim3(THREADS), ad, 0,
+                                          P->stream));
+                list = ls;
+                cnt = ct;
+                dup = dp;
+                mint = mnt;
+                P->launches++;
+            }
             timing_end(P, 0, e0);
             const unsigned gc = (unsigned)std::min<uint64_t>(P->blocks_cls,
                                                              (nt + CLS_WARPS - 1) / CLS_WARPS);
-            uint64_t lo = start, hi = end;
-            const TileRec *crecs = recs;
-            void *ac[] = {&P->kp, &tt, &crecs, &tile0, &nt, &lo, &hi, &P->agg};
+            P->tiles_built += nt;
+            void *ac[] = {&P->kp, &tt, &crecs, &tile0, &nt, &lo, &hi, &P->agg,
+                          &list, &cnt, &dup, &mint, &P->d_tstats};
             cudaEvent_t e1 = timing_begin(P);
             CUDA_TRY(cudaLaunchKernel(fc, dim3(gc), dim3(THREADS), ac, P->smem_cls, P->stream));
             timing_end(P, 1, e1);

@@ -350,3 +350,52 @@ def test_two_rank_sharded_sweep_equals_single_process():
                        capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-2000:]
     assert "sharded == single: True" in p.stdout
+
+
+@pytest.mark.parametrize("name,raw,a,n", [
+    ("delaunay-7", True, 0x5A5A5A5A0 + 3, (1 << 24) + 1001),
+    ("delaunay-6", True, 12345, 1 << 24),
+    ("delaunay-6", False, 0, 1 << 25),
+    ("bowtie8", False, (1 << 38) + 17, 1 << 25),
+    ("delaunay-8", False, 1 << 39, 1 << 24),
+])
+def test_tile_dedup_is_exact(api, name, raw, a, n):
+    """Classifying each distinct contracted tile once, weighted by its
+    multiplicity, gives the identical report (counts, histogram, witnesses)."""
+    T = api.builtin(name)
+    c = api.Classifier(T)
+    reps = {}
+    for on in (False, True):
+        c.native.set_dedup(on)
+        c.native.tile_stats()
+        r = api.sweep(T, api.SweepRange(a, a + n), raw_space=raw, classifier=c)
+        built, classified = c.native.tile_stats()
+        reps[on] = (r.oval_histogram, sorted(r.scheme_map.items()), r.total_classified)
+        if on:
+            assert 0 < classified <= built
+        else:
+            assert classified == built  # every tile classified
+    c.native.set_dedup(None)
+    assert reps[True] == reps[False]
+
+
+def test_tile_dedup_chunk_size_invariance():
+    """Small contraction chunks (fewer duplicates per chunk) give the same report."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json,sys; sys.path.insert(0, %r)\n"
+        "from paper_2604_09221_b200 import builtin, sweep, SweepRange\n"
+        "r = sweep(builtin('delaunay-7'), SweepRange(99, 99 + (1 << 25)), raw_space=True)\n"
+        "print(json.dumps([list(r.oval_histogram), sorted(r.scheme_map.items())]))\n"
+        % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    res = {}
+    for lg in ("14", "21"):
+        env = dict(os.environ, TCG_CHUNK_LOG2=lg)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        assert p.returncode == 0, p.stderr
+        res[lg] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["14"] == res["21"]
