@@ -1870,7 +1870,8 @@ struct tcg_plan {
     int64_t launches = 0;
     // tile contraction (sweeps): per domain (raw, representative)
     TileTables *d_tiles = nullptr;   // [2]
-    TileRec *d_recs = nullptr;       // [chunk_tiles()]
+    TileRec *d_recs = nullptr;       // [chunk_cap]
+    uint32_t chunk_cap = 0;          // tiles the record / dedup buffers hold (power of two)
     uint32_t *d_dedup = nullptr;     // slots[2C] | mint[C] | dup[C] | count[1] | list[C]
     unsigned long long *d_tstats = nullptr;  // [1] tiles classified after deduplication
     int dedup = -1;                  // -1: TCG_NO_DEDUP decides
@@ -1988,15 +1989,25 @@ size_t cls_smem(int K) {
     return (size_t)32 * K * K * 4 + TABLE_SMEM + sizeof(TileTables) + CLS_WARPS * sizeof(TileRec);
 }
 
-// Tiles per contraction chunk (records: 1 KiB each).  Larger chunks find more
-// duplicate tiles; TCG_CHUNK_LOG2 (14..21) overrides the default.
+// Tiles per contraction chunk (records: 1 KiB each).  Deduplication works
+// within a chunk, and larger chunks find many more duplicates (C3: 1.6x at
+// 2^20 tiles, 2.4x at 2^23), so the default is 2^23 tiles (8.9 GB of records,
+// allocated on demand and only as large as the sweep needs, halved while it
+// would take more than a quarter of the free HBM).  TCG_CHUNK_LOG2 (14..23)
+// overrides.
 static uint32_t chunk_tiles() {
     static const uint32_t c = [] {
-        int lg = 20;
-        if (const char *e = std::getenv("TCG_CHUNK_LOG2")) lg = std::max(14, std::min(21, std::atoi(e)));
+        int lg = 23;
+        if (const char *e = std::getenv("TCG_CHUNK_LOG2")) lg = std::max(14, std::min(23, std::atoi(e)));
         return 1u << lg;
     }();
     return c;
+}
+
+static uint32_t next_pow2(uint32_t x) {
+    uint32_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
 }
 
 void *pick_batch(int K, bool even) {
@@ -2342,6 +2353,8 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
     for (int mode = 0; mode < 3; ++mode) {
         void *fn = pick_enum(K, P->even, mode);
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_enum);
+        if (const char *c = std::getenv("TCG_ENUM_CARVEOUT"))
+            cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(c));
     }
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_enum(K, P->even, MODE_RAW),
                                                            THREADS, P->smem_enum)) != cudaSuccess)
@@ -2584,18 +2597,38 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
     P->pending_mask = mask;
     if (mode != MODE_SAMPLE && P->tiles_ok[mode] && end > start) {
         // chunks of chunk_tiles() tiles: contract, deduplicate, classify
-        if (!P->d_recs) {  // contraction records: allocated on the first tiled sweep
-            CUDA_TRY(cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)chunk_tiles()));
-            CUDA_TRY(cudaMalloc(&P->d_tstats, sizeof(unsigned long long)));
-            CUDA_TRY(cudaMemsetAsync(P->d_tstats, 0, sizeof(unsigned long long), P->stream));
-        }
         void *fb = pick_build(P->K, mode);
         void *fc = pick_cls(P->K, P->even, mode);
         const TileTables *tt = P->d_tiles + mode;
         const int bits = P->tile_bits[mode];
         const uint64_t t_end = ((end - 1) >> bits) + 1;
         // per-CTA scheme counters are 32-bit: keep a launch below 2^31 patchworks
-        const uint32_t chunk = std::min<uint32_t>(chunk_tiles(), 1u << (31 - bits));
+        uint32_t chunk = std::min<uint32_t>(chunk_tiles(), 1u << (31 - bits));
+        chunk = std::min<uint32_t>(chunk, next_pow2((uint32_t)std::min<uint64_t>(
+                                              t_end - (start >> bits), 1u << 30)));
+        if (chunk > P->chunk_cap) {  // (re)allocate the contraction records + dedup table
+            CUDA_TRY(cudaStreamSynchronize(P->stream));
+            size_t fr = 0, tot = 0;
+            CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+            if (P->d_recs) fr += sizeof(TileRec) * (size_t)P->chunk_cap;
+            const size_t per_tile = sizeof(TileRec) + 5 * sizeof(uint32_t);
+            while (chunk > (1u << 14) && (size_t)chunk * per_tile > fr / 4) chunk >>= 1;
+            if (chunk > P->chunk_cap) {
+                cudaFree(P->d_recs);
+                cudaFree(P->d_dedup);
+                P->d_recs = nullptr;
+                P->d_dedup = nullptr;
+                P->chunk_cap = 0;
+                CUDA_TRY(cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)chunk));
+                CUDA_TRY(cudaMalloc(&P->d_dedup, sizeof(uint32_t) * (5 * (size_t)chunk + 1)));
+                P->chunk_cap = chunk;
+            }
+        }
+        chunk = std::min(chunk, P->chunk_cap);
+        if (!P->d_tstats) {
+            CUDA_TRY(cudaMalloc(&P->d_tstats, sizeof(unsigned long long)));
+            CUDA_TRY(cudaMemsetAsync(P->d_tstats, 0, sizeof(unsigned long long), P->stream));
+        }
         for (uint64_t t0 = start >> bits; t0 < t_end; t0 += chunk) {
             uint32_t nt = (uint32_t)std::min<uint64_t>(chunk, t_end - t0);
             uint64_t tile0 = t0;
@@ -2614,13 +2647,14 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             const TileRec *crecs = recs;
             const uint32_t *list = nullptr, *cnt = nullptr, *dup = nullptr, *mint = nullptr;
             if (P->dedup < 0 ? dedup_enabled() : P->dedup != 0) {
-                const size_t C = chunk_tiles();
-                if (!P->d_dedup) CUDA_TRY(cudaMalloc(&P->d_dedup, sizeof(uint32_t) * (5 * C + 1)));
+                const size_t C = P->chunk_cap, Cn = next_pow2(nt);  // Cn <= C
                 uint32_t *slots = P->d_dedup, *mnt = slots + 2 * C, *dp = mnt + C, *ct = dp + C,
                          *ls = ct + 1;
-                CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(uint32_t) * 3 * C, P->stream));
-                CUDA_TRY(cudaMemsetAsync(dp, 0, sizeof(uint32_t) * (C + 1), P->stream));
-                uint32_t smask = (uint32_t)(2 * C - 1);
+                CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(uint32_t) * 2 * Cn, P->stream));
+                CUDA_TRY(cudaMemsetAsync(mnt, 0xff, sizeof(uint32_t) * nt, P->stream));
+                CUDA_TRY(cudaMemsetAsync(dp, 0, sizeof(uint32_t) * nt, P->stream));
+                CUDA_TRY(cudaMemsetAsync(ct, 0, sizeof(uint32_t), P->stream));
+                uint32_t smask = (uint32_t)(2 * Cn - 1);
                 int ibits = bits;
                 void *ad[] = {&crecs, &nt, &tile0, &ibits, &lo, &hi, &slots, &smask, &dp, &mnt, &ls, &ct};
                 const unsigned gd = (unsigned)std::min<uint64_t>(
