@@ -1871,8 +1871,8 @@ struct tcg_plan {
     // tile contraction (sweeps): per domain (raw, representative)
     TileTables *d_tiles = nullptr;   // [2]
     TileRec *d_recs = nullptr;       // [chunk_cap]
-    uint32_t chunk_cap = 0;          // tiles the record / dedup buffers hold (power of two)
-    uint32_t *d_dedup = nullptr;     // slots[2C] | mint[C] | dup[C] | count[1] | list[C]
+    uint32_t chunk_cap = 0;          // tiles the record / dedup buffers hold
+    uint32_t *d_dedup = nullptr;     // slots[2 pow2(C)] | mint[C] | dup[C] | count[1] | list[C]
     unsigned long long *d_tstats = nullptr;  // [1] tiles classified after deduplication
     int dedup = -1;                  // -1: TCG_NO_DEDUP decides
     int64_t tiles_built = 0;
@@ -1991,14 +1991,14 @@ size_t cls_smem(int K) {
 
 // Tiles per contraction chunk (records: 1 KiB each).  Deduplication works
 // within a chunk, and larger chunks find many more duplicates (C3: 1.6x at
-// 2^20 tiles, 2.4x at 2^23), so the default is 2^23 tiles (8.9 GB of records,
+// 2^20 tiles, 2.4x at 2^23), so the default is 2^24 tiles (18 GB of records,
 // allocated on demand and only as large as the sweep needs, halved while it
-// would take more than a quarter of the free HBM).  TCG_CHUNK_LOG2 (14..23)
+// would take more than a quarter of the free HBM).  TCG_CHUNK_LOG2 (14..24)
 // overrides.
 static uint32_t chunk_tiles() {
     static const uint32_t c = [] {
-        int lg = 23;
-        if (const char *e = std::getenv("TCG_CHUNK_LOG2")) lg = std::max(14, std::min(23, std::atoi(e)));
+        int lg = 24;
+        if (const char *e = std::getenv("TCG_CHUNK_LOG2")) lg = std::max(14, std::min(24, std::atoi(e)));
         return 1u << lg;
     }();
     return c;
@@ -2602,8 +2602,8 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
         const TileTables *tt = P->d_tiles + mode;
         const int bits = P->tile_bits[mode];
         const uint64_t t_end = ((end - 1) >> bits) + 1;
-        // per-CTA scheme counters are 32-bit: keep a launch below 2^31 patchworks
-        uint32_t chunk = std::min<uint32_t>(chunk_tiles(), 1u << (31 - bits));
+        // per-CTA scheme counters are 32-bit: a launch covers < 2^32 patchworks
+        uint32_t chunk = std::min<uint32_t>(chunk_tiles(), (uint32_t)(0xffffffffull >> bits));
         chunk = std::min<uint32_t>(chunk, next_pow2((uint32_t)std::min<uint64_t>(
                                               t_end - (start >> bits), 1u << 30)));
         if (chunk > P->chunk_cap) {  // (re)allocate the contraction records + dedup table
@@ -2611,7 +2611,7 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             size_t fr = 0, tot = 0;
             CUDA_TRY(cudaMemGetInfo(&fr, &tot));
             if (P->d_recs) fr += sizeof(TileRec) * (size_t)P->chunk_cap;
-            const size_t per_tile = sizeof(TileRec) + 5 * sizeof(uint32_t);
+            const size_t per_tile = sizeof(TileRec) + 7 * sizeof(uint32_t);
             while (chunk > (1u << 14) && (size_t)chunk * per_tile > fr / 4) chunk >>= 1;
             if (chunk > P->chunk_cap) {
                 cudaFree(P->d_recs);
@@ -2620,7 +2620,8 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 P->d_dedup = nullptr;
                 P->chunk_cap = 0;
                 CUDA_TRY(cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)chunk));
-                CUDA_TRY(cudaMalloc(&P->d_dedup, sizeof(uint32_t) * (5 * (size_t)chunk + 1)));
+                CUDA_TRY(cudaMalloc(&P->d_dedup, sizeof(uint32_t) * (2 * (size_t)next_pow2(chunk) +
+                                                                     3 * (size_t)chunk + 1)));
                 P->chunk_cap = chunk;
             }
         }
@@ -2647,9 +2648,9 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             const TileRec *crecs = recs;
             const uint32_t *list = nullptr, *cnt = nullptr, *dup = nullptr, *mint = nullptr;
             if (P->dedup < 0 ? dedup_enabled() : P->dedup != 0) {
-                const size_t C = P->chunk_cap, Cn = next_pow2(nt);  // Cn <= C
-                uint32_t *slots = P->d_dedup, *mnt = slots + 2 * C, *dp = mnt + C, *ct = dp + C,
-                         *ls = ct + 1;
+                const size_t C = P->chunk_cap, Cn = next_pow2(nt);  // Cn <= next_pow2(C)
+                uint32_t *slots = P->d_dedup, *mnt = slots + 2 * (size_t)next_pow2(P->chunk_cap),
+                         *dp = mnt + C, *ct = dp + C, *ls = ct + 1;
                 CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(uint32_t) * 2 * Cn, P->stream));
                 CUDA_TRY(cudaMemsetAsync(mnt, 0xff, sizeof(uint32_t) * nt, P->stream));
                 CUDA_TRY(cudaMemsetAsync(dp, 0, sizeof(uint32_t) * nt, P->stream));
