@@ -402,8 +402,8 @@ def run_ours(args, rank, world, local_rank):
             "dedup": {"tiles": tiles_built, "tiles_classified": tiles_classified,
                       "factor": tiles_built / tiles_classified if tiles_classified else None,
                       "note": "tiles with identical contracted records are classified once "
-                              "and counted with their multiplicity (exact; per chunk of "
-                              "2^20 tiles)"},
+                              "and counted with their multiplicity (exact; within each sweep "
+                              "call, chunks of up to 2^24-1 tiles; never across steps)"},
         },
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "patchworks/s", "h2d_bytes_per_step": 16,
