@@ -123,10 +123,19 @@ int tcg_kernel_times(tcg_plan *plan, double *ms, int64_t *counts);
  * witness is taken from the group's smallest tile, so reports are unchanged).
  * enable: 1 on, 0 off, -1 default (on unless TCG_NO_DEDUP=1). */
 int tcg_plan_set_dedup(tcg_plan *plan, int enable);
-/* out[0] = tiles contracted, out[1] = tiles classified (= out[0] without
- * deduplication) since the last call
+/* out[0] = tiles contracted, out[1] = distinct tiles (level-1 representatives;
+ * = out[0] without deduplication) since the last call
  * (synchronises the plan's stream); resets both. */
 int tcg_tile_stats(tcg_plan *plan, int64_t *out);
+/* Level-2 contraction (odd degree sweeps, on by default with deduplication;
+ * TCG_NO_L2=1 or enable=0 turns it off): each representative tile is split
+ * into 2^(b-5) records of 32 patchworks with the other tile bits fixed, and
+ * equal records are classified once (exact, like tile deduplication).
+ * tcg_level2_stats: out[0] = records built, out[1] = records classified,
+ * out[2] = tiles the level-1 classifier took while level 2 ran (range ends,
+ * graphs over 32 nodes, fallback tiles); all since the last call. */
+int tcg_plan_set_level2(tcg_plan *plan, int enable);
+int tcg_level2_stats(tcg_plan *plan, int64_t *out);
 
 /* classify_bits_kernel, batched.  sigma[t] bit k = sign of point k.
  * Outputs per patchwork: tree key, oval count, region count, status. */

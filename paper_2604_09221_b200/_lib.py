@@ -66,6 +66,8 @@ def load():
         L.tcg_kernel_times.argtypes = [P, C.c_void_p, C.c_void_p]
         L.tcg_plan_set_dedup.argtypes = [P, C.c_int]
         L.tcg_tile_stats.argtypes = [P, C.c_void_p]
+        L.tcg_plan_set_level2.argtypes = [P, C.c_int]
+        L.tcg_level2_stats.argtypes = [P, C.c_void_p]
         L.tcg_classify_batch.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p]
         L.tcg_classify_batch_device.argtypes = L.tcg_classify_batch.argtypes
@@ -103,6 +105,7 @@ def load():
 EXPORTS = (
     "tcg_plan_create", "tcg_plan_destroy", "tcg_plan_set_stream", "tcg_plan_info",
     "tcg_plan_set_timing", "tcg_kernel_times", "tcg_plan_set_dedup", "tcg_tile_stats",
+    "tcg_plan_set_level2", "tcg_level2_stats",
     "tcg_classify_batch", "tcg_classify_batch_device", "tcg_sweep", "tcg_sample",
     "tcg_agg_reset", "tcg_sweep_async", "tcg_sample_async", "tcg_agg_fetch",
     "tcg_sweep_multi", "tcg_sample_multi", "tcg_last_error", "tcg_device_count",
@@ -326,6 +329,18 @@ class NativePlan:
         """Tile deduplication on / off / None = default (see tcg.h)."""
         flag = -1 if enable is None else int(bool(enable))
         _check(self._L.tcg_plan_set_dedup(self.h, flag), "tcg_plan_set_dedup")
+
+    def set_level2(self, enable: bool | None):
+        """Level-2 contraction on / off / None = default (see tcg.h)."""
+        flag = -1 if enable is None else int(bool(enable))
+        _check(self._L.tcg_plan_set_level2(self.h, flag), "tcg_plan_set_level2")
+
+    def level2_stats(self):
+        """(level-2 records built, level-2 records classified, tiles left to the
+        level-1 classifier while level 2 ran) since the last call."""
+        out = np.zeros(3, np.int64)
+        _check(self._L.tcg_level2_stats(self.h, out.ctypes.data), "tcg_level2_stats")
+        return int(out[0]), int(out[1]), int(out[2])
 
     def tile_stats(self):
         """(tiles contracted, tiles classified) since the last call."""

@@ -870,7 +870,7 @@ constexpr int TILE_BITS_MAX = 12;
 constexpr int MAXC = 48;  // fixed components per tile
 constexpr int MAXF = 32;  // free vertices
 
-struct TileTables {  // per plan and domain (raw / representative), device memory
+struct alignas(16) TileTables {  // per plan and domain (raw / representative), device memory
     int nf, nfixed, bits, maxnodes;  // maxnodes: contraction size limit (64; lower only in tests)
     uint32_t fixed[MAXK];                  // used and not free (layout mask)
     uint32_t fword[MAXF], fbit[MAXF];      // layout word / bit of free node f
@@ -881,6 +881,13 @@ struct TileTables {  // per plan and domain (raw / representative), device memor
     // free-node sign words for the tile-local index: fsign[0][low & 63] ^
     // fsign[1][(low >> 6) & 63] (parity folded into fsign[0])
     unsigned long long fsign[2][64];
+    // level-2 contraction (odd degree): index bits 0..4 are the B points (one
+    // per lane), bits 5..bits-1 the A points fixed per level-2 record
+    int l2, nB, NA, la;                     // enabled, B nodes, A patterns = 2^la
+    uint32_t fa, fbm;                       // free-node masks of A and B nodes
+    int8_t l2j[MAXF];                       // free node -> B index (or -1)
+    uint32_t l2adjB[16], l2linkB[16];       // B-B adjacency / links (B index space)
+    uint32_t l2bsign[32];                   // B-node signs for tile-local bits 0..4
 };
 
 // Contracted tile, written by k_tile_build and staged into shared memory by
@@ -1369,13 +1376,25 @@ __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restric
     const int lane = threadIdx.x & 31;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    // representatives found by this warp are buffered one per lane and
+    // appended 32 at a time (one atomic per 32 instead of one per tile)
+    uint32_t mine = 0, nmine = 0;
+    auto push = [&](uint32_t t) {
+        if (lane == (int)nmine) mine = t;
+        if (++nmine == 32u) {
+            uint32_t at = 0;
+            if (lane == 0) at = atomicAdd(count, 32u);
+            list[__shfl_sync(0xffffffffu, at, 0) + lane] = mine;
+            nmine = 0;
+        }
+    };
     for (uint32_t t = warp; t < ntiles; t += nwarps) {
         const TileRec *r = recs + t;
         const int nn = r->nnodes, n = r->n;
         const unsigned long long sg = r->sgn_fixed;
         const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
         if (r->fallback || b0 < start || b1 > end) {
-            if (lane == 0) list[atomicAdd(count, 1u)] = t;
+            push(t);
             continue;
         }
         const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
@@ -1396,10 +1415,11 @@ __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restric
         uint4 ra, rb;
         load(r, ra, rb);
         unsigned long long h =
-            mix64(((unsigned long long)ra.y << 32 | ra.x) + 0x9E3779B97F4A7C15ull * (lane + 1)) ^
-            mix64(((unsigned long long)ra.w << 32 | ra.z) + 0xD1B54A32D192ED03ull * (lane + 1)) ^
-            mix64(((unsigned long long)rb.y << 32 | rb.x) + 0x8CB92BA72F3D8DD7ull * (lane + 1)) ^
-            mix64(((unsigned long long)rb.w << 32 | rb.z) + 0xABC98388FB8FAC03ull * (lane + 1));
+            mix64(((unsigned long long)ra.z << 32 | ra.x) + 0x9E3779B97F4A7C15ull * (lane + 1));
+        if (nn > 32)  // warp-uniform
+            h ^= mix64(((unsigned long long)ra.w << 32 | ra.y) + 0xD1B54A32D192ED03ull * (lane + 1)) ^
+                 mix64(((unsigned long long)rb.y << 32 | rb.x) + 0x8CB92BA72F3D8DD7ull * (lane + 1)) ^
+                 mix64(((unsigned long long)rb.w << 32 | rb.z) + 0xABC98388FB8FAC03ull * (lane + 1));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
         h ^= mix64(sg ^ ((unsigned long long)nn << 56) ^ ((unsigned long long)n << 48));
@@ -1415,7 +1435,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restric
             }
             cur = __shfl_sync(0xffffffffu, cur, 0);
             if (cur == t) {  // new representative
-                if (lane == 0) list[atomicAdd(count, 1u)] = t;
+                push(t);
                 break;
             }
             const TileRec *o = recs + cur;
@@ -1435,6 +1455,12 @@ __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restric
             }
             at = (at + 1) & smask;
         }
+    }
+    if (nmine) {  // flush the partial buffer
+        uint32_t at = 0;
+        if (lane == 0) at = atomicAdd(count, nmine);
+        at = __shfl_sync(0xffffffffu, at, 0);
+        if (lane < (int)nmine) list[at + lane] = mine;
     }
 }
 
@@ -1542,6 +1568,302 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
             }
             tab.add<true>(g, k, r.nreg, m, weight);
         }
+        __syncwarp();
+    }
+    __syncthreads();
+    tab.flush(g);
+}
+
+// ------------------------------------------------------------ level 2
+// Level-2 contraction of a representative tile (odd degree, <= 32 nodes).
+// Fix the signs of the A points (tile-local index bits 5..bits-1) as well:
+// the fixed components and the A nodes then merge, through same-sign edges
+// and antipodal links, into "super-nodes" -- subsets of regions whatever
+// the B signs (bits 0..4) are.  A super-node mixes signs, so its edges to a
+// B node are recorded by the sign of the member they leave from (plusB /
+// minusB); edges between two super-nodes are always crossed (a same-sign
+// edge would have merged them).  One record (header + one u64 per
+// super-node) describes 32 patchworks, one per lane.  Records built from
+// different tiles coincide far more often than level-1 records do, and are
+// deduplicated the same way (exact comparison, weights add, witness = the
+// smallest (tile, A) position of the group).
+//   word[s] = crossS | (plusB | minusB << nB | linkB << 2nB | self << 3nB) << 32
+constexpr uint32_t L2_EMPTY = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t l2_compress(const TileTables &tt, uint32_t freemask) {
+    uint32_t r = 0;
+    while (freemask) {
+        const int f = __ffs(freemask) - 1;
+        freemask &= freemask - 1u;
+        r |= 1u << tt.l2j[f];
+    }
+    return r;
+}
+
+// One thread per (representative tile, A pattern) of list1[i0 .. i0+nb).
+__global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restrict__ tt_g,
+                                                      const TileRec *__restrict__ recs,
+                                                      const uint32_t *__restrict__ list1,
+                                                      const uint32_t *__restrict__ dup1,
+                                                      const uint32_t *__restrict__ mint1,
+                                                      uint32_t i0, uint32_t nb, uint64_t tile0,
+                                                      uint64_t start, uint64_t end,
+                                                      unsigned long long *__restrict__ pool,
+                                                      uint32_t stride,
+                                                      unsigned long long *__restrict__ hashes,
+                                                      uint32_t *__restrict__ wts,
+                                                      uint32_t *__restrict__ poss,
+                                                      uint32_t *__restrict__ oldlist,
+                                                      uint32_t *__restrict__ oldcount) {
+    __shared__ TileTables tts;
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    __syncthreads();
+    const TileTables &tt = tts;
+    const int la = tt.la, nB = tt.nB, bits = tt.bits;
+    const uint32_t nrec = nb << la;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nrec; j += gridDim.x * blockDim.x) {
+        const uint32_t i = i0 + (j >> la), a = j & ((1u << la) - 1u);
+        const uint32_t t = list1[i];
+        const TileRec *rec = recs + t;
+        const int nn = rec->nnodes, n = rec->n;
+        const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
+        if (rec->fallback || nn > 32 || b0 < start || b1 > end) {
+            if (a == 0) oldlist[atomicAdd(oldcount, 1u)] = t;
+            wts[j] = 0u;
+            continue;
+        }
+        const uint2 *R = rows2(rec);
+        const uint32_t lowA = a << 5;
+        const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
+        const uint32_t sg1 = (uint32_t)rec->sgn_fixed | ((uint32_t)fsA & tt.fa) << n;
+        const uint32_t G = (n >= 32 ? ~0u : ((1u << n) - 1u)) | (tt.fa << n);
+        const uint32_t FBn = tt.fbm << n;
+        uint32_t Mem[32], CG[32], HI[32];
+        uint32_t unv = G;
+        int m = 0;
+        while (unv) {
+            uint32_t f = unv & (0u - unv);
+            unv ^= f;
+            uint32_t M = f, cg = 0, pb = 0, mb = 0, lb = 0;
+            while (f) {
+                const int u = __ffs(f) - 1;
+                f &= f - 1u;
+                const uint2 row = R[u];
+                const uint32_t diff = sg1 ^ (0u - ((sg1 >> u) & 1u));  // nodes of the other sign
+                const uint32_t nw = ((row.x & ~diff) | row.y) & unv;
+                unv ^= nw;
+                f |= nw;
+                M |= nw;
+                cg |= row.x & G & diff;
+                const uint32_t bp = row.x & FBn;
+                if ((sg1 >> u) & 1u) pb |= bp;
+                else mb |= bp;
+                lb |= row.y & FBn;
+            }
+            Mem[m] = M;
+            CG[m] = cg;
+            HI[m] = l2_compress(tt, pb >> n) | l2_compress(tt, mb >> n) << nB |
+                    l2_compress(tt, lb >> n) << (2 * nB);
+            ++m;
+        }
+        unsigned long long *out = pool + (size_t)j * stride;
+        unsigned long long h = mix64(0x51ED2701u + (unsigned long long)m);
+        out[0] = (unsigned long long)m;
+        for (int q = 0; q < m; ++q) {
+            uint32_t cs = 0;
+            for (int q2 = 0; q2 < m; ++q2)
+                if (CG[q] & Mem[q2]) cs |= 1u << q2;
+            const uint32_t self = (cs >> q) & 1u;
+            cs &= ~(1u << q);
+            const unsigned long long w =
+                (unsigned long long)cs |
+                (unsigned long long)(HI[q] | self << (3 * nB)) << 32;
+            out[1 + q] = w;
+            h = mix64(h ^ (w + 0x9E3779B97F4A7C15ull * (q + 1)));
+        }
+        hashes[j] = h;
+        wts[j] = 1u + dup1[t];
+        poss[j] = (min(t, mint1[t]) << la) | a;
+    }
+}
+
+// One thread per level-2 record: exact deduplication (hash, then word-by-word).
+__global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *__restrict__ pool,
+                                                      uint32_t stride, uint32_t nrec,
+                                                      const unsigned long long *__restrict__ hashes,
+                                                      const uint32_t *__restrict__ wts,
+                                                      const uint32_t *__restrict__ poss,
+                                                      uint32_t *__restrict__ slots, uint32_t smask,
+                                                      uint32_t *__restrict__ w2,
+                                                      uint32_t *__restrict__ pos2,
+                                                      uint32_t *__restrict__ list2,
+                                                      uint32_t *__restrict__ count2) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t tot = gridDim.x * blockDim.x;
+    const uint32_t jmax = (nrec + 31u) & ~31u;  // whole warps iterate together
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < jmax; j += tot) {
+        bool isnew = false;
+        if (j < nrec && wts[j]) {
+            const unsigned long long h = hashes[j];
+            const unsigned long long *mine = pool + (size_t)j * stride;
+            const int m = (int)mine[0];
+            uint32_t at = (uint32_t)(h >> 17) & smask;
+            while (true) {
+                uint32_t cur = slots[at];
+                if (cur == L2_EMPTY) {
+                    const uint32_t prev = atomicCAS(&slots[at], L2_EMPTY, j);
+                    cur = prev == L2_EMPTY ? j : prev;
+                }
+                if (cur == j) {
+                    isnew = true;
+                    atomicAdd(&w2[j], wts[j]);
+                    atomicMin(&pos2[j], poss[j]);
+                    break;
+                }
+                bool eq = hashes[cur] == h;
+                if (eq) {
+                    const unsigned long long *o = pool + (size_t)cur * stride;
+                    eq = (int)o[0] == m;
+                    for (int q = 1; q <= m && eq; ++q) eq = o[q] == mine[q];
+                }
+                if (eq) {
+                    atomicAdd(&w2[cur], wts[j]);
+                    atomicMin(&pos2[cur], poss[j]);
+                    break;
+                }
+                at = (at + 1) & smask;
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, isnew);
+        if (bal) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(count2, (uint32_t)__popc(bal));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (isnew) list2[base + __popc(bal & ((1u << lane) - 1u))] = j;
+        }
+    }
+}
+
+// Level-2 node pass.  Node rows (shared memory, SoA by node):
+//   same  = (A & ~T) | (B & T) | (s_v ? Cp : Cm) | L
+//   cross = (A &  T) | (B & ~T) | (s_v ? Cm : Cp) | X,   T = S ^ (s_v ? ~0 : 0)
+// super-node: A = minusB, B = plusB, Cp = Cm = 0, L = linkB, X = crossS | self
+// B node:     A = adjB, B = 0, Cp = plusS, Cm = minusS, L = linkBB | linkS, X = 0
+// (S = the lane's B-node signs; super-nodes carry sign 0).
+struct L2Rows {
+    uint32_t A[32], B[32], Cp[32], Cm[32], L[32], X[32];
+    unsigned long long W[32];
+};
+
+__device__ __forceinline__ void l2_node_pass(const L2Rows &rw, uint32_t S, int nn,
+                                             Regions<1> &out) {
+    uint32_t un = nn >= 32 ? ~0u : ((1u << nn) - 1u), f = 0, x = 0, r = 0;
+    int nreg = 0;
+    auto seed = [&]() {
+        f = un & (0u - un);
+        r = un;
+        un ^= f;
+        x = 0u;
+    };
+    seed();
+    for (int it = 0; it < nn; ++it) {
+        if (f == 0u) {
+            if (nreg < MAXR) {
+                out.R[nreg][0] = r ^ un;
+                out.X[nreg][0] = x;
+            }
+            ++nreg;
+            seed();
+        }
+        const int v = __ffs(f) - 1;
+        f &= f - 1u;
+        const uint32_t sv = (S >> v) & 1u;
+        const uint32_t T = S ^ (0u - sv);
+        const uint32_t a = rw.A[v], b = rw.B[v], cp = rw.Cp[v], cm = rw.Cm[v];
+        const uint32_t same = (a & ~T) | (b & T) | (sv ? cp : cm) | rw.L[v];
+        x |= (a & T) | (b & ~T) | (sv ? cm : cp) | rw.X[v];
+        const uint32_t nw = same & un;
+        un ^= nw;
+        f |= nw;
+    }
+    if (nreg < MAXR) {
+        out.R[nreg][0] = r ^ un;
+        out.X[nreg][0] = x;
+    }
+    out.nreg = nreg + 1;
+    out.oddmask = 0u;
+}
+
+constexpr size_t L2_CLS_SMEM = TABLE_SMEM + sizeof(TileTables) + CLS_WARPS * sizeof(L2Rows);
+
+// One warp per representative level-2 record; lane b classifies B pattern b.
+__global__ void __launch_bounds__(THREADS) k_l2_classify(KParams p,
+                                                         const TileTables *__restrict__ tt_g,
+                                                         const unsigned long long *__restrict__ pool,
+                                                         uint32_t stride,
+                                                         const uint32_t *__restrict__ list2,
+                                                         const uint32_t *__restrict__ count2,
+                                                         const uint32_t *__restrict__ w2,
+                                                         const uint32_t *__restrict__ pos2,
+                                                         uint64_t tile0, DevAgg g,
+                                                         unsigned long long *__restrict__ tstats) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    CtaTable tab = carve_table(smem);
+    TileTables *tt = reinterpret_cast<TileTables *>(reinterpret_cast<char *>(smem) + TABLE_SMEM);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    L2Rows *rw = reinterpret_cast<L2Rows *>(tt + 1) + w;
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    tab.init();
+    __syncthreads();
+    const int nB = tt->nB, bits = tt->bits;
+    const uint32_t bm = (1u << nB) - 1u;
+    const uint32_t n2 = *count2;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(tstats, (unsigned long long)n2);
+    const uint32_t Sb = tt->l2bsign[lane];
+    for (uint32_t i = blockIdx.x * CLS_WARPS + w; i < n2; i += gridDim.x * CLS_WARPS) {
+        const uint32_t j = list2[i];
+        const unsigned long long *rec = pool + (size_t)j * stride;
+        const int m = (int)rec[0];
+        if (lane < m) rw->W[lane] = rec[1 + lane];
+        __syncwarp();
+        if (lane < m) {
+            const unsigned long long wd = rw->W[lane];
+            const uint32_t hi = (uint32_t)(wd >> 32);
+            rw->A[lane] = ((hi >> nB) & bm) << m;
+            rw->B[lane] = (hi & bm) << m;
+            rw->Cp[lane] = 0u;
+            rw->Cm[lane] = 0u;
+            rw->L[lane] = ((hi >> (2 * nB)) & bm) << m;
+            rw->X[lane] = (uint32_t)wd | (((hi >> (3 * nB)) & 1u) << lane);
+        }
+        if (lane < nB) {
+            uint32_t ps = 0, ms = 0, ls = 0;
+            for (int q = 0; q < m; ++q) {
+                const uint32_t hi = (uint32_t)(rw->W[q] >> 32);
+                ps |= ((hi >> lane) & 1u) << q;
+                ms |= ((hi >> (nB + lane)) & 1u) << q;
+                ls |= ((hi >> (2 * nB + lane)) & 1u) << q;
+            }
+            const int v = m + lane;
+            rw->A[v] = tt->l2adjB[lane] << m;
+            rw->B[v] = 0u;
+            rw->Cp[v] = ps;
+            rw->Cm[v] = ms;
+            rw->L[v] = (tt->l2linkB[lane] << m) | ls;
+            rw->X[v] = 0u;
+        }
+        __syncwarp();
+        Regions<1> rg;
+        l2_node_pass(*rw, Sb << m, m + nB, rg);
+        const uint32_t SG1[1] = {0u};
+        const Result r = finish<1, false, false>(p, SG1, rg, p.maxreg);
+        const uint64_t mw = (tile0 << bits) + ((uint64_t)pos2[j] << 5) + lane;
+        uint64_t k = 0;
+        if (r.status == TCG_OK) k = r.key;
+        else atomicMin(g.bad, (unsigned long long)mw);
+        tab.add<true>(g, k, r.nreg, mw, w2[j]);
         __syncwarp();
     }
     __syncthreads();
@@ -1873,7 +2195,17 @@ struct tcg_plan {
     TileRec *d_recs = nullptr;       // [chunk_cap]
     uint32_t chunk_cap = 0;          // tiles the record / dedup buffers hold
     uint32_t *d_dedup = nullptr;     // slots[2 pow2(C)] | mint[C] | dup[C] | count[1] | list[C]
-    unsigned long long *d_tstats = nullptr;  // [1] tiles classified after deduplication
+    unsigned long long *d_tstats = nullptr;  // [0] level-1 reps classified, [1] level-2 reps
+    int l2_ok[2] = {0, 0};           // level-2 contraction available per domain
+    TileTables h_tiles[2];           // host copies of the tile tables
+    int blocks_l2cls = 0;
+    int l2 = -1;                     // -1: TCG_NO_L2 decides
+    int l2_stride = 0;               // u64 words per level-2 record
+    size_t l2_cap = 0;               // level-2 records the buffers hold
+    unsigned long long *d_l2pool = nullptr, *d_l2hash = nullptr;
+    uint32_t *d_l2u32 = nullptr;     // wts | poss | w2 | pos2 | list2 | slots(2 pow2) | count2
+    uint32_t *d_oldlist = nullptr;   // [chunk_cap + 1]: count, then tiles for the level-1 path
+    int64_t reps1_host = 0, l2_built = 0;
     int dedup = -1;                  // -1: TCG_NO_DEDUP decides
     int64_t tiles_built = 0;
     int tiles_ok[2] = {0, 0};
@@ -2124,6 +2456,40 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
             T.fadj[fv] |= 1ull << fu;
         }
     }
+    // level-2 tables (filled after fadj / fpl below)
+    auto l2_tables = [&]() {
+        T.l2 = 0;
+        if (d % 2 == 0 || bits < 6 || bits > 10 || nf > 32) return;
+        uint32_t fb = 0, fa = 0;
+        for (int i = 0; i < bits; ++i) (i < 5 ? fb : fa) |= (uint32_t)T.fcopy[i];
+        const int nB = __builtin_popcount(fb);
+        if (nB > 10 || nB == 0) return;
+        T.fbm = fb;
+        T.fa = fa;
+        T.nB = nB;
+        T.la = bits - 5;
+        T.NA = 1 << T.la;
+        int j = 0;
+        int fj[32];
+        for (int f = 0; f < MAXF; ++f) T.l2j[f] = -1;
+        for (int f = 0; f < nf; ++f)
+            if ((fb >> f) & 1u) {
+                T.l2j[f] = (int8_t)j;
+                fj[j++] = f;
+            }
+        auto comp = [&](unsigned long long x) {
+            uint32_t r = 0;
+            for (int f = 0; f < nf; ++f)
+                if (((x >> f) & 1ull) && T.l2j[f] >= 0) r |= 1u << T.l2j[f];
+            return r;
+        };
+        for (int q = 0; q < nB; ++q) {
+            T.l2adjB[q] = comp(T.fadj[fj[q]] & fb);
+            T.l2linkB[q] = comp(T.fpl[fj[q]] & fb);
+        }
+        for (int b = 0; b < 32; ++b) T.l2bsign[b] = comp(T.fsign[0][b] & fb);
+        T.l2 = 1;
+    };
     for (int a = 0; a < D->nap; ++a) {
         const int fu = fnode[D->ap_u[a]], fv = fnode[D->ap_v[a]];
         if ((fu >= 0) != (fv >= 0)) return false;  // cannot happen: p and -p share src
@@ -2132,6 +2498,7 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
             T.fpl[fv] |= 1ull << fu;
         }
     }
+    l2_tables();
     return T.nfixed > 0 && nf > 0;
 }
 
@@ -2330,6 +2697,8 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
             P->tiles_ok[mode] = (!no_tiles || !*no_tiles || no_tiles[0] == '0') &&
                                 build_tiles(D, L, mode, tt[mode]);
             P->tile_bits[mode] = P->tiles_ok[mode] ? tt[mode].bits : 0;
+            P->l2_ok[mode] = P->tiles_ok[mode] && tt[mode].l2;
+            P->h_tiles[mode] = tt[mode];
         }
         if ((e = cudaMalloc(&P->d_tiles, sizeof(tt))) != cudaSuccess) return bail(e, "malloc tiles");
         cudaMemcpy(P->d_tiles, tt, sizeof(tt), cudaMemcpyHostToDevice);
@@ -2359,6 +2728,7 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_enum(K, P->even, MODE_RAW),
                                                            THREADS, P->smem_enum)) != cudaSuccess)
         return bail(e, "occupancy");
+    if (const char *e = std::getenv("TCG_ENUM_BPS")) bps = std::min(bps, std::max(1, std::atoi(e)));
     P->blocks_enum = std::max(1, bps) * P->nsm;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, pick_batch(K, P->even), THREADS,
                                                            P->smem_batch)) != cudaSuccess)
@@ -2383,6 +2753,14 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
                                                            THREADS, P->smem_cls)) != cudaSuccess)
         return bail(e, "occupancy");
     P->blocks_cls = std::max(1, bps) * P->nsm;
+    cudaFuncSetAttribute((void *)k_l2_classify, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)L2_CLS_SMEM);
+    cudaFuncSetAttribute((void *)k_l2_classify, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         std::getenv("TCG_CARVEOUT") ? std::atoi(std::getenv("TCG_CARVEOUT")) : 38);
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (void *)k_l2_classify, THREADS,
+                                                           L2_CLS_SMEM)) != cudaSuccess)
+        return bail(e, "occupancy");
+    P->blocks_l2cls = std::max(1, bps) * P->nsm;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
              &bps, pick_build(K, MODE_RAW), build_per_warp() ? 32 * BUILD_WARPS : THREADS,
              P->smem_build)) != cudaSuccess)
@@ -2408,7 +2786,7 @@ int tcg_plan_destroy(tcg_plan *P) {
     DeviceGuard guard(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     timing_resolve(P);
-    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_oldlist, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
@@ -2457,8 +2835,31 @@ int tcg_tile_stats(tcg_plan *P, int64_t *out) {
         CUDA_TRY(cudaMemset(P->d_tstats, 0, sizeof(c)));
     }
     out[0] = P->tiles_built;
-    out[1] = (int64_t)c;
+    out[1] = (int64_t)c + P->reps1_host;
     P->tiles_built = 0;
+    P->reps1_host = 0;
+    return TCG_OK;
+}
+
+int tcg_plan_set_level2(tcg_plan *P, int enable) {
+    if (!P) return fail(TCG_E_ARG, "null plan");
+    P->l2 = enable < 0 ? -1 : (enable ? 1 : 0);
+    return TCG_OK;
+}
+
+int tcg_level2_stats(tcg_plan *P, int64_t *out) {
+    if (!P || !out) return fail(TCG_E_ARG, "null argument");
+    DeviceGuard guard(P->device);
+    unsigned long long c[2] = {0, 0};
+    if (P->d_tstats) {
+        CUDA_TRY(cudaStreamSynchronize(P->stream));
+        CUDA_TRY(cudaMemcpy(c, P->d_tstats + 1, sizeof(c), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemset(P->d_tstats + 1, 0, sizeof(c)));
+    }
+    out[0] = P->l2_built;
+    out[1] = (int64_t)c[0];
+    out[2] = (int64_t)c[1];
+    P->l2_built = 0;
     return TCG_OK;
 }
 
@@ -2576,6 +2977,98 @@ int tcg_agg_reset(tcg_plan *P) {
     return TCG_OK;
 }
 
+// TCG_NO_L2=1 keeps sweeps on the level-1 tile classifier; results are identical.
+static bool l2_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("TCG_NO_L2");
+        return !(e && e[0] && e[0] != '0');
+    }();
+    return on;
+}
+
+// Level-2 stage of one chunk (after the level-1 dedup): build the records of
+// every (representative tile, A pattern), deduplicate them, classify the
+// representatives.  Tiles the level-2 path does not take (range ends,
+// fallback, > 32 nodes) are listed in d_oldlist for the level-1 classifier.
+// The level-1 representative count comes back to the host (one small copy)
+// to size the batches.
+static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec *recs,
+                      const uint32_t *list1, const uint32_t *count1, const uint32_t *dup1,
+                      const uint32_t *mint1, uint64_t tile0, uint64_t lo, uint64_t hi) {
+    const TileTables &T = P->h_tiles[mode];
+    uint32_t n1 = 0;
+    CUDA_TRY(cudaMemcpyAsync(&n1, count1, sizeof(n1), cudaMemcpyDeviceToHost, P->stream));
+    CUDA_TRY(cudaStreamSynchronize(P->stream));
+    P->reps1_host += n1;
+    CUDA_TRY(cudaMemsetAsync(P->d_oldlist, 0, sizeof(uint32_t), P->stream));
+    if (n1 == 0) return TCG_OK;
+    const int la = T.la;
+    const uint32_t stride = (uint32_t)(1 + 32 - T.nB);
+    const size_t want = (size_t)n1 << la;
+    const size_t per_rec = stride * 8 + 8 + 4 * 7 + 8;
+    if (want > P->l2_cap || (int)stride != P->l2_stride) {
+        size_t fr = 0, tot = 0;
+        CUDA_TRY(cudaMemGetInfo(&fr, &tot));
+        fr += P->l2_cap * per_rec;
+        size_t cap = std::max<size_t>(want, P->l2_cap);
+        while (cap > ((size_t)1 << 16) && cap * per_rec > fr / 3) cap >>= 1;
+        if (cap > P->l2_cap || (int)stride != P->l2_stride) {
+            cudaFree(P->d_l2pool);
+            cudaFree(P->d_l2hash);
+            cudaFree(P->d_l2u32);
+            P->d_l2pool = nullptr;
+            P->d_l2hash = nullptr;
+            P->d_l2u32 = nullptr;
+            P->l2_cap = 0;
+            CUDA_TRY(cudaMalloc(&P->d_l2pool, sizeof(unsigned long long) * stride * cap));
+            CUDA_TRY(cudaMalloc(&P->d_l2hash, sizeof(unsigned long long) * cap));
+            CUDA_TRY(cudaMalloc(&P->d_l2u32, sizeof(uint32_t) * (5 * cap + 2 * (size_t)next_pow2((uint32_t)cap) + 1)));
+            P->l2_cap = cap;
+            P->l2_stride = (int)stride;
+        }
+    }
+    const size_t cap = P->l2_cap;
+    uint32_t *wts = P->d_l2u32, *poss = wts + cap, *w2 = poss + cap, *pos2 = w2 + cap,
+             *list2 = pos2 + cap, *slots = list2 + cap,
+             *count2 = slots + 2 * (size_t)next_pow2((uint32_t)cap);
+    const uint32_t nbmax = (uint32_t)(cap >> la);
+    for (uint32_t i0 = 0; i0 < n1; i0 += nbmax) {
+        uint32_t nb = std::min(nbmax, n1 - i0);
+        uint32_t nrec = nb << la;
+        const uint32_t np2 = next_pow2(nrec);
+        CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(uint32_t) * 2 * (size_t)np2, P->stream));
+        CUDA_TRY(cudaMemsetAsync(w2, 0, sizeof(uint32_t) * nrec, P->stream));
+        CUDA_TRY(cudaMemsetAsync(pos2, 0xff, sizeof(uint32_t) * nrec, P->stream));
+        CUDA_TRY(cudaMemsetAsync(count2, 0, sizeof(uint32_t), P->stream));
+        const unsigned g12 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8,
+                                                          (nrec + THREADS - 1) / THREADS);
+        unsigned long long *pool = P->d_l2pool, *hashes = P->d_l2hash;
+        uint32_t *oldlist = P->d_oldlist + 1, *oldcount = P->d_oldlist;
+        uint64_t t0 = tile0, a = lo, b = hi;
+        void *a1[] = {&tt, &recs, &list1, &dup1, &mint1, &i0, &nb, &t0, &a, &b, &pool,
+                      (void *)&stride, &hashes, &wts, &poss, &oldlist, &oldcount};
+        cudaEvent_t e0 = timing_begin(P);
+        CUDA_TRY(cudaLaunchKernel((void *)k_l2_build, dim3(g12), dim3(THREADS), a1, 0, P->stream));
+        uint32_t smask = 2 * np2 - 1;
+        void *a2[] = {&pool, (void *)&stride, &nrec, &hashes, &wts, &poss, &slots, &smask, &w2,
+                      &pos2, &list2, &count2};
+        CUDA_TRY(cudaLaunchKernel((void *)k_l2_dedup, dim3(g12), dim3(THREADS), a2, 0, P->stream));
+        timing_end(P, 0, e0);
+        P->l2_built += nrec;
+        const unsigned g3 = (unsigned)std::min<uint64_t>(P->blocks_l2cls,
+                                                         (nrec + CLS_WARPS - 1) / CLS_WARPS);
+        unsigned long long *ts = P->d_tstats + 1;
+        void *a3[] = {&P->kp, &tt, &pool, (void *)&stride, &list2, &count2, &w2, &pos2, &t0,
+                      &P->agg, &ts};
+        cudaEvent_t e = timing_begin(P);
+        CUDA_TRY(cudaLaunchKernel((void *)k_l2_classify, dim3(g3), dim3(THREADS), a3,
+                                  L2_CLS_SMEM, P->stream));
+        timing_end(P, 1, e);
+        P->launches += 3;
+    }
+    return TCG_OK;
+}
+
 // TCG_NO_DEDUP=1 classifies every tile (A/B and debugging); results are identical.
 static bool dedup_enabled() {
     static const bool on = [] {
@@ -2619,7 +3112,10 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 P->d_recs = nullptr;
                 P->d_dedup = nullptr;
                 P->chunk_cap = 0;
+                cudaFree(P->d_oldlist);
+                P->d_oldlist = nullptr;
                 CUDA_TRY(cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)chunk));
+                CUDA_TRY(cudaMalloc(&P->d_oldlist, sizeof(uint32_t) * ((size_t)chunk + 1)));
                 CUDA_TRY(cudaMalloc(&P->d_dedup, sizeof(uint32_t) * (2 * (size_t)next_pow2(chunk) +
                                                                      3 * (size_t)chunk + 1)));
                 P->chunk_cap = chunk;
@@ -2627,8 +3123,8 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
         }
         chunk = std::min(chunk, P->chunk_cap);
         if (!P->d_tstats) {
-            CUDA_TRY(cudaMalloc(&P->d_tstats, sizeof(unsigned long long)));
-            CUDA_TRY(cudaMemsetAsync(P->d_tstats, 0, sizeof(unsigned long long), P->stream));
+            CUDA_TRY(cudaMalloc(&P->d_tstats, 3 * sizeof(unsigned long long)));
+            CUDA_TRY(cudaMemsetAsync(P->d_tstats, 0, 3 * sizeof(unsigned long long), P->stream));
         }
         for (uint64_t t0 = start >> bits; t0 < t_end; t0 += chunk) {
             uint32_t nt = (uint32_t)std::min<uint64_t>(chunk, t_end - t0);
@@ -2668,12 +3164,21 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 mint = mnt;
                 P->launches++;
             }
+            unsigned long long *tstats = P->d_tstats;
             timing_end(P, 0, e0);
+            if (list && P->l2_ok[mode] && (P->l2 < 0 ? l2_enabled() : P->l2 != 0)) {
+                // level 2: the level-1 representatives' (tile, A) records, deduplicated
+                int rc = run_level2(P, mode, tt, crecs, list, cnt, dup, mint, tile0, lo, hi);
+                if (rc) return rc;
+                list = P->d_oldlist + 1;  // tiles left to the level-1 classifier
+                cnt = P->d_oldlist;
+                tstats = P->d_tstats + 2;  // tiles the level-1 classifier takes
+            }
             const unsigned gc = (unsigned)std::min<uint64_t>(P->blocks_cls,
                                                              (nt + CLS_WARPS - 1) / CLS_WARPS);
             P->tiles_built += nt;
             void *ac[] = {&P->kp, &tt, &crecs, &tile0, &nt, &lo, &hi, &P->agg,
-                          &list, &cnt, &dup, &mint, &P->d_tstats};
+                          &list, &cnt, &dup, &mint, &tstats};
             cudaEvent_t e1 = timing_begin(P);
             CUDA_TRY(cudaLaunchKernel(fc, dim3(gc), dim3(THREADS), ac, P->smem_cls, P->stream));
             timing_end(P, 1, e1);

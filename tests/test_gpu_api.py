@@ -399,3 +399,29 @@ def test_tile_dedup_chunk_size_invariance():
         assert p.returncode == 0, p.stderr
         res[lg] = json.loads(p.stdout.strip().splitlines()[-1])
     assert res["14"] == res["21"]
+
+
+@pytest.mark.parametrize("name,raw,a,n", [
+    ("delaunay-7", True, 0x5A5A5A5A0 + 3, (1 << 24) + 1001),
+    ("delaunay-7", False, 777, 1 << 24),
+    ("delaunay-5", True, 0, 1 << 21),
+    ("delaunay-7", True, 0, 1 << 26),
+])
+def test_level2_contraction_is_exact(api, name, raw, a, n):
+    """Level-2 records (A points fixed, super-nodes) deduplicated and
+    classified per lane give the identical report as the level-1 path."""
+    T = api.builtin(name)
+    c = api.Classifier(T)
+    reps = {}
+    for on in (False, True):
+        c.native.set_level2(on)
+        c.native.level2_stats()
+        r = api.sweep(T, api.SweepRange(a, a + n), raw_space=raw, classifier=c)
+        built, classified, _ = c.native.level2_stats()
+        reps[on] = (r.oval_histogram, sorted(r.scheme_map.items()), r.total_classified)
+        if on and T.degree == 7:
+            assert 0 < classified < built
+        if not on:
+            assert built == 0
+    c.native.set_level2(None)
+    assert reps[True] == reps[False]
