@@ -114,8 +114,17 @@ int tcg_plan_set_stream(tcg_plan *plan, void *cuda_stream);
 int tcg_plan_info(const tcg_plan *plan, int32_t *info, int ninfo);
 /* Per-kernel device time (CUDA events on the plan's stream around every
  * launch) while enabled.  tcg_kernel_times returns and clears the totals:
- * ms[0..3] / counts[0..3] = tile contraction, tile classification, flat
- * enumeration, batch classification. */
+ * ms[TCG_NKINDS] / counts[TCG_NKINDS], indexed by the TCG_KT_* kinds. */
+#define TCG_KT_TILE_BUILD 0    /* k_tile_from_super (+ k_tile_build_lanes): tile contraction */
+#define TCG_KT_TILE_CLASSIFY 1 /* k_tile_classify: level-1 tile classification */
+#define TCG_KT_ENUMERATE 2     /* k_enumerate: flat per-patchwork sweeps / sampling */
+#define TCG_KT_BATCH 3         /* k_batch: explicit sign words */
+#define TCG_KT_TILE_DEDUP 4    /* k_tile_dedup: level-1 record deduplication */
+#define TCG_KT_L2_BUILD 5      /* k_l2_build: level-2 records */
+#define TCG_KT_L2_DEDUP 6      /* k_l2_dedup: level-2 record deduplication */
+#define TCG_KT_L2_CLASSIFY 7   /* k_l2_classify: level-2 classification */
+#define TCG_KT_SUPER_BUILD 8   /* k_super_build: super-tile contraction */
+#define TCG_NKINDS 9
 int tcg_plan_set_timing(tcg_plan *plan, int enable);
 int tcg_kernel_times(tcg_plan *plan, double *ms, int64_t *counts);
 /* Tile deduplication (exhaustive sweeps): tiles whose contracted records are

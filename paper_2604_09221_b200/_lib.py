@@ -115,6 +115,11 @@ EXPORTS = (
 )
 
 
+# tcg.h TCG_KT_* order (tcg_kernel_times)
+KERNEL_KINDS = ("tile_build", "tile_classify", "enumerate", "batch", "tile_dedup",
+                "l2_build", "l2_dedup", "l2_classify", "super_build")
+
+
 def last_error() -> str:
     return load().tcg_last_error().decode(errors="replace")
 
@@ -319,11 +324,11 @@ class NativePlan:
 
     def kernel_times(self):
         """{kind: (ms, launches)} since the last call; kinds as in tcg.h."""
-        ms = np.zeros(4, np.float64)
-        n = np.zeros(4, np.int64)
+        names = KERNEL_KINDS
+        ms = np.zeros(len(names), np.float64)
+        n = np.zeros(len(names), np.int64)
         _check(self._L.tcg_kernel_times(self.h, ms.ctypes.data, n.ctypes.data), "tcg_kernel_times")
-        names = ("tile_build", "tile_classify", "enumerate", "batch")
-        return {names[i]: (float(ms[i]), int(n[i])) for i in range(4)}
+        return {names[i]: (float(ms[i]), int(n[i])) for i in range(len(names))}
 
     def set_dedup(self, enable: bool | None):
         """Tile deduplication on / off / None = default (see tcg.h)."""

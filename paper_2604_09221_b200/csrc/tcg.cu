@@ -869,6 +869,8 @@ __global__ void __launch_bounds__(THREADS, K == 6 ? TCG_ENUM_MINB6 : 1) k_enumer
 constexpr int TILE_BITS_MAX = 12;
 constexpr int MAXC = 48;  // fixed components per tile
 constexpr int MAXF = 32;  // free vertices
+constexpr int MAXM = 24;  // mid vertices of a super-tile
+constexpr int SUPER_BITS_MAX = 6;
 
 struct alignas(16) TileTables {  // per plan and domain (raw / representative), device memory
     int nf, nfixed, bits, maxnodes;  // maxnodes: contraction size limit (64; lower only in tests)
@@ -888,6 +890,14 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     int8_t l2j[MAXF];                       // free node -> B index (or -1)
     uint32_t l2adjB[16], l2linkB[16];       // B-B adjacency / links (B index space)
     uint32_t l2bsign[32];                   // B-node signs for tile-local bits 0..4
+    uint32_t freem[MAXK];                   // free vertices (layout mask)
+    int8_t vfree[32 * MAXK];                // layout position -> free node (or -1)
+    // super-tiles (k_super_build / k_tile_from_super): 2^sh consecutive tiles share
+    // every sign except those of the "mid" points (tile-index bits 0..sh-1)
+    int sh, nm, nsfixed, pad2;              // sh = 0: off
+    uint32_t sfixed[MAXK];                  // fixed vertices that are not mid vertices
+    uint16_t mpos[MAXM];                    // layout positions of the mid vertices, ascending
+    uint32_t msign[1 << SUPER_BITS_MAX];    // mid-vertex signs (bit j) for mid pattern x
 };
 
 // Contracted tile, written by k_tile_build and staged into shared memory by
@@ -1271,19 +1281,10 @@ __global__ void __launch_bounds__(32 * BUILD_WARPS) k_tile_build(KParams p,
 // Contract tiles one per LANE (no redundant SIMT work): each thread runs the
 // COMPS-mode region pass for its own tile and writes its node rows.
 template <int K, int MODE>
-__global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
-                                                              const TileTables *__restrict__ tt_g,
-                                                              uint64_t tile0, uint32_t ntiles,
-                                                              TileRec *__restrict__ recs) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t *adj_s = smem;
-    TileTables *tt = reinterpret_cast<TileTables *>(smem + 32 * K * K);
-    stage_adj<K>(p, adj_s);
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    __syncthreads();
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= ntiles) return;
+__device__ __forceinline__ void build_lane(const KParams &p, const uint32_t *__restrict__ adj_s,
+                                           const TileTables &tt_r, uint64_t tile0, uint32_t t,
+                                           TileRec *__restrict__ recs) {
+    const TileTables *tt = &tt_r;
     const uint64_t base = (tile0 + t) << tt->bits;
     const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, base) : base;
     uint32_t SG[K], fixed[K], zero[K];
@@ -1346,6 +1347,293 @@ __global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
     rec->n = n;
     rec->nnodes = nn;
     rec->fallback = fits ? 0 : 1;
+}
+
+// list != nullptr: only the tiles list[0 .. *count) (the ones k_tile_from_super
+// left: super-tiles whose contraction does not fit), grid-stride.
+template <int K, int MODE>
+__global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
+                                                              const TileTables *__restrict__ tt_g,
+                                                              uint64_t tile0, uint32_t ntiles,
+                                                              TileRec *__restrict__ recs,
+                                                              const uint32_t *__restrict__ list,
+                                                              const uint32_t *__restrict__ count) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *adj_s = smem;
+    TileTables *tt = reinterpret_cast<TileTables *>(smem + 32 * K * K);
+    stage_adj<K>(p, adj_s);
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    __syncthreads();
+    const uint32_t nwork = list ? *count : ntiles;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nwork;
+         i += gridDim.x * blockDim.x)
+        build_lane<K, MODE>(p, adj_s, *tt, tile0, list ? list[i] : i, recs);
+}
+
+
+// ------------------------------------------------------------ super-tiles
+// A super-tile is 2^sh consecutive tiles: they share the signs of every
+// fixed vertex except the "mid" vertices (copies of the points of tile-index
+// bits 0..sh-1).  k_super_build contracts the remaining ("super-fixed")
+// vertices once per super-tile, exactly as k_tile_build_lanes contracts a
+// tile, and keeps the mid vertices as single nodes: SN nodes = super
+// components + mid vertices, ordered by their lowest layout position.
+// k_tile_from_super then gives each tile (one per lane) its mid signs and
+// merges same-sign SN neighbours -- a breadth-first pass over <= 64 nodes
+// instead of ~100 vertices -- and emits the tile record.  Components come out
+// ordered by their lowest vertex, as in k_tile_build_lanes, so the records
+// are byte-identical to the direct contraction (tested: dedup counts and
+// reports agree with TCG_BUILD_GENERIC=1).
+struct SuperRec {
+    unsigned long long adj[64];   // SN-node adjacency (no self bit)
+    unsigned long long link[64];  // SN-node antipodal links (self bit: pair inside the node)
+    unsigned long long fsn[MAXF]; // free node -> adjacent SN nodes
+    uint32_t fadj[64];            // SN node -> adjacent free nodes
+    unsigned long long sgn;       // signs of the component nodes (mid nodes: 0)
+    uint8_t msn[MAXM];            // SN index of mid vertex j
+    int nsn, fallback;
+};
+
+template <int K, int MODE>
+__global__ void __launch_bounds__(THREADS) k_super_build(KParams p,
+                                                         const TileTables *__restrict__ tt_g,
+                                                         uint64_t s0, uint32_t nsup,
+                                                         SuperRec *__restrict__ srecs) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t *adj_s = smem;
+    TileTables *tt = reinterpret_cast<TileTables *>(smem + 32 * K * K);
+    stage_adj<K>(p, adj_s);
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    __syncthreads();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nsup;
+         i += gridDim.x * blockDim.x) {
+        const uint64_t base = ((s0 + i) << tt->sh) << tt->bits;
+        const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, base) : base;
+        uint32_t SG[K], sf[K], zero[K];
+        sign_words<K>(p, sigma, SG);
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            sf[k] = tt->sfixed[k];
+            zero[k] = 0u;
+        }
+        Regions<K, MAXC> comps;
+        region_pass<K, false, false, true, MAXC>(adj_s, SG, sf, zero, tt->nsfixed, comps);
+        SuperRec *S = srecs + i;
+        const int n = comps.nreg, nm = tt->nm, nsn = n + nm;
+        if (n > MAXC || nsn > 64) {
+            S->nsn = nsn;
+            S->fallback = 1;
+            continue;
+        }
+        // SN order: merge the components (ascending lowest vertex) with the mid vertices
+        uint8_t ord[64];  // c, or 64 + j for mid vertex j
+        {
+            int ci = 0, mj = 0;
+            for (int q = 0; q < nsn; ++q) {
+                bool takec = ci < n;
+                if (takec && mj < nm) {
+                    int w, b;
+                    uint32_t R[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) R[k] = comps.R[ci][k];
+                    lowest<K>(R, w, b);
+                    takec = 32 * w + b < (int)tt->mpos[mj];
+                }
+                ord[q] = takec ? (uint8_t)ci++ : (uint8_t)(64 + mj++);
+            }
+        }
+        auto node = [&](int q, uint32_t (&R)[K], uint32_t (&NB)[K]) {
+            const int o = ord[q];
+            if (o < 64) {
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    R[k] = comps.R[o][k];
+                    NB[k] = comps.X[o][k];
+                }
+            } else {
+                const int pos = tt->mpos[o - 64];
+                uint32_t dummy[K];
+                load_row<K, false>(adj_s, pos, NB, dummy);
+#pragma unroll
+                for (int k = 0; k < K; ++k) R[k] = (k == (pos >> 5)) ? (1u << (pos & 31)) : 0u;
+            }
+        };
+        unsigned long long sgn = 0;
+        unsigned long long fsn[MAXF];
+        for (int f = 0; f < tt->nf; ++f) fsn[f] = 0ull;
+        for (int q = 0; q < nsn; ++q) {
+            uint32_t R[K], NB[K], P[K];
+            node(q, R, NB);
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int ks = (k + K / 2) % K;
+                P[k] = R[ks] & p.bd[ks];
+            }
+            unsigned long long adj = 0, pl = 0;
+            for (int q2 = 0; q2 < nsn; ++q2) {
+                uint32_t R2[K], NB2[K];
+                const int o2 = ord[q2];
+                if (o2 < 64) {
+#pragma unroll
+                    for (int k = 0; k < K; ++k) R2[k] = comps.R[o2][k];
+                } else {
+                    const int pos = tt->mpos[o2 - 64];
+#pragma unroll
+                    for (int k = 0; k < K; ++k)
+                        R2[k] = (k == (pos >> 5)) ? (1u << (pos & 31)) : 0u;
+                }
+                (void)NB2;
+                uint32_t a = 0, l = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    a |= NB[k] & R2[k];
+                    l |= P[k] & R2[k];
+                }
+                if (a && q2 != q) adj |= 1ull << q2;
+                if (l) pl |= 1ull << q2;
+            }
+            uint32_t fb = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                uint32_t x = NB[k] & tt->freem[k];
+                while (x) {
+                    const int f = tt->vfree[32 * k + __ffs(x) - 1];
+                    x &= x - 1u;
+                    fb |= 1u << f;
+                    fsn[f] |= 1ull << q;
+                }
+            }
+            S->adj[q] = adj;
+            S->link[q] = pl;
+            S->fadj[q] = fb;
+            const int o = ord[q];
+            if (o < 64) {
+                uint32_t sg = 0;
+#pragma unroll
+                for (int k = 0; k < K; ++k) sg |= R[k] & SG[k];
+                if (sg) sgn |= 1ull << q;
+            } else {
+                S->msn[o - 64] = (uint8_t)q;
+            }
+        }
+        for (int f = 0; f < tt->nf; ++f) S->fsn[f] = fsn[f];
+        S->sgn = sgn;
+        S->nsn = nsn;
+        S->fallback = 0;
+    }
+}
+
+// One tile per lane: mid signs, merge same-sign SN neighbours (labels are
+// lane-private bytes in shared memory, bank = lane), then one more pass per
+// component to collect its neighbours, links and free neighbours and write
+// the row.  Tiles of fallback super-tiles are listed in ovf for
+// k_tile_build_lanes.
+constexpr size_t FROM_SUPER_SMEM = sizeof(TileTables) + 16 * 4 * THREADS;
+
+__global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *__restrict__ tt_g,
+                                                             const SuperRec *__restrict__ srecs,
+                                                             uint64_t tile0, uint32_t ntiles,
+                                                             TileRec *__restrict__ recs,
+                                                             uint32_t *__restrict__ ovf) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    TileTables *tt = reinterpret_cast<TileTables *>(smem);
+    uint8_t *lb = reinterpret_cast<uint8_t *>(smem + sizeof(TileTables) / 4 + threadIdx.x);
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    __syncthreads();
+    const int h = tt->sh, nf = tt->nf, nm = tt->nm;
+    const uint64_t sbase = tile0 >> h;
+    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles;
+         t += gridDim.x * blockDim.x) {
+        const uint64_t gt = tile0 + t;
+        const SuperRec *S = srecs + ((gt >> h) - sbase);
+        TileRec *rec = recs + t;
+        if (S->fallback) {
+            ovf[1 + atomicAdd(ovf, 1u)] = t;
+            continue;
+        }
+        const int nsn = S->nsn;
+        const uint32_t ms = tt->msign[gt & ((1u << h) - 1u)];
+        unsigned long long sg = S->sgn;
+        for (int j = 0; j < nm; ++j) sg |= (unsigned long long)((ms >> j) & 1u) << S->msn[j];
+        const unsigned long long all = nsn >= 64 ? ~0ull : ((1ull << nsn) - 1ull);
+        unsigned long long unv = all, seeds = 0, sbits = 0;
+        int n = 0;
+        while (unv) {  // pass 1: label the merged components
+            const unsigned long long seed = unv & (0ull - unv);
+            const bool s1 = (sg & seed) != 0ull;
+            const unsigned long long same = s1 ? sg : ~sg;
+            unsigned long long F = seed;
+            unv ^= seed;
+            seeds |= seed;
+            while (F) {
+                const int v = __ffsll((long long)F) - 1;
+                F &= F - 1ull;
+                lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)n;
+                const unsigned long long nw = S->adj[v] & unv & same;
+                unv ^= nw;
+                F |= nw;
+            }
+            if (s1) sbits |= 1ull << n;
+            ++n;
+        }
+        const int nn = n + nf;
+        const bool fits = n <= MAXC && nn <= tt->maxnodes;
+        if (fits) {  // pass 2: rows
+            unsigned long long sd = seeds;
+            unv = all;
+            for (int c = 0; c < n; ++c) {
+                const unsigned long long seed = sd & (0ull - sd);
+                sd ^= seed;
+                const unsigned long long same = (sg & seed) ? sg : ~sg;
+                unsigned long long F = seed, M = 0, CG = 0, LK = 0;
+                uint32_t FB = 0;
+                unv ^= seed;
+                while (F) {
+                    const int v = __ffsll((long long)F) - 1;
+                    F &= F - 1ull;
+                    M |= 1ull << v;
+                    const unsigned long long a = S->adj[v];
+                    CG |= a;
+                    LK |= S->link[v];
+                    FB |= S->fadj[v];
+                    const unsigned long long nw = a & unv & same;
+                    unv ^= nw;
+                    F |= nw;
+                }
+                unsigned long long adj = (unsigned long long)FB << n, pl = 0;
+                unsigned long long x = CG & ~M;
+                while (x) {
+                    const int v = __ffsll((long long)x) - 1;
+                    x &= x - 1ull;
+                    adj |= 1ull << label(v);
+                }
+                x = LK;
+                while (x) {
+                    const int v = __ffsll((long long)x) - 1;
+                    x &= x - 1ull;
+                    pl |= 1ull << label(v);
+                }
+                store_row(rec, c, nn, adj, pl);
+            }
+            for (int f = 0; f < nf; ++f) {
+                unsigned long long x = S->fsn[f], fc = 0;
+                while (x) {
+                    const int v = __ffsll((long long)x) - 1;
+                    x &= x - 1ull;
+                    fc |= 1ull << label(v);
+                }
+                store_row(rec, n + f, nn, (tt->fadj[f] << n) | fc, tt->fpl[f] << n);
+            }
+        }
+        rec->sgn_fixed = fits ? sbits : 0ull;
+        rec->n = n;
+        rec->nnodes = nn;
+        rec->fallback = fits ? 0 : 1;
+    }
 }
 
 // Tile deduplication.  A tile's classification depends only on its contracted
@@ -2205,6 +2493,10 @@ struct tcg_plan {
     unsigned long long *d_l2pool = nullptr, *d_l2hash = nullptr;
     uint32_t *d_l2u32 = nullptr;     // wts | poss | w2 | pos2 | list2 | slots(2 pow2) | count2
     uint32_t *d_oldlist = nullptr;   // [chunk_cap + 1]: count, then tiles for the level-1 path
+    uint32_t *d_ovf = nullptr;       // [chunk_cap + 1]: count, then tiles of fallback super-tiles
+    SuperRec *d_super = nullptr;     // [super_cap]
+    size_t super_cap = 0;
+    int blocks_bgen = 0;             // grid of the list-driven k_tile_build_lanes
     int64_t reps1_host = 0, l2_built = 0;
     int dedup = -1;                  // -1: TCG_NO_DEDUP decides
     int64_t tiles_built = 0;
@@ -2215,8 +2507,8 @@ struct tcg_plan {
     // optional per-kernel timing (CUDA events on the launching stream)
     int timing = 0;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;  // kind, start, stop
-    double t_ms[4] = {0, 0, 0, 0};   // build, classify (tiles), enumerate, batch
-    int64_t t_n[4] = {0, 0, 0, 0};
+    double t_ms[TCG_NKINDS] = {};    // per kernel kind, see tcg.h
+    int64_t t_n[TCG_NKINDS] = {};
     // split-phase bookkeeping: how to map a failing index back to its sign word
     int pending_mode = -1;
     uint64_t pending_seed = 0, pending_mask = 0;
@@ -2292,6 +2584,17 @@ void *build_fn(int mode) {
 }
 
 bool build_per_warp() { return std::getenv("TCG_BUILD_WARP") != nullptr; }
+
+template <int K>
+void *super_fn(int mode) {
+    return mode == MODE_RAW ? (void *)k_super_build<K, MODE_RAW> : (void *)k_super_build<K, MODE_REP>;
+}
+
+void *pick_super(int K, int mode) {
+    if (K == 2) return super_fn<2>(mode);
+    if (K == 4) return super_fn<4>(mode);
+    return super_fn<6>(mode);
+}
 
 void *pick_build(int K, int mode) {
     if (K == 2) return build_fn<2>(mode);
@@ -2414,6 +2717,7 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
     const int dom_bits = mode == MODE_RAW ? npts : npts - 3;
     if (d < 5 || bits > TILE_BITS_MAX || dom_bits < bits + 2) return false;
     std::memset(&T, 0, sizeof(T));
+    std::memset(T.vfree, 0xff, sizeof(T.vfree));
     T.bits = bits;
     T.maxnodes = 64;
     if (const char *e = std::getenv("TCG_TILE_MAXNODES")) T.maxnodes = std::max(0, std::min(64, std::atoi(e)));
@@ -2437,6 +2741,8 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
         fnode[v] = nf;
         T.fword[nf] = (uint32_t)(pos >> 5);
         T.fbit[nf] = 1u << (pos & 31);
+        T.freem[pos >> 5] |= 1u << (pos & 31);
+        T.vfree[pos] = (int8_t)nf;
         T.fpar |= (unsigned long long)(D->par[v] & 1) << nf;
         T.fcopy[bit] |= 1ull << nf;
         ++nf;
@@ -2499,6 +2805,42 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
         }
     }
     l2_tables();
+    // super-tiles: mid points = index bits bits .. bits+sh-1 (TCG_SUPER_BITS, default 4)
+    T.sh = 0;
+    {
+        int h = 4;
+        if (const char *e = std::getenv("TCG_SUPER_BITS")) h = std::atoi(e);
+        if (const char *e = std::getenv("TCG_BUILD_GENERIC"))
+            if (e[0] && e[0] != '0') h = 0;
+        h = std::max(0, std::min(h, SUPER_BITS_MAX));
+        if (h > 0 && dom_bits >= bits + h + 1) {
+            auto point_of = [&](int ib) {  // index bit -> lattice point
+                return mode == MODE_RAW ? ib : (ib < d - 1 ? ib + 2 : ib - (d - 1) + d + 2);
+            };
+            std::vector<std::pair<int, int>> mids;  // (layout position, vertex)
+            std::vector<int> mbit(D->nv, -1);
+            for (int v = 0; v < D->nv; ++v) {
+                if (!D->used[v] || fnode[v] >= 0) continue;
+                for (int i = 0; i < h; ++i)
+                    if (point_of(bits + i) == D->src[v]) mbit[v] = i;
+                if (mbit[v] >= 0) mids.push_back({L.pos[v], v});
+            }
+            std::sort(mids.begin(), mids.end());
+            if ((int)mids.size() <= MAXM && !mids.empty()) {
+                T.sh = h;
+                T.nm = (int)mids.size();
+                for (int k = 0; k < MAXK; ++k) T.sfixed[k] = T.fixed[k];
+                for (int j = 0; j < T.nm; ++j) {
+                    const int pos = mids[j].first, v = mids[j].second;
+                    T.mpos[j] = (uint16_t)pos;
+                    T.sfixed[pos >> 5] &= ~(1u << (pos & 31));
+                    for (int x = 0; x < (1 << h); ++x)
+                        T.msign[x] |= (uint32_t)(((x >> mbit[v]) & 1) ^ (D->par[v] & 1)) << j;
+                }
+                T.nsfixed = T.nfixed - T.nm;
+            }
+        }
+    }
     return T.nfixed > 0 && nf > 0;
 }
 
@@ -2735,6 +3077,15 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
         return bail(e, "occupancy");
     P->blocks_batch = std::max(1, bps) * P->nsm;
     P->smem_build = build_smem(K);
+    for (int mode = 0; mode < 2; ++mode)
+        if ((e = cudaFuncSetAttribute(pick_super(K, mode),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)build_smem(K))) != cudaSuccess)
+            return bail(e, "super smem");
+    if ((e = cudaFuncSetAttribute((void *)k_tile_from_super,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)FROM_SUPER_SMEM)) != cudaSuccess)
+        return bail(e, "from-super smem");
     P->smem_cls = cls_smem(K);
     for (int mode = 0; mode < 2; ++mode) {
         cudaFuncSetAttribute(pick_build(K, mode), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2766,6 +3117,7 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
              P->smem_build)) != cudaSuccess)
         return bail(e, "occupancy");
     P->blocks_build = std::max(1, bps) * P->nsm;
+    P->blocks_bgen = std::max(1, bps) * P->nsm;
     *out = P;
     int rc2 = tcg_agg_reset(P);
     if (rc2) {
@@ -2786,7 +3138,7 @@ int tcg_plan_destroy(tcg_plan *P) {
     DeviceGuard guard(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     timing_resolve(P);
-    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_oldlist, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_oldlist, P->d_ovf, P->d_super, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
@@ -2867,7 +3219,7 @@ int tcg_kernel_times(tcg_plan *P, double *ms, int64_t *counts) {
     if (!P || !ms || !counts) return fail(TCG_E_ARG, "null argument");
     DeviceGuard guard(P->device);
     timing_resolve(P);
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < TCG_NKINDS; ++i) {
         ms[i] = P->t_ms[i];
         counts[i] = P->t_n[i];
         P->t_ms[i] = 0;
@@ -2895,7 +3247,7 @@ static int launch_batch(tcg_plan *P, const uint64_t *d_sig, int64_t n, uint64_t 
     cudaEvent_t e3 = timing_begin(P, stream);
     CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)blocks), dim3(THREADS), args, P->smem_batch,
                               stream));
-    timing_end(P, 3, e3, stream);
+    timing_end(P, TCG_KT_BATCH, e3, stream);
     P->launches++;
     return TCG_OK;
 }
@@ -3049,11 +3401,13 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
                       (void *)&stride, &hashes, &wts, &poss, &oldlist, &oldcount};
         cudaEvent_t e0 = timing_begin(P);
         CUDA_TRY(cudaLaunchKernel((void *)k_l2_build, dim3(g12), dim3(THREADS), a1, 0, P->stream));
+        timing_end(P, TCG_KT_L2_BUILD, e0);
         uint32_t smask = 2 * np2 - 1;
         void *a2[] = {&pool, (void *)&stride, &nrec, &hashes, &wts, &poss, &slots, &smask, &w2,
                       &pos2, &list2, &count2};
+        cudaEvent_t e0d = timing_begin(P);
         CUDA_TRY(cudaLaunchKernel((void *)k_l2_dedup, dim3(g12), dim3(THREADS), a2, 0, P->stream));
-        timing_end(P, 0, e0);
+        timing_end(P, TCG_KT_L2_DEDUP, e0d);
         P->l2_built += nrec;
         const unsigned g3 = (unsigned)std::min<uint64_t>(P->blocks_l2cls,
                                                          (nrec + CLS_WARPS - 1) / CLS_WARPS);
@@ -3063,7 +3417,7 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
         cudaEvent_t e = timing_begin(P);
         CUDA_TRY(cudaLaunchKernel((void *)k_l2_classify, dim3(g3), dim3(THREADS), a3,
                                   L2_CLS_SMEM, P->stream));
-        timing_end(P, 1, e);
+        timing_end(P, TCG_KT_L2_CLASSIFY, e);
         P->launches += 3;
     }
     return TCG_OK;
@@ -3114,6 +3468,9 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 P->chunk_cap = 0;
                 cudaFree(P->d_oldlist);
                 P->d_oldlist = nullptr;
+                cudaFree(P->d_ovf);
+                P->d_ovf = nullptr;
+                CUDA_TRY(cudaMalloc(&P->d_ovf, sizeof(uint32_t) * ((size_t)chunk + 1)));
                 CUDA_TRY(cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)chunk));
                 CUDA_TRY(cudaMalloc(&P->d_oldlist, sizeof(uint32_t) * ((size_t)chunk + 1)));
                 CUDA_TRY(cudaMalloc(&P->d_dedup, sizeof(uint32_t) * (2 * (size_t)next_pow2(chunk) +
@@ -3135,11 +3492,52 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                                     ? (unsigned)std::min<uint64_t>(P->blocks_build,
                                                                    (nt + per_block - 1) / per_block)
                                     : (unsigned)((nt + per_block - 1) / per_block);
-            void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs};
+            const uint32_t *nolist = nullptr, *nocount = nullptr;
             cudaEvent_t e0 = timing_begin(P);
-            CUDA_TRY(cudaLaunchKernel(fb, dim3(gb), dim3(build_per_warp() ? 32 * BUILD_WARPS
-                                                                           : THREADS),
-                                      ab, P->smem_build, P->stream));
+            const int sh = P->h_tiles[mode].sh;
+            if (!build_per_warp() && sh > 0) {
+                // super-tiles: contract the shared part once per 2^sh tiles, then
+                // each tile from its super record; fallback super-tiles go to the
+                // generic kernel
+                const uint64_t s0 = tile0 >> sh;
+                const uint32_t nsup = (uint32_t)(((tile0 + nt - 1) >> sh) - s0 + 1);
+                if (nsup > P->super_cap) {
+                    CUDA_TRY(cudaStreamSynchronize(P->stream));
+                    cudaFree(P->d_super);
+                    P->d_super = nullptr;
+                    P->super_cap = 0;
+                    const size_t cap = std::max<size_t>(nsup, (P->chunk_cap >> sh) + 2);
+                    CUDA_TRY(cudaMalloc(&P->d_super, sizeof(SuperRec) * cap));
+                    P->super_cap = cap;
+                }
+                SuperRec *sr = P->d_super;
+                uint64_t s0v = s0;
+                uint32_t nsv = nsup;
+                void *as[] = {&P->kp, &tt, &s0v, &nsv, &sr};
+                CUDA_TRY(cudaLaunchKernel(pick_super(P->K, mode),
+                                          dim3((nsup + THREADS - 1) / THREADS), dim3(THREADS), as,
+                                          P->smem_build, P->stream));
+                timing_end(P, TCG_KT_SUPER_BUILD, e0);
+                e0 = timing_begin(P);
+                uint32_t *ovf = P->d_ovf;
+                CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), P->stream));
+                const SuperRec *csr = sr;
+                void *af[] = {&tt, &csr, &tile0, &nt, &recs, &ovf};
+                CUDA_TRY(cudaLaunchKernel((void *)k_tile_from_super,
+                                          dim3((nt + THREADS - 1) / THREADS), dim3(THREADS), af,
+                                          FROM_SUPER_SMEM, P->stream));
+                const uint32_t *ol = ovf + 1, *oc = ovf;
+                void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs, &ol, &oc};
+                CUDA_TRY(cudaLaunchKernel(fb, dim3(P->blocks_bgen), dim3(THREADS), ab,
+                                          P->smem_build, P->stream));
+                P->launches += 2;
+            } else {
+                void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs, &nolist, &nocount};
+                CUDA_TRY(cudaLaunchKernel(fb, dim3(gb), dim3(build_per_warp() ? 32 * BUILD_WARPS
+                                                                               : THREADS),
+                                          ab, P->smem_build, P->stream));
+            }
+            timing_end(P, TCG_KT_TILE_BUILD, e0);
             uint64_t lo = start, hi = end;
             const TileRec *crecs = recs;
             const uint32_t *list = nullptr, *cnt = nullptr, *dup = nullptr, *mint = nullptr;
@@ -3156,8 +3554,10 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 void *ad[] = {&crecs, &nt, &tile0, &ibits, &lo, &hi, &slots, &smask, &dp, &mnt, &ls, &ct};
                 const unsigned gd = (unsigned)std::min<uint64_t>(
                     (uint64_t)P->nsm * 8, (nt + CLS_WARPS - 1) / CLS_WARPS);
+                cudaEvent_t ed = timing_begin(P);
                 CUDA_TRY(cudaLaunchKernel((void *)k_tile_dedup, dim3(gd), dim3(THREADS), ad, 0,
                                           P->stream));
+                timing_end(P, TCG_KT_TILE_DEDUP, ed);
                 list = ls;
                 cnt = ct;
                 dup = dp;
@@ -3165,7 +3565,6 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 P->launches++;
             }
             unsigned long long *tstats = P->d_tstats;
-            timing_end(P, 0, e0);
             if (list && P->l2_ok[mode] && (P->l2 < 0 ? l2_enabled() : P->l2 != 0)) {
                 // level 2: the level-1 representatives' (tile, A) records, deduplicated
                 int rc = run_level2(P, mode, tt, crecs, list, cnt, dup, mint, tile0, lo, hi);
@@ -3181,7 +3580,7 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                           &list, &cnt, &dup, &mint, &tstats};
             cudaEvent_t e1 = timing_begin(P);
             CUDA_TRY(cudaLaunchKernel(fc, dim3(gc), dim3(THREADS), ac, P->smem_cls, P->stream));
-            timing_end(P, 1, e1);
+            timing_end(P, TCG_KT_TILE_CLASSIFY, e1);
             P->launches += 2;
         }
         return TCG_OK;
@@ -3196,7 +3595,7 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
         void *args[] = {&P->kp, &base, &count, &seed, &mask, &P->agg};
         cudaEvent_t e2 = timing_begin(P);
         CUDA_TRY(cudaLaunchKernel(fn, dim3(blocks), dim3(THREADS), args, P->smem_enum, P->stream));
-        timing_end(P, 2, e2);
+        timing_end(P, TCG_KT_ENUMERATE, e2);
         P->launches++;
         a += n;
     }

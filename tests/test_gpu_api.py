@@ -425,3 +425,43 @@ def test_level2_contraction_is_exact(api, name, raw, a, n):
             assert built == 0
     c.native.set_level2(None)
     assert reps[True] == reps[False]
+
+
+def test_super_tile_records_identical_to_direct_contraction():
+    """Tiles contracted from their super-tile's record (TCG_SUPER_BITS 4 and 6)
+    are byte-identical to the direct contraction (TCG_BUILD_GENERIC=1): the
+    deduplication finds exactly the same number of distinct tiles, and the
+    reports are equal."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json,sys; sys.path.insert(0, %r)\n"
+        "import random\n"
+        "from paper_2604_09221_b200 import builtin, sweep, SweepRange, Classifier\n"
+        "from paper_2604_09221_b200.lifting import random_unimodular\n"
+        "out = []\n"
+        "cases = [(builtin('delaunay-7'), True, 0x5A5A5A5A0 + 3, (1 << 24) + 1001),\n"
+        "         (builtin('delaunay-6'), False, 777, 1 << 22),\n"
+        "         (builtin('delaunay-5'), True, 5, 1 << 20),\n"
+        "         (builtin('bowtie8'), False, (1 << 38) + 17, 1 << 23),\n"
+        "         (builtin('delaunay-8'), False, 1 << 39, 1 << 22),\n"
+        "         (random_unimodular(7, random.Random(0xB7)), True, 1 << 33, 1 << 22)]\n"
+        "for T, raw, a, n in cases:\n"
+        "    c = Classifier(T)\n"
+        "    c.native.tile_stats()\n"
+        "    r = sweep(T, SweepRange(a, a + n), raw_space=raw, classifier=c)\n"
+        "    out.append([list(r.oval_histogram), sorted(r.scheme_map.items()),\n"
+        "                list(c.native.tile_stats())])\n"
+        "print(json.dumps(out))\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    res = {}
+    for tag, extra in (("generic", {"TCG_BUILD_GENERIC": "1"}), ("super4", {"TCG_SUPER_BITS": "4"}),
+                       ("super6", {"TCG_SUPER_BITS": "6"})):
+        env = dict(os.environ, **extra)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        assert p.returncode == 0, p.stderr
+        res[tag] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["super4"] == res["generic"]
+    assert res["super6"] == res["generic"]
