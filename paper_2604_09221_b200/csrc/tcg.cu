@@ -924,85 +924,29 @@ __device__ __forceinline__ void store_row(TileRec *rec, int node, int nn, unsign
                                      (uint32_t)(pl >> 32));
 }
 
-// One warp contracts one tile: same-sign components of the fixed vertices
-// (region_pass in COMPS mode, identical in all lanes), then lane-parallel
-// node rows.  comps: per-warp shared scratch; rec: global output.
-template <int K, int MODE>
-__device__ void build_tile(const KParams &p, const TileTables &tt, uint64_t base,
-                           const uint32_t *__restrict__ adj_s, Regions<K, MAXC> &comps,
-                           TileRec *__restrict__ rec) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, base) : base;
-    uint32_t SG[K], fixed[K], zero[K];
-    sign_words<K>(p, sigma, SG);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        fixed[k] = tt.fixed[k];
-        zero[k] = 0u;
-    }
-    // identical in all 32 lanes: the shared-memory writes are benign
-    region_pass<K, false, false, true, MAXC>(adj_s, SG, fixed, zero, tt.nfixed, comps);
-    __syncwarp();
-    const int n = comps.nreg;
-    const int nn = n + tt.nf;
-    const bool fits = n <= MAXC && nn <= tt.maxnodes;
-    unsigned long long sbits = 0;
-    if (fits) {
-        for (int node = lane; node < nn; node += 32) {
-            unsigned long long adj = 0, pl = 0;
-            if (node < n) {
-                uint32_t X[K], R[K], P[K];
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    X[k] = comps.X[node][k];
-                    R[k] = comps.R[node][k];
-                }
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    const int ks = (k + K / 2) % K;
-                    P[k] = R[ks] & p.bd[ks];
-                }
-                for (int c = 0; c < n; ++c) {
-                    uint32_t a = 0, q = 0;
-#pragma unroll
-                    for (int k = 0; k < K; ++k) {
-                        a |= X[k] & comps.R[c][k];
-                        q |= P[k] & comps.R[c][k];
-                    }
-                    if (a && c != node) adj |= 1ull << c;
-                    if (q) pl |= 1ull << c;  // includes a self link (pair inside one component)
-                }
-                for (int f = 0; f < tt.nf; ++f)
-                    if (sel<K>(X, tt.fword[f]) & tt.fbit[f]) adj |= 1ull << (n + f);
-                uint32_t sg = 0;
-#pragma unroll
-                for (int k = 0; k < K; ++k) sg |= R[k] & SG[k];
-                if (sg) sbits |= 1ull << node;
-            } else {
-                const int f = node - n;
-                adj = tt.fadj[f] << n;
-                pl = tt.fpl[f] << n;
-                const uint32_t w = tt.fword[f], b = tt.fbit[f];
-                for (int c = 0; c < n; ++c) {
-                    uint32_t x[K];
-#pragma unroll
-                    for (int k = 0; k < K; ++k) x[k] = comps.X[c][k];
-                    if (sel<K>(x, w) & b) adj |= 1ull << c;
-                }
-            }
-            store_row(rec, node, nn, adj, pl);
-        }
-    }
-    unsigned long long sg = sbits;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sg |= __shfl_xor_sync(0xffffffffu, sg, o);
-    if (lane == 0) {
-        rec->sgn_fixed = sg;
-        rec->n = n;
-        rec->nnodes = nn;
-        rec->fallback = fits ? 0 : 1;
-    }
+// Record hash, accumulated by the builders as they write the rows (the
+// deduplication only uses it to find candidates; equality is decided by
+// comparing the records word by word).
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
 }
+
+struct RecHash {
+    uint32_t h1 = 0x243F6A88u, h2 = 0x85A308D3u;
+    __device__ __forceinline__ void row(unsigned long long adj, unsigned long long pl) {
+        const uint32_t ah = (uint32_t)(adj >> 32), ph = (uint32_t)(pl >> 32);
+        h1 = (h1 ^ (uint32_t)adj ^ __funnelshift_l(ah, ah, 16)) * 0x9E3779B1u;
+        h1 ^= h1 >> 15;
+        h2 = (h2 ^ (uint32_t)pl ^ __funnelshift_l(ph, ph, 16)) * 0x85EBCA77u;
+        h2 ^= h2 >> 13;
+    }
+    __device__ __forceinline__ unsigned long long fin(unsigned long long sgn, int n, int nn) const {
+        return mix64(((unsigned long long)h1 << 32 | h2) ^
+                     mix64(sgn ^ ((unsigned long long)nn << 56) ^ ((unsigned long long)n << 48)));
+    }
+};
 
 // Region pass over a contracted graph (<= 64 nodes, one u64 per set) without
 // layers: antipodal links are followed in the same step as edges, so a lane
@@ -1257,33 +1201,12 @@ __device__ __forceinline__ Result classify_tile(const KParams &p, const TileTabl
     return finish<2, EVEN, false>(p, SG, rg, p.maxreg);
 }
 
-constexpr int BUILD_WARPS = 8;  // warps (= tiles in flight) per build CTA
-
-// Contract tiles tile0 .. tile0+ntiles-1 (one warp per tile).
-template <int K, int MODE>
-__global__ void __launch_bounds__(32 * BUILD_WARPS) k_tile_build(KParams p,
-                                                                 const TileTables *__restrict__ tt_g,
-                                                                 uint64_t tile0, uint32_t ntiles,
-                                                                 TileRec *__restrict__ recs) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t *adj_s = smem;
-    TileTables *tt = reinterpret_cast<TileTables *>(smem + 32 * K * K);
-    Regions<K, MAXC> *comps = reinterpret_cast<Regions<K, MAXC> *>(tt + 1);
-    stage_adj<K>(p, adj_s);
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    __syncthreads();
-    const int w = threadIdx.x >> 5;
-    for (uint32_t t = blockIdx.x * BUILD_WARPS + w; t < ntiles; t += gridDim.x * BUILD_WARPS)
-        build_tile<K, MODE>(p, *tt, (tile0 + t) << tt->bits, adj_s, comps[w], recs + t);
-}
-
-// Contract tiles one per LANE (no redundant SIMT work): each thread runs the
-// COMPS-mode region pass for its own tile and writes its node rows.
 template <int K, int MODE>
 __device__ __forceinline__ void build_lane(const KParams &p, const uint32_t *__restrict__ adj_s,
                                            const TileTables &tt_r, uint64_t tile0, uint32_t t,
-                                           TileRec *__restrict__ recs) {
+                                           TileRec *__restrict__ recs,
+                                           unsigned long long *__restrict__ hashes) {
+    RecHash hs;
     const TileTables *tt = &tt_r;
     const uint64_t base = (tile0 + t) << tt->bits;
     const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, base) : base;
@@ -1336,19 +1259,21 @@ __device__ __forceinline__ void build_lane(const KParams &p, const uint32_t *__r
             for (int k = 0; k < K; ++k) sg |= R[k] & SG[k];
             if (sg) sbits |= 1ull << c;
             store_row(rec, c, nn, adj, pl);
+            hs.row(adj, pl);
         }
         for (int f = 0; f < nf; ++f) {
             const unsigned long long adj = (tt->fadj[f] << n) | fadj_c[f];
             const unsigned long long pl = tt->fpl[f] << n;
             store_row(rec, n + f, nn, adj, pl);
+            hs.row(adj, pl);
         }
     }
+    hashes[t] = hs.fin(sbits, n, nn);
     rec->sgn_fixed = sbits;
     rec->n = n;
     rec->nnodes = nn;
     rec->fallback = fits ? 0 : 1;
 }
-
 // list != nullptr: only the tiles list[0 .. *count) (the ones k_tile_from_super
 // left: super-tiles whose contraction does not fit), grid-stride.
 template <int K, int MODE>
@@ -1356,6 +1281,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
                                                               const TileTables *__restrict__ tt_g,
                                                               uint64_t tile0, uint32_t ntiles,
                                                               TileRec *__restrict__ recs,
+                                                              unsigned long long *__restrict__ hashes,
                                                               const uint32_t *__restrict__ list,
                                                               const uint32_t *__restrict__ count) {
     extern __shared__ __align__(16) uint32_t smem[];
@@ -1368,7 +1294,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
     const uint32_t nwork = list ? *count : ntiles;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nwork;
          i += gridDim.x * blockDim.x)
-        build_lane<K, MODE>(p, adj_s, *tt, tile0, list ? list[i] : i, recs);
+        build_lane<K, MODE>(p, adj_s, *tt, tile0, list ? list[i] : i, recs, hashes);
 }
 
 
@@ -1536,6 +1462,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
                                                              const SuperRec *__restrict__ srecs,
                                                              uint64_t tile0, uint32_t ntiles,
                                                              TileRec *__restrict__ recs,
+                                                             unsigned long long *__restrict__ hashes,
                                                              uint32_t *__restrict__ ovf) {
     extern __shared__ __align__(16) uint32_t smem[];
     TileTables *tt = reinterpret_cast<TileTables *>(smem);
@@ -1560,50 +1487,43 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
         unsigned long long sg = S->sgn;
         for (int j = 0; j < nm; ++j) sg |= (unsigned long long)((ms >> j) & 1u) << S->msn[j];
         const unsigned long long all = nsn >= 64 ? ~0ull : ((1ull << nsn) - 1ull);
-        unsigned long long unv = all, seeds = 0, sbits = 0;
-        int n = 0;
-        while (unv) {  // pass 1: label the merged components
-            const unsigned long long seed = unv & (0ull - unv);
-            const bool s1 = (sg & seed) != 0ull;
-            const unsigned long long same = s1 ? sg : ~sg;
-            unsigned long long F = seed;
-            unv ^= seed;
-            seeds |= seed;
-            while (F) {
-                const int v = __ffsll((long long)F) - 1;
-                F &= F - 1ull;
-                lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)n;
-                const unsigned long long nw = S->adj[v] & unv & same;
-                unv ^= nw;
-                F |= nw;
+        // pass 1: label the merged components.  One flat loop of nsn pops (every
+        // lane of a warp shares the super record, so the trip count is uniform);
+        // a component closes when its frontier empties.
+        unsigned long long unv = all, seeds = 0, sbits = 0, F = 0, same = 0;
+        int n = -1;
+        for (int it = 0; it < nsn; ++it) {
+            if (F == 0ull) {
+                const unsigned long long seed = unv & (0ull - unv);
+                const bool s1 = (sg & seed) != 0ull;
+                same = s1 ? sg : ~sg;
+                F = seed;
+                unv ^= seed;
+                seeds |= seed;
+                ++n;
+                if (s1) sbits |= 1ull << n;
             }
-            if (s1) sbits |= 1ull << n;
-            ++n;
+            const int v = __ffsll((long long)F) - 1;
+            F &= F - 1ull;
+            lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)n;
+            const unsigned long long nw = S->adj[v] & unv & same;
+            unv ^= nw;
+            F |= nw;
         }
+        ++n;
         const int nn = n + nf;
         const bool fits = n <= MAXC && nn <= tt->maxnodes;
-        if (fits) {  // pass 2: rows
-            unsigned long long sd = seeds;
+        RecHash hs;
+        if (fits) {
+            // pass 2: the same traversal again, collecting each component's
+            // neighbours / links / free neighbours; rows are written as the
+            // components close
+            unsigned long long sd = seeds, M = 0, CG = 0, LK = 0;
+            uint32_t FB = 0;
             unv = all;
-            for (int c = 0; c < n; ++c) {
-                const unsigned long long seed = sd & (0ull - sd);
-                sd ^= seed;
-                const unsigned long long same = (sg & seed) ? sg : ~sg;
-                unsigned long long F = seed, M = 0, CG = 0, LK = 0;
-                uint32_t FB = 0;
-                unv ^= seed;
-                while (F) {
-                    const int v = __ffsll((long long)F) - 1;
-                    F &= F - 1ull;
-                    M |= 1ull << v;
-                    const unsigned long long a = S->adj[v];
-                    CG |= a;
-                    LK |= S->link[v];
-                    FB |= S->fadj[v];
-                    const unsigned long long nw = a & unv & same;
-                    unv ^= nw;
-                    F |= nw;
-                }
+            F = 0;
+            int c = -1;
+            auto close = [&]() {
                 unsigned long long adj = (unsigned long long)FB << n, pl = 0;
                 unsigned long long x = CG & ~M;
                 while (x) {
@@ -1618,7 +1538,32 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
                     pl |= 1ull << label(v);
                 }
                 store_row(rec, c, nn, adj, pl);
+                hs.row(adj, pl);
+            };
+            for (int it = 0; it < nsn; ++it) {
+                if (F == 0ull) {
+                    if (c >= 0) close();
+                    const unsigned long long seed = sd & (0ull - sd);
+                    sd ^= seed;
+                    same = (sg & seed) ? sg : ~sg;
+                    F = seed;
+                    unv ^= seed;
+                    M = CG = LK = 0ull;
+                    FB = 0u;
+                    ++c;
+                }
+                const int v = __ffsll((long long)F) - 1;
+                F &= F - 1ull;
+                M |= 1ull << v;
+                const unsigned long long a = S->adj[v];
+                CG |= a;
+                LK |= S->link[v];
+                FB |= S->fadj[v];
+                const unsigned long long nw = a & unv & same;
+                unv ^= nw;
+                F |= nw;
             }
+            close();
             for (int f = 0; f < nf; ++f) {
                 unsigned long long x = S->fsn[f], fc = 0;
                 while (x) {
@@ -1626,10 +1571,14 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
                     x &= x - 1ull;
                     fc |= 1ull << label(v);
                 }
-                store_row(rec, n + f, nn, (tt->fadj[f] << n) | fc, tt->fpl[f] << n);
+                const unsigned long long adj = (tt->fadj[f] << n) | fc, pl = tt->fpl[f] << n;
+                store_row(rec, n + f, nn, adj, pl);
+                hs.row(adj, pl);
             }
         }
-        rec->sgn_fixed = fits ? sbits : 0ull;
+        const unsigned long long sgf = fits ? sbits : 0ull;
+        hashes[t] = hs.fin(sgf, n, nn);
+        rec->sgn_fixed = sgf;
         rec->n = n;
         rec->nnodes = nn;
         rec->fallback = fits ? 0 : 1;
@@ -1638,117 +1587,92 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
 
 // Tile deduplication.  A tile's classification depends only on its contracted
 // record (rows, fixed signs, sizes) and the tile-local index, so tiles with
-// byte-identical records produce identical results index by index.  One warp
-// per tile hashes the record and inserts it into an open-addressing table of
-// tile ids; an equal record already present (compared word by word, never by
-// hash alone) takes the tile as a duplicate: dup[rep] += 1, mint[rep] = min
-// tile id (the witness of every scheme in the group is the smallest index,
-// which lies in the group's smallest tile).  Representatives are appended to
-// list[]; partial tiles (range ends) and fallback tiles are never merged.
-constexpr uint32_t DEDUP_EMPTY = 0xffffffffu;
+// byte-identical records produce identical results index by index.  One
+// thread per tile probes an open-addressing table keyed by the record hash
+// the builder computed (slot = hash tag << 32 | tile); a slot whose tag
+// matches is compared word by word (never by hash alone) and an equal record
+// absorbs the tile: dup[rep] += 1, mint[rep] = min tile id (the witness of
+// every scheme in the group is the smallest index, which lies in the group's
+// smallest tile).  Representatives are appended to list[] (warp-aggregated);
+// partial tiles (range ends) and fallback tiles are never merged.
+constexpr unsigned long long SLOT_EMPTY = ~0ull;
 
-__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
+__device__ __forceinline__ bool rec_equal(const TileRec *__restrict__ a,
+                                          const TileRec *__restrict__ b) {
+    if (a->n != b->n || a->nnodes != b->nnodes || a->sgn_fixed != b->sgn_fixed) return false;
+    const int nn = a->nnodes;
+    uint32_t diff = 0;
+    if (nn <= 32) {  // uint2 rows: compare two per uint4, the last one by halves
+        const uint4 *x = a->rows, *y = b->rows;
+        const int full = nn >> 1;
+#pragma unroll 4
+        for (int i = 0; i < full; ++i) {
+            const uint4 p = x[i], q = y[i];
+            diff |= (p.x ^ q.x) | (p.y ^ q.y) | (p.z ^ q.z) | (p.w ^ q.w);
+        }
+        if (nn & 1) {
+            const uint2 p = rows2(a)[nn - 1], q = rows2(b)[nn - 1];
+            diff |= (p.x ^ q.x) | (p.y ^ q.y);
+        }
+    } else {
+#pragma unroll 4
+        for (int i = 0; i < nn; ++i) {
+            const uint4 p = a->rows[i], q = b->rows[i];
+            diff |= (p.x ^ q.x) | (p.y ^ q.y) | (p.z ^ q.z) | (p.w ^ q.w);
+        }
+    }
+    return diff == 0u;
 }
 
 __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restrict__ recs,
+                                                        const unsigned long long *__restrict__ hashes,
                                                         uint32_t ntiles, uint64_t tile0, int bits,
                                                         uint64_t start, uint64_t end,
-                                                        uint32_t *__restrict__ slots,
+                                                        unsigned long long *__restrict__ slots,
                                                         uint32_t smask, uint32_t *__restrict__ dup,
                                                         uint32_t *__restrict__ mint,
                                                         uint32_t *__restrict__ list,
                                                         uint32_t *__restrict__ count) {
     const int lane = threadIdx.x & 31;
-    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    // representatives found by this warp are buffered one per lane and
-    // appended 32 at a time (one atomic per 32 instead of one per tile)
-    uint32_t mine = 0, nmine = 0;
-    auto push = [&](uint32_t t) {
-        if (lane == (int)nmine) mine = t;
-        if (++nmine == 32u) {
-            uint32_t at = 0;
-            if (lane == 0) at = atomicAdd(count, 32u);
-            list[__shfl_sync(0xffffffffu, at, 0) + lane] = mine;
-            nmine = 0;
-        }
-    };
-    for (uint32_t t = warp; t < ntiles; t += nwarps) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    bool rep = false;
+    if (t < ntiles) {
         const TileRec *r = recs + t;
-        const int nn = r->nnodes, n = r->n;
-        const unsigned long long sg = r->sgn_fixed;
         const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
         if (r->fallback || b0 < start || b1 > end) {
-            push(t);
-            continue;
-        }
-        const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
-        auto load = [&](const TileRec *q, uint4 &a, uint4 &b) {
-            a = z4;
-            b = z4;
-            if (nn <= 32) {
-                if (lane < nn) {
-                    const uint2 w = rows2(q)[lane];
-                    a.x = w.x;
-                    a.z = w.y;
+            rep = true;
+        } else {
+            const unsigned long long h = hashes[t];
+            const unsigned long long tag = (h >> 32) << 32;
+            uint32_t at = (uint32_t)h & smask;
+            while (true) {
+                unsigned long long cur = slots[at];
+                if (cur == SLOT_EMPTY) {
+                    const unsigned long long prev = atomicCAS(&slots[at], SLOT_EMPTY, tag | t);
+                    if (prev == SLOT_EMPTY) {
+                        rep = true;
+                        break;
+                    }
+                    cur = prev;
                 }
-            } else {
-                if (lane < nn) a = q->rows[lane];
-                if (lane + 32 < nn) b = q->rows[lane + 32];
-            }
-        };
-        uint4 ra, rb;
-        load(r, ra, rb);
-        unsigned long long h =
-            mix64(((unsigned long long)ra.z << 32 | ra.x) + 0x9E3779B97F4A7C15ull * (lane + 1));
-        if (nn > 32)  // warp-uniform
-            h ^= mix64(((unsigned long long)ra.w << 32 | ra.y) + 0xD1B54A32D192ED03ull * (lane + 1)) ^
-                 mix64(((unsigned long long)rb.y << 32 | rb.x) + 0x8CB92BA72F3D8DD7ull * (lane + 1)) ^
-                 mix64(((unsigned long long)rb.w << 32 | rb.z) + 0xABC98388FB8FAC03ull * (lane + 1));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
-        h ^= mix64(sg ^ ((unsigned long long)nn << 56) ^ ((unsigned long long)n << 48));
-        uint32_t at = (uint32_t)(h >> 20) & smask;
-        while (true) {
-            uint32_t cur = 0;
-            if (lane == 0) {
-                cur = slots[at];
-                if (cur == DEDUP_EMPTY) {
-                    const uint32_t prev = atomicCAS(&slots[at], DEDUP_EMPTY, t);
-                    cur = prev == DEDUP_EMPTY ? t : prev;
+                if ((cur & 0xffffffff00000000ull) == tag) {
+                    const uint32_t o = (uint32_t)cur;
+                    if (rec_equal(r, recs + o)) {
+                        atomicAdd(&dup[o], 1u);
+                        atomicMin(&mint[o], t);
+                        break;
+                    }
                 }
+                at = (at + 1) & smask;
             }
-            cur = __shfl_sync(0xffffffffu, cur, 0);
-            if (cur == t) {  // new representative
-                push(t);
-                break;
-            }
-            const TileRec *o = recs + cur;
-            bool eq = o->nnodes == nn && o->n == n && o->sgn_fixed == sg;
-            if (eq) {
-                uint4 oa, ob;
-                load(o, oa, ob);
-                eq = oa.x == ra.x && oa.y == ra.y && oa.z == ra.z && oa.w == ra.w &&
-                     ob.x == rb.x && ob.y == rb.y && ob.z == rb.z && ob.w == rb.w;
-            }
-            if (__all_sync(0xffffffffu, eq)) {
-                if (lane == 0) {
-                    atomicAdd(&dup[cur], 1u);
-                    atomicMin(&mint[cur], t);
-                }
-                break;
-            }
-            at = (at + 1) & smask;
         }
     }
-    if (nmine) {  // flush the partial buffer
-        uint32_t at = 0;
-        if (lane == 0) at = atomicAdd(count, nmine);
-        at = __shfl_sync(0xffffffffu, at, 0);
-        if (lane < (int)nmine) list[at + lane] = mine;
+    const unsigned bal = __ballot_sync(0xffffffffu, rep);
+    if (bal) {
+        uint32_t base = 0;
+        if (lane == __ffs(bal) - 1) base = atomicAdd(count, (uint32_t)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+        if (rep) list[base + __popc(bal & ((1u << lane) - 1u))] = t;
     }
 }
 
@@ -2495,6 +2419,8 @@ struct tcg_plan {
     uint32_t *d_oldlist = nullptr;   // [chunk_cap + 1]: count, then tiles for the level-1 path
     uint32_t *d_ovf = nullptr;       // [chunk_cap + 1]: count, then tiles of fallback super-tiles
     SuperRec *d_super = nullptr;     // [super_cap]
+    unsigned long long *d_hash = nullptr;   // [chunk_cap] record hashes (written by the builders)
+    unsigned long long *d_slots = nullptr;  // [2 pow2(chunk_cap)] dedup table: tag << 32 | tile
     size_t super_cap = 0;
     int blocks_bgen = 0;             // grid of the list-driven k_tile_build_lanes
     int64_t reps1_host = 0, l2_built = 0;
@@ -2577,13 +2503,10 @@ void *pick_enum(int K, bool even, int mode) {
 
 template <int K>
 void *build_fn(int mode) {
-    if (std::getenv("TCG_BUILD_WARP"))
-        return mode == MODE_RAW ? (void *)k_tile_build<K, MODE_RAW> : (void *)k_tile_build<K, MODE_REP>;
     return mode == MODE_RAW ? (void *)k_tile_build_lanes<K, MODE_RAW>
                             : (void *)k_tile_build_lanes<K, MODE_REP>;
 }
 
-bool build_per_warp() { return std::getenv("TCG_BUILD_WARP") != nullptr; }
 
 template <int K>
 void *super_fn(int mode) {
@@ -2617,7 +2540,8 @@ void *pick_cls(int K, bool even, int mode) {
 size_t build_smem(int K) {
     const size_t rg = K == 2 ? sizeof(Regions<2, MAXC>)
                              : (K == 4 ? sizeof(Regions<4, MAXC>) : sizeof(Regions<6, MAXC>));
-    return (size_t)32 * K * K * 4 + sizeof(TileTables) + (build_per_warp() ? BUILD_WARPS * rg : 0);
+    (void)rg;
+    return (size_t)32 * K * K * 4 + sizeof(TileTables);
 }
 
 size_t cls_smem(int K) {
@@ -3113,7 +3037,7 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
         return bail(e, "occupancy");
     P->blocks_l2cls = std::max(1, bps) * P->nsm;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-             &bps, pick_build(K, MODE_RAW), build_per_warp() ? 32 * BUILD_WARPS : THREADS,
+             &bps, pick_build(K, MODE_RAW), THREADS,
              P->smem_build)) != cudaSuccess)
         return bail(e, "occupancy");
     P->blocks_build = std::max(1, bps) * P->nsm;
@@ -3138,7 +3062,7 @@ int tcg_plan_destroy(tcg_plan *P) {
     DeviceGuard guard(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     timing_resolve(P);
-    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_oldlist, P->d_ovf, P->d_super, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_oldlist, P->d_ovf, P->d_super, P->d_hash, P->d_slots, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
@@ -3458,7 +3382,7 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             size_t fr = 0, tot = 0;
             CUDA_TRY(cudaMemGetInfo(&fr, &tot));
             if (P->d_recs) fr += sizeof(TileRec) * (size_t)P->chunk_cap;
-            const size_t per_tile = sizeof(TileRec) + 7 * sizeof(uint32_t);
+            const size_t per_tile = sizeof(TileRec) + 6 * sizeof(uint32_t) + 5 * 8;
             while (chunk > (1u << 14) && (size_t)chunk * per_tile > fr / 4) chunk >>= 1;
             if (chunk > P->chunk_cap) {
                 cudaFree(P->d_recs);
@@ -3473,8 +3397,14 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 CUDA_TRY(cudaMalloc(&P->d_ovf, sizeof(uint32_t) * ((size_t)chunk + 1)));
                 CUDA_TRY(cudaMalloc(&P->d_recs, sizeof(TileRec) * (size_t)chunk));
                 CUDA_TRY(cudaMalloc(&P->d_oldlist, sizeof(uint32_t) * ((size_t)chunk + 1)));
-                CUDA_TRY(cudaMalloc(&P->d_dedup, sizeof(uint32_t) * (2 * (size_t)next_pow2(chunk) +
-                                                                     3 * (size_t)chunk + 1)));
+                CUDA_TRY(cudaMalloc(&P->d_dedup, sizeof(uint32_t) * (3 * (size_t)chunk + 1)));
+                cudaFree(P->d_hash);
+                cudaFree(P->d_slots);
+                P->d_hash = nullptr;
+                P->d_slots = nullptr;
+                CUDA_TRY(cudaMalloc(&P->d_hash, sizeof(unsigned long long) * (size_t)chunk));
+                CUDA_TRY(cudaMalloc(&P->d_slots,
+                                    sizeof(unsigned long long) * 2 * (size_t)next_pow2(chunk)));
                 P->chunk_cap = chunk;
             }
         }
@@ -3487,15 +3417,12 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             uint32_t nt = (uint32_t)std::min<uint64_t>(chunk, t_end - t0);
             uint64_t tile0 = t0;
             TileRec *recs = P->d_recs;
-            const unsigned per_block = build_per_warp() ? BUILD_WARPS : THREADS;
-            const unsigned gb = build_per_warp()
-                                    ? (unsigned)std::min<uint64_t>(P->blocks_build,
-                                                                   (nt + per_block - 1) / per_block)
-                                    : (unsigned)((nt + per_block - 1) / per_block);
+            unsigned long long *hashes = P->d_hash;
+            const unsigned gb = (unsigned)((nt + THREADS - 1) / THREADS);
             const uint32_t *nolist = nullptr, *nocount = nullptr;
             cudaEvent_t e0 = timing_begin(P);
             const int sh = P->h_tiles[mode].sh;
-            if (!build_per_warp() && sh > 0) {
+            if (sh > 0) {
                 // super-tiles: contract the shared part once per 2^sh tiles, then
                 // each tile from its super record; fallback super-tiles go to the
                 // generic kernel
@@ -3522,20 +3449,19 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 uint32_t *ovf = P->d_ovf;
                 CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), P->stream));
                 const SuperRec *csr = sr;
-                void *af[] = {&tt, &csr, &tile0, &nt, &recs, &ovf};
+                void *af[] = {&tt, &csr, &tile0, &nt, &recs, &hashes, &ovf};
                 CUDA_TRY(cudaLaunchKernel((void *)k_tile_from_super,
                                           dim3((nt + THREADS - 1) / THREADS), dim3(THREADS), af,
                                           FROM_SUPER_SMEM, P->stream));
                 const uint32_t *ol = ovf + 1, *oc = ovf;
-                void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs, &ol, &oc};
+                void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs, &hashes, &ol, &oc};
                 CUDA_TRY(cudaLaunchKernel(fb, dim3(P->blocks_bgen), dim3(THREADS), ab,
                                           P->smem_build, P->stream));
                 P->launches += 2;
             } else {
-                void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs, &nolist, &nocount};
-                CUDA_TRY(cudaLaunchKernel(fb, dim3(gb), dim3(build_per_warp() ? 32 * BUILD_WARPS
-                                                                               : THREADS),
-                                          ab, P->smem_build, P->stream));
+                void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs, &hashes, &nolist, &nocount};
+                CUDA_TRY(cudaLaunchKernel(fb, dim3(gb), dim3(THREADS), ab, P->smem_build,
+                                          P->stream));
             }
             timing_end(P, TCG_KT_TILE_BUILD, e0);
             uint64_t lo = start, hi = end;
@@ -3543,17 +3469,18 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             const uint32_t *list = nullptr, *cnt = nullptr, *dup = nullptr, *mint = nullptr;
             if (P->dedup < 0 ? dedup_enabled() : P->dedup != 0) {
                 const size_t C = P->chunk_cap, Cn = next_pow2(nt);  // Cn <= next_pow2(C)
-                uint32_t *slots = P->d_dedup, *mnt = slots + 2 * (size_t)next_pow2(P->chunk_cap),
-                         *dp = mnt + C, *ct = dp + C, *ls = ct + 1;
-                CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(uint32_t) * 2 * Cn, P->stream));
+                unsigned long long *slots = P->d_slots;
+                uint32_t *mnt = P->d_dedup, *dp = mnt + C, *ct = dp + C, *ls = ct + 1;
+                const unsigned long long *chash = hashes;
+                CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(unsigned long long) * 2 * Cn, P->stream));
                 CUDA_TRY(cudaMemsetAsync(mnt, 0xff, sizeof(uint32_t) * nt, P->stream));
                 CUDA_TRY(cudaMemsetAsync(dp, 0, sizeof(uint32_t) * nt, P->stream));
                 CUDA_TRY(cudaMemsetAsync(ct, 0, sizeof(uint32_t), P->stream));
                 uint32_t smask = (uint32_t)(2 * Cn - 1);
                 int ibits = bits;
-                void *ad[] = {&crecs, &nt, &tile0, &ibits, &lo, &hi, &slots, &smask, &dp, &mnt, &ls, &ct};
-                const unsigned gd = (unsigned)std::min<uint64_t>(
-                    (uint64_t)P->nsm * 8, (nt + CLS_WARPS - 1) / CLS_WARPS);
+                void *ad[] = {&crecs, &chash, &nt, &tile0, &ibits, &lo, &hi, &slots, &smask, &dp,
+                              &mnt, &ls, &ct};
+                const unsigned gd = (unsigned)((nt + THREADS - 1) / THREADS);
                 cudaEvent_t ed = timing_begin(P);
                 CUDA_TRY(cudaLaunchKernel((void *)k_tile_dedup, dim3(gd), dim3(THREADS), ad, 0,
                                           P->stream));
