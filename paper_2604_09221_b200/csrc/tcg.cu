@@ -1712,7 +1712,11 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
     const uint32_t nwork = list ? *count : ntiles;
     if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(tstats, (unsigned long long)nwork);
     for (uint32_t i = blockIdx.x * CLS_WARPS + w; i < nwork; i += gridDim.x * CLS_WARPS) {
-        const uint32_t t = list ? list[i] : i;
+        // list entries: tile, or tile | (a + 1) << 24 for the 32-index slice of
+        // A pattern a only (a slice the level-2 path could not take)
+        const uint32_t e = list ? list[i] : i;
+        const uint32_t t = e & 0xffffffu, sub = e >> 24;
+        const uint32_t lo0 = sub ? (sub - 1u) << 5 : 0u, lo1 = sub ? lo0 + 32u : tsize;
         const uint32_t weight = list ? 1u + dup[t] : 1u;
         const uint32_t tw = list ? min(t, mint[t]) : t;
         const TileRec *src = recs + t;
@@ -1735,7 +1739,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
         const unsigned long long sgf = src->sgn_fixed;
         __syncwarp();
         const uint64_t base = (tile0 + tw) << bits;
-        if (!fb && nn <= 32) {  // two patchworks per thread (tile sizes are >= 64)
+        if (!fb && nn <= 32 && !sub) {  // two patchworks per thread (tile sizes are >= 64)
             const uint32_t used = nn >= 32 ? ~0u : ((1u << nn) - 1u);
             for (uint32_t low = lane; low < tsize; low += 64) {
                 const unsigned long long fa =
@@ -1763,7 +1767,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
             __syncwarp();
             continue;
         }
-        for (uint32_t low = lane; low < tsize; low += 32) {
+        for (uint32_t low = lo0 + lane; low < lo1; low += 32) {
             const uint64_t m = base + low;
             const bool valid = m >= start && m < end;
             Result r;
@@ -1787,7 +1791,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
 }
 
 // ------------------------------------------------------------ level 2
-// Level-2 contraction of a representative tile (odd degree, <= 32 nodes).
+// Level-2 contraction of a representative tile (odd degree, <= 64 nodes).
 // Fix the signs of the A points (tile-local index bits 5..bits-1) as well:
 // the fixed components and the A nodes then merge, through same-sign edges
 // and antipodal links, into "super-nodes" -- subsets of regions whatever
@@ -1812,7 +1816,85 @@ __device__ __forceinline__ uint32_t l2_compress(const TileTables &tt, uint32_t f
     return r;
 }
 
+// Super-node BFS of one (tile, A pattern); MT = uint32_t for <= 32-node
+// records (uint2 rows), unsigned long long for 33..64 (uint4 rows).  Writes
+// the record words to out[0 .. m] and returns m, or -1 when m > mmax (the
+// level-2 classifier needs m + nB <= 32 nodes; only possible above 32 nodes).
+template <typename MT>
+__device__ __forceinline__ int l2_build_one(const TileTables &tt, const TileRec *__restrict__ rec,
+                                            uint32_t a, int mmax, unsigned long long *out,
+                                            unsigned long long &hout) {
+    const int n = rec->n, nB = tt.nB;
+    constexpr bool WIDE = sizeof(MT) == 8;
+    auto row = [&](int u, MT &rx, MT &ry) {
+        if constexpr (WIDE) {
+            const uint4 r4 = rec->rows[u];
+            rx = (MT)r4.x | ((MT)r4.y << 32);
+            ry = (MT)r4.z | ((MT)r4.w << 32);
+        } else {
+            const uint2 r2 = rows2(rec)[u];
+            rx = r2.x;
+            ry = r2.y;
+        }
+    };
+    const uint32_t lowA = a << 5;
+    const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
+    const MT one = 1;
+    const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa) << n);
+    const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa << n);
+    const MT FBn = (MT)tt.fbm << n;
+    MT Mem[32], CG[32];
+    uint32_t HI[32];
+    MT unv = G;
+    int m = 0;
+    while (unv) {
+        if (m == mmax) return -1;
+        MT f = unv & ((MT)0 - unv);
+        unv ^= f;
+        MT M = f, cg = 0, pb = 0, mb = 0, lb = 0;
+        while (f) {
+            const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
+            f &= f - one;
+            MT rx, ry;
+            row(u, rx, ry);
+            const MT diff = sg1 ^ ((MT)0 - ((sg1 >> u) & one));  // nodes of the other sign
+            const MT nw = ((rx & ~diff) | ry) & unv;
+            unv ^= nw;
+            f |= nw;
+            M |= nw;
+            cg |= rx & G & diff;
+            const MT bp = rx & FBn;
+            if ((sg1 >> u) & one) pb |= bp;
+            else mb |= bp;
+            lb |= ry & FBn;
+        }
+        Mem[m] = M;
+        CG[m] = cg;
+        HI[m] = l2_compress(tt, (uint32_t)(pb >> n)) | l2_compress(tt, (uint32_t)(mb >> n)) << nB |
+                l2_compress(tt, (uint32_t)(lb >> n)) << (2 * nB);
+        ++m;
+    }
+    unsigned long long h = mix64(0x51ED2701u + (unsigned long long)m);
+    out[0] = (unsigned long long)m;
+    for (int q = 0; q < m; ++q) {
+        uint32_t cs = 0;
+        for (int q2 = 0; q2 < m; ++q2)
+            if (CG[q] & Mem[q2]) cs |= 1u << q2;
+        const uint32_t self = (cs >> q) & 1u;
+        cs &= ~(1u << q);
+        const unsigned long long w =
+            (unsigned long long)cs | (unsigned long long)(HI[q] | self << (3 * nB)) << 32;
+        out[1 + q] = w;
+        h = mix64(h ^ (w + 0x9E3779B97F4A7C15ull * (q + 1)));
+    }
+    hout = h;
+    return m;
+}
+
 // One thread per (representative tile, A pattern) of list1[i0 .. i0+nb).
+// Tiles the level-2 path cannot take go to oldlist for the level-1
+// classifier: whole tiles (entry = tile: range ends, fallback) or single A
+// slices whose super-node graph is too large (entry = tile | (a + 1) << 24).
 __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restrict__ tt_g,
                                                       const TileRec *__restrict__ recs,
                                                       const uint32_t *__restrict__ list1,
@@ -1832,67 +1914,28 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
         reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
     __syncthreads();
     const TileTables &tt = tts;
-    const int la = tt.la, nB = tt.nB, bits = tt.bits;
+    const int la = tt.la, bits = tt.bits;
+    const int mmax = 32 - tt.nB;
     const uint32_t nrec = nb << la;
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nrec; j += gridDim.x * blockDim.x) {
         const uint32_t i = i0 + (j >> la), a = j & ((1u << la) - 1u);
         const uint32_t t = list1[i];
         const TileRec *rec = recs + t;
-        const int nn = rec->nnodes, n = rec->n;
+        const int nn = rec->nnodes;
         const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
-        if (rec->fallback || nn > 32 || b0 < start || b1 > end) {
+        if (rec->fallback || b0 < start || b1 > end) {
             if (a == 0) oldlist[atomicAdd(oldcount, 1u)] = t;
             wts[j] = 0u;
             continue;
         }
-        const uint2 *R = rows2(rec);
-        const uint32_t lowA = a << 5;
-        const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
-        const uint32_t sg1 = (uint32_t)rec->sgn_fixed | ((uint32_t)fsA & tt.fa) << n;
-        const uint32_t G = (n >= 32 ? ~0u : ((1u << n) - 1u)) | (tt.fa << n);
-        const uint32_t FBn = tt.fbm << n;
-        uint32_t Mem[32], CG[32], HI[32];
-        uint32_t unv = G;
-        int m = 0;
-        while (unv) {
-            uint32_t f = unv & (0u - unv);
-            unv ^= f;
-            uint32_t M = f, cg = 0, pb = 0, mb = 0, lb = 0;
-            while (f) {
-                const int u = __ffs(f) - 1;
-                f &= f - 1u;
-                const uint2 row = R[u];
-                const uint32_t diff = sg1 ^ (0u - ((sg1 >> u) & 1u));  // nodes of the other sign
-                const uint32_t nw = ((row.x & ~diff) | row.y) & unv;
-                unv ^= nw;
-                f |= nw;
-                M |= nw;
-                cg |= row.x & G & diff;
-                const uint32_t bp = row.x & FBn;
-                if ((sg1 >> u) & 1u) pb |= bp;
-                else mb |= bp;
-                lb |= row.y & FBn;
-            }
-            Mem[m] = M;
-            CG[m] = cg;
-            HI[m] = l2_compress(tt, pb >> n) | l2_compress(tt, mb >> n) << nB |
-                    l2_compress(tt, lb >> n) << (2 * nB);
-            ++m;
-        }
         unsigned long long *out = pool + (size_t)j * stride;
-        unsigned long long h = mix64(0x51ED2701u + (unsigned long long)m);
-        out[0] = (unsigned long long)m;
-        for (int q = 0; q < m; ++q) {
-            uint32_t cs = 0;
-            for (int q2 = 0; q2 < m; ++q2)
-                if (CG[q] & Mem[q2]) cs |= 1u << q2;
-            const uint32_t self = (cs >> q) & 1u;
-            cs &= ~(1u << q);
-            const unsigned long long w =
-                (unsigned long long)cs |
-                (unsigned long long)(HI[q] | self << (3 * nB)) << 32;
-            out[1 + q] = w;
-            h = mix64(h ^ (w + 0x9E3779B97F4A7C15ull * (q + 1)));
+        unsigned long long h = 0;
+        const int m = nn <= 32 ? l2_build_one<uint32_t>(tt, rec, a, mmax, out, h)
+                               : l2_build_one<unsigned long long>(tt, rec, a, mmax, out, h);
+        if (m < 0) {
+            oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << 24);
+            wts[j] = 0u;
+            continue;
         }
         hashes[j] = h;
         wts[j] = 1u + dup1[t];
