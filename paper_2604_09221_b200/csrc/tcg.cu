@@ -886,6 +886,7 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     // level-2 contraction (odd degree): index bits 0..4 are the B points (one
     // per lane), bits 5..bits-1 the A points fixed per level-2 record
     int l2, nB, NA, la;                     // enabled, B nodes, A patterns = 2^la
+    int l2shift, pad3;                      // B nodes = free nodes l2shift .. +nB-1 (or -1)
     uint32_t fa, fbm;                       // free-node masks of A and B nodes
     int8_t l2j[MAXF];                       // free node -> B index (or -1)
     uint32_t l2adjB[16], l2linkB[16];       // B-B adjacency / links (B index space)
@@ -1804,9 +1805,9 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
 // deduplicated the same way (exact comparison, weights add, witness = the
 // smallest (tile, A) position of the group).
 //   word[s] = crossS | (plusB | minusB << nB | linkB << 2nB | self << 3nB) << 32
-constexpr uint32_t L2_EMPTY = 0xffffffffu;
 
 __device__ __forceinline__ uint32_t l2_compress(const TileTables &tt, uint32_t freemask) {
+    if (tt.l2shift >= 0) return (freemask >> tt.l2shift) & ((1u << tt.nB) - 1u);
     uint32_t r = 0;
     while (freemask) {
         const int f = __ffs(freemask) - 1;
@@ -1874,20 +1875,104 @@ __device__ __forceinline__ int l2_build_one(const TileTables &tt, const TileRec 
                 l2_compress(tt, (uint32_t)(lb >> n)) << (2 * nB);
         ++m;
     }
-    unsigned long long h = mix64(0x51ED2701u + (unsigned long long)m);
     out[0] = (unsigned long long)m;
+    uint32_t hh = 0x9E3779B9u, hl = 0xC2B2AE3Du;  // same hash as l2_build_narrow
     for (int q = 0; q < m; ++q) {
         uint32_t cs = 0;
         for (int q2 = 0; q2 < m; ++q2)
             if (CG[q] & Mem[q2]) cs |= 1u << q2;
         const uint32_t self = (cs >> q) & 1u;
         cs &= ~(1u << q);
-        const unsigned long long w =
-            (unsigned long long)cs | (unsigned long long)(HI[q] | self << (3 * nB)) << 32;
-        out[1 + q] = w;
-        h = mix64(h ^ (w + 0x9E3779B97F4A7C15ull * (q + 1)));
+        const uint32_t hi = HI[q] | self << (3 * nB);
+        out[1 + q] = (unsigned long long)cs | (unsigned long long)hi << 32;
+        hh = (hh ^ hi) * 0x85EBCA77u;
+        hh ^= hh >> 13;
+        hl = (hl ^ cs) * 0x9E3779B1u;
+        hl ^= hl >> 15;
     }
-    hout = h;
+    hout = mix64(((unsigned long long)hh << 32 | hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
+    return m;
+}
+
+// <= 32-node records (98 % at d=7): the same super-node BFS without
+// per-super-node arrays in local memory.  Node labels (bytes) and the
+// cross-adjacency words cs[q] are lane-private shared memory (bank = lane);
+// when super-node q closes, its crossed neighbours that are already labelled
+// (earlier super-nodes) set cs[q] and cs[q2] -- every pair is met once, from
+// its later end -- and the record's high half (B-node words, self flag) is
+// written immediately; the low halves (cs) follow at the end.
+constexpr int L2B_WORDS = 8 + 32;  // labels (32 nodes, 4 per word) | cs[32]
+constexpr size_t L2B_SMEM = (size_t)L2B_WORDS * 4 * THREADS + 256 * THREADS;  // + staged rows
+
+__device__ __forceinline__ int l2_build_narrow(const TileTables &tt,
+                                               const TileRec *__restrict__ rec,
+                                               const uint2 *__restrict__ R, uint32_t a,
+                                               unsigned long long *out, unsigned long long &hout,
+                                               uint32_t *mine) {
+    const int n = rec->n, nB = tt.nB;
+    uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
+    uint32_t *cs = mine + 8 * THREADS;
+    const uint32_t lowA = a << 5;
+    const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
+    const uint32_t sg1 = (uint32_t)rec->sgn_fixed | (((uint32_t)fsA & tt.fa) << n);
+    const uint32_t G = (n >= 32 ? ~0u : ((1u << n) - 1u)) | (tt.fa << n);
+    const uint32_t FBn = tt.fbm << n;
+    uint32_t *out32 = reinterpret_cast<uint32_t *>(out);
+    uint32_t unv = G, done = 0, hh = 0x9E3779B9u;
+    int m = 0;
+    while (unv) {
+        uint32_t f = unv & (0u - unv);
+        unv ^= f;
+        uint32_t M = f, cg = 0, pb = 0, mb = 0, lk = 0;
+        while (f) {
+            const int u = __ffs(f) - 1;
+            f &= f - 1u;
+            lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
+            const uint2 row = R[u];
+            const uint32_t s = (sg1 >> u) & 1u;
+            const uint32_t diff = sg1 ^ (0u - s);  // nodes of the other sign
+            const uint32_t nw = ((row.x & ~diff) | row.y) & unv;
+            unv ^= nw;
+            f |= nw;
+            M |= nw;
+            cg |= row.x & G & diff;
+            const uint32_t bp = row.x & FBn;
+            pb |= s ? bp : 0u;
+            mb |= s ? 0u : bp;
+            lk |= row.y & FBn;
+        }
+        // crossed neighbours in earlier super-nodes (labelled): both ends' cs words
+        uint32_t c = 0, x = cg & done;
+        while (x) {
+            const int v = __ffs(x) - 1;
+            x &= x - 1u;
+            const uint32_t q2 = lb[(v >> 2) * (4 * THREADS) + (v & 3)];
+            c |= 1u << q2;
+        }
+        cs[m * THREADS] = c;
+        for (uint32_t y = c; y;) {
+            const int q2 = __ffs(y) - 1;
+            y &= y - 1u;
+            cs[q2 * THREADS] |= 1u << m;
+        }
+        const uint32_t self = (cg & M) != 0u;
+        const uint32_t hi = l2_compress(tt, pb >> n) | l2_compress(tt, mb >> n) << nB |
+                            l2_compress(tt, lk >> n) << (2 * nB) | self << (3 * nB);
+        out32[2 * (1 + m) + 1] = hi;
+        hh = (hh ^ hi) * 0x85EBCA77u;
+        hh ^= hh >> 13;
+        done |= M;
+        ++m;
+    }
+    out[0] = (unsigned long long)m;
+    uint32_t hl = 0xC2B2AE3Du;
+    for (int q = 0; q < m; ++q) {
+        const uint32_t c = cs[q * THREADS];
+        out32[2 * (1 + q)] = c;
+        hl = (hl ^ c) * 0x9E3779B1u;
+        hl ^= hl >> 15;
+    }
+    hout = mix64(((unsigned long long)hh << 32 | hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
     return m;
 }
 
@@ -1910,6 +1995,8 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
                                                       uint32_t *__restrict__ oldlist,
                                                       uint32_t *__restrict__ oldcount) {
     __shared__ TileTables tts;
+    extern __shared__ __align__(16) uint32_t l2smem[];
+    uint32_t *mine = l2smem + threadIdx.x;
     for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
         reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
     __syncthreads();
@@ -1917,29 +2004,47 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
     const int la = tt.la, bits = tt.bits;
     const int mmax = 32 - tt.nB;
     const uint32_t nrec = nb << la;
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nrec; j += gridDim.x * blockDim.x) {
+    // the 2^la lanes of one tile stage its (<= 32-node) rows in shared memory
+    // first: the breadth-first pass then reads rows at shared-memory latency
+    const int lane = threadIdx.x & 31, lpt = la < 5 ? la : 5;
+    uint4 *slot = reinterpret_cast<uint4 *>(l2smem + L2B_WORDS * THREADS) +
+                  16 * ((threadIdx.x >> 5) * (32 >> lpt) + (lane >> lpt));
+    for (uint32_t jb = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); jb < nrec;
+         jb += gridDim.x * blockDim.x) {  // warp-uniform
+        const uint32_t j = jb + lane;
+        const bool valid = j < nrec;
         const uint32_t i = i0 + (j >> la), a = j & ((1u << la) - 1u);
-        const uint32_t t = list1[i];
+        const uint32_t t = valid ? list1[i] : 0u;
         const TileRec *rec = recs + t;
-        const int nn = rec->nnodes;
-        const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
-        if (rec->fallback || b0 < start || b1 > end) {
-            if (a == 0) oldlist[atomicAdd(oldcount, 1u)] = t;
-            wts[j] = 0u;
-            continue;
+        if (valid) {
+            const uint4 *src = rec->rows;
+            for (int q = lane & ((1 << lpt) - 1); q < 16; q += 1 << lpt) slot[q] = src[q];
         }
-        unsigned long long *out = pool + (size_t)j * stride;
-        unsigned long long h = 0;
-        const int m = nn <= 32 ? l2_build_one<uint32_t>(tt, rec, a, mmax, out, h)
-                               : l2_build_one<unsigned long long>(tt, rec, a, mmax, out, h);
-        if (m < 0) {
-            oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << 24);
-            wts[j] = 0u;
-            continue;
+        __syncwarp();
+        if (valid) {
+            const int nn = rec->nnodes;
+            const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
+            if (rec->fallback || b0 < start || b1 > end) {
+                if (a == 0) oldlist[atomicAdd(oldcount, 1u)] = t;
+                wts[j] = 0u;
+            } else {
+                unsigned long long *out = pool + (size_t)j * stride;
+                unsigned long long h = 0;
+                const int m =
+                    nn <= 32 ? l2_build_narrow(tt, rec, reinterpret_cast<const uint2 *>(slot), a,
+                                               out, h, mine)
+                             : l2_build_one<unsigned long long>(tt, rec, a, mmax, out, h);
+                if (m < 0) {
+                    oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << 24);
+                    wts[j] = 0u;
+                } else {
+                    hashes[j] = h;
+                    wts[j] = 1u + dup1[t];
+                    poss[j] = (min(t, mint1[t]) << la) | a;
+                }
+            }
         }
-        hashes[j] = h;
-        wts[j] = 1u + dup1[t];
-        poss[j] = (min(t, mint1[t]) << la) | a;
+        __syncwarp();
     }
 }
 
@@ -1949,43 +2054,48 @@ __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *
                                                       const unsigned long long *__restrict__ hashes,
                                                       const uint32_t *__restrict__ wts,
                                                       const uint32_t *__restrict__ poss,
-                                                      uint32_t *__restrict__ slots, uint32_t smask,
+                                                      unsigned long long *__restrict__ slots,
+                                                      uint32_t smask,
                                                       uint32_t *__restrict__ w2,
                                                       uint32_t *__restrict__ pos2,
                                                       uint32_t *__restrict__ list2,
                                                       uint32_t *__restrict__ count2) {
+    // slot = hash tag << 32 | record; a tag match is confirmed word by word
     const int lane = threadIdx.x & 31;
     const uint32_t tot = gridDim.x * blockDim.x;
     const uint32_t jmax = (nrec + 31u) & ~31u;  // whole warps iterate together
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < jmax; j += tot) {
         bool isnew = false;
-        if (j < nrec && wts[j]) {
+        const uint32_t wj = j < nrec ? wts[j] : 0u;
+        if (wj) {
             const unsigned long long h = hashes[j];
+            const unsigned long long tag = (h >> 32) << 32;
             const unsigned long long *mine = pool + (size_t)j * stride;
-            const int m = (int)mine[0];
-            uint32_t at = (uint32_t)(h >> 17) & smask;
+            const unsigned long long m = mine[0];
+            uint32_t at = (uint32_t)h & smask;
             while (true) {
-                uint32_t cur = slots[at];
-                if (cur == L2_EMPTY) {
-                    const uint32_t prev = atomicCAS(&slots[at], L2_EMPTY, j);
-                    cur = prev == L2_EMPTY ? j : prev;
+                unsigned long long cur = slots[at];
+                if (cur == SLOT_EMPTY) {
+                    const unsigned long long prev = atomicCAS(&slots[at], SLOT_EMPTY, tag | j);
+                    if (prev == SLOT_EMPTY) {
+                        isnew = true;
+                        atomicAdd(&w2[j], wj);
+                        atomicMin(&pos2[j], poss[j]);
+                        break;
+                    }
+                    cur = prev;
                 }
-                if (cur == j) {
-                    isnew = true;
-                    atomicAdd(&w2[j], wts[j]);
-                    atomicMin(&pos2[j], poss[j]);
-                    break;
-                }
-                bool eq = hashes[cur] == h;
-                if (eq) {
-                    const unsigned long long *o = pool + (size_t)cur * stride;
-                    eq = (int)o[0] == m;
-                    for (int q = 1; q <= m && eq; ++q) eq = o[q] == mine[q];
-                }
-                if (eq) {
-                    atomicAdd(&w2[cur], wts[j]);
-                    atomicMin(&pos2[cur], poss[j]);
-                    break;
+                if ((cur & 0xffffffff00000000ull) == tag) {
+                    const uint32_t o = (uint32_t)cur;
+                    const unsigned long long *ow = pool + (size_t)o * stride;
+                    unsigned long long diff = ow[0] ^ m;
+#pragma unroll 4
+                    for (int q = 1; q <= (int)m; ++q) diff |= ow[q] ^ mine[q];
+                    if (diff == 0ull) {
+                        atomicAdd(&w2[o], wj);
+                        atomicMin(&pos2[o], poss[j]);
+                        break;
+                    }
                 }
                 at = (at + 1) & smask;
             }
@@ -2458,7 +2568,8 @@ struct tcg_plan {
     int l2_stride = 0;               // u64 words per level-2 record
     size_t l2_cap = 0;               // level-2 records the buffers hold
     unsigned long long *d_l2pool = nullptr, *d_l2hash = nullptr;
-    uint32_t *d_l2u32 = nullptr;     // wts | poss | w2 | pos2 | list2 | slots(2 pow2) | count2
+    uint32_t *d_l2u32 = nullptr;     // wts | poss | w2 | pos2 | list2 | count2
+    unsigned long long *d_l2slots = nullptr;  // [2 pow2(l2_cap)] tag << 32 | record
     uint32_t *d_oldlist = nullptr;   // [chunk_cap + 1]: count, then tiles for the level-1 path
     uint32_t *d_ovf = nullptr;       // [chunk_cap + 1]: count, then tiles of fallback super-tiles
     SuperRec *d_super = nullptr;     // [super_cap]
@@ -2761,6 +2872,8 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
             T.l2linkB[q] = comp(T.fpl[fj[q]] & fb);
         }
         for (int b = 0; b < 32; ++b) T.l2bsign[b] = comp(T.fsign[0][b] & fb);
+        T.l2shift = -1;
+        if (fb >> __builtin_ctz(fb) == (1u << nB) - 1u) T.l2shift = __builtin_ctz(fb);
         T.l2 = 1;
     };
     for (int a = 0; a < D->nap; ++a) {
@@ -3049,6 +3162,9 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)build_smem(K))) != cudaSuccess)
             return bail(e, "super smem");
+    if ((e = cudaFuncSetAttribute((void *)k_l2_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L2B_SMEM)) != cudaSuccess)
+        return bail(e, "l2 build smem");
     if ((e = cudaFuncSetAttribute((void *)k_tile_from_super,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)FROM_SUPER_SMEM)) != cudaSuccess)
@@ -3105,7 +3221,7 @@ int tcg_plan_destroy(tcg_plan *P) {
     DeviceGuard guard(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     timing_resolve(P);
-    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_oldlist, P->d_ovf, P->d_super, P->d_hash, P->d_slots, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_l2slots, P->d_oldlist, P->d_ovf, P->d_super, P->d_hash, P->d_slots, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
@@ -3323,8 +3439,10 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
     if (n1 == 0) return TCG_OK;
     const int la = T.la;
     const uint32_t stride = (uint32_t)(1 + 32 - T.nB);
-    const size_t want = (size_t)n1 << la;
-    const size_t per_rec = stride * 8 + 8 + 4 * 7 + 8;
+    // sized once for the whole chunk (every level-1 tile a representative), so
+    // that later sweeps never reallocate inside a timed region
+    const size_t want = std::max((size_t)n1, (size_t)P->chunk_cap) << la;
+    const size_t per_rec = stride * 8 + 8 + 4 * 6 + 16;
     if (want > P->l2_cap || (int)stride != P->l2_stride) {
         size_t fr = 0, tot = 0;
         CUDA_TRY(cudaMemGetInfo(&fr, &tot));
@@ -3341,21 +3459,26 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
             P->l2_cap = 0;
             CUDA_TRY(cudaMalloc(&P->d_l2pool, sizeof(unsigned long long) * stride * cap));
             CUDA_TRY(cudaMalloc(&P->d_l2hash, sizeof(unsigned long long) * cap));
-            CUDA_TRY(cudaMalloc(&P->d_l2u32, sizeof(uint32_t) * (5 * cap + 2 * (size_t)next_pow2((uint32_t)cap) + 1)));
+            CUDA_TRY(cudaMalloc(&P->d_l2u32, sizeof(uint32_t) * (5 * cap + 1)));
+            cudaFree(P->d_l2slots);
+            P->d_l2slots = nullptr;
+            CUDA_TRY(cudaMalloc(&P->d_l2slots, sizeof(unsigned long long) * 2 *
+                                                   (size_t)next_pow2((uint32_t)cap)));
             P->l2_cap = cap;
             P->l2_stride = (int)stride;
         }
     }
     const size_t cap = P->l2_cap;
     uint32_t *wts = P->d_l2u32, *poss = wts + cap, *w2 = poss + cap, *pos2 = w2 + cap,
-             *list2 = pos2 + cap, *slots = list2 + cap,
-             *count2 = slots + 2 * (size_t)next_pow2((uint32_t)cap);
+             *list2 = pos2 + cap, *count2 = list2 + cap;
+    unsigned long long *slots = P->d_l2slots;
     const uint32_t nbmax = (uint32_t)(cap >> la);
     for (uint32_t i0 = 0; i0 < n1; i0 += nbmax) {
         uint32_t nb = std::min(nbmax, n1 - i0);
         uint32_t nrec = nb << la;
         const uint32_t np2 = next_pow2(nrec);
-        CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(uint32_t) * 2 * (size_t)np2, P->stream));
+        CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(unsigned long long) * 2 * (size_t)np2,
+                                 P->stream));
         CUDA_TRY(cudaMemsetAsync(w2, 0, sizeof(uint32_t) * nrec, P->stream));
         CUDA_TRY(cudaMemsetAsync(pos2, 0xff, sizeof(uint32_t) * nrec, P->stream));
         CUDA_TRY(cudaMemsetAsync(count2, 0, sizeof(uint32_t), P->stream));
@@ -3367,7 +3490,10 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
         void *a1[] = {&tt, &recs, &list1, &dup1, &mint1, &i0, &nb, &t0, &a, &b, &pool,
                       (void *)&stride, &hashes, &wts, &poss, &oldlist, &oldcount};
         cudaEvent_t e0 = timing_begin(P);
-        CUDA_TRY(cudaLaunchKernel((void *)k_l2_build, dim3(g12), dim3(THREADS), a1, 0, P->stream));
+        const size_t l2b_smem = (size_t)L2B_WORDS * 4 * THREADS +
+                                (size_t)(THREADS / 32) * (32 >> std::min(la, 5)) * 256;
+        CUDA_TRY(cudaLaunchKernel((void *)k_l2_build, dim3(g12), dim3(THREADS), a1, l2b_smem,
+                                  P->stream));
         timing_end(P, TCG_KT_L2_BUILD, e0);
         uint32_t smask = 2 * np2 - 1;
         void *a2[] = {&pool, (void *)&stride, &nrec, &hashes, &wts, &poss, &slots, &smask, &w2,
