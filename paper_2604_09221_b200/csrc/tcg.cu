@@ -1457,7 +1457,8 @@ __global__ void __launch_bounds__(THREADS) k_super_build(KParams p,
 // component to collect its neighbours, links and free neighbours and write
 // the row.  Tiles of fallback super-tiles are listed in ovf for
 // k_tile_build_lanes.
-constexpr size_t FROM_SUPER_SMEM = sizeof(TileTables) + 16 * 4 * THREADS;
+constexpr size_t FROM_SUPER_SMEM = sizeof(TileTables) + (16 + MAXF) * 4 * THREADS;  // max
+inline size_t from_super_smem(int nf) { return sizeof(TileTables) + (size_t)(16 + nf) * 4 * THREADS; }
 
 __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *__restrict__ tt_g,
                                                              const SuperRec *__restrict__ srecs,
@@ -1474,6 +1475,15 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
     const int h = tt->sh, nf = tt->nf, nm = tt->nm;
     const uint64_t sbase = tile0 >> h;
     auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
+    // labels of the SN nodes in x, as a node mask (one lookup per set bit;
+    // 32-bit halves: __ffs is cheaper than __ffsll)
+    auto labels_of = [&](unsigned long long x) -> unsigned long long {
+        unsigned long long r = 0;
+        for (uint32_t w = (uint32_t)x; w; w &= w - 1u) r |= 1ull << label(__ffs(w) - 1);
+        for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) r |= 1ull << label(31 + __ffs(w));
+        return r;
+    };
+    uint32_t *FCs = smem + sizeof(TileTables) / 4 + 16 * THREADS + threadIdx.x;  // [nf] lane-private
     for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles;
          t += gridDim.x * blockDim.x) {
         const uint64_t gt = tile0 + t;
@@ -1524,20 +1534,14 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
             unv = all;
             F = 0;
             int c = -1;
+            const bool fcs = n <= 32;  // free rows by scattering the components' free bits
+            if (fcs)
+                for (int f = 0; f < nf; ++f) FCs[f * THREADS] = 0u;
             auto close = [&]() {
-                unsigned long long adj = (unsigned long long)FB << n, pl = 0;
-                unsigned long long x = CG & ~M;
-                while (x) {
-                    const int v = __ffsll((long long)x) - 1;
-                    x &= x - 1ull;
-                    adj |= 1ull << label(v);
-                }
-                x = LK;
-                while (x) {
-                    const int v = __ffsll((long long)x) - 1;
-                    x &= x - 1ull;
-                    pl |= 1ull << label(v);
-                }
+                const unsigned long long adj = ((unsigned long long)FB << n) | labels_of(CG & ~M);
+                const unsigned long long pl = labels_of(LK);
+                if (fcs)
+                    for (uint32_t y = FB; y; y &= y - 1u) FCs[(__ffs(y) - 1) * THREADS] |= 1u << c;
                 store_row(rec, c, nn, adj, pl);
                 hs.row(adj, pl);
             };
@@ -1566,12 +1570,8 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
             }
             close();
             for (int f = 0; f < nf; ++f) {
-                unsigned long long x = S->fsn[f], fc = 0;
-                while (x) {
-                    const int v = __ffsll((long long)x) - 1;
-                    x &= x - 1ull;
-                    fc |= 1ull << label(v);
-                }
+                const unsigned long long fc = fcs ? (unsigned long long)FCs[f * THREADS]
+                                                  : labels_of(S->fsn[f]);
                 const unsigned long long adj = (tt->fadj[f] << n) | fc, pl = tt->fpl[f] << n;
                 store_row(rec, n + f, nn, adj, pl);
                 hs.row(adj, pl);
@@ -3621,7 +3621,7 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 void *af[] = {&tt, &csr, &tile0, &nt, &recs, &hashes, &ovf};
                 CUDA_TRY(cudaLaunchKernel((void *)k_tile_from_super,
                                           dim3((nt + THREADS - 1) / THREADS), dim3(THREADS), af,
-                                          FROM_SUPER_SMEM, P->stream));
+                                          from_super_smem(P->h_tiles[mode].nf), P->stream));
                 const uint32_t *ol = ovf + 1, *oc = ovf;
                 void *ab[] = {&P->kp, &tt, &tile0, &nt, &recs, &hashes, &ol, &oc};
                 CUDA_TRY(cudaLaunchKernel(fb, dim3(P->blocks_bgen), dim3(THREADS), ab,
