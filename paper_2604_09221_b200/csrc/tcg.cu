@@ -2885,15 +2885,15 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
         }
     }
     l2_tables();
-    // super-tiles: mid points = index bits bits .. bits+sh-1 (TCG_SUPER_BITS, default 4)
+    // super-tiles: mid points = index bits bits .. bits+sh-1; the largest sh <= 6
+    // (TCG_SUPER_BITS) whose mid vertices fit MAXM
     T.sh = 0;
-    {
-        int h = 4;
-        if (const char *e = std::getenv("TCG_SUPER_BITS")) h = std::atoi(e);
-        if (const char *e = std::getenv("TCG_BUILD_GENERIC"))
-            if (e[0] && e[0] != '0') h = 0;
-        h = std::max(0, std::min(h, SUPER_BITS_MAX));
-        if (h > 0 && dom_bits >= bits + h + 1) {
+    int hmax = SUPER_BITS_MAX;
+    if (const char *e = std::getenv("TCG_SUPER_BITS")) hmax = std::atoi(e);
+    if (const char *e = std::getenv("TCG_BUILD_GENERIC"))
+        if (e[0] && e[0] != '0') hmax = 0;
+    for (int h = std::max(0, std::min(hmax, SUPER_BITS_MAX)); h > 0 && T.sh == 0; --h) {
+        if (dom_bits >= bits + h + 1) {
             auto point_of = [&](int ib) {  // index bit -> lattice point
                 return mode == MODE_RAW ? ib : (ib < d - 1 ? ib + 2 : ib - (d - 1) + d + 2);
             };
@@ -2931,9 +2931,12 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
 // word: at most 16 free vertices (d=7 raw: 2^8 indices, the j-axis).
 // Degree 8-9 graphs exceed 32 nodes anyway, so they take 2^10.
 // TCG_TILE_BITS overrides.
+// Odd degrees up to 7 run level 2 (which also takes 33..64-node tiles), so
+// they allow 18 free vertices: d=7 raw tiles are 2^9 indices (measured on
+// C3: 1.78e11 vs 1.59e11 patchworks/s at 2^8 and 1.63e11 at 2^10).
 bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
     int want = D->degree >= 8 ? 10 : 12;
-    int fmax = D->degree >= 8 ? 28 : 16;
+    int fmax = D->degree >= 8 ? 28 : (D->degree % 2 ? 18 : 16);
     if (const char *e = std::getenv("TCG_TILE_BITS")) {
         want = std::atoi(e);
         fmax = 28;
