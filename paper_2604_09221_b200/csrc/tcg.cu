@@ -1817,83 +1817,6 @@ __device__ __forceinline__ uint32_t l2_compress(const TileTables &tt, uint32_t f
     return r;
 }
 
-// Super-node BFS of one (tile, A pattern); MT = uint32_t for <= 32-node
-// records (uint2 rows), unsigned long long for 33..64 (uint4 rows).  Writes
-// the record words to out[0 .. m] and returns m, or -1 when m > mmax (the
-// level-2 classifier needs m + nB <= 32 nodes; only possible above 32 nodes).
-template <typename MT>
-__device__ __forceinline__ int l2_build_one(const TileTables &tt, const TileRec *__restrict__ rec,
-                                            uint32_t a, int mmax, unsigned long long *out,
-                                            unsigned long long &hout) {
-    const int n = rec->n, nB = tt.nB;
-    constexpr bool WIDE = sizeof(MT) == 8;
-    auto row = [&](int u, MT &rx, MT &ry) {
-        if constexpr (WIDE) {
-            const uint4 r4 = rec->rows[u];
-            rx = (MT)r4.x | ((MT)r4.y << 32);
-            ry = (MT)r4.z | ((MT)r4.w << 32);
-        } else {
-            const uint2 r2 = rows2(rec)[u];
-            rx = r2.x;
-            ry = r2.y;
-        }
-    };
-    const uint32_t lowA = a << 5;
-    const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
-    const MT one = 1;
-    const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa) << n);
-    const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa << n);
-    const MT FBn = (MT)tt.fbm << n;
-    MT Mem[32], CG[32];
-    uint32_t HI[32];
-    MT unv = G;
-    int m = 0;
-    while (unv) {
-        if (m == mmax) return -1;
-        MT f = unv & ((MT)0 - unv);
-        unv ^= f;
-        MT M = f, cg = 0, pb = 0, mb = 0, lb = 0;
-        while (f) {
-            const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
-            f &= f - one;
-            MT rx, ry;
-            row(u, rx, ry);
-            const MT diff = sg1 ^ ((MT)0 - ((sg1 >> u) & one));  // nodes of the other sign
-            const MT nw = ((rx & ~diff) | ry) & unv;
-            unv ^= nw;
-            f |= nw;
-            M |= nw;
-            cg |= rx & G & diff;
-            const MT bp = rx & FBn;
-            if ((sg1 >> u) & one) pb |= bp;
-            else mb |= bp;
-            lb |= ry & FBn;
-        }
-        Mem[m] = M;
-        CG[m] = cg;
-        HI[m] = l2_compress(tt, (uint32_t)(pb >> n)) | l2_compress(tt, (uint32_t)(mb >> n)) << nB |
-                l2_compress(tt, (uint32_t)(lb >> n)) << (2 * nB);
-        ++m;
-    }
-    out[0] = (unsigned long long)m;
-    uint32_t hh = 0x9E3779B9u, hl = 0xC2B2AE3Du;  // same hash as l2_build_narrow
-    for (int q = 0; q < m; ++q) {
-        uint32_t cs = 0;
-        for (int q2 = 0; q2 < m; ++q2)
-            if (CG[q] & Mem[q2]) cs |= 1u << q2;
-        const uint32_t self = (cs >> q) & 1u;
-        cs &= ~(1u << q);
-        const uint32_t hi = HI[q] | self << (3 * nB);
-        out[1 + q] = (unsigned long long)cs | (unsigned long long)hi << 32;
-        hh = (hh ^ hi) * 0x85EBCA77u;
-        hh ^= hh >> 13;
-        hl = (hl ^ cs) * 0x9E3779B1u;
-        hl ^= hl >> 15;
-    }
-    hout = mix64(((unsigned long long)hh << 32 | hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
-    return m;
-}
-
 // <= 32-node records (98 % at d=7): the same super-node BFS without
 // per-super-node arrays in local memory.  Node labels (bytes) and the
 // cross-adjacency words cs[q] are lane-private shared memory (bank = lane);
@@ -1901,63 +1824,75 @@ __device__ __forceinline__ int l2_build_one(const TileTables &tt, const TileRec 
 // (earlier super-nodes) set cs[q] and cs[q2] -- every pair is met once, from
 // its later end -- and the record's high half (B-node words, self flag) is
 // written immediately; the low halves (cs) follow at the end.
-constexpr int L2B_WORDS = 8 + 32;  // labels (32 nodes, 4 per word) | cs[32]
-constexpr size_t L2B_SMEM = (size_t)L2B_WORDS * 4 * THREADS + 256 * THREADS;  // + staged rows
+constexpr int L2B_WORDS = 16 + 32;  // labels (64 nodes, 4 per word) | cs[32]
+constexpr int L2B_SLOT = 1024;      // staged rows per tile: 64 x uint4 (or 32 x uint2)
+// level 2 needs tile bits >= 6 (la >= 1): at most 16 tiles per warp
+constexpr size_t L2B_SMEM = (size_t)L2B_WORDS * 4 * THREADS + (THREADS / 32) * 16 * L2B_SLOT;
 
-__device__ __forceinline__ int l2_build_narrow(const TileTables &tt,
-                                               const TileRec *__restrict__ rec,
-                                               const uint2 *__restrict__ R, uint32_t a,
-                                               unsigned long long *out, unsigned long long &hout,
-                                               uint32_t *mine) {
+template <typename MT>
+__device__ __forceinline__ int l2_build_lbl(const TileTables &tt,
+                                            const TileRec *__restrict__ rec,
+                                            const uint4 *__restrict__ R4, uint32_t a, int mmax,
+                                            unsigned long long *out, unsigned long long &hout,
+                                            uint32_t *mine) {
+    constexpr bool WIDE = sizeof(MT) == 8;
     const int n = rec->n, nB = tt.nB;
     uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
-    uint32_t *cs = mine + 8 * THREADS;
+    uint32_t *cs = mine + 16 * THREADS;
     const uint32_t lowA = a << 5;
     const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
-    const uint32_t sg1 = (uint32_t)rec->sgn_fixed | (((uint32_t)fsA & tt.fa) << n);
-    const uint32_t G = (n >= 32 ? ~0u : ((1u << n) - 1u)) | (tt.fa << n);
-    const uint32_t FBn = tt.fbm << n;
+    const MT one = 1;
+    const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa) << n);
+    const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa << n);
+    const MT FBn = (MT)tt.fbm << n;
     uint32_t *out32 = reinterpret_cast<uint32_t *>(out);
-    uint32_t unv = G, done = 0, hh = 0x9E3779B9u;
+    MT unv = G, done = 0;
+    uint32_t hh = 0x9E3779B9u;
     int m = 0;
+    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
     while (unv) {
-        uint32_t f = unv & (0u - unv);
+        if (m == mmax) return -1;
+        MT f = unv & ((MT)0 - unv);
         unv ^= f;
-        uint32_t M = f, cg = 0, pb = 0, mb = 0, lk = 0;
+        MT M = f, cg = 0, pb = 0, mb = 0, lk = 0;
         while (f) {
-            const int u = __ffs(f) - 1;
-            f &= f - 1u;
+            const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
+            f &= f - one;
             lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
-            const uint2 row = R[u];
-            const uint32_t s = (sg1 >> u) & 1u;
-            const uint32_t diff = sg1 ^ (0u - s);  // nodes of the other sign
-            const uint32_t nw = ((row.x & ~diff) | row.y) & unv;
+            MT rx, ry;
+            if constexpr (WIDE) {
+                const uint4 r = R4[u];
+                rx = (MT)r.x | ((MT)r.y << 32);
+                ry = (MT)r.z | ((MT)r.w << 32);
+            } else {
+                const uint2 r = reinterpret_cast<const uint2 *>(R4)[u];
+                rx = r.x;
+                ry = r.y;
+            }
+            const MT s = (sg1 >> u) & one;
+            const MT diff = sg1 ^ ((MT)0 - s);  // nodes of the other sign
+            const MT nw = ((rx & ~diff) | ry) & unv;
             unv ^= nw;
             f |= nw;
             M |= nw;
-            cg |= row.x & G & diff;
-            const uint32_t bp = row.x & FBn;
-            pb |= s ? bp : 0u;
-            mb |= s ? 0u : bp;
-            lk |= row.y & FBn;
+            cg |= rx & G & diff;
+            const MT bp = rx & FBn;
+            pb |= s ? bp : (MT)0;
+            mb |= s ? (MT)0 : bp;
+            lk |= ry & FBn;
         }
         // crossed neighbours in earlier super-nodes (labelled): both ends' cs words
-        uint32_t c = 0, x = cg & done;
-        while (x) {
-            const int v = __ffs(x) - 1;
-            x &= x - 1u;
-            const uint32_t q2 = lb[(v >> 2) * (4 * THREADS) + (v & 3)];
-            c |= 1u << q2;
-        }
+        uint32_t c = 0;
+        const MT x = cg & done;
+        for (uint32_t w = (uint32_t)x; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
+        if constexpr (WIDE)
+            for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) c |= 1u << label(31 + __ffs(w));
         cs[m * THREADS] = c;
-        for (uint32_t y = c; y;) {
-            const int q2 = __ffs(y) - 1;
-            y &= y - 1u;
-            cs[q2 * THREADS] |= 1u << m;
-        }
-        const uint32_t self = (cg & M) != 0u;
-        const uint32_t hi = l2_compress(tt, pb >> n) | l2_compress(tt, mb >> n) << nB |
-                            l2_compress(tt, lk >> n) << (2 * nB) | self << (3 * nB);
+        for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
+        const uint32_t self = (cg & M) != (MT)0;
+        const uint32_t hi = l2_compress(tt, (uint32_t)(pb >> n)) |
+                            l2_compress(tt, (uint32_t)(mb >> n)) << nB |
+                            l2_compress(tt, (uint32_t)(lk >> n)) << (2 * nB) | self << (3 * nB);
         out32[2 * (1 + m) + 1] = hi;
         hh = (hh ^ hi) * 0x85EBCA77u;
         hh ^= hh >> 13;
@@ -2008,7 +1943,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
     // first: the breadth-first pass then reads rows at shared-memory latency
     const int lane = threadIdx.x & 31, lpt = la < 5 ? la : 5;
     uint4 *slot = reinterpret_cast<uint4 *>(l2smem + L2B_WORDS * THREADS) +
-                  16 * ((threadIdx.x >> 5) * (32 >> lpt) + (lane >> lpt));
+                  (L2B_SLOT / 16) * ((threadIdx.x >> 5) * (32 >> lpt) + (lane >> lpt));
     for (uint32_t jb = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); jb < nrec;
          jb += gridDim.x * blockDim.x) {  // warp-uniform
         const uint32_t j = jb + lane;
@@ -2016,9 +1951,10 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
         const uint32_t i = i0 + (j >> la), a = j & ((1u << la) - 1u);
         const uint32_t t = valid ? list1[i] : 0u;
         const TileRec *rec = recs + t;
-        if (valid) {
+        if (valid) {  // 256 bytes of uint2 rows, or 1 KB of uint4 rows above 32 nodes
             const uint4 *src = rec->rows;
-            for (int q = lane & ((1 << lpt) - 1); q < 16; q += 1 << lpt) slot[q] = src[q];
+            const int nq = rec->nnodes <= 32 ? 16 : 64;
+            for (int q = lane & ((1 << lpt) - 1); q < nq; q += 1 << lpt) slot[q] = src[q];
         }
         __syncwarp();
         if (valid) {
@@ -2031,9 +1967,9 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
                 unsigned long long *out = pool + (size_t)j * stride;
                 unsigned long long h = 0;
                 const int m =
-                    nn <= 32 ? l2_build_narrow(tt, rec, reinterpret_cast<const uint2 *>(slot), a,
-                                               out, h, mine)
-                             : l2_build_one<unsigned long long>(tt, rec, a, mmax, out, h);
+                    nn <= 32 ? l2_build_lbl<uint32_t>(tt, rec, slot, a, mmax, out, h, mine)
+                             : l2_build_lbl<unsigned long long>(tt, rec, slot, a, mmax, out, h,
+                                                                mine);
                 if (m < 0) {
                     oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << 24);
                     wts[j] = 0u;
@@ -3494,7 +3430,7 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
                       (void *)&stride, &hashes, &wts, &poss, &oldlist, &oldcount};
         cudaEvent_t e0 = timing_begin(P);
         const size_t l2b_smem = (size_t)L2B_WORDS * 4 * THREADS +
-                                (size_t)(THREADS / 32) * (32 >> std::min(la, 5)) * 256;
+                                (size_t)(THREADS / 32) * (32 >> std::min(la, 5)) * L2B_SLOT;
         CUDA_TRY(cudaLaunchKernel((void *)k_l2_build, dim3(g12), dim3(THREADS), a1, l2b_smem,
                                   P->stream));
         timing_end(P, TCG_KT_L2_BUILD, e0);
