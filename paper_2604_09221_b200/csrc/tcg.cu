@@ -62,7 +62,7 @@ constexpr int TBL_PROBES = 64;
 constexpr int GCAP_BITS = 16;  // global scheme table: 65,536 slots (as the reference's agg)
 constexpr int GCAP = 1 << GCAP_BITS;
 constexpr int NHIST = 64;
-constexpr uint64_t LAUNCH_MAX = 1ull << 33;  // indices per launch (u32 per-CTA counters)
+constexpr uint64_t LAUNCH_MAX = 1ull << 33;  // indices per flat launch
 
 enum Mode { MODE_RAW = 0, MODE_REP = 1, MODE_SAMPLE = 2 };
 
@@ -736,17 +736,17 @@ __device__ void global_insert(const DevAgg &g, uint64_t key, uint64_t cnt, uint6
 }
 
 // Per-CTA scheme table in shared memory (flushed to the global table).
-struct CtaTable {
+struct CtaTable {  // 64-bit counts: a tiled launch covers up to 2^32 weighted patchworks
     unsigned long long *key, *wit;
-    uint32_t *cnt, *hist;
+    unsigned long long *cnt, *hist;
 
     __device__ void init() {
         for (int i = threadIdx.x; i < TBL; i += blockDim.x) {
             key[i] = 0ull;
             wit[i] = ~0ull;
-            cnt[i] = 0u;
+            cnt[i] = 0ull;
         }
-        for (int i = threadIdx.x; i < NHIST; i += blockDim.x) hist[i] = 0u;
+        for (int i = threadIdx.x; i < NHIST; i += blockDim.x) hist[i] = 0ull;
     }
 
     // Warp-aggregated insert of one result per lane (all 32 lanes call).
@@ -772,7 +772,7 @@ struct CtaTable {
                 }
                 h = (h + 1) & (TBL - 1);
             }
-            const uint32_t c = __popc(grp) * weight;
+            const unsigned long long c = (unsigned long long)__popc(grp) * weight;
             atomicAdd(&hist[nreg - 1], c);
             if (slot >= 0) {
                 atomicAdd(&cnt[slot], c);
@@ -794,18 +794,18 @@ struct CtaTable {
             if (kk != 0ull) global_insert(g, kk, cnt[i], wit[i]);
         }
         for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
-            if (hist[i]) atomicAdd(&g.hist[i], (unsigned long long)hist[i]);
+            if (hist[i]) atomicAdd(&g.hist[i], hist[i]);
     }
 };
 
-constexpr size_t TABLE_SMEM = TBL * (2 * sizeof(unsigned long long) + sizeof(uint32_t)) +
-                              NHIST * sizeof(uint32_t);
+constexpr size_t TABLE_SMEM = TBL * 3 * sizeof(unsigned long long) +
+                              NHIST * sizeof(unsigned long long);
 
 __device__ __forceinline__ CtaTable carve_table(void *at) {
     CtaTable t;
     t.key = reinterpret_cast<unsigned long long *>(at);
     t.wit = t.key + TBL;
-    t.cnt = reinterpret_cast<uint32_t *>(t.wit + TBL);
+    t.cnt = t.wit + TBL;
     t.hist = t.cnt + TBL;
     return t;
 }
@@ -2667,10 +2667,7 @@ void *pick_batch(int K, bool even) {
 
 size_t adj_bytes(int K) { return (size_t)32 * K * K * sizeof(uint32_t); }
 
-size_t enum_smem(int K) {
-    return adj_bytes(K) + TBL * (2 * sizeof(unsigned long long) + sizeof(uint32_t)) +
-           NHIST * sizeof(uint32_t);
-}
+size_t enum_smem(int K) { return adj_bytes(K) + TABLE_SMEM; }
 
 // Vertex layout.  H = 16K bits per half.  P-half (points p > -p
 // lexicographically, i.e. i > 0 or (i == 0 and j > 0)):
@@ -3481,8 +3478,8 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
         const TileTables *tt = P->d_tiles + mode;
         const int bits = P->tile_bits[mode];
         const uint64_t t_end = ((end - 1) >> bits) + 1;
-        // per-CTA scheme counters are 32-bit: a launch covers < 2^32 patchworks
-        uint32_t chunk = std::min<uint32_t>(chunk_tiles(), (uint32_t)(0xffffffffull >> bits));
+        // a chunk covers <= 2^32 indices (tile ids < 2^24, level-2 positions fit 32 bits)
+        uint32_t chunk = (uint32_t)std::min<uint64_t>(chunk_tiles(), (1ull << 32) >> bits);
         chunk = std::min<uint32_t>(chunk, next_pow2((uint32_t)std::min<uint64_t>(
                                               t_end - (start >> bits), 1u << 30)));
         if (chunk > P->chunk_cap) {  // (re)allocate the contraction records + dedup table
