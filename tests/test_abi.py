@@ -57,3 +57,16 @@ def test_product_does_not_import_oracle():
                 with open(os.path.join(dirpath, f)) as fh:
                     src = fh.read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", src).replace("oracle_", ""), f
+
+
+def test_kernel_kinds_match_header():
+    """tcg_kernel_times fills TCG_NKINDS slots, named by the TCG_KT_* kinds."""
+    from paper_2604_09221_b200 import _lib
+
+    with open(os.path.join(ROOT, "include", "tcg.h")) as fh:
+        text = fh.read()
+    n = int(re.search(r"#define TCG_NKINDS (\d+)", text).group(1))
+    kinds = dict((int(v), k.lower()) for k, v in re.findall(r"#define TCG_KT_([A-Z0-9_]+) (\d+)", text))
+    assert len(_lib.KERNEL_KINDS) == n == len(kinds)
+    for i, name in enumerate(_lib.KERNEL_KINDS):
+        assert kinds[i] == name, (i, name, kinds[i])
