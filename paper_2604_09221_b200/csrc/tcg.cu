@@ -886,7 +886,7 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     // level-2 contraction (odd degree): index bits 0..4 are the B points (one
     // per lane), bits 5..bits-1 the A points fixed per level-2 record
     int l2, nB, NA, la;                     // enabled, B nodes, A patterns = 2^la
-    int l2shift, pad3;                      // B nodes = free nodes l2shift .. +nB-1 (or -1)
+    int l2shift, l2even;                    // B nodes = free nodes l2shift .. +nB-1 (or -1)
     uint32_t fa, fbm;                       // free-node masks of A and B nodes
     int8_t l2j[MAXF];                       // free node -> B index (or -1)
     uint32_t l2adjB[16], l2linkB[16];       // B-B adjacency / links (B index space)
@@ -1911,10 +1911,109 @@ __device__ __forceinline__ int l2_build_lbl(const TileTables &tt,
     return m;
 }
 
+// Level 2 in even degree.  Antipodal partners carry the same sign, and a
+// region's orientation matters (the root is its unique region with an
+// orientation-reversing cycle), so a super-node keeps each member's parity
+// relative to its seed (same-sign edges keep it, links flip it) and an odd
+// flag (a member reached with both parities).  Its record is two words:
+//   word0 = cs | self << 30 | odd << 31
+//   word1 = P10 | P11 << nB | P00 << 2nB | P01 << 3nB | LK0 << 4nB | LK1 << 5nB
+// where Psp = B nodes adjacent to members of sign s and parity p, LKp = B
+// nodes linked to members of parity p.
+template <typename MT>
+__device__ __forceinline__ int l2_build_even(const TileTables &tt,
+                                             const TileRec *__restrict__ rec,
+                                             const uint4 *__restrict__ R4, uint32_t a, int mmax,
+                                             unsigned long long *out, unsigned long long &hout,
+                                             uint32_t *mine) {
+    constexpr bool WIDE = sizeof(MT) == 8;
+    const int n = rec->n, nB = tt.nB;
+    uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
+    uint32_t *cs = mine + 16 * THREADS;
+    const uint32_t lowA = a << 5;
+    const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
+    const MT one = 1;
+    const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa) << n);
+    const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa << n);
+    const MT FBn = (MT)tt.fbm << n;
+    MT unv = G, done = 0, q = 0;  // q: parity-1 nodes (relative to their super-node's seed)
+    unsigned long long hh = 0x9E3779B97F4A7C15ull;
+    int m = 0;
+    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
+    auto cmp = [&](MT x) -> unsigned long long { return l2_compress(tt, (uint32_t)(x >> n)); };
+    while (unv) {
+        if (m == mmax) return -1;
+        MT f = unv & ((MT)0 - unv);
+        unv ^= f;
+        MT M = f, cg = 0, p10 = 0, p11 = 0, p00 = 0, p01 = 0, lk0 = 0, lk1 = 0;
+        bool odd = false;
+        while (f) {
+            const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
+            f &= f - one;
+            lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
+            MT rx, ry;
+            if constexpr (WIDE) {
+                const uint4 r = R4[u];
+                rx = (MT)r.x | ((MT)r.y << 32);
+                ry = (MT)r.z | ((MT)r.w << 32);
+            } else {
+                const uint2 r = reinterpret_cast<const uint2 *>(R4)[u];
+                rx = r.x;
+                ry = r.y;
+            }
+            const MT s = (sg1 >> u) & one, pu = (q >> u) & one;
+            const MT diff = sg1 ^ ((MT)0 - s);        // nodes of the other sign
+            const MT eqm = pu ? q : ~q;                 // nodes with u's parity
+            const MT te = rx & ~diff & G, tl = ry & G;  // same-sign edges keep, links flip
+            const MT nt = te & unv, np = tl & unv;
+            odd |= ((nt & np) | (te & ~unv & ~eqm) | (tl & ~unv & eqm)) != (MT)0;
+            q |= pu ? nt : np;
+            const MT nw = nt | np;
+            unv ^= nw;
+            f |= nw;
+            M |= nw;
+            cg |= rx & G & diff;
+            const MT bp = rx & FBn, bl = ry & FBn;
+            if (s) {
+                if (pu) p11 |= bp; else p10 |= bp;
+            } else {
+                if (pu) p01 |= bp; else p00 |= bp;
+            }
+            if (pu) lk1 |= bl; else lk0 |= bl;
+        }
+        uint32_t c = 0;
+        const MT x = cg & done;
+        for (uint32_t w = (uint32_t)x; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
+        if constexpr (WIDE)
+            for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) c |= 1u << label(31 + __ffs(w));
+        const uint32_t self = (cg & M) != (MT)0;
+        cs[m * THREADS] = c | self << 30 | (uint32_t)odd << 31;
+        for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
+        const unsigned long long w1 = cmp(p10) | cmp(p11) << nB | cmp(p00) << (2 * nB) |
+                                      cmp(p01) << (3 * nB) | cmp(lk0) << (4 * nB) |
+                                      cmp(lk1) << (5 * nB);
+        out[2 + 2 * m] = w1;
+        hh = mix64(hh ^ w1);
+        done |= M;
+        ++m;
+    }
+    out[0] = (unsigned long long)m;
+    uint32_t hl = 0xC2B2AE3Du;
+    for (int k = 0; k < m; ++k) {
+        const uint32_t c = cs[k * THREADS];
+        out[1 + 2 * k] = c;
+        hl = (hl ^ c) * 0x9E3779B1u;
+        hl ^= hl >> 15;
+    }
+    hout = mix64((hh ^ hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
+    return m;
+}
+
 // One thread per (representative tile, A pattern) of list1[i0 .. i0+nb).
 // Tiles the level-2 path cannot take go to oldlist for the level-1
 // classifier: whole tiles (entry = tile: range ends, fallback) or single A
 // slices whose super-node graph is too large (entry = tile | (a + 1) << 24).
+template <bool EVEN>
 __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restrict__ tt_g,
                                                       const TileRec *__restrict__ recs,
                                                       const uint32_t *__restrict__ list1,
@@ -1966,10 +2065,15 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
             } else {
                 unsigned long long *out = pool + (size_t)j * stride;
                 unsigned long long h = 0;
-                const int m =
-                    nn <= 32 ? l2_build_lbl<uint32_t>(tt, rec, slot, a, mmax, out, h, mine)
-                             : l2_build_lbl<unsigned long long>(tt, rec, slot, a, mmax, out, h,
-                                                                mine);
+                int m;
+                if constexpr (EVEN)
+                    m = nn <= 32 ? l2_build_even<uint32_t>(tt, rec, slot, a, mmax, out, h, mine)
+                                 : l2_build_even<unsigned long long>(tt, rec, slot, a, mmax, out,
+                                                                     h, mine);
+                else
+                    m = nn <= 32 ? l2_build_lbl<uint32_t>(tt, rec, slot, a, mmax, out, h, mine)
+                                 : l2_build_lbl<unsigned long long>(tt, rec, slot, a, mmax, out,
+                                                                    h, mine);
                 if (m < 0) {
                     oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << 24);
                     wts[j] = 0u;
@@ -1995,8 +2099,9 @@ __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *
                                                       uint32_t *__restrict__ w2,
                                                       uint32_t *__restrict__ pos2,
                                                       uint32_t *__restrict__ list2,
-                                                      uint32_t *__restrict__ count2) {
+                                                      uint32_t *__restrict__ count2, int wps) {
     // slot = hash tag << 32 | record; a tag match is confirmed word by word
+    // (wps = record words per super-node: 1 odd degree, 2 even)
     const int lane = threadIdx.x & 31;
     const uint32_t tot = gridDim.x * blockDim.x;
     const uint32_t jmax = (nrec + 31u) & ~31u;  // whole warps iterate together
@@ -2026,7 +2131,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *
                     const unsigned long long *ow = pool + (size_t)o * stride;
                     unsigned long long diff = ow[0] ^ m;
 #pragma unroll 4
-                    for (int q = 1; q <= (int)m; ++q) diff |= ow[q] ^ mine[q];
+                    for (int q = 1; q <= wps * (int)m; ++q) diff |= ow[q] ^ mine[q];
                     if (diff == 0ull) {
                         atomicAdd(&w2[o], wj);
                         atomicMin(&pos2[o], poss[j]);
@@ -2160,6 +2265,146 @@ __global__ void __launch_bounds__(THREADS) k_l2_classify(KParams p,
         l2_node_pass(*rw, Sb << m, m + nB, rg);
         const uint32_t SG1[1] = {0u};
         const Result r = finish<1, false, false>(p, SG1, rg, p.maxreg);
+        const uint64_t mw = (tile0 << bits) + ((uint64_t)pos2[j] << 5) + lane;
+        uint64_t k = 0;
+        if (r.status == TCG_OK) k = r.key;
+        else atomicMin(g.bad, (unsigned long long)mw);
+        tab.add<true>(g, k, r.nreg, mw, w2[j]);
+        __syncwarp();
+    }
+    __syncthreads();
+    tab.flush(g);
+}
+
+// Even-degree level-2 classification.  Rows per node v (super-nodes 0..m-1,
+// B nodes m..m+nB-1), with T = the lane's B-sign mask S for a super-node
+// and all-ones / all-zeros by the B node's own sign:
+//   E0 = T&F0 | ~T&F2 | F5 | AB&~(S^T)    neighbours at the same parity
+//   E1 = T&F1 | ~T&F3 | F4 | LB           neighbours at the other parity
+//   X  = T&(F2|F3) | ~T&(F0|F1) | CS | AB&(S^T)   crossed neighbours
+// F0..F5 = P10, P11, P00, P01, LK0, LK1 (super-nodes: B masks; B nodes: the
+// transposed super-node masks), AB / LB = static B-B adjacency / links, CS =
+// super-node crossed adjacency (+ self bit), ODD = odd super-nodes.
+struct L2RowsE {
+    uint32_t F[6][32], AB[32], LB[32], CS[32];
+    unsigned long long W0[32], W1[32];
+};
+
+__device__ __forceinline__ void l2_node_pass_even(const L2RowsE &rw, uint32_t S, uint32_t oddn,
+                                                  int m, int nn, Regions<1> &out) {
+    uint32_t un = nn >= 32 ? ~0u : ((1u << nn) - 1u), f = 0, x = 0, r = 0, q = 0, oddmask = 0;
+    bool odd = false;
+    int nreg = 0;
+    auto seed = [&]() {
+        f = un & (0u - un);
+        r = un;
+        un ^= f;
+        x = 0u;
+        odd = false;
+    };
+    auto close = [&]() {
+        if (nreg < MAXR) {
+            out.R[nreg][0] = r ^ un;
+            out.X[nreg][0] = x;
+            if (odd) oddmask |= 1u << nreg;
+        }
+        ++nreg;
+    };
+    seed();
+    for (int it = 0; it < nn; ++it) {
+        if (f == 0u) {
+            close();
+            seed();
+        }
+        const int v = __ffs(f) - 1;
+        f &= f - 1u;
+        const uint32_t T = v < m ? S : (0u - ((S >> v) & 1u));
+        const uint32_t f0 = rw.F[0][v], f1 = rw.F[1][v], f2 = rw.F[2][v], f3 = rw.F[3][v];
+        const uint32_t ab = rw.AB[v];
+        const uint32_t e0 = (T & f0) | (~T & f2) | rw.F[5][v] | (ab & ~(S ^ T));
+        const uint32_t e1 = (T & f1) | (~T & f3) | rw.F[4][v] | rw.LB[v];
+        x |= (T & (f2 | f3)) | (~T & (f0 | f1)) | rw.CS[v] | (ab & (S ^ T));
+        const uint32_t pv = (q >> v) & 1u;
+        const uint32_t eqm = pv ? q : ~q;
+        const uint32_t nt = e0 & un, np = e1 & un;
+        odd |= ((nt & np) | (e0 & ~un & ~eqm) | (e1 & ~un & eqm) | (oddn & (1u << v))) != 0u;
+        q |= pv ? nt : np;
+        un ^= nt | np;
+        f |= nt | np;
+    }
+    close();
+    out.nreg = nreg;
+    out.oddmask = oddmask;
+}
+
+constexpr size_t L2E_CLS_SMEM = TABLE_SMEM + sizeof(TileTables) + CLS_WARPS * sizeof(L2RowsE);
+
+__global__ void __launch_bounds__(THREADS) k_l2_classify_even(KParams p,
+                                                              const TileTables *__restrict__ tt_g,
+                                                              const unsigned long long *__restrict__ pool,
+                                                              uint32_t stride,
+                                                              const uint32_t *__restrict__ list2,
+                                                              const uint32_t *__restrict__ count2,
+                                                              const uint32_t *__restrict__ w2,
+                                                              const uint32_t *__restrict__ pos2,
+                                                              uint64_t tile0, DevAgg g,
+                                                              unsigned long long *__restrict__ tstats) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    CtaTable tab = carve_table(smem);
+    TileTables *tt = reinterpret_cast<TileTables *>(reinterpret_cast<char *>(smem) + TABLE_SMEM);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    L2RowsE *rw = reinterpret_cast<L2RowsE *>(tt + 1) + w;
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    tab.init();
+    __syncthreads();
+    const int nB = tt->nB, bits = tt->bits;
+    const uint32_t bm = (1u << nB) - 1u;
+    const uint32_t n2 = *count2;
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(tstats, (unsigned long long)n2);
+    const uint32_t Sb = tt->l2bsign[lane];
+    for (uint32_t i = blockIdx.x * CLS_WARPS + w; i < n2; i += gridDim.x * CLS_WARPS) {
+        const uint32_t j = list2[i];
+        const unsigned long long *rec = pool + (size_t)j * stride;
+        const int m = (int)rec[0];
+        if (lane < m) {
+            rw->W0[lane] = rec[1 + 2 * lane];
+            rw->W1[lane] = rec[2 + 2 * lane];
+        }
+        __syncwarp();
+        uint32_t oddn = 0;
+        {
+            const bool od = lane < m && ((uint32_t)rw->W0[lane] >> 31);
+            oddn = __ballot_sync(0xffffffffu, od);
+        }
+        if (lane < m) {
+            const uint32_t c = (uint32_t)rw->W0[lane];
+            const unsigned long long w1 = rw->W1[lane];
+#pragma unroll
+            for (int k = 0; k < 6; ++k) rw->F[k][lane] = (uint32_t)((w1 >> (k * nB)) & bm) << m;
+            rw->AB[lane] = 0u;
+            rw->LB[lane] = 0u;
+            rw->CS[lane] = (c & 0x3fffffffu) | (((c >> 30) & 1u) << lane);
+        }
+        if (lane < nB) {
+            uint32_t t[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+            for (int s = 0; s < m; ++s) {
+                const unsigned long long w1 = rw->W1[s];
+#pragma unroll
+                for (int k = 0; k < 6; ++k) t[k] |= (uint32_t)((w1 >> (k * nB + lane)) & 1u) << s;
+            }
+            const int v = m + lane;
+#pragma unroll
+            for (int k = 0; k < 6; ++k) rw->F[k][v] = t[k];
+            rw->AB[v] = tt->l2adjB[lane] << m;
+            rw->LB[v] = tt->l2linkB[lane] << m;
+            rw->CS[v] = 0u;
+        }
+        __syncwarp();
+        Regions<1> rg;
+        l2_node_pass_even(*rw, Sb << m, oddn, m, m + nB, rg);
+        const uint32_t SG1[1] = {0u};
+        const Result r = finish<1, true, false>(p, SG1, rg, p.maxreg);
         const uint64_t mw = (tile0 << bits) + ((uint64_t)pos2[j] << 5) + lane;
         uint64_t k = 0;
         if (r.status == TCG_OK) k = r.key;
@@ -2776,7 +3021,8 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
     // level-2 tables (filled after fadj / fpl below)
     auto l2_tables = [&]() {
         T.l2 = 0;
-        if (d % 2 == 0 || bits < 6 || bits > 10 || nf > 32) return;
+        if (bits < 6 || bits > 10 || nf > 32) return;
+        T.l2even = d % 2 == 0;
         uint32_t fb = 0, fa = 0;
         for (int i = 0; i < bits; ++i) (i < 5 ? fb : fa) |= (uint32_t)T.fcopy[i];
         const int nB = __builtin_popcount(fb);
@@ -3098,9 +3344,14 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)build_smem(K))) != cudaSuccess)
             return bail(e, "super smem");
-    if ((e = cudaFuncSetAttribute((void *)k_l2_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)L2B_SMEM)) != cudaSuccess)
-        return bail(e, "l2 build smem");
+    for (void *kb : {(void *)k_l2_build<false>, (void *)k_l2_build<true>})
+        if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)L2B_SMEM)) != cudaSuccess)
+            return bail(e, "l2 build smem");
+    cudaFuncSetAttribute((void *)k_l2_classify_even, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)L2E_CLS_SMEM);
+    cudaFuncSetAttribute((void *)k_l2_classify_even, cudaFuncAttributePreferredSharedMemoryCarveout,
+                         std::getenv("TCG_CARVEOUT") ? std::atoi(std::getenv("TCG_CARVEOUT")) : 38);
     if ((e = cudaFuncSetAttribute((void *)k_tile_from_super,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)FROM_SUPER_SMEM)) != cudaSuccess)
@@ -3374,7 +3625,8 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
     CUDA_TRY(cudaMemsetAsync(P->d_oldlist, 0, sizeof(uint32_t), P->stream));
     if (n1 == 0) return TCG_OK;
     const int la = T.la;
-    const uint32_t stride = (uint32_t)(1 + 32 - T.nB);
+    const int wps = T.l2even ? 2 : 1;  // record words per super-node
+    const uint32_t stride = (uint32_t)(1 + wps * (32 - T.nB));
     // sized once for the whole chunk (every level-1 tile a representative), so
     // that later sweeps never reallocate inside a timed region
     const size_t want = std::max((size_t)n1, (size_t)P->chunk_cap) << la;
@@ -3428,12 +3680,14 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
         cudaEvent_t e0 = timing_begin(P);
         const size_t l2b_smem = (size_t)L2B_WORDS * 4 * THREADS +
                                 (size_t)(THREADS / 32) * (32 >> std::min(la, 5)) * L2B_SLOT;
-        CUDA_TRY(cudaLaunchKernel((void *)k_l2_build, dim3(g12), dim3(THREADS), a1, l2b_smem,
+        void *kb = T.l2even ? (void *)k_l2_build<true> : (void *)k_l2_build<false>;
+        CUDA_TRY(cudaLaunchKernel(kb, dim3(g12), dim3(THREADS), a1, l2b_smem,
                                   P->stream));
         timing_end(P, TCG_KT_L2_BUILD, e0);
         uint32_t smask = 2 * np2 - 1;
+        int wpsv = wps;
         void *a2[] = {&pool, (void *)&stride, &nrec, &hashes, &wts, &poss, &slots, &smask, &w2,
-                      &pos2, &list2, &count2};
+                      &pos2, &list2, &count2, &wpsv};
         cudaEvent_t e0d = timing_begin(P);
         CUDA_TRY(cudaLaunchKernel((void *)k_l2_dedup, dim3(g12), dim3(THREADS), a2, 0, P->stream));
         timing_end(P, TCG_KT_L2_DEDUP, e0d);
@@ -3444,8 +3698,12 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
         void *a3[] = {&P->kp, &tt, &pool, (void *)&stride, &list2, &count2, &w2, &pos2, &t0,
                       &P->agg, &ts};
         cudaEvent_t e = timing_begin(P);
-        CUDA_TRY(cudaLaunchKernel((void *)k_l2_classify, dim3(g3), dim3(THREADS), a3,
-                                  L2_CLS_SMEM, P->stream));
+        if (T.l2even)
+            CUDA_TRY(cudaLaunchKernel((void *)k_l2_classify_even, dim3(g3), dim3(THREADS), a3,
+                                      L2E_CLS_SMEM, P->stream));
+        else
+            CUDA_TRY(cudaLaunchKernel((void *)k_l2_classify, dim3(g3), dim3(THREADS), a3,
+                                      L2_CLS_SMEM, P->stream));
         timing_end(P, TCG_KT_L2_CLASSIFY, e);
         P->launches += 3;
     }

@@ -406,6 +406,12 @@ def test_tile_dedup_chunk_size_invariance():
     ("delaunay-7", False, 777, 1 << 24),
     ("delaunay-5", True, 0, 1 << 21),
     ("delaunay-7", True, 0, 1 << 26),
+    ("delaunay-6", True, 12345, 1 << 24),
+    ("delaunay-6", False, 0, 1 << 25),
+    ("bowtie8", False, (1 << 38) + 17, 1 << 25),
+    ("delaunay-8", False, 1 << 39, 1 << 24),
+    ("fig2-middle8", False, 3 << 38, 1 << 24),
+    ("fig2-right8", False, 5 << 37, 1 << 24),
 ])
 def test_level2_contraction_is_exact(api, name, raw, a, n):
     """Level-2 records (A points fixed, super-nodes) deduplicated and
@@ -419,7 +425,7 @@ def test_level2_contraction_is_exact(api, name, raw, a, n):
         r = api.sweep(T, api.SweepRange(a, a + n), raw_space=raw, classifier=c)
         built, classified, _ = c.native.level2_stats()
         reps[on] = (r.oval_histogram, sorted(r.scheme_map.items()), r.total_classified)
-        if on and T.degree == 7:
+        if on and T.degree in (6, 7):
             assert 0 < classified < built
         if not on:
             assert built == 0
