@@ -1824,7 +1824,8 @@ __device__ __forceinline__ uint32_t l2_compress(const TileTables &tt, uint32_t f
 // (earlier super-nodes) set cs[q] and cs[q2] -- every pair is met once, from
 // its later end -- and the record's high half (B-node words, self flag) is
 // written immediately; the low halves (cs) follow at the end.
-constexpr int L2B_WORDS = 16 + 32;  // labels (64 nodes, 4 per word) | cs[32]
+constexpr int L2B_CS = 24;          // super-nodes per level-2 record (also <= 32 - nB)
+constexpr int L2B_WORDS = 16 + L2B_CS;  // labels (64 nodes, 4 per word) | cs[L2B_CS]
 constexpr int L2B_SLOT = 1024;      // staged rows per tile: 64 x uint4 (or 32 x uint2)
 // level 2 needs tile bits >= 6 (la >= 1): at most 16 tiles per warp
 constexpr size_t L2B_SMEM = (size_t)L2B_WORDS * 4 * THREADS + (THREADS / 32) * 16 * L2B_SLOT;
@@ -2036,7 +2037,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
     __syncthreads();
     const TileTables &tt = tts;
     const int la = tt.la, bits = tt.bits;
-    const int mmax = 32 - tt.nB;
+    const int mmax = min(32 - tt.nB, L2B_CS);
     const uint32_t nrec = nb << la;
     // the 2^la lanes of one tile stage its (<= 32-node) rows in shared memory
     // first: the breadth-first pass then reads rows at shared-memory latency
