@@ -558,90 +558,6 @@ __device__ __forceinline__ Result finish(const KParams &p, const uint32_t (&SG)[
     return res;
 }
 
-// Layer-free variant of region_pass for the full diamond (same output):
-// each popped vertex uses its own sign and pushes its antipodal partner
-// (swap of mask halves) in the same step, parity tracked per vertex in even
-// degree -- the node_pass scheme on K-word masks.
-template <int K, bool EVEN>
-__device__ __forceinline__ void flat_node_pass(const uint32_t *__restrict__ rows,
-                                               const uint32_t (&SG)[K], const uint32_t (&USED)[K],
-                                               const uint32_t (&BD)[K], int nused,
-                                               Regions<K> &out) {
-    constexpr int HK = K / 2;
-    uint32_t un[K], f[K], x[K], r[K], q[K];
-    bool odd = false;
-    int nreg = 0;
-    uint32_t oddmask = 0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        un[k] = USED[k];
-        q[k] = 0u;
-    }
-    auto seed = [&]() {
-        int w, b;
-        lowest<K>(un, w, b);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            r[k] = un[k];
-            f[k] = (k == w) ? (1u << b) : 0u;
-            un[k] ^= f[k];
-            x[k] = 0u;
-            if (EVEN) q[k] = 0u;
-        }
-        odd = false;
-    };
-    auto close = [&]() {
-        if (nreg < MAXR) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                out.R[nreg][k] = r[k] ^ un[k];
-                out.X[nreg][k] = x[k];
-            }
-            if (EVEN && odd) oddmask |= 1u << nreg;
-        }
-        ++nreg;
-    };
-    seed();
-    for (int it = 0; it < nused; ++it) {
-        if (!any<K>(f)) {
-            close();
-            seed();
-        }
-        int w, b;
-        lowest<K>(f, w, b);
-        const uint32_t bit = 1u << b;
-        uint32_t a[K], dummy[K];
-        load_row<K, false>(rows, 32 * w + b, a, dummy);
-        const uint32_t sv = (uint32_t)((int32_t)(sel<K>(SG, w) << (31 - b)) >> 31);
-        const int pw = w < HK ? w + HK : w - HK;
-        const uint32_t pbit = sel<K>(BD, w) & bit;  // partner at (pw, b) when v is on the boundary
-        uint32_t pv = 0u, bad = 0u;
-        if constexpr (EVEN) pv = (uint32_t)((int32_t)(sel<K>(q, w) << (31 - b)) >> 31);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t o = SG[k] ^ sv;
-            const uint32_t pk = (k == pw) ? pbit : 0u;
-            x[k] |= a[k] & o;
-            uint32_t n;
-            if (EVEN) {
-                const uint32_t te = a[k] & ~o, nt = te & un[k], np = pk & un[k];
-                const uint32_t eq = ~(q[k] ^ pv);
-                bad |= (nt & np) | (te & ~un[k] & ~eq) | (pk & ~un[k] & eq);
-                q[k] |= (nt & pv) | (np & ~pv);
-                n = nt | np;
-            } else {
-                n = ((a[k] & ~o) | pk) & un[k];
-            }
-            un[k] ^= n;
-            f[k] = (f[k] ^ ((k == w) ? bit : 0u)) | n;
-        }
-        if (EVEN) odd |= bad != 0u;
-    }
-    close();
-    out.nreg = nreg;
-    out.oddmask = oddmask;
-}
-
 template <int K, bool EVEN>
 __device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__restrict__ adj,
                                            uint64_t sigma) {
@@ -654,11 +570,7 @@ __device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__r
         bd[k] = p.bd[k];
     }
     Regions<K> rg;
-#ifdef TCG_FLAT_NODES  // layer-free variant: faster on bowtie8, slower on delaunay-8
-    flat_node_pass<K, EVEN>(adj, SG, used, bd, p.nused, rg);
-#else
     region_pass<K, EVEN, false>(adj, SG, used, bd, p.nused, rg);
-#endif
     return finish<K, EVEN, true>(p, SG, rg, p.maxreg);
 }
 
@@ -2873,12 +2785,7 @@ void *pick_cls(int K, bool even, int mode) {
     return even ? cls_fn<6, true>(mode) : cls_fn<6, false>(mode);
 }
 
-size_t build_smem(int K) {
-    const size_t rg = K == 2 ? sizeof(Regions<2, MAXC>)
-                             : (K == 4 ? sizeof(Regions<4, MAXC>) : sizeof(Regions<6, MAXC>));
-    (void)rg;
-    return (size_t)32 * K * K * 4 + sizeof(TileTables);
-}
+size_t build_smem(int K) { return (size_t)32 * K * K * 4 + sizeof(TileTables); }
 
 size_t cls_smem(int K) {
     return (size_t)32 * K * K * 4 + TABLE_SMEM + sizeof(TileTables) + CLS_WARPS * sizeof(TileRec);
