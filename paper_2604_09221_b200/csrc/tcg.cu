@@ -2797,6 +2797,18 @@ size_t cls_smem(int K) {
 // allocated on demand and only as large as the sweep needs, halved while it
 // would take more than a quarter of the free HBM).  TCG_CHUNK_LOG2 (14..24)
 // overrides.
+// indices per chunk (TCG_CHUNK_INDEX_LOG2, 32..34; default 2^33): larger chunks
+// deduplicate over a larger window (C3: 158x at 2^32, 244x at 2^33 -> +16 %);
+// tile ids stay < 2^24 (chunk_tiles)
+static uint64_t chunk_index_limit() {
+    static const uint64_t c = [] {
+        int lg = 33;
+        if (const char *e = std::getenv("TCG_CHUNK_INDEX_LOG2")) lg = std::max(32, std::min(34, std::atoi(e)));
+        return 1ull << lg;
+    }();
+    return c;
+}
+
 static uint32_t chunk_tiles() {
     static const uint32_t c = [] {
         int lg = 24;
@@ -3644,8 +3656,9 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
         const TileTables *tt = P->d_tiles + mode;
         const int bits = P->tile_bits[mode];
         const uint64_t t_end = ((end - 1) >> bits) + 1;
-        // a chunk covers <= 2^32 indices (tile ids < 2^24, level-2 positions fit 32 bits)
-        uint32_t chunk = (uint32_t)std::min<uint64_t>(chunk_tiles(), (1ull << 32) >> bits);
+        // a chunk covers <= chunk_index_limit() indices and <= 2^24 tiles (tile ids and
+        // level-2 positions fit 32 bits)
+        uint32_t chunk = (uint32_t)std::min<uint64_t>(chunk_tiles(), chunk_index_limit() >> bits);
         chunk = std::min<uint32_t>(chunk, next_pow2((uint32_t)std::min<uint64_t>(
                                               t_end - (start >> bits), 1u << 30)));
         if (chunk > P->chunk_cap) {  // (re)allocate the contraction records + dedup table
