@@ -4,9 +4,9 @@ enumeration (BASELINE.json metric, config C3), 1..N B200.
 
 Workload (config C3): T = delaunay-7 (the staircase), raw index space,
 lower half [0, 2^35) = the 2^36 sign space modulo the global sign flip
-(SURVEY.md section 0.1).  A step is one slice of 2^33 consecutive indices
+(SURVEY.md section 0.1).  A step is one slice of 2^34 consecutive indices
 per GPU (weak scaling: rank r of N sweeps slice s*N + r); at N=1 the
-default 4 timed steps are the complete enumeration.  Indices are generated
+default 2 timed steps are the complete enumeration.  Indices are generated
 on the device (there is no input tensor), so `value` is kernel-resident
 throughput; `e2e` runs the same slices through the public API
 (`paper_2604_09221_b200.sweep`), host round trip and string rendering
@@ -430,7 +430,7 @@ def run_ours(args, rank, world, local_rank):
                       "factor": args.steps * sl / classified_pw if classified_pw else None,
                       "note": "identical contracted tiles, then identical level-2 records "
                               "(32 patchworks each), are classified once and counted with "
-                              "their multiplicity (exact; within each chunk of up to 2^33 "
+                              "their multiplicity (exact; within each chunk of up to 2^34 "
                               "indices of one sweep call; never across steps)"},
         },
         "cpu_baseline": cpu,
@@ -451,10 +451,10 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--slice-log2", type=int, default=33)
+    ap.add_argument("--slice-log2", type=int, default=34)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--offset", type=lambda x: int(x, 0), default=0,
                     help="first index of the timed slices (profiling away from the easy low prefix)")

@@ -782,6 +782,9 @@ constexpr int TILE_BITS_MAX = 12;
 constexpr int MAXC = 48;  // fixed components per tile
 constexpr int MAXF = 32;  // free vertices
 constexpr int MAXM = 24;  // mid vertices of a super-tile
+// level-1 list entries for a single A slice: tile | (a + 1) << SLICE_SHIFT
+// (tile ids < 2^26 >= chunk_tiles(), a < 2^5)
+constexpr int SLICE_SHIFT = 26;
 constexpr int SUPER_BITS_MAX = 6;
 
 struct alignas(16) TileTables {  // per plan and domain (raw / representative), device memory
@@ -1628,7 +1631,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
         // list entries: tile, or tile | (a + 1) << 24 for the 32-index slice of
         // A pattern a only (a slice the level-2 path could not take)
         const uint32_t e = list ? list[i] : i;
-        const uint32_t t = e & 0xffffffu, sub = e >> 24;
+        const uint32_t t = e & ((1u << SLICE_SHIFT) - 1u), sub = e >> SLICE_SHIFT;
         const uint32_t lo0 = sub ? (sub - 1u) << 5 : 0u, lo1 = sub ? lo0 + 32u : tsize;
         const uint32_t weight = list ? 1u + dup[t] : 1u;
         const uint32_t tw = list ? min(t, mint[t]) : t;
@@ -1988,7 +1991,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
                                  : l2_build_lbl<unsigned long long>(tt, rec, slot, a, mmax, out,
                                                                     h, mine);
                 if (m < 0) {
-                    oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << 24);
+                    oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << SLICE_SHIFT);
                     wts[j] = 0u;
                 } else {
                     hashes[j] = h;
@@ -2797,12 +2800,12 @@ size_t cls_smem(int K) {
 // allocated on demand and only as large as the sweep needs, halved while it
 // would take more than a quarter of the free HBM).  TCG_CHUNK_LOG2 (14..24)
 // overrides.
-// indices per chunk (TCG_CHUNK_INDEX_LOG2, 32..34; default 2^33): larger chunks
-// deduplicate over a larger window (C3: 158x at 2^32, 244x at 2^33 -> +16 %);
-// tile ids stay < 2^24 (chunk_tiles)
+// indices per chunk (TCG_CHUNK_INDEX_LOG2, 32..34; default 2^34): larger chunks
+// deduplicate over a larger window (C3: 158x at 2^32, 244x at 2^33);
+// at most chunk_tiles() = 2^25 tiles
 static uint64_t chunk_index_limit() {
     static const uint64_t c = [] {
-        int lg = 33;
+        int lg = 34;
         if (const char *e = std::getenv("TCG_CHUNK_INDEX_LOG2")) lg = std::max(32, std::min(34, std::atoi(e)));
         return 1ull << lg;
     }();
@@ -2811,8 +2814,8 @@ static uint64_t chunk_index_limit() {
 
 static uint32_t chunk_tiles() {
     static const uint32_t c = [] {
-        int lg = 24;
-        if (const char *e = std::getenv("TCG_CHUNK_LOG2")) lg = std::max(14, std::min(24, std::atoi(e)));
+        int lg = 25;
+        if (const char *e = std::getenv("TCG_CHUNK_LOG2")) lg = std::max(14, std::min(25, std::atoi(e)));
         return 1u << lg;
     }();
     return c;
@@ -3549,14 +3552,14 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
     const uint32_t stride = (uint32_t)(1 + wps * (32 - T.nB));
     // sized once for the whole chunk (every level-1 tile a representative), so
     // that later sweeps never reallocate inside a timed region
-    const size_t want = std::max((size_t)n1, (size_t)P->chunk_cap) << la;
+    const size_t want = std::max((size_t)n1, (size_t)P->chunk_cap / 2) << la;
     const size_t per_rec = stride * 8 + 8 + 4 * 6 + 16;
     if (want > P->l2_cap || (int)stride != P->l2_stride) {
         size_t fr = 0, tot = 0;
         CUDA_TRY(cudaMemGetInfo(&fr, &tot));
         fr += P->l2_cap * per_rec;
         size_t cap = std::max<size_t>(want, P->l2_cap);
-        while (cap > ((size_t)1 << 16) && cap * per_rec > fr / 3) cap >>= 1;
+        while (cap > ((size_t)1 << 16) && cap * per_rec > fr / 2) cap >>= 1;
         if (cap > P->l2_cap || (int)stride != P->l2_stride) {
             cudaFree(P->d_l2pool);
             cudaFree(P->d_l2hash);
@@ -3656,7 +3659,7 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
         const TileTables *tt = P->d_tiles + mode;
         const int bits = P->tile_bits[mode];
         const uint64_t t_end = ((end - 1) >> bits) + 1;
-        // a chunk covers <= chunk_index_limit() indices and <= 2^24 tiles (tile ids and
+        // a chunk covers <= chunk_index_limit() indices and <= 2^25 tiles (tile ids and
         // level-2 positions fit 32 bits)
         uint32_t chunk = (uint32_t)std::min<uint64_t>(chunk_tiles(), chunk_index_limit() >> bits);
         chunk = std::min<uint32_t>(chunk, next_pow2((uint32_t)std::min<uint64_t>(
