@@ -802,6 +802,15 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     // per lane), bits 5..bits-1 the A points fixed per level-2 record
     int l2, nB, NA, la;                     // enabled, B nodes, A patterns = 2^la
     int l2shift, l2even;                    // B nodes = free nodes l2shift .. +nB-1 (or -1)
+    // two-stage level 2 (odd degree, 4 A bits): stage 1 fixes A1 = tile bits 5,6,
+    // stage 2 the A2 = bits 7,8.  F space (stage-1 free nodes) = B nodes 0..nB-1,
+    // then A2 nodes nB..nB+nA2-1.
+    int ts, nA2;
+    uint32_t fa1, fa2;                      // free-node masks of A1 / A2 nodes
+    int8_t l15F[MAXF];                      // free node -> F index (or -1)
+    uint32_t a2sign[4];                     // A2-node signs (A2 index space) per A2 pattern
+    uint32_t a2adjA2[8], a2linkA2[8];       // A2-A2 adjacency / links (A2 space)
+    uint32_t a2adjB[8], a2linkB[8];         // A2-B adjacency / links (B space)
     uint32_t fa, fbm;                       // free-node masks of A and B nodes
     int8_t l2j[MAXF];                       // free node -> B index (or -1)
     uint32_t l2adjB[16], l2linkB[16];       // B-B adjacency / links (B index space)
@@ -2004,6 +2013,291 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
     }
 }
 
+// ---------------------------------------------------- two-stage level 2
+// Stage 1 (k_l15_build, one lane per (representative tile, A1 pattern)):
+// fix the A1 nodes (tile bits 5, 6) and merge components + A1 nodes into
+// super-nodes, keeping their relations to the F nodes (B and A2) by member
+// sign; records are two words per super-node,
+//   word0 = cs | self << 31,   word1 = plusF | minusF << nF | linkF << 2nF,
+// and are deduplicated like level-2 records.  Stage 2 (k_l2_from_l15, one
+// lane per (distinct stage-1 record, A2 pattern)) fixes the A2 nodes and
+// merges again, emitting ordinary level-2 records (same format and hash as
+// k_l2_build, so the rest of the pipeline is unchanged).  Either stage sets
+// *fail when a record would exceed its super-node budget; the host then
+// redoes the batch on the direct path.
+constexpr int L15_MAXM = L2B_CS;  // stage-1 super-nodes (cs bit 31 is the self flag)
+
+__device__ __forceinline__ unsigned long long l15_compress(const TileTables &tt, uint32_t fm) {
+    unsigned long long r = 0;
+    for (; fm; fm &= fm - 1u) r |= 1ull << tt.l15F[__ffs(fm) - 1];
+    return r;
+}
+
+template <typename MT>
+__device__ __forceinline__ int l15_build(const TileTables &tt, const TileRec *__restrict__ rec,
+                                         const uint4 *__restrict__ R4, uint32_t a1,
+                                         unsigned long long *out, unsigned long long &hout,
+                                         uint32_t *mine) {
+    constexpr bool WIDE = sizeof(MT) == 8;
+    const int n = rec->n, nF = tt.nB + tt.nA2;
+    uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
+    uint32_t *cs = mine + 16 * THREADS;
+    const uint32_t lowA = a1 << 5;
+    const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
+    const MT one = 1;
+    const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa1) << n);
+    const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa1 << n);
+    const MT FBn = (MT)(tt.fbm | tt.fa2) << n;
+    MT unv = G, done = 0;
+    unsigned long long hh = 0x9E3779B97F4A7C15ull;
+    int m = 0;
+    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
+    while (unv) {
+        if (m == L15_MAXM) return -1;
+        MT f = unv & ((MT)0 - unv);
+        unv ^= f;
+        MT M = f, cg = 0, pb = 0, mb = 0, lk = 0;
+        while (f) {
+            const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
+            f &= f - one;
+            lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
+            MT rx, ry;
+            if constexpr (WIDE) {
+                const uint4 r = R4[u];
+                rx = (MT)r.x | ((MT)r.y << 32);
+                ry = (MT)r.z | ((MT)r.w << 32);
+            } else {
+                const uint2 r = reinterpret_cast<const uint2 *>(R4)[u];
+                rx = r.x;
+                ry = r.y;
+            }
+            const MT s = (sg1 >> u) & one;
+            const MT diff = sg1 ^ ((MT)0 - s);
+            const MT nw = ((rx & ~diff) | ry) & unv;
+            unv ^= nw;
+            f |= nw;
+            M |= nw;
+            cg |= rx & G & diff;
+            const MT bp = rx & FBn;
+            pb |= s ? bp : (MT)0;
+            mb |= s ? (MT)0 : bp;
+            lk |= ry & FBn;
+        }
+        uint32_t c = 0;
+        const MT x = cg & done;
+        for (uint32_t w = (uint32_t)x; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
+        if constexpr (WIDE)
+            for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) c |= 1u << label(31 + __ffs(w));
+        const uint32_t self = (cg & M) != (MT)0;
+        cs[m * THREADS] = c | self << 31;
+        for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
+        const unsigned long long w1 = l15_compress(tt, (uint32_t)(pb >> n)) |
+                                      l15_compress(tt, (uint32_t)(mb >> n)) << nF |
+                                      l15_compress(tt, (uint32_t)(lk >> n)) << (2 * nF);
+        out[2 + 2 * m] = w1;
+        hh = mix64(hh ^ w1);
+        done |= M;
+        ++m;
+    }
+    out[0] = (unsigned long long)m;
+    uint32_t hl = 0xC2B2AE3Du;
+    for (int k = 0; k < m; ++k) {
+        const uint32_t c = cs[k * THREADS];
+        out[1 + 2 * k] = c;
+        hl = (hl ^ c) * 0x9E3779B1u;
+        hl ^= hl >> 15;
+    }
+    hout = mix64((hh ^ hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
+    return m;
+}
+
+// One lane per (representative tile, A1 pattern) of list1[i0 .. i0+nb): 4 per tile.
+__global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restrict__ tt_g,
+                                                       const TileRec *__restrict__ recs,
+                                                       const uint32_t *__restrict__ list1,
+                                                       const uint32_t *__restrict__ dup1,
+                                                       const uint32_t *__restrict__ mint1,
+                                                       uint32_t i0, uint32_t nb, uint64_t tile0,
+                                                       uint64_t start, uint64_t end,
+                                                       unsigned long long *__restrict__ pool,
+                                                       uint32_t stride,
+                                                       unsigned long long *__restrict__ hashes,
+                                                       uint32_t *__restrict__ wts,
+                                                       uint32_t *__restrict__ poss,
+                                                       uint32_t *__restrict__ oldlist,
+                                                       uint32_t *__restrict__ oldcount,
+                                                       uint32_t *__restrict__ fail) {
+    __shared__ TileTables tts;
+    extern __shared__ __align__(16) uint32_t l2smem[];
+    uint32_t *mine = l2smem + threadIdx.x;
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    __syncthreads();
+    const TileTables &tt = tts;
+    const int bits = tt.bits;
+    const uint32_t nrec = nb << 2;
+    const int lane = threadIdx.x & 31;
+    uint4 *slot = reinterpret_cast<uint4 *>(l2smem + L2B_WORDS * THREADS) +
+                  (L2B_SLOT / 16) * ((threadIdx.x >> 5) * 8 + (lane >> 2));
+    for (uint32_t jb = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); jb < nrec;
+         jb += gridDim.x * blockDim.x) {  // warp-uniform
+        const uint32_t j = jb + lane;
+        const bool valid = j < nrec;
+        const uint32_t i = i0 + (j >> 2), a1 = j & 3u;
+        const uint32_t t = valid ? list1[i] : 0u;
+        const TileRec *rec = recs + t;
+        if (valid) {
+            const uint4 *src = rec->rows;
+            const int nq = rec->nnodes <= 32 ? 16 : 64;
+            for (int q = lane & 3; q < nq; q += 4) slot[q] = src[q];
+        }
+        __syncwarp();
+        if (valid) {
+            const int nn = rec->nnodes;
+            const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
+            if (rec->fallback || b0 < start || b1 > end) {
+                if (a1 == 0) oldlist[atomicAdd(oldcount, 1u)] = t;
+                wts[j] = 0u;
+            } else {
+                unsigned long long *out = pool + (size_t)j * stride;
+                unsigned long long h = 0;
+                const int m = nn <= 32 ? l15_build<uint32_t>(tt, rec, slot, a1, out, h, mine)
+                                       : l15_build<unsigned long long>(tt, rec, slot, a1, out, h,
+                                                                       mine);
+                if (m < 0) {
+                    atomicOr(fail, 1u);
+                    wts[j] = 0u;
+                } else {
+                    hashes[j] = h;
+                    wts[j] = 1u + dup1[t];
+                    poss[j] = (min(t, mint1[t]) << 2) | a1;
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// One lane per (distinct stage-1 record list15[i], A2 pattern): 4 per record.
+__global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__restrict__ tt_g,
+                                                         const unsigned long long *__restrict__ pool1,
+                                                         uint32_t stride1,
+                                                         const uint32_t *__restrict__ list15,
+                                                         const uint32_t *__restrict__ count15,
+                                                         const uint32_t *__restrict__ w15,
+                                                         const uint32_t *__restrict__ pos15,
+                                                         unsigned long long *__restrict__ pool,
+                                                         uint32_t stride,
+                                                         unsigned long long *__restrict__ hashes,
+                                                         uint32_t *__restrict__ wts,
+                                                         uint32_t *__restrict__ poss,
+                                                         uint32_t *__restrict__ fail) {
+    __shared__ TileTables tts;
+    extern __shared__ __align__(16) uint32_t l2smem[];
+    uint32_t *mine = l2smem + threadIdx.x;
+    uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
+    uint32_t *cs = mine + 16 * THREADS;
+    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    __syncthreads();
+    const TileTables &tt = tts;
+    const int nB = tt.nB, nA2 = tt.nA2, nF = nB + nA2;
+    const uint32_t bm = (1u << nB) - 1u, a2m = (1u << nA2) - 1u;
+    const unsigned long long fm = (1ull << nF) - 1ull;
+    const int mmax = min(32 - nB, L2B_CS);
+    const uint32_t nrec = *count15 << 2;
+    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nrec; j += gridDim.x * blockDim.x) {
+        const uint32_t j1 = list15[j >> 2], a2 = j & 3u;
+        const unsigned long long *r1 = pool1 + (size_t)j1 * stride1;
+        const int m1 = (int)r1[0];
+        const uint32_t SA2 = tt.a2sign[a2];
+        // A2 rows toward the stage-1 super-nodes (same-sign or linked / crossed)
+        uint32_t sameA[8], crossA[8];
+        for (int k = 0; k < nA2; ++k) sameA[k] = crossA[k] = 0u;
+        for (int s = 0; s < m1; ++s) {
+            const unsigned long long w1 = r1[2 + 2 * s];
+            const uint32_t pA = (uint32_t)(w1 >> nB) & a2m, mA = (uint32_t)(w1 >> (nF + nB)) & a2m,
+                           lA = (uint32_t)(w1 >> (2 * nF + nB)) & a2m;
+            const uint32_t same = (pA & SA2) | (mA & ~SA2) | lA, cross = (pA & ~SA2) | (mA & SA2);
+            for (uint32_t y = same; y; y &= y - 1u) sameA[__ffs(y) - 1] |= 1u << s;
+            for (uint32_t y = cross; y; y &= y - 1u) crossA[__ffs(y) - 1] |= 1u << s;
+        }
+        const int nn = m1 + nA2;
+        const uint32_t G = nn >= 32 ? ~0u : ((1u << nn) - 1u);
+        uint32_t unv = G, done = 0, hh = 0x9E3779B9u;
+        unsigned long long *out = pool + (size_t)j * stride;
+        uint32_t *out32 = reinterpret_cast<uint32_t *>(out);
+        int m = 0;
+        bool bad = false;
+        while (unv) {
+            if (m == mmax) { bad = true; break; }
+            uint32_t f = unv & (0u - unv);
+            unv ^= f;
+            uint32_t M = f, cg = 0, pb = 0, mb = 0, lk = 0, selfany = 0;
+            while (f) {
+                const int v = __ffs(f) - 1;
+                f &= f - 1u;
+                lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)m;
+                uint32_t same, cross;
+                if (v < m1) {
+                    const unsigned long long w0 = r1[1 + 2 * v], w1 = r1[2 + 2 * v];
+                    const uint32_t pA = (uint32_t)(w1 >> nB) & a2m,
+                                   mA = (uint32_t)(w1 >> (nF + nB)) & a2m,
+                                   lA = (uint32_t)(w1 >> (2 * nF + nB)) & a2m;
+                    same = ((pA & SA2) | (mA & ~SA2) | lA) << m1;
+                    cross = ((uint32_t)w0 & 0x7fffffffu) | (((pA & ~SA2) | (mA & SA2)) << m1);
+                    selfany |= (uint32_t)w0 >> 31;
+                    pb |= (uint32_t)(w1 & fm) & bm;
+                    mb |= (uint32_t)((w1 >> nF) & fm) & bm;
+                    lk |= (uint32_t)((w1 >> (2 * nF)) & fm) & bm;
+                } else {
+                    const int k = v - m1;
+                    const uint32_t sk = (SA2 >> k) & 1u, own = sk ? SA2 : ~SA2;
+                    same = sameA[k] | (((tt.a2adjA2[k] & own) | tt.a2linkA2[k]) << m1);
+                    cross = crossA[k] | ((tt.a2adjA2[k] & ~own & a2m) << m1);
+                    if (sk) pb |= tt.a2adjB[k];
+                    else mb |= tt.a2adjB[k];
+                    lk |= tt.a2linkB[k];
+                }
+                const uint32_t nw = same & unv;
+                unv ^= nw;
+                f |= nw;
+                M |= nw;
+                cg |= cross;
+            }
+            uint32_t c = 0;
+            for (uint32_t w = cg & done; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
+            cs[m * THREADS] = c;
+            for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
+            const uint32_t self = ((cg & M) != 0u) | selfany;
+            const uint32_t hi = pb | mb << nB | lk << (2 * nB) | self << (3 * nB);
+            out32[2 * (1 + m) + 1] = hi;
+            hh = (hh ^ hi) * 0x85EBCA77u;
+            hh ^= hh >> 13;
+            done |= M;
+            ++m;
+        }
+        if (bad) {
+            atomicOr(fail, 1u);
+            wts[j] = 0u;
+            continue;
+        }
+        out[0] = (unsigned long long)m;
+        uint32_t hl = 0xC2B2AE3Du;
+        for (int q = 0; q < m; ++q) {
+            const uint32_t c = cs[q * THREADS];
+            out32[2 * (1 + q)] = c;
+            hl = (hl ^ c) * 0x9E3779B1u;
+            hl ^= hl >> 15;
+        }
+        hashes[j] = mix64(((unsigned long long)hh << 32 | hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
+        wts[j] = w15[j1];
+        const uint32_t p1 = pos15[j1];
+        poss[j] = ((p1 >> 2) << 4) | (a2 << 2) | (p1 & 3u);
+    }
+}
+
 // One thread per level-2 record: exact deduplication (hash, then word-by-word).
 __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *__restrict__ pool,
                                                       uint32_t stride, uint32_t nrec,
@@ -2667,6 +2961,11 @@ struct tcg_plan {
     unsigned long long *d_l2pool = nullptr, *d_l2hash = nullptr;
     uint32_t *d_l2u32 = nullptr;     // wts | poss | w2 | pos2 | list2 | count2
     unsigned long long *d_l2slots = nullptr;  // [2 pow2(l2_cap)] tag << 32 | record
+    // two-stage level 2: stage-1 records and their dedup state
+    size_t l15_cap = 0;
+    unsigned long long *d_l15pool = nullptr, *d_l15hash = nullptr, *d_l15slots = nullptr;
+    uint32_t *d_l15u32 = nullptr;    // wts | poss | w15 | pos15 | list15 | count15 | fail | saved
+    int64_t l15_built = 0, l15_fallbacks = 0;
     uint32_t *d_oldlist = nullptr;   // [chunk_cap + 1]: count, then tiles for the level-1 path
     uint32_t *d_ovf = nullptr;       // [chunk_cap + 1]: count, then tiles of fallback super-tiles
     SuperRec *d_super = nullptr;     // [super_cap]
@@ -2977,6 +3276,45 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
         T.l2shift = -1;
         if (fb >> __builtin_ctz(fb) == (1u << nB) - 1u) T.l2shift = __builtin_ctz(fb);
         T.l2 = 1;
+        // two-stage tables
+        T.ts = 0;
+        const uint32_t fa1 = (uint32_t)(T.fcopy[5] | T.fcopy[6]);
+        const uint32_t fa2 = T.la == 4 ? (uint32_t)(T.fcopy[7] | T.fcopy[8]) : 0u;
+        const int nA2 = __builtin_popcount(fa2);
+        if (!T.l2even && T.la == 4 && nA2 > 0 && nA2 <= 8 && nB + nA2 <= 20) {
+            T.fa1 = fa1;
+            T.fa2 = fa2;
+            T.nA2 = nA2;
+            int a2j[MAXF], a2f[8], k = 0;
+            for (int f = 0; f < MAXF; ++f) { T.l15F[f] = -1; a2j[f] = -1; }
+            for (int f = 0; f < nf; ++f) {
+                if (T.l2j[f] >= 0) T.l15F[f] = T.l2j[f];
+                if ((fa2 >> f) & 1u) {
+                    a2j[f] = k;
+                    a2f[k] = f;
+                    T.l15F[f] = (int8_t)(nB + k);
+                    ++k;
+                }
+            }
+            auto compA2 = [&](unsigned long long x) {
+                uint32_t r = 0;
+                for (int f = 0; f < nf; ++f)
+                    if (((x >> f) & 1ull) && a2j[f] >= 0) r |= 1u << a2j[f];
+                return r;
+            };
+            for (int q = 0; q < nA2; ++q) {
+                const int f = a2f[q];
+                T.a2adjA2[q] = compA2(T.fadj[f] & fa2);
+                T.a2linkA2[q] = compA2(T.fpl[f] & fa2);
+                T.a2adjB[q] = comp(T.fadj[f] & fb);
+                T.a2linkB[q] = comp(T.fpl[f] & fb);
+            }
+            for (int x = 0; x < 4; ++x) {  // tile-local index x << 7 (bits 7, 8)
+                const uint32_t low = (uint32_t)x << 7;
+                T.a2sign[x] = compA2((T.fsign[0][low & 63u] ^ T.fsign[1][(low >> 6) & 63u]) & fa2);
+            }
+            T.ts = 1;
+        }
     };
     for (int a = 0; a < D->nap; ++a) {
         const int fu = fnode[D->ap_u[a]], fv = fnode[D->ap_v[a]];
@@ -3271,6 +3609,10 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
         if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)L2B_SMEM)) != cudaSuccess)
             return bail(e, "l2 build smem");
+    for (void *kb : {(void *)k_l15_build, (void *)k_l2_from_l15})
+        if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)L2B_SMEM)) != cudaSuccess)
+            return bail(e, "l15 smem");
     cudaFuncSetAttribute((void *)k_l2_classify_even, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)L2E_CLS_SMEM);
     cudaFuncSetAttribute((void *)k_l2_classify_even, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -3331,7 +3673,7 @@ int tcg_plan_destroy(tcg_plan *P) {
     DeviceGuard guard(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     timing_resolve(P);
-    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_l2slots, P->d_oldlist, P->d_ovf, P->d_super, P->d_hash, P->d_slots, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_l2slots, P->d_l15pool, P->d_l15hash, P->d_l15slots, P->d_l15u32, P->d_oldlist, P->d_ovf, P->d_super, P->d_hash, P->d_slots, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
@@ -3531,6 +3873,126 @@ static bool l2_enabled() {
     return on;
 }
 
+static int l2_tail(tcg_plan *P, const TileTables &T, const TileTables *tt, uint32_t nrec,
+                   uint32_t stride, uint64_t tile0);
+
+// Two-stage level 2 for one batch of level-1 representatives.  Returns true
+// when the batch is done; false (nothing consumed) when a record exceeded its
+// super-node budget or the stage-2 records do not fit, and the caller runs the
+// direct path.
+static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const TileRec *recs,
+                          const uint32_t *list1, const uint32_t *dup1, const uint32_t *mint1,
+                          uint32_t i0, uint32_t nb, uint64_t tile0, uint64_t lo, uint64_t hi,
+                          size_t cap, uint32_t stride, int &rc) {
+    const TileTables &T = P->h_tiles[mode];
+    const uint32_t stride1 = (uint32_t)(1 + 2 * L15_MAXM);
+    const uint32_t nrec1 = nb << 2;
+    auto cuda_ok = [&](cudaError_t e, const char *what) {
+        if (e != cudaSuccess) rc = fail(TCG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        return e == cudaSuccess;
+    };
+    if (nrec1 > P->l15_cap) {
+        size_t fr = 0, tot = 0;
+        if (!cuda_ok(cudaStreamSynchronize(P->stream), "sync")) return false;
+        if (!cuda_ok(cudaMemGetInfo(&fr, &tot), "meminfo")) return false;
+        const size_t per = (size_t)stride1 * 8 + 8 + 4 * 6 + 16;
+        fr += P->l15_cap * per;
+        if ((size_t)nrec1 * per > fr / 2) return false;  // no room: direct path
+        const size_t c1 = std::max<size_t>(nrec1, (P->chunk_cap / 2) << 2);
+        const size_t c = c1 * per <= fr / 2 ? c1 : nrec1;
+        cudaFree(P->d_l15pool);
+        cudaFree(P->d_l15hash);
+        cudaFree(P->d_l15slots);
+        cudaFree(P->d_l15u32);
+        P->d_l15pool = nullptr;
+        P->d_l15hash = nullptr;
+        P->d_l15slots = nullptr;
+        P->d_l15u32 = nullptr;
+        P->l15_cap = 0;
+        if (!cuda_ok(cudaMalloc(&P->d_l15pool, sizeof(unsigned long long) * stride1 * c), "malloc l15") ||
+            !cuda_ok(cudaMalloc(&P->d_l15hash, sizeof(unsigned long long) * c), "malloc l15") ||
+            !cuda_ok(cudaMalloc(&P->d_l15slots, sizeof(unsigned long long) * 2 *
+                                                    (size_t)next_pow2((uint32_t)c)), "malloc l15") ||
+            !cuda_ok(cudaMalloc(&P->d_l15u32, sizeof(uint32_t) * (5 * c + 3)), "malloc l15"))
+            return false;
+        P->l15_cap = c;
+    }
+    const size_t c = P->l15_cap;
+    uint32_t *wts1 = P->d_l15u32, *poss1 = wts1 + c, *w15 = poss1 + c, *pos15 = w15 + c,
+             *list15 = pos15 + c, *count15 = list15 + c, *failp = count15 + 1, *saved = failp + 1;
+    unsigned long long *slots1 = P->d_l15slots, *pool1 = P->d_l15pool, *hash1 = P->d_l15hash;
+    cudaStream_t st = P->stream;
+    const uint32_t np2 = next_pow2(nrec1);
+    if (!cuda_ok(cudaMemcpyAsync(saved, P->d_oldlist, 4, cudaMemcpyDeviceToDevice, st), "save") ||
+        !cuda_ok(cudaMemsetAsync(failp, 0, 4, st), "memset") ||
+        !cuda_ok(cudaMemsetAsync(count15, 0, 4, st), "memset") ||
+        !cuda_ok(cudaMemsetAsync(slots1, 0xff, sizeof(unsigned long long) * 2 * (size_t)np2, st), "memset") ||
+        !cuda_ok(cudaMemsetAsync(w15, 0, sizeof(uint32_t) * nrec1, st), "memset") ||
+        !cuda_ok(cudaMemsetAsync(pos15, 0xff, sizeof(uint32_t) * nrec1, st), "memset"))
+        return false;
+    uint32_t *oldlist = P->d_oldlist + 1, *oldcount = P->d_oldlist;
+    uint64_t t0 = tile0, a = lo, b = hi;
+    uint32_t i0v = i0, nbv = nb, s1 = stride1;
+    const unsigned g1 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8, (nrec1 + THREADS - 1) / THREADS);
+    void *ab[] = {&tt, &recs, &list1, &dup1, &mint1, &i0v, &nbv, &t0, &a, &b, &pool1, &s1,
+                  &hash1, &wts1, &poss1, &oldlist, &oldcount, &failp};
+    const size_t smem1 = (size_t)L2B_WORDS * 4 * THREADS + (size_t)(THREADS / 32) * 8 * L2B_SLOT;
+    cudaEvent_t e0 = timing_begin(P);
+    if (!cuda_ok(cudaLaunchKernel((void *)k_l15_build, dim3(g1), dim3(THREADS), ab, smem1, st), "l15 build"))
+        return false;
+    uint32_t smask1 = 2 * np2 - 1;
+    int wps2 = 2;
+    uint32_t nr1 = nrec1;
+    void *ad[] = {&pool1, &s1, &nr1, &hash1, &wts1, &poss1, &slots1, &smask1, &w15, &pos15,
+                  &list15, &count15, &wps2};
+    if (!cuda_ok(cudaLaunchKernel((void *)k_l2_dedup, dim3(g1), dim3(THREADS), ad, 0, st), "l15 dedup"))
+        return false;
+    uint32_t hostv[2] = {0, 0};  // count15, fail
+    if (!cuda_ok(cudaMemcpyAsync(hostv, count15, 8, cudaMemcpyDeviceToHost, st), "copy") ||
+        !cuda_ok(cudaStreamSynchronize(st), "sync"))
+        return false;
+    timing_end(P, TCG_KT_L2_BUILD, e0);
+    P->l15_built += nrec1;
+    P->launches += 2;
+    const uint32_t n15 = hostv[0];
+    auto fallback = [&]() {
+        P->l15_fallbacks++;
+        cuda_ok(cudaMemcpyAsync(P->d_oldlist, saved, 4, cudaMemcpyDeviceToDevice, st), "restore");
+        return false;
+    };
+    if (hostv[1] || (size_t)n15 * 4 > cap) return fallback();
+    // stage 2 into the ordinary level-2 buffers
+    const uint32_t nrec = n15 << 2;
+    uint32_t *wts = P->d_l2u32, *poss = wts + cap;
+    unsigned long long *pool = P->d_l2pool, *hashes = P->d_l2hash;
+    const unsigned g2 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8, (nrec + THREADS - 1) / THREADS);
+    uint32_t s2 = stride;
+    void *a2[] = {&tt, &pool1, &s1, &list15, &count15, &w15, &pos15, &pool, &s2, &hashes, &wts,
+                  &poss, &failp};
+    const size_t smem2 = (size_t)L2B_WORDS * 4 * THREADS;
+    cudaEvent_t e1 = timing_begin(P);
+    if (!cuda_ok(cudaLaunchKernel((void *)k_l2_from_l15, dim3(std::max(1u, g2)), dim3(THREADS), a2, smem2, st),
+                 "l2 from l15"))
+        return false;
+    if (!cuda_ok(cudaMemcpyAsync(hostv + 1, failp, 4, cudaMemcpyDeviceToHost, st), "copy") ||
+        !cuda_ok(cudaStreamSynchronize(st), "sync"))
+        return false;
+    timing_end(P, TCG_KT_L2_BUILD, e1);
+    P->launches++;
+    if (hostv[1]) return fallback();
+    rc = l2_tail(P, T, tt, nrec, stride, tile0);
+    return rc == 0;
+}
+
+// TCG_L2_TWOSTAGE=0 builds level-2 records directly (A/B); same results.
+static bool l2_twostage_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("TCG_L2_TWOSTAGE");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 // Level-2 stage of one chunk (after the level-1 dedup): build the records of
 // every (representative tile, A pattern), deduplicate them, classify the
 // representatives.  Tiles the level-2 path does not take (range ends,
@@ -3580,22 +4042,21 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
         }
     }
     const size_t cap = P->l2_cap;
-    uint32_t *wts = P->d_l2u32, *poss = wts + cap, *w2 = poss + cap, *pos2 = w2 + cap,
-             *list2 = pos2 + cap, *count2 = list2 + cap;
-    unsigned long long *slots = P->d_l2slots;
     const uint32_t nbmax = (uint32_t)(cap >> la);
     for (uint32_t i0 = 0; i0 < n1; i0 += nbmax) {
         uint32_t nb = std::min(nbmax, n1 - i0);
         uint32_t nrec = nb << la;
-        const uint32_t np2 = next_pow2(nrec);
-        CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(unsigned long long) * 2 * (size_t)np2,
-                                 P->stream));
-        CUDA_TRY(cudaMemsetAsync(w2, 0, sizeof(uint32_t) * nrec, P->stream));
-        CUDA_TRY(cudaMemsetAsync(pos2, 0xff, sizeof(uint32_t) * nrec, P->stream));
-        CUDA_TRY(cudaMemsetAsync(count2, 0, sizeof(uint32_t), P->stream));
+        if (T.ts && l2_twostage_enabled()) {
+            int rc2 = 0;
+            const bool done = run_two_stage(P, mode, tt, recs, list1, dup1, mint1, i0, nb, tile0,
+                                            lo, hi, cap, stride, rc2);
+            if (rc2) return rc2;
+            if (done) continue;
+        }
         const unsigned g12 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8,
                                                           (nrec + THREADS - 1) / THREADS);
         unsigned long long *pool = P->d_l2pool, *hashes = P->d_l2hash;
+        uint32_t *wts = P->d_l2u32, *poss = wts + cap;
         uint32_t *oldlist = P->d_oldlist + 1, *oldcount = P->d_oldlist;
         uint64_t t0 = tile0, a = lo, b = hi;
         void *a1[] = {&tt, &recs, &list1, &dup1, &mint1, &i0, &nb, &t0, &a, &b, &pool,
@@ -3607,29 +4068,55 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
         CUDA_TRY(cudaLaunchKernel(kb, dim3(g12), dim3(THREADS), a1, l2b_smem,
                                   P->stream));
         timing_end(P, TCG_KT_L2_BUILD, e0);
-        uint32_t smask = 2 * np2 - 1;
-        int wpsv = wps;
-        void *a2[] = {&pool, (void *)&stride, &nrec, &hashes, &wts, &poss, &slots, &smask, &w2,
-                      &pos2, &list2, &count2, &wpsv};
-        cudaEvent_t e0d = timing_begin(P);
-        CUDA_TRY(cudaLaunchKernel((void *)k_l2_dedup, dim3(g12), dim3(THREADS), a2, 0, P->stream));
-        timing_end(P, TCG_KT_L2_DEDUP, e0d);
-        P->l2_built += nrec;
-        const unsigned g3 = (unsigned)std::min<uint64_t>(P->blocks_l2cls,
-                                                         (nrec + CLS_WARPS - 1) / CLS_WARPS);
-        unsigned long long *ts = P->d_tstats + 1;
-        void *a3[] = {&P->kp, &tt, &pool, (void *)&stride, &list2, &count2, &w2, &pos2, &t0,
-                      &P->agg, &ts};
-        cudaEvent_t e = timing_begin(P);
-        if (T.l2even)
-            CUDA_TRY(cudaLaunchKernel((void *)k_l2_classify_even, dim3(g3), dim3(THREADS), a3,
-                                      L2E_CLS_SMEM, P->stream));
-        else
-            CUDA_TRY(cudaLaunchKernel((void *)k_l2_classify, dim3(g3), dim3(THREADS), a3,
-                                      L2_CLS_SMEM, P->stream));
-        timing_end(P, TCG_KT_L2_CLASSIFY, e);
-        P->launches += 3;
+        P->launches++;
+        const int rc = l2_tail(P, T, tt, nrec, stride, tile0);
+        if (rc) return rc;
     }
+    return TCG_OK;
+}
+
+// Deduplicate nrec level-2 records (pool / hashes / wts / poss as built) and
+// classify the distinct ones.
+static int l2_tail(tcg_plan *P, const TileTables &T, const TileTables *tt, uint32_t nrec,
+                   uint32_t stride, uint64_t tile0) {
+    if (nrec == 0) return TCG_OK;
+    const size_t cap = P->l2_cap;
+    uint32_t *wts = P->d_l2u32, *poss = wts + cap, *w2 = poss + cap, *pos2 = w2 + cap,
+             *list2 = pos2 + cap, *count2 = list2 + cap;
+    unsigned long long *slots = P->d_l2slots, *pool = P->d_l2pool, *hashes = P->d_l2hash;
+    const int wps = T.l2even ? 2 : 1;
+    const uint32_t np2 = next_pow2(nrec);
+    CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(unsigned long long) * 2 * (size_t)np2,
+                             P->stream));
+    CUDA_TRY(cudaMemsetAsync(w2, 0, sizeof(uint32_t) * nrec, P->stream));
+    CUDA_TRY(cudaMemsetAsync(pos2, 0xff, sizeof(uint32_t) * nrec, P->stream));
+    CUDA_TRY(cudaMemsetAsync(count2, 0, sizeof(uint32_t), P->stream));
+    const unsigned g12 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8,
+                                                      (nrec + THREADS - 1) / THREADS);
+    uint32_t smask = 2 * np2 - 1;
+    int wpsv = wps;
+    uint32_t nr = nrec, sv = stride;
+    void *a2[] = {&pool, &sv, &nr, &hashes, &wts, &poss, &slots, &smask, &w2,
+                  &pos2, &list2, &count2, &wpsv};
+    cudaEvent_t e0d = timing_begin(P);
+    CUDA_TRY(cudaLaunchKernel((void *)k_l2_dedup, dim3(g12), dim3(THREADS), a2, 0, P->stream));
+    timing_end(P, TCG_KT_L2_DEDUP, e0d);
+    P->l2_built += nrec;
+    const unsigned g3 = (unsigned)std::min<uint64_t>(P->blocks_l2cls,
+                                                     (nrec + CLS_WARPS - 1) / CLS_WARPS);
+    unsigned long long *ts = P->d_tstats + 1;
+    uint64_t t0 = tile0;
+    void *a3[] = {&P->kp, &tt, &pool, &sv, &list2, &count2, &w2, &pos2, &t0,
+                  &P->agg, &ts};
+    cudaEvent_t e = timing_begin(P);
+    if (T.l2even)
+        CUDA_TRY(cudaLaunchKernel((void *)k_l2_classify_even, dim3(g3), dim3(THREADS), a3,
+                                  L2E_CLS_SMEM, P->stream));
+    else
+        CUDA_TRY(cudaLaunchKernel((void *)k_l2_classify, dim3(g3), dim3(THREADS), a3,
+                                  L2_CLS_SMEM, P->stream));
+    timing_end(P, TCG_KT_L2_CLASSIFY, e);
+    P->launches += 2;
     return TCG_OK;
 }
 

@@ -471,3 +471,33 @@ def test_super_tile_records_identical_to_direct_contraction():
         res[tag] = json.loads(p.stdout.strip().splitlines()[-1])
     assert res["super4"] == res["generic"]
     assert res["super6"] == res["generic"]
+
+
+def test_two_stage_level2_identical_to_direct():
+    """Two-stage level-2 records (A1 bits fixed, deduplicated, then A2) give
+    the same reports as building level-2 records directly (TCG_L2_TWOSTAGE=0)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json,sys; sys.path.insert(0, %r)\n"
+        "import random\n"
+        "from paper_2604_09221_b200 import builtin, sweep, SweepRange\n"
+        "from paper_2604_09221_b200.lifting import random_unimodular\n"
+        "out = []\n"
+        "for T, raw, a, n in [(builtin('delaunay-7'), True, 0x5A5A5A5A0 + 3, (1 << 25) + 1001),\n"
+        "                     (builtin('delaunay-7'), True, 0, 1 << 26),\n"
+        "                     (builtin('delaunay-7'), False, 777, 1 << 24),\n"
+        "                     (random_unimodular(7, random.Random(0xB7)), True, 1 << 33, 1 << 24)]:\n"
+        "    r = sweep(T, SweepRange(a, a + n), raw_space=raw)\n"
+        "    out.append([list(r.oval_histogram), sorted(r.scheme_map.items())])\n"
+        "print(json.dumps(out))\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    res = {}
+    for flag in ("0", "1"):
+        env = dict(os.environ, TCG_L2_TWOSTAGE=flag)
+        p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
+        assert p.returncode == 0, p.stderr
+        res[flag] = json.loads(p.stdout.strip().splitlines()[-1])
+    assert res["0"] == res["1"]
