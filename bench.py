@@ -378,9 +378,10 @@ def run_ours(args, rank, world, local_rank):
     kernel_names = {"tile_classify": "k_tile_classify<K=4,odd,raw>",
                     "enumerate": "k_enumerate<K=4,odd,raw>",
                     "tile_build": "k_tile_from_super", "tile_dedup": "k_tile_dedup",
-                    "l2_build": "k_l2_build", "l2_dedup": "k_l2_dedup",
+                    "l2_build": "k_l2_from_l15 (+ k_l2_build)", "l2_dedup": "k_l2_dedup",
                     "l2_classify": "k_l2_classify", "batch": "k_batch",
-                    "super_build": "k_super_build<K=4,raw>"}
+                    "super_build": "k_super_build<K=4,raw>", "l15_build": "k_l15_build",
+                    "l15_dedup": "k_l2_dedup (stage 1)"}
     total_kernel_ms = sum(v[0] for v in ktimes.values())
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

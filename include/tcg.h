@@ -120,11 +120,13 @@ int tcg_plan_info(const tcg_plan *plan, int32_t *info, int ninfo);
 #define TCG_KT_ENUMERATE 2     /* k_enumerate: flat per-patchwork sweeps / sampling */
 #define TCG_KT_BATCH 3         /* k_batch: explicit sign words */
 #define TCG_KT_TILE_DEDUP 4    /* k_tile_dedup: level-1 record deduplication */
-#define TCG_KT_L2_BUILD 5      /* k_l2_build: level-2 records */
+#define TCG_KT_L2_BUILD 5      /* k_l2_build / k_l2_from_l15: level-2 records */
 #define TCG_KT_L2_DEDUP 6      /* k_l2_dedup: level-2 record deduplication */
 #define TCG_KT_L2_CLASSIFY 7   /* k_l2_classify: level-2 classification */
 #define TCG_KT_SUPER_BUILD 8   /* k_super_build: super-tile contraction */
-#define TCG_NKINDS 9
+#define TCG_KT_L15_BUILD 9     /* k_l15_build: two-stage level 2, stage 1 */
+#define TCG_KT_L15_DEDUP 10    /* k_l2_dedup on the stage-1 records */
+#define TCG_NKINDS 11
 int tcg_plan_set_timing(tcg_plan *plan, int enable);
 int tcg_kernel_times(tcg_plan *plan, double *ms, int64_t *counts);
 /* Tile deduplication (exhaustive sweeps): tiles whose contracted records are

@@ -117,7 +117,7 @@ EXPORTS = (
 
 # tcg.h TCG_KT_* order (tcg_kernel_times)
 KERNEL_KINDS = ("tile_build", "tile_classify", "enumerate", "batch", "tile_dedup",
-                "l2_build", "l2_dedup", "l2_classify", "super_build")
+                "l2_build", "l2_dedup", "l2_classify", "super_build", "l15_build", "l15_dedup")
 
 
 def last_error() -> str:

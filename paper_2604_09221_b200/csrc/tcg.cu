@@ -2033,7 +2033,7 @@ __device__ __forceinline__ unsigned long long l15_compress(const TileTables &tt,
     return r;
 }
 
-template <typename MT>
+template <typename MT, bool PACK>
 __device__ __forceinline__ int l15_build(const TileTables &tt, const TileRec *__restrict__ rec,
                                          const uint4 *__restrict__ R4, uint32_t a1,
                                          unsigned long long *out, unsigned long long &hout,
@@ -2094,7 +2094,12 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const TileRec *__
         const unsigned long long w1 = l15_compress(tt, (uint32_t)(pb >> n)) |
                                       l15_compress(tt, (uint32_t)(mb >> n)) << nF |
                                       l15_compress(tt, (uint32_t)(lk >> n)) << (2 * nF);
-        out[2 + 2 * m] = w1;
+        if (PACK) {  // low half now; the high half (w1 >> 32, cs, self) at the end
+            reinterpret_cast<uint32_t *>(out)[2 * (1 + m)] = (uint32_t)w1;
+            cs[m * THREADS] |= (uint32_t)(w1 >> 32) << 24;  // <= 7 bits: 3 nF <= 39
+        } else {
+            out[2 + 2 * m] = w1;
+        }
         hh = mix64(hh ^ w1);
         done |= M;
         ++m;
@@ -2103,7 +2108,12 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const TileRec *__
     uint32_t hl = 0xC2B2AE3Du;
     for (int k = 0; k < m; ++k) {
         const uint32_t c = cs[k * THREADS];
-        out[1 + 2 * k] = c;
+        if (PACK)  // word bits 32..: w1 >> 32, then cs (24 bits) and self from bit 3 nF
+            reinterpret_cast<uint32_t *>(out)[2 * (1 + k) + 1] =
+                ((c >> 24) & 0x7fu) | ((c & 0xffffffu) << (3 * nF - 32)) |
+                ((c >> 31) << (3 * nF - 32 + 24));
+        else
+            out[1 + 2 * k] = c;
         hl = (hl ^ c) * 0x9E3779B1u;
         hl ^= hl >> 15;
     }
@@ -2161,9 +2171,15 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
             } else {
                 unsigned long long *out = pool + (size_t)j * stride;
                 unsigned long long h = 0;
-                const int m = nn <= 32 ? l15_build<uint32_t>(tt, rec, slot, a1, out, h, mine)
-                                       : l15_build<unsigned long long>(tt, rec, slot, a1, out, h,
-                                                                       mine);
+                const int nF = tt.nB + tt.nA2;
+                const bool pk = nF >= 11 && nF <= 13;  // one word per super-node
+                const int m =
+                    nn <= 32
+                        ? (pk ? l15_build<uint32_t, true>(tt, rec, slot, a1, out, h, mine)
+                              : l15_build<uint32_t, false>(tt, rec, slot, a1, out, h, mine))
+                        : (pk ? l15_build<unsigned long long, true>(tt, rec, slot, a1, out, h, mine)
+                              : l15_build<unsigned long long, false>(tt, rec, slot, a1, out, h,
+                                                                     mine));
                 if (m < 0) {
                     atomicOr(fail, 1u);
                     wts[j] = 0u;
@@ -2206,6 +2222,16 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
     const unsigned long long fm = (1ull << nF) - 1ull;
     const int mmax = min(32 - nB, L2B_CS);
     const uint32_t nrec = *count15 << 2;
+    const bool pk = nF >= 11 && nF <= 13;  // stage-1 records packed one word per super-node
+    // stage-1 super-node s: w1 = F relations, w0 = cs | self << 31
+    auto rw1 = [&](const unsigned long long *r1, int s2) -> unsigned long long {
+        return pk ? (r1[1 + s2] & ((1ull << (3 * nF)) - 1ull)) : r1[2 + 2 * s2];
+    };
+    auto rw0 = [&](const unsigned long long *r1, int s2) -> uint32_t {
+        if (!pk) return (uint32_t)r1[1 + 2 * s2];
+        const uint32_t x = (uint32_t)(r1[1 + s2] >> (3 * nF));
+        return (x & 0xffffffu) | ((x >> 24) & 1u) << 31;
+    };
     auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nrec; j += gridDim.x * blockDim.x) {
         const uint32_t j1 = list15[j >> 2], a2 = j & 3u;
@@ -2216,7 +2242,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
         uint32_t sameA[8], crossA[8];
         for (int k = 0; k < nA2; ++k) sameA[k] = crossA[k] = 0u;
         for (int s = 0; s < m1; ++s) {
-            const unsigned long long w1 = r1[2 + 2 * s];
+            const unsigned long long w1 = rw1(r1, s);
             const uint32_t pA = (uint32_t)(w1 >> nB) & a2m, mA = (uint32_t)(w1 >> (nF + nB)) & a2m,
                            lA = (uint32_t)(w1 >> (2 * nF + nB)) & a2m;
             const uint32_t same = (pA & SA2) | (mA & ~SA2) | lA, cross = (pA & ~SA2) | (mA & SA2);
@@ -2241,7 +2267,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
                 lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)m;
                 uint32_t same, cross;
                 if (v < m1) {
-                    const unsigned long long w0 = r1[1 + 2 * v], w1 = r1[2 + 2 * v];
+                    const unsigned long long w0 = rw0(r1, v), w1 = rw1(r1, v);
                     const uint32_t pA = (uint32_t)(w1 >> nB) & a2m,
                                    mA = (uint32_t)(w1 >> (nF + nB)) & a2m,
                                    lA = (uint32_t)(w1 >> (2 * nF + nB)) & a2m;
@@ -3885,7 +3911,8 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
                           uint32_t i0, uint32_t nb, uint64_t tile0, uint64_t lo, uint64_t hi,
                           size_t cap, uint32_t stride, int &rc) {
     const TileTables &T = P->h_tiles[mode];
-    const uint32_t stride1 = (uint32_t)(1 + 2 * L15_MAXM);
+    const bool pk = T.nB + T.nA2 >= 11 && T.nB + T.nA2 <= 13;  // one word per super-node
+    const uint32_t stride1 = (uint32_t)(1 + (pk ? 1 : 2) * L15_MAXM);
     const uint32_t nrec1 = nb << 2;
     auto cuda_ok = [&](cudaError_t e, const char *what) {
         if (e != cudaSuccess) rc = fail(TCG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -3940,8 +3967,10 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     cudaEvent_t e0 = timing_begin(P);
     if (!cuda_ok(cudaLaunchKernel((void *)k_l15_build, dim3(g1), dim3(THREADS), ab, smem1, st), "l15 build"))
         return false;
+    timing_end(P, TCG_KT_L15_BUILD, e0);
+    e0 = timing_begin(P);
     uint32_t smask1 = 2 * np2 - 1;
-    int wps2 = 2;
+    int wps2 = pk ? 1 : 2;
     uint32_t nr1 = nrec1;
     void *ad[] = {&pool1, &s1, &nr1, &hash1, &wts1, &poss1, &slots1, &smask1, &w15, &pos15,
                   &list15, &count15, &wps2};
@@ -3951,7 +3980,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     if (!cuda_ok(cudaMemcpyAsync(hostv, count15, 8, cudaMemcpyDeviceToHost, st), "copy") ||
         !cuda_ok(cudaStreamSynchronize(st), "sync"))
         return false;
-    timing_end(P, TCG_KT_L2_BUILD, e0);
+    timing_end(P, TCG_KT_L15_DEDUP, e0);
     P->l15_built += nrec1;
     P->launches += 2;
     const uint32_t n15 = hostv[0];
