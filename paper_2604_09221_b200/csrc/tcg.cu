@@ -1750,7 +1750,7 @@ __device__ __forceinline__ uint32_t l2_compress(const TileTables &tt, uint32_t f
 // written immediately; the low halves (cs) follow at the end.
 constexpr int L2B_CS = 24;          // super-nodes per level-2 record (also <= 32 - nB)
 constexpr int L2B_WORDS = 16 + L2B_CS;  // labels (64 nodes, 4 per word) | cs[L2B_CS]
-constexpr int L2B_SLOT = 1024;      // staged rows per tile: 64 x uint4 (or 32 x uint2)
+constexpr int L2B_SLOT = 256;       // staged rows per tile: 32 x uint2 (wider tiles read global)
 // level 2 needs tile bits >= 6 (la >= 1): at most 16 tiles per warp
 constexpr size_t L2B_SMEM = (size_t)L2B_WORDS * 4 * THREADS + (THREADS / 32) * 16 * L2B_SLOT;
 
@@ -1975,10 +1975,9 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
         const uint32_t i = i0 + (j >> la), a = j & ((1u << la) - 1u);
         const uint32_t t = valid ? list1[i] : 0u;
         const TileRec *rec = recs + t;
-        if (valid) {  // 256 bytes of uint2 rows, or 1 KB of uint4 rows above 32 nodes
+        if (valid && rec->nnodes <= 32) {  // 256 bytes of uint2 rows
             const uint4 *src = rec->rows;
-            const int nq = rec->nnodes <= 32 ? 16 : 64;
-            for (int q = lane & ((1 << lpt) - 1); q < nq; q += 1 << lpt) slot[q] = src[q];
+            for (int q = lane & ((1 << lpt) - 1); q < 16; q += 1 << lpt) slot[q] = src[q];
         }
         __syncwarp();
         if (valid) {
@@ -1993,11 +1992,11 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
                 int m;
                 if constexpr (EVEN)
                     m = nn <= 32 ? l2_build_even<uint32_t>(tt, rec, slot, a, mmax, out, h, mine)
-                                 : l2_build_even<unsigned long long>(tt, rec, slot, a, mmax, out,
+                                 : l2_build_even<unsigned long long>(tt, rec, rec->rows, a, mmax, out,
                                                                      h, mine);
                 else
                     m = nn <= 32 ? l2_build_lbl<uint32_t>(tt, rec, slot, a, mmax, out, h, mine)
-                                 : l2_build_lbl<unsigned long long>(tt, rec, slot, a, mmax, out,
+                                 : l2_build_lbl<unsigned long long>(tt, rec, rec->rows, a, mmax, out,
                                                                     h, mine);
                 if (m < 0) {
                     oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << SLICE_SHIFT);
@@ -2156,10 +2155,9 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
         const uint32_t i = i0 + (j >> 2), a1 = j & 3u;
         const uint32_t t = valid ? list1[i] : 0u;
         const TileRec *rec = recs + t;
-        if (valid) {
+        if (valid && rec->nnodes <= 32) {  // 256 bytes of uint2 rows
             const uint4 *src = rec->rows;
-            const int nq = rec->nnodes <= 32 ? 16 : 64;
-            for (int q = lane & 3; q < nq; q += 4) slot[q] = src[q];
+            for (int q = lane & 3; q < 16; q += 4) slot[q] = src[q];
         }
         __syncwarp();
         if (valid) {
@@ -2177,8 +2175,8 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
                     nn <= 32
                         ? (pk ? l15_build<uint32_t, true>(tt, rec, slot, a1, out, h, mine)
                               : l15_build<uint32_t, false>(tt, rec, slot, a1, out, h, mine))
-                        : (pk ? l15_build<unsigned long long, true>(tt, rec, slot, a1, out, h, mine)
-                              : l15_build<unsigned long long, false>(tt, rec, slot, a1, out, h,
+                        : (pk ? l15_build<unsigned long long, true>(tt, rec, rec->rows, a1, out, h, mine)
+                              : l15_build<unsigned long long, false>(tt, rec, rec->rows, a1, out, h,
                                                                      mine));
                 if (m < 0) {
                     atomicOr(fail, 1u);

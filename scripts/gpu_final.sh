@@ -9,5 +9,5 @@ timeout 400 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpur
 cat gpurun_out/bench_ref.json
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
 $CMD > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-$CMD > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k "regex:k_super_build|k_tile_from_super|k_tile_dedup|k_l2_build|k_l2_dedup|k_l2_classify" -s 6 -c 6 -o gpurun_out/prof_${TAG} -f $CMD > gpurun_out/ncu_full.log 2>&1
+$CMD > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k "regex:k_super_build|k_tile_from_super|k_tile_dedup|k_l15_build|k_l2_from_l15|k_l2_dedup|k_l2_classify" -s 8 -c 8 -o gpurun_out/prof_${TAG} -f $CMD > gpurun_out/ncu_full.log 2>&1
 tail -1 gpurun_out/ncu_full.log

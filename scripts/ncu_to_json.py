@@ -13,6 +13,8 @@ NAMES = {  # ncu kernel name prefix -> bench.py kernel label
     "k_super_build<4, 0>": "k_super_build<K=4,raw>",
     "k_tile_dedup": "k_tile_dedup",
     "k_l2_build": "k_l2_build",
+    "k_l15_build": "k_l15_build",
+    "k_l2_from_l15": "k_l2_from_l15 (+ k_l2_build)",
     "k_l2_dedup": "k_l2_dedup",
     "k_l2_classify": "k_l2_classify",
     "k_tile_classify<4, 0, 0>": "k_tile_classify<K=4,odd,raw>",
@@ -31,6 +33,8 @@ def main(path, launch, source):
         name = d["Kernel Name"].replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
         name = name.replace("void ", "")
         label = next((v for k, v in NAMES.items() if name.startswith(k)), None)
+        if label == "k_l2_dedup" and "k_l2_dedup (stage 1)" not in out:
+            label = "k_l2_dedup (stage 1)"  # the first dedup of a step is stage 1's
         if label is None or label in out:
             continue
         f = lambda k: float(d[k].replace(",", "")) if d.get(k) else None  # noqa: E731
