@@ -808,6 +808,7 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     int ts, nA2;
     uint32_t fa1, fa2;                      // free-node masks of A1 / A2 nodes
     int8_t l15F[MAXF];                      // free node -> F index (or -1)
+    uint16_t l15lut[4][256];                // byte b of a free mask -> its F bits
     uint32_t a2sign[4];                     // A2-node signs (A2 index space) per A2 pattern
     uint32_t a2adjA2[8], a2linkA2[8];       // A2-A2 adjacency / links (A2 space)
     uint32_t a2adjB[8], a2linkB[8];         // A2-B adjacency / links (B space)
@@ -2027,9 +2028,8 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
 constexpr int L15_MAXM = L2B_CS;  // stage-1 super-nodes (cs bit 31 is the self flag)
 
 __device__ __forceinline__ unsigned long long l15_compress(const TileTables &tt, uint32_t fm) {
-    unsigned long long r = 0;
-    for (; fm; fm &= fm - 1u) r |= 1ull << tt.l15F[__ffs(fm) - 1];
-    return r;
+    return (unsigned long long)(tt.l15lut[0][fm & 0xffu] | tt.l15lut[1][(fm >> 8) & 0xffu] |
+                                tt.l15lut[2][(fm >> 16) & 0xffu] | tt.l15lut[3][fm >> 24]);
 }
 
 template <typename MT, bool PACK>
@@ -3305,7 +3305,7 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
         const uint32_t fa1 = (uint32_t)(T.fcopy[5] | T.fcopy[6]);
         const uint32_t fa2 = T.la == 4 ? (uint32_t)(T.fcopy[7] | T.fcopy[8]) : 0u;
         const int nA2 = __builtin_popcount(fa2);
-        if (!T.l2even && T.la == 4 && nA2 > 0 && nA2 <= 8 && nB + nA2 <= 20) {
+        if (!T.l2even && T.la == 4 && nA2 > 0 && nA2 <= 8 && nB + nA2 <= 16) {
             T.fa1 = fa1;
             T.fa2 = fa2;
             T.nA2 = nA2;
@@ -3320,6 +3320,15 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
                     ++k;
                 }
             }
+            for (int byte = 0; byte < 4; ++byte)
+                for (int v = 0; v < 256; ++v) {
+                    uint32_t r = 0;
+                    for (int bit = 0; bit < 8; ++bit) {
+                        const int f = 8 * byte + bit;
+                        if (((v >> bit) & 1) && f < MAXF && T.l15F[f] >= 0) r |= 1u << T.l15F[f];
+                    }
+                    T.l15lut[byte][v] = (uint16_t)r;
+                }
             auto compA2 = [&](unsigned long long x) {
                 uint32_t r = 0;
                 for (int f = 0; f < nf; ++f)
