@@ -808,7 +808,6 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     int ts, nA2;
     uint32_t fa1, fa2;                      // free-node masks of A1 / A2 nodes
     int8_t l15F[MAXF];                      // free node -> F index (or -1)
-    uint16_t l15lut[4][256];                // byte b of a free mask -> its F bits
     uint32_t a2sign[4];                     // A2-node signs (A2 index space) per A2 pattern
     uint32_t a2adjA2[8], a2linkA2[8];       // A2-A2 adjacency / links (A2 space)
     uint32_t a2adjB[8], a2linkB[8];         // A2-B adjacency / links (B space)
@@ -2027,13 +2026,19 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
 // redoes the batch on the direct path.
 constexpr int L15_MAXM = L2B_CS;  // stage-1 super-nodes (cs bit 31 is the self flag)
 
-__device__ __forceinline__ unsigned long long l15_compress(const TileTables &tt, uint32_t fm) {
-    return (unsigned long long)(tt.l15lut[0][fm & 0xffu] | tt.l15lut[1][(fm >> 8) & 0xffu] |
-                                tt.l15lut[2][(fm >> 16) & 0xffu] | tt.l15lut[3][fm >> 24]);
+// F-space compression by byte lookup tables (k_l15_build stages them in shared memory)
+struct L15Lut {
+    uint16_t b[4][256];  // byte k of a free-node mask -> its F bits
+};
+
+__device__ __forceinline__ unsigned long long l15_compress(const L15Lut &L, uint32_t fm) {
+    return (unsigned long long)(L.b[0][fm & 0xffu] | L.b[1][(fm >> 8) & 0xffu] |
+                                L.b[2][(fm >> 16) & 0xffu] | L.b[3][fm >> 24]);
 }
 
 template <typename MT, bool PACK>
-__device__ __forceinline__ int l15_build(const TileTables &tt, const TileRec *__restrict__ rec,
+__device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut,
+                                         const TileRec *__restrict__ rec,
                                          const uint4 *__restrict__ R4, uint32_t a1,
                                          unsigned long long *out, unsigned long long &hout,
                                          uint32_t *mine) {
@@ -2090,9 +2095,9 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const TileRec *__
         const uint32_t self = (cg & M) != (MT)0;
         cs[m * THREADS] = c | self << 31;
         for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
-        const unsigned long long w1 = l15_compress(tt, (uint32_t)(pb >> n)) |
-                                      l15_compress(tt, (uint32_t)(mb >> n)) << nF |
-                                      l15_compress(tt, (uint32_t)(lk >> n)) << (2 * nF);
+        const unsigned long long w1 = l15_compress(lut, (uint32_t)(pb >> n)) |
+                                      l15_compress(lut, (uint32_t)(mb >> n)) << nF |
+                                      l15_compress(lut, (uint32_t)(lk >> n)) << (2 * nF);
         if (PACK) {  // low half now; the high half (w1 >> 32, cs, self) at the end
             reinterpret_cast<uint32_t *>(out)[2 * (1 + m)] = (uint32_t)w1;
             cs[m * THREADS] |= (uint32_t)(w1 >> 32) << 24;  // <= 7 bits: 3 nF <= 39
@@ -2135,12 +2140,16 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
                                                        uint32_t *__restrict__ poss,
                                                        uint32_t *__restrict__ oldlist,
                                                        uint32_t *__restrict__ oldcount,
-                                                       uint32_t *__restrict__ fail) {
+                                                       uint32_t *__restrict__ fail,
+                                                       const L15Lut *__restrict__ lut_g) {
     __shared__ TileTables tts;
+    __shared__ L15Lut luts;
     extern __shared__ __align__(16) uint32_t l2smem[];
     uint32_t *mine = l2smem + threadIdx.x;
     for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
         reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
+    for (int i = threadIdx.x; i < (int)(sizeof(L15Lut) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t *>(&luts)[i] = reinterpret_cast<const uint32_t *>(lut_g)[i];
     __syncthreads();
     const TileTables &tt = tts;
     const int bits = tt.bits;
@@ -2173,10 +2182,10 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
                 const bool pk = nF >= 11 && nF <= 13;  // one word per super-node
                 const int m =
                     nn <= 32
-                        ? (pk ? l15_build<uint32_t, true>(tt, rec, slot, a1, out, h, mine)
-                              : l15_build<uint32_t, false>(tt, rec, slot, a1, out, h, mine))
-                        : (pk ? l15_build<unsigned long long, true>(tt, rec, rec->rows, a1, out, h, mine)
-                              : l15_build<unsigned long long, false>(tt, rec, rec->rows, a1, out, h,
+                        ? (pk ? l15_build<uint32_t, true>(tt, luts, rec, slot, a1, out, h, mine)
+                              : l15_build<uint32_t, false>(tt, luts, rec, slot, a1, out, h, mine))
+                        : (pk ? l15_build<unsigned long long, true>(tt, luts, rec, rec->rows, a1, out, h, mine)
+                              : l15_build<unsigned long long, false>(tt, luts, rec, rec->rows, a1, out, h,
                                                                      mine));
                 if (m < 0) {
                     atomicOr(fail, 1u);
@@ -2972,6 +2981,7 @@ struct tcg_plan {
     int64_t launches = 0;
     // tile contraction (sweeps): per domain (raw, representative)
     TileTables *d_tiles = nullptr;   // [2]
+    L15Lut *d_lut = nullptr;         // [2] stage-1 F-space tables
     TileRec *d_recs = nullptr;       // [chunk_cap]
     uint32_t chunk_cap = 0;          // tiles the record / dedup buffers hold
     uint32_t *d_dedup = nullptr;     // slots[2 pow2(C)] | mint[C] | dup[C] | count[1] | list[C]
@@ -3320,15 +3330,6 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
                     ++k;
                 }
             }
-            for (int byte = 0; byte < 4; ++byte)
-                for (int v = 0; v < 256; ++v) {
-                    uint32_t r = 0;
-                    for (int bit = 0; bit < 8; ++bit) {
-                        const int f = 8 * byte + bit;
-                        if (((v >> bit) & 1) && f < MAXF && T.l15F[f] >= 0) r |= 1u << T.l15F[f];
-                    }
-                    T.l15lut[byte][v] = (uint16_t)r;
-                }
             auto compA2 = [&](unsigned long long x) {
                 uint32_t r = 0;
                 for (int f = 0; f < nf; ++f)
@@ -3600,6 +3601,20 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
         }
         if ((e = cudaMalloc(&P->d_tiles, sizeof(tt))) != cudaSuccess) return bail(e, "malloc tiles");
         cudaMemcpy(P->d_tiles, tt, sizeof(tt), cudaMemcpyHostToDevice);
+        L15Lut luts[2];
+        for (int m = 0; m < 2; ++m)
+            for (int byte = 0; byte < 4; ++byte)
+                for (int v = 0; v < 256; ++v) {
+                    uint32_t r = 0;
+                    for (int bit = 0; bit < 8; ++bit) {
+                        const int f = 8 * byte + bit;
+                        if (((v >> bit) & 1) && f < MAXF && tt[m].ts && tt[m].l15F[f] >= 0)
+                            r |= 1u << tt[m].l15F[f];
+                    }
+                    luts[m].b[byte][v] = (uint16_t)r;
+                }
+        if ((e = cudaMalloc(&P->d_lut, sizeof(luts))) != cudaSuccess) return bail(e, "malloc lut");
+        cudaMemcpy(P->d_lut, luts, sizeof(luts), cudaMemcpyHostToDevice);
     }
     DevAgg &g = P->agg;
     if ((e = cudaMalloc(&g.keys, GCAP * 8)) != cudaSuccess) return bail(e, "malloc agg");
@@ -3706,7 +3721,7 @@ int tcg_plan_destroy(tcg_plan *P) {
     DeviceGuard guard(P->device);
     if (P->stream) cudaStreamSynchronize(P->stream);
     timing_resolve(P);
-    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_l2slots, P->d_l15pool, P->d_l15hash, P->d_l15slots, P->d_l15u32, P->d_oldlist, P->d_ovf, P->d_super, P->d_hash, P->d_slots, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
+    void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_lut, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_l2slots, P->d_l15pool, P->d_l15hash, P->d_l15slots, P->d_l15u32, P->d_oldlist, P->d_ovf, P->d_super, P->d_hash, P->d_slots, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
     for (void *p : ptrs)
@@ -3968,8 +3983,9 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     uint64_t t0 = tile0, a = lo, b = hi;
     uint32_t i0v = i0, nbv = nb, s1 = stride1;
     const unsigned g1 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8, (nrec1 + THREADS - 1) / THREADS);
+    const L15Lut *lutp = P->d_lut + mode;
     void *ab[] = {&tt, &recs, &list1, &dup1, &mint1, &i0v, &nbv, &t0, &a, &b, &pool1, &s1,
-                  &hash1, &wts1, &poss1, &oldlist, &oldcount, &failp};
+                  &hash1, &wts1, &poss1, &oldlist, &oldcount, &failp, &lutp};
     const size_t smem1 = (size_t)L2B_WORDS * 4 * THREADS + (size_t)(THREADS / 32) * 8 * L2B_SLOT;
     cudaEvent_t e0 = timing_begin(P);
     if (!cuda_ok(cudaLaunchKernel((void *)k_l15_build, dim3(g1), dim3(THREADS), ab, smem1, st), "l15 build"))
