@@ -808,7 +808,8 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     int ts, nA2;
     uint32_t fa1, fa2;                      // free-node masks of A1 / A2 nodes
     int8_t l15F[MAXF];                      // free node -> F index (or -1)
-    uint32_t a2sign[4];                     // A2-node signs (A2 index space) per A2 pattern
+    uint32_t a2sign[8];                     // A2-node signs (A2 index space) per A2 pattern
+    int la2;                                // A2 bits (tile bits 7 .. 7+la2-1): la - 2
     uint32_t a2adjA2[8], a2linkA2[8];       // A2-A2 adjacency / links (A2 space)
     uint32_t a2adjB[8], a2linkB[8];         // A2-B adjacency / links (B space)
     uint32_t fa, fbm;                       // free-node masks of A and B nodes
@@ -2028,7 +2029,7 @@ constexpr int L15_MAXM = L2B_CS;  // stage-1 super-nodes (cs bit 31 is the self 
 
 // F-space compression by byte lookup tables (k_l15_build stages them in shared memory)
 struct L15Lut {
-    uint16_t b[4][256];  // byte k of a free-node mask -> its F bits
+    uint32_t b[4][256];  // byte k of a free-node mask -> its F bits
 };
 
 __device__ __forceinline__ unsigned long long l15_compress(const L15Lut &L, uint32_t fm) {
@@ -2228,7 +2229,8 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
     const uint32_t bm = (1u << nB) - 1u, a2m = (1u << nA2) - 1u;
     const unsigned long long fm = (1ull << nF) - 1ull;
     const int mmax = min(32 - nB, L2B_CS);
-    const uint32_t nrec = *count15 << 2;
+    const int la2 = tt.la2;
+    const uint32_t nrec = *count15 << la2;
     const bool pk = nF >= 11 && nF <= 13;  // stage-1 records packed one word per super-node
     // stage-1 super-node s: w1 = F relations, w0 = cs | self << 31
     auto rw1 = [&](const unsigned long long *r1, int s2) -> unsigned long long {
@@ -2241,7 +2243,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
     };
     auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nrec; j += gridDim.x * blockDim.x) {
-        const uint32_t j1 = list15[j >> 2], a2 = j & 3u;
+        const uint32_t j1 = list15[j >> la2], a2 = j & ((1u << la2) - 1u);
         const unsigned long long *r1 = pool1 + (size_t)j1 * stride1;
         const int m1 = (int)r1[0];
         const uint32_t SA2 = tt.a2sign[a2];
@@ -2327,7 +2329,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
         hashes[j] = mix64(((unsigned long long)hh << 32 | hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
         wts[j] = w15[j1];
         const uint32_t p1 = pos15[j1];
-        poss[j] = ((p1 >> 2) << 4) | (a2 << 2) | (p1 & 3u);
+        poss[j] = ((p1 >> 2) << (2 + la2)) | (a2 << 2) | (p1 & 3u);
     }
 }
 
@@ -3313,9 +3315,11 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
         // two-stage tables
         T.ts = 0;
         const uint32_t fa1 = (uint32_t)(T.fcopy[5] | T.fcopy[6]);
-        const uint32_t fa2 = T.la == 4 ? (uint32_t)(T.fcopy[7] | T.fcopy[8]) : 0u;
+        uint32_t fa2 = 0;
+        for (int i = 7; i < bits; ++i) fa2 |= (uint32_t)T.fcopy[i];
         const int nA2 = __builtin_popcount(fa2);
-        if (!T.l2even && T.la == 4 && nA2 > 0 && nA2 <= 8 && nB + nA2 <= 16) {
+        if (!T.l2even && (T.la == 4 || T.la == 5) && nA2 > 0 && nA2 <= 8 && nB + nA2 <= 21) {
+            T.la2 = T.la - 2;
             T.fa1 = fa1;
             T.fa2 = fa2;
             T.nA2 = nA2;
@@ -3343,7 +3347,7 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
                 T.a2adjB[q] = comp(T.fadj[f] & fb);
                 T.a2linkB[q] = comp(T.fpl[f] & fb);
             }
-            for (int x = 0; x < 4; ++x) {  // tile-local index x << 7 (bits 7, 8)
+            for (int x = 0; x < (1 << T.la2); ++x) {  // tile-local index x << 7 (A2 bits)
                 const uint32_t low = (uint32_t)x << 7;
                 T.a2sign[x] = compA2((T.fsign[0][low & 63u] ^ T.fsign[1][(low >> 6) & 63u]) & fa2);
             }
@@ -3405,12 +3409,13 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
 // word: at most 16 free vertices (d=7 raw: 2^8 indices, the j-axis).
 // Degree 8-9 graphs exceed 32 nodes anyway, so they take 2^10.
 // TCG_TILE_BITS overrides.
-// Odd degrees up to 7 run level 2 (which also takes 33..64-node tiles), so
-// they allow 18 free vertices: d=7 raw tiles are 2^9 indices (measured on
-// C3: 1.78e11 vs 1.59e11 patchworks/s at 2^8 and 1.63e11 at 2^10).
+// Odd degrees up to 7 run the two-stage level 2 (which also takes 33..64-node
+// tiles), so they allow 21 free vertices: d=7 raw tiles are 2^10 indices
+// (measured on C3: 5.08e11 vs 3.49e11 patchworks/s at 2^9; with the direct
+// level 2, 2^9 had been best).
 bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
     int want = D->degree >= 8 ? 10 : 12;
-    int fmax = D->degree >= 8 ? 28 : (D->degree % 2 ? 18 : 16);
+    int fmax = D->degree >= 8 ? 28 : (D->degree % 2 ? 21 : 16);
     if (const char *e = std::getenv("TCG_TILE_BITS")) {
         want = std::atoi(e);
         fmax = 28;
@@ -3611,7 +3616,7 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
                         if (((v >> bit) & 1) && f < MAXF && tt[m].ts && tt[m].l15F[f] >= 0)
                             r |= 1u << tt[m].l15F[f];
                     }
-                    luts[m].b[byte][v] = (uint16_t)r;
+                    luts[m].b[byte][v] = r;
                 }
         if ((e = cudaMalloc(&P->d_lut, sizeof(luts))) != cudaSuccess) return bail(e, "malloc lut");
         cudaMemcpy(P->d_lut, luts, sizeof(luts), cudaMemcpyHostToDevice);
@@ -4012,9 +4017,9 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
         cuda_ok(cudaMemcpyAsync(P->d_oldlist, saved, 4, cudaMemcpyDeviceToDevice, st), "restore");
         return false;
     };
-    if (hostv[1] || (size_t)n15 * 4 > cap) return fallback();
+    if (hostv[1] || ((size_t)n15 << T.la2) > cap) return fallback();
     // stage 2 into the ordinary level-2 buffers
-    const uint32_t nrec = n15 << 2;
+    const uint32_t nrec = n15 << T.la2;
     uint32_t *wts = P->d_l2u32, *poss = wts + cap;
     unsigned long long *pool = P->d_l2pool, *hashes = P->d_l2hash;
     const unsigned g2 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8, (nrec + THREADS - 1) / THREADS);
