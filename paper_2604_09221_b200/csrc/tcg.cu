@@ -782,9 +782,10 @@ constexpr int TILE_BITS_MAX = 12;
 constexpr int MAXC = 48;  // fixed components per tile
 constexpr int MAXF = 32;  // free vertices
 constexpr int MAXM = 24;  // mid vertices of a super-tile
-// level-1 list entries for a single A slice: tile | (a + 1) << SLICE_SHIFT
-// (tile ids < 2^26 >= chunk_tiles(), a < 2^5)
-constexpr int SLICE_SHIFT = 26;
+// level-1 list entries for a single A slice: tile | (a + 1) << slice_shift(la)
+// (a + 1 <= 2^la takes la + 1 bits; tile ids < 2^(31 - la), which the chunk
+// size guarantees: <= 2^34 indices = 2^(29 - la) tiles)
+__host__ __device__ constexpr int slice_shift(int la) { return 31 - la; }
 constexpr int SUPER_BITS_MAX = 6;
 
 struct alignas(16) TileTables {  // per plan and domain (raw / representative), device memory
@@ -808,10 +809,10 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     int ts, nA2;
     uint32_t fa1, fa2;                      // free-node masks of A1 / A2 nodes
     int8_t l15F[MAXF];                      // free node -> F index (or -1)
-    uint32_t a2sign[8];                     // A2-node signs (A2 index space) per A2 pattern
+    uint32_t a2sign[16];                    // A2-node signs (A2 index space) per A2 pattern
     int la2;                                // A2 bits (tile bits 7 .. 7+la2-1): la - 2
-    uint32_t a2adjA2[8], a2linkA2[8];       // A2-A2 adjacency / links (A2 space)
-    uint32_t a2adjB[8], a2linkB[8];         // A2-B adjacency / links (B space)
+    uint32_t a2adjA2[16], a2linkA2[16];     // A2-A2 adjacency / links (A2 space)
+    uint32_t a2adjB[16], a2linkB[16];       // A2-B adjacency / links (B space)
     uint32_t fa, fbm;                       // free-node masks of A and B nodes
     int8_t l2j[MAXF];                       // free node -> B index (or -1)
     uint32_t l2adjB[16], l2linkB[16];       // B-B adjacency / links (B index space)
@@ -1641,7 +1642,8 @@ __global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
         // list entries: tile, or tile | (a + 1) << 24 for the 32-index slice of
         // A pattern a only (a slice the level-2 path could not take)
         const uint32_t e = list ? list[i] : i;
-        const uint32_t t = e & ((1u << SLICE_SHIFT) - 1u), sub = e >> SLICE_SHIFT;
+        const int ssh = slice_shift(tt->la);
+        const uint32_t t = e & ((1u << ssh) - 1u), sub = e >> ssh;
         const uint32_t lo0 = sub ? (sub - 1u) << 5 : 0u, lo1 = sub ? lo0 + 32u : tsize;
         const uint32_t weight = list ? 1u + dup[t] : 1u;
         const uint32_t tw = list ? min(t, mint[t]) : t;
@@ -2000,7 +2002,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
                                  : l2_build_lbl<unsigned long long>(tt, rec, rec->rows, a, mmax, out,
                                                                     h, mine);
                 if (m < 0) {
-                    oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << SLICE_SHIFT);
+                    oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << slice_shift(la));
                     wts[j] = 0u;
                 } else {
                     hashes[j] = h;
@@ -2248,7 +2250,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
         const int m1 = (int)r1[0];
         const uint32_t SA2 = tt.a2sign[a2];
         // A2 rows toward the stage-1 super-nodes (same-sign or linked / crossed)
-        uint32_t sameA[8], crossA[8];
+        uint32_t sameA[16], crossA[16];
         for (int k = 0; k < nA2; ++k) sameA[k] = crossA[k] = 0u;
         for (int s = 0; s < m1; ++s) {
             const unsigned long long w1 = rw1(r1, s);
@@ -2259,6 +2261,11 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
             for (uint32_t y = cross; y; y &= y - 1u) crossA[__ffs(y) - 1] |= 1u << s;
         }
         const int nn = m1 + nA2;
+        if (nn > 32) {  // 32-bit node masks: the host redoes the batch directly
+            atomicOr(fail, 1u);
+            wts[j] = 0u;
+            continue;
+        }
         const uint32_t G = nn >= 32 ? ~0u : ((1u << nn) - 1u);
         uint32_t unv = G, done = 0, hh = 0x9E3779B9u;
         unsigned long long *out = pool + (size_t)j * stride;
@@ -3279,7 +3286,7 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
     // level-2 tables (filled after fadj / fpl below)
     auto l2_tables = [&]() {
         T.l2 = 0;
-        if (bits < 6 || bits > 10 || nf > 32) return;
+        if (bits < 6 || bits > 11 || nf > 32) return;
         T.l2even = d % 2 == 0;
         uint32_t fb = 0, fa = 0;
         for (int i = 0; i < bits; ++i) (i < 5 ? fb : fa) |= (uint32_t)T.fcopy[i];
@@ -3318,12 +3325,12 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
         uint32_t fa2 = 0;
         for (int i = 7; i < bits; ++i) fa2 |= (uint32_t)T.fcopy[i];
         const int nA2 = __builtin_popcount(fa2);
-        if (!T.l2even && (T.la == 4 || T.la == 5) && nA2 > 0 && nA2 <= 8 && nB + nA2 <= 21) {
+        if (!T.l2even && T.la >= 4 && T.la <= 6 && nA2 > 0 && nA2 <= 16 && nB + nA2 <= 21) {
             T.la2 = T.la - 2;
             T.fa1 = fa1;
             T.fa2 = fa2;
             T.nA2 = nA2;
-            int a2j[MAXF], a2f[8], k = 0;
+            int a2j[MAXF], a2f[16], k = 0;
             for (int f = 0; f < MAXF; ++f) { T.l15F[f] = -1; a2j[f] = -1; }
             for (int f = 0; f < nf; ++f) {
                 if (T.l2j[f] >= 0) T.l15F[f] = T.l2j[f];
@@ -3410,12 +3417,12 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
 // Degree 8-9 graphs exceed 32 nodes anyway, so they take 2^10.
 // TCG_TILE_BITS overrides.
 // Odd degrees up to 7 run the two-stage level 2 (which also takes 33..64-node
-// tiles), so they allow 21 free vertices: d=7 raw tiles are 2^10 indices
-// (measured on C3: 5.08e11 vs 3.49e11 patchworks/s at 2^9; with the direct
-// level 2, 2^9 had been best).
+// tiles), so they allow 25 free vertices: d=7 raw tiles are 2^11 indices
+// (measured on C3: 7.0e11 vs 5.07e11 patchworks/s at 2^10 and 3.49e11 at 2^9;
+// with the direct level 2, 2^9 had been best).
 bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
     int want = D->degree >= 8 ? 10 : 12;
-    int fmax = D->degree >= 8 ? 28 : (D->degree % 2 ? 21 : 16);
+    int fmax = D->degree >= 8 ? 28 : (D->degree % 2 ? 25 : 16);
     if (const char *e = std::getenv("TCG_TILE_BITS")) {
         want = std::atoi(e);
         fmax = 28;
