@@ -810,7 +810,7 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     uint32_t fa1, fa2;                      // free-node masks of A1 / A2 nodes
     int8_t l15F[MAXF];                      // free node -> F index (or -1)
     uint32_t a2sign[16];                    // A2-node signs (A2 index space) per A2 pattern
-    int la2;                                // A2 bits (tile bits 7 .. 7+la2-1): la - 2
+    int la1, la2;                           // A1 = tile bits 5 .. 4+la1, A2 = the la2 = la - la1 above
     uint32_t a2adjA2[16], a2linkA2[16];     // A2-A2 adjacency / links (A2 space)
     uint32_t a2adjB[16], a2linkB[16];       // A2-B adjacency / links (B space)
     uint32_t fa, fbm;                       // free-node masks of A and B nodes
@@ -2156,20 +2156,21 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
     __syncthreads();
     const TileTables &tt = tts;
     const int bits = tt.bits;
-    const uint32_t nrec = nb << 2;
+    const int la1 = tt.la1;
+    const uint32_t nrec = nb << la1;
     const int lane = threadIdx.x & 31;
     uint4 *slot = reinterpret_cast<uint4 *>(l2smem + L2B_WORDS * THREADS) +
-                  (L2B_SLOT / 16) * ((threadIdx.x >> 5) * 8 + (lane >> 2));
+                  (L2B_SLOT / 16) * ((threadIdx.x >> 5) * (32 >> tt.la1) + (lane >> tt.la1));
     for (uint32_t jb = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); jb < nrec;
          jb += gridDim.x * blockDim.x) {  // warp-uniform
         const uint32_t j = jb + lane;
         const bool valid = j < nrec;
-        const uint32_t i = i0 + (j >> 2), a1 = j & 3u;
+        const uint32_t i = i0 + (j >> la1), a1 = j & ((1u << la1) - 1u);
         const uint32_t t = valid ? list1[i] : 0u;
         const TileRec *rec = recs + t;
         if (valid && rec->nnodes <= 32) {  // 256 bytes of uint2 rows
             const uint4 *src = rec->rows;
-            for (int q = lane & 3; q < 16; q += 4) slot[q] = src[q];
+            for (int q = lane & ((1 << la1) - 1); q < 16; q += 1 << la1) slot[q] = src[q];
         }
         __syncwarp();
         if (valid) {
@@ -2196,7 +2197,7 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
                 } else {
                     hashes[j] = h;
                     wts[j] = 1u + dup1[t];
-                    poss[j] = (min(t, mint1[t]) << 2) | a1;
+                    poss[j] = (min(t, mint1[t]) << la1) | a1;
                 }
             }
         }
@@ -2336,7 +2337,8 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
         hashes[j] = mix64(((unsigned long long)hh << 32 | hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
         wts[j] = w15[j1];
         const uint32_t p1 = pos15[j1];
-        poss[j] = ((p1 >> 2) << (2 + la2)) | (a2 << 2) | (p1 & 3u);
+        const int la1 = tt.la1;
+        poss[j] = ((p1 >> la1) << (la1 + la2)) | (a2 << la1) | (p1 & ((1u << la1) - 1u));
     }
 }
 
@@ -3286,7 +3288,7 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
     // level-2 tables (filled after fadj / fpl below)
     auto l2_tables = [&]() {
         T.l2 = 0;
-        if (bits < 6 || bits > 11 || nf > 32) return;
+        if (bits < 6 || bits > 12 || nf > 32) return;
         T.l2even = d % 2 == 0;
         uint32_t fb = 0, fa = 0;
         for (int i = 0; i < bits; ++i) (i < 5 ? fb : fa) |= (uint32_t)T.fcopy[i];
@@ -3321,12 +3323,20 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
         T.l2 = 1;
         // two-stage tables
         T.ts = 0;
-        const uint32_t fa1 = (uint32_t)(T.fcopy[5] | T.fcopy[6]);
-        uint32_t fa2 = 0;
-        for (int i = 7; i < bits; ++i) fa2 |= (uint32_t)T.fcopy[i];
-        const int nA2 = __builtin_popcount(fa2);
-        if (!T.l2even && T.la >= 4 && T.la <= 6 && nA2 > 0 && nA2 <= 16 && nB + nA2 <= 21) {
-            T.la2 = T.la - 2;
+        // A1 = the fewest low A bits (>= 2) that leave an F space of <= 21 nodes
+        int la1 = 2;
+        uint32_t fa1 = 0, fa2 = 0;
+        int nA2 = 0;
+        for (; la1 <= T.la - 1; ++la1) {
+            fa1 = fa2 = 0;
+            for (int i = 5; i < bits; ++i) (i < 5 + la1 ? fa1 : fa2) |= (uint32_t)T.fcopy[i];
+            nA2 = __builtin_popcount(fa2);
+            if (nA2 <= 16 && nB + nA2 <= 21) break;
+        }
+        if (!T.l2even && T.la >= 4 && la1 <= 4 && la1 < T.la && nA2 > 0 && nA2 <= 16 &&
+            nB + nA2 <= 21) {
+            T.la1 = la1;
+            T.la2 = T.la - la1;
             T.fa1 = fa1;
             T.fa2 = fa2;
             T.nA2 = nA2;
@@ -3354,8 +3364,8 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
                 T.a2adjB[q] = comp(T.fadj[f] & fb);
                 T.a2linkB[q] = comp(T.fpl[f] & fb);
             }
-            for (int x = 0; x < (1 << T.la2); ++x) {  // tile-local index x << 7 (A2 bits)
-                const uint32_t low = (uint32_t)x << 7;
+            for (int x = 0; x < (1 << T.la2); ++x) {  // tile-local index of the A2 bits
+                const uint32_t low = (uint32_t)x << (5 + la1);
                 T.a2sign[x] = compA2((T.fsign[0][low & 63u] ^ T.fsign[1][(low >> 6) & 63u]) & fa2);
             }
             T.ts = 1;
@@ -3417,15 +3427,15 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
 // Degree 8-9 graphs exceed 32 nodes anyway, so they take 2^10.
 // TCG_TILE_BITS overrides.
 // Odd degrees up to 7 run the two-stage level 2 (which also takes 33..64-node
-// tiles), so they allow 25 free vertices: d=7 raw tiles are 2^11 indices
-// (measured on C3: 7.0e11 vs 5.07e11 patchworks/s at 2^10 and 3.49e11 at 2^9;
-// with the direct level 2, 2^9 had been best).
+// tiles), so they allow 29 free vertices: d=7 raw tiles are 2^12 indices
+// (measured on C3: 7.48e11 patchworks/s vs 7.11e11 at 2^11, 5.07e11 at 2^10,
+// 3.49e11 at 2^9; with the direct level 2, 2^9 had been best).
 bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
     int want = D->degree >= 8 ? 10 : 12;
-    int fmax = D->degree >= 8 ? 28 : (D->degree % 2 ? 25 : 16);
+    int fmax = D->degree >= 8 ? 28 : (D->degree % 2 ? 29 : 16);
     if (const char *e = std::getenv("TCG_TILE_BITS")) {
         want = std::atoi(e);
-        fmax = 28;
+        fmax = MAXF;
     }
     for (int bits = std::min(want, TILE_BITS_MAX); bits >= 6; --bits)
         if (build_tiles_bits(D, L, mode, bits, T) && T.nf <= fmax) return true;
@@ -3947,7 +3957,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     const TileTables &T = P->h_tiles[mode];
     const bool pk = T.nB + T.nA2 >= 11 && T.nB + T.nA2 <= 13;  // one word per super-node
     const uint32_t stride1 = (uint32_t)(1 + (pk ? 1 : 2) * L15_MAXM);
-    const uint32_t nrec1 = nb << 2;
+    const uint32_t nrec1 = nb << T.la1;
     auto cuda_ok = [&](cudaError_t e, const char *what) {
         if (e != cudaSuccess) rc = fail(TCG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
         return e == cudaSuccess;
@@ -3959,7 +3969,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
         const size_t per = (size_t)stride1 * 8 + 8 + 4 * 6 + 16;
         fr += P->l15_cap * per;
         if ((size_t)nrec1 * per > fr / 2) return false;  // no room: direct path
-        const size_t c1 = std::max<size_t>(nrec1, (P->chunk_cap / 2) << 2);
+        const size_t c1 = std::max<size_t>(nrec1, (P->chunk_cap / 2) << T.la1);
         const size_t c = c1 * per <= fr / 2 ? c1 : nrec1;
         cudaFree(P->d_l15pool);
         cudaFree(P->d_l15hash);
@@ -3998,7 +4008,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     const L15Lut *lutp = P->d_lut + mode;
     void *ab[] = {&tt, &recs, &list1, &dup1, &mint1, &i0v, &nbv, &t0, &a, &b, &pool1, &s1,
                   &hash1, &wts1, &poss1, &oldlist, &oldcount, &failp, &lutp};
-    const size_t smem1 = (size_t)L2B_WORDS * 4 * THREADS + (size_t)(THREADS / 32) * 8 * L2B_SLOT;
+    const size_t smem1 = (size_t)L2B_WORDS * 4 * THREADS + (size_t)(THREADS / 32) * (32 >> T.la1) * L2B_SLOT;
     cudaEvent_t e0 = timing_begin(P);
     if (!cuda_ok(cudaLaunchKernel((void *)k_l15_build, dim3(g1), dim3(THREADS), ab, smem1, st), "l15 build"))
         return false;
