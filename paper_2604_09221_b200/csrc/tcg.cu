@@ -811,6 +811,7 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     int8_t l15F[MAXF];                      // free node -> F index (or -1)
     uint32_t a2sign[16];                    // A2-node signs (A2 index space) per A2 pattern
     int la1, la2;                           // A1 = tile bits 5 .. 4+la1, A2 = the la2 = la - la1 above
+    int l15max;                             // stage-1 super-node budget (TCG_L15_MAXM tests the fallback)
     uint32_t a2adjA2[16], a2linkA2[16];     // A2-A2 adjacency / links (A2 space)
     uint32_t a2adjB[16], a2linkB[16];       // A2-B adjacency / links (B space)
     uint32_t fa, fbm;                       // free-node masks of A and B nodes
@@ -2060,7 +2061,7 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
     int m = 0;
     auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
     while (unv) {
-        if (m == L15_MAXM) return -1;
+        if (m == tt.l15max) return -1;
         MT f = unv & ((MT)0 - unv);
         unv ^= f;
         MT M = f, cg = 0, pb = 0, mb = 0, lk = 0;
@@ -3337,6 +3338,9 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
             nB + nA2 <= 21) {
             T.la1 = la1;
             T.la2 = T.la - la1;
+            T.l15max = L15_MAXM;
+            if (const char *e = std::getenv("TCG_L15_MAXM"))
+                T.l15max = std::max(1, std::min(L15_MAXM, std::atoi(e)));
             T.fa1 = fa1;
             T.fa2 = fa2;
             T.nA2 = nA2;

@@ -475,7 +475,8 @@ def test_super_tile_records_identical_to_direct_contraction():
 
 def test_two_stage_level2_identical_to_direct():
     """Two-stage level-2 records (A1 bits fixed, deduplicated, then A2) give
-    the same reports as building level-2 records directly (TCG_L2_TWOSTAGE=0)."""
+    the same reports as building level-2 records directly (TCG_L2_TWOSTAGE=0),
+    also when a small stage-1 budget sends batches back to the direct build."""
     import json
     import os
     import subprocess
@@ -495,9 +496,10 @@ def test_two_stage_level2_identical_to_direct():
         "    out.append([list(r.oval_histogram), sorted(r.scheme_map.items())])\n"
         "print(json.dumps(out))\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     res = {}
-    for flag in ("0", "1"):
-        env = dict(os.environ, TCG_L2_TWOSTAGE=flag)
+    for flag, extra in (("0", {}), ("1", {}), ("1", {"TCG_L15_MAXM": "6"})):
+        env = dict(os.environ, TCG_L2_TWOSTAGE=flag, **extra)
         p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
         assert p.returncode == 0, p.stderr
-        res[flag] = json.loads(p.stdout.strip().splitlines()[-1])
-    assert res["0"] == res["1"]
+        res[flag + "".join(extra)] = json.loads(p.stdout.strip().splitlines()[-1])
+    # the third run forces stage-1 budget overflows: batches go back to the direct build
+    assert res["0"] == res["1"] == res["1TCG_L15_MAXM"]
