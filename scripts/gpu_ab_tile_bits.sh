@@ -1,3 +1,4 @@
+# A/B: tile sizes (TCG_TILE_BITS) and super-tile sizes on the C3 bench (same binary)
 python -c "import __graft_entry__ as g; g.build()" > /dev/null
 mkdir -p gpurun_out
 for cfg in "TCG_TILE_BITS=11" "TCG_TILE_BITS=12" "TCG_TILE_BITS=12 TCG_SUPER_BITS=5"; do

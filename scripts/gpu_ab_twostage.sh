@@ -1,3 +1,4 @@
+# A/B: two-stage vs direct level 2 (TCG_L2_TWOSTAGE), after the related GPU tests
 python -c "import __graft_entry__ as g; g.build()" > /dev/null
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -x -q -m gpu -k "two_stage or level2 or parity or dedup or super_tile" 2>&1 | tail -3

@@ -1,3 +1,4 @@
+# one ncu launch list + one --set full capture of the sweep kernels (TAG=v23)
 python -c "import __graft_entry__ as g; g.build()" > /dev/null
 mkdir -p gpurun_out
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline"
