@@ -2224,7 +2224,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
     extern __shared__ __align__(16) uint32_t l2smem[];
     uint32_t *mine = l2smem + threadIdx.x;
     uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
-    uint32_t *cs = mine + 16 * THREADS;
+    uint32_t *cs = mine + 16 * THREADS, *hw = cs + L2B_CS * THREADS;
     for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
         reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
     __syncthreads();
@@ -2271,7 +2271,6 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
         const uint32_t G = nn >= 32 ? ~0u : ((1u << nn) - 1u);
         uint32_t unv = G, done = 0, hh = 0x9E3779B9u;
         unsigned long long *out = pool + (size_t)j * stride;
-        uint32_t *out32 = reinterpret_cast<uint32_t *>(out);
         int m = 0;
         bool bad = false;
         while (unv) {
@@ -2315,10 +2314,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
             cs[m * THREADS] = c;
             for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
             const uint32_t self = ((cg & M) != 0u) | selfany;
-            const uint32_t hi = pb | mb << nB | lk << (2 * nB) | self << (3 * nB);
-            out32[2 * (1 + m) + 1] = hi;
-            hh = (hh ^ hi) * 0x85EBCA77u;
-            hh ^= hh >> 13;
+            hw[m * THREADS] = pb | mb << nB | lk << (2 * nB) | self << (3 * nB);
             done |= M;
             ++m;
         }
@@ -2327,11 +2323,32 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
             wts[j] = 0u;
             continue;
         }
+        // canonical order: super-nodes sorted by their B-relation word (stable),
+        // so that equal graphs reached through different node numberings give
+        // equal records (the classification is invariant under relabelling)
+        // rank of super-node q in label slot q, the inverse in slot 32 + rank
+        // (lane-private bytes: slot v at (v >> 2) * 4 * THREADS + (v & 3))
+        auto slot8 = [&](int v) -> uint8_t & { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
+        for (int q = 0; q < m; ++q) {
+            const uint32_t hq = hw[q * THREADS];
+            int r = 0;
+            for (int q2 = 0; q2 < m; ++q2) {
+                const uint32_t h2 = hw[q2 * THREADS];
+                r += (h2 < hq) || (h2 == hq && q2 < q);
+            }
+            slot8(q) = (uint8_t)r;
+            slot8(32 + r) = (uint8_t)q;
+        }
         out[0] = (unsigned long long)m;
         uint32_t hl = 0xC2B2AE3Du;
-        for (int q = 0; q < m; ++q) {
-            const uint32_t c = cs[q * THREADS];
-            out32[2 * (1 + q)] = c;
+        for (int r = 0; r < m; ++r) {
+            const int q = slot8(32 + r);
+            uint32_t c = 0;
+            for (uint32_t y = cs[q * THREADS]; y; y &= y - 1u) c |= 1u << slot8(__ffs(y) - 1);
+            const uint32_t hi = hw[q * THREADS];
+            out[1 + r] = (unsigned long long)c | (unsigned long long)hi << 32;
+            hh = (hh ^ hi) * 0x85EBCA77u;
+            hh ^= hh >> 13;
             hl = (hl ^ c) * 0x9E3779B1u;
             hl ^= hl >> 15;
         }
@@ -4047,7 +4064,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     uint32_t s2 = stride;
     void *a2[] = {&tt, &pool1, &s1, &list15, &count15, &w15, &pos15, &pool, &s2, &hashes, &wts,
                   &poss, &failp};
-    const size_t smem2 = (size_t)L2B_WORDS * 4 * THREADS;
+    const size_t smem2 = (size_t)(L2B_WORDS + L2B_CS) * 4 * THREADS;  // + B-relation words
     cudaEvent_t e1 = timing_begin(P);
     if (!cuda_ok(cudaLaunchKernel((void *)k_l2_from_l15, dim3(std::max(1u, g2)), dim3(THREADS), a2, smem2, st),
                  "l2 from l15"))
