@@ -2028,6 +2028,9 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
 // k_l2_build, so the rest of the pipeline is unchanged).  Either stage sets
 // *fail when a record would exceed its super-node budget; the host then
 // redoes the batch on the direct path.
+// dynamic shared memory of k_l15_build: labels | cs, then one 1 KB row slot
+// per tile of each warp (at least 2 A1 bits: <= 8 tiles per warp)
+constexpr size_t L15_SMEM_MAX = (size_t)L2B_WORDS * 4 * THREADS + (THREADS / 32) * 8 * 1024;
 constexpr int L15_MAXM = L2B_CS;  // stage-1 super-nodes (cs bit 31 is the self flag)
 
 // F-space compression by byte lookup tables (k_l15_build stages them in shared memory)
@@ -2145,7 +2148,8 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
                                                        uint32_t *__restrict__ oldlist,
                                                        uint32_t *__restrict__ oldcount,
                                                        uint32_t *__restrict__ fail,
-                                                       const L15Lut *__restrict__ lut_g) {
+                                                       const L15Lut *__restrict__ lut_g,
+                                                       int stage_wide) {
     __shared__ TileTables tts;
     __shared__ L15Lut luts;
     extern __shared__ __align__(16) uint32_t l2smem[];
@@ -2160,8 +2164,12 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
     const int la1 = tt.la1;
     const uint32_t nrec = nb << la1;
     const int lane = threadIdx.x & 31;
+    // one row slot per tile of the warp: 256 B (<= 32-node rows), or with
+    // stage_wide the full 1 KB so that 33..64-node tiles (all of d = 7 at
+    // 2^12-index tiles) also run the breadth-first pass from shared memory
+    const int slotq = stage_wide ? 64 : L2B_SLOT / 16;
     uint4 *slot = reinterpret_cast<uint4 *>(l2smem + L2B_WORDS * THREADS) +
-                  (L2B_SLOT / 16) * ((threadIdx.x >> 5) * (32 >> tt.la1) + (lane >> tt.la1));
+                  slotq * ((threadIdx.x >> 5) * (32 >> tt.la1) + (lane >> tt.la1));
     for (uint32_t jb = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); jb < nrec;
          jb += gridDim.x * blockDim.x) {  // warp-uniform
         const uint32_t j = jb + lane;
@@ -2169,9 +2177,10 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
         const uint32_t i = i0 + (j >> la1), a1 = j & ((1u << la1) - 1u);
         const uint32_t t = valid ? list1[i] : 0u;
         const TileRec *rec = recs + t;
-        if (valid && rec->nnodes <= 32) {  // 256 bytes of uint2 rows
+        if (valid && (rec->nnodes <= 32 || stage_wide)) {  // uint2 rows, or nnodes uint4 rows
             const uint4 *src = rec->rows;
-            for (int q = lane & ((1 << la1) - 1); q < 16; q += 1 << la1) slot[q] = src[q];
+            const int nq = rec->nnodes <= 32 ? 16 : rec->nnodes;
+            for (int q = lane & ((1 << la1) - 1); q < nq; q += 1 << la1) slot[q] = src[q];
         }
         __syncwarp();
         if (valid) {
@@ -2189,9 +2198,10 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
                     nn <= 32
                         ? (pk ? l15_build<uint32_t, true>(tt, luts, rec, slot, a1, out, h, mine)
                               : l15_build<uint32_t, false>(tt, luts, rec, slot, a1, out, h, mine))
-                        : (pk ? l15_build<unsigned long long, true>(tt, luts, rec, rec->rows, a1, out, h, mine)
-                              : l15_build<unsigned long long, false>(tt, luts, rec, rec->rows, a1, out, h,
-                                                                     mine));
+                        : (pk ? l15_build<unsigned long long, true>(tt, luts, rec, stage_wide ? slot : rec->rows,
+                                                                    a1, out, h, mine)
+                              : l15_build<unsigned long long, false>(tt, luts, rec, stage_wide ? slot : rec->rows,
+                                                                     a1, out, h, mine));
                 if (m < 0) {
                     atomicOr(fail, 1u);
                     wts[j] = 0u;
@@ -3700,10 +3710,11 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
         if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)L2B_SMEM)) != cudaSuccess)
             return bail(e, "l2 build smem");
-    for (void *kb : {(void *)k_l15_build, (void *)k_l2_from_l15})
-        if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)L2B_SMEM)) != cudaSuccess)
-            return bail(e, "l15 smem");
+    if ((e = cudaFuncSetAttribute((void *)k_l2_from_l15, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L2B_SMEM)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute((void *)k_l15_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L15_SMEM_MAX)) != cudaSuccess)
+        return bail(e, "l15 smem");
     cudaFuncSetAttribute((void *)k_l2_classify_even, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)L2E_CLS_SMEM);
     cudaFuncSetAttribute((void *)k_l2_classify_even, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -4027,9 +4038,15 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     uint32_t i0v = i0, nbv = nb, s1 = stride1;
     const unsigned g1 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8, (nrec1 + THREADS - 1) / THREADS);
     const L15Lut *lutp = P->d_lut + mode;
+    static const int stage_wide = [] {
+        const char *e = std::getenv("TCG_L15_STAGE");
+        return e ? std::atoi(e) : 1;
+    }();
+    int sw = stage_wide;
     void *ab[] = {&tt, &recs, &list1, &dup1, &mint1, &i0v, &nbv, &t0, &a, &b, &pool1, &s1,
-                  &hash1, &wts1, &poss1, &oldlist, &oldcount, &failp, &lutp};
-    const size_t smem1 = (size_t)L2B_WORDS * 4 * THREADS + (size_t)(THREADS / 32) * (32 >> T.la1) * L2B_SLOT;
+                  &hash1, &wts1, &poss1, &oldlist, &oldcount, &failp, &lutp, &sw};
+    const size_t smem1 = (size_t)L2B_WORDS * 4 * THREADS +
+                         (size_t)(THREADS / 32) * (32 >> T.la1) * (sw ? 1024 : L2B_SLOT);
     cudaEvent_t e0 = timing_begin(P);
     if (!cuda_ok(cudaLaunchKernel((void *)k_l15_build, dim3(g1), dim3(THREADS), ab, smem1, st), "l15 build"))
         return false;
