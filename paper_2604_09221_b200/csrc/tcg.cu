@@ -2030,7 +2030,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
 // redoes the batch on the direct path.
 // dynamic shared memory of k_l15_build: labels | cs, then one 1 KB row slot
 // per tile of each warp (at least 2 A1 bits: <= 8 tiles per warp)
-constexpr size_t L15_SMEM_MAX = (size_t)L2B_WORDS * 4 * THREADS + (THREADS / 32) * 8 * 1024;
+constexpr size_t L15_SMEM_MAX = (size_t)L2B_WORDS * 4 * THREADS + (THREADS / 32) * 8 * 1024 + 4096;
 constexpr int L15_MAXM = L2B_CS;  // stage-1 super-nodes (cs bit 31 is the self flag)
 
 // F-space compression by byte lookup tables (k_l15_build stages them in shared memory)
@@ -2149,25 +2149,28 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
                                                        uint32_t *__restrict__ oldcount,
                                                        uint32_t *__restrict__ fail,
                                                        const L15Lut *__restrict__ lut_g,
-                                                       int stage_wide) {
+                                                       int slotq, int lut_smem) {
     __shared__ TileTables tts;
-    __shared__ L15Lut luts;
     extern __shared__ __align__(16) uint32_t l2smem[];
     uint32_t *mine = l2smem + threadIdx.x;
+    // dynamic shared memory: labels | cs (lane-private), one row slot of
+    // slotq uint4 rows per tile of each warp, then (lut_smem) the lookup tables
+    const int nslot = (THREADS / 32) * (32 >> tt_g->la1);
+    uint32_t *lutsm = l2smem + L2B_WORDS * THREADS + nslot * slotq * 4;
+    const L15Lut &luts = lut_smem ? *reinterpret_cast<const L15Lut *>(lutsm) : *lut_g;
     for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
         reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
     for (int i = threadIdx.x; i < (int)(sizeof(L15Lut) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(&luts)[i] = reinterpret_cast<const uint32_t *>(lut_g)[i];
+        if (lut_smem) lutsm[i] = reinterpret_cast<const uint32_t *>(lut_g)[i];
     __syncthreads();
     const TileTables &tt = tts;
     const int bits = tt.bits;
     const int la1 = tt.la1;
     const uint32_t nrec = nb << la1;
     const int lane = threadIdx.x & 31;
-    // one row slot per tile of the warp: 256 B (<= 32-node rows), or with
-    // stage_wide the full 1 KB so that 33..64-node tiles (all of d = 7 at
-    // 2^12-index tiles) also run the breadth-first pass from shared memory
-    const int slotq = stage_wide ? 64 : L2B_SLOT / 16;
+    // one row slot per tile of the warp: 16 uint4 hold <= 32-node rows (uint2);
+    // tiles of 33..slotq nodes (all of d = 7 at 2^12-index tiles have > 32)
+    // are staged too, wider ones read their rows from global memory
     uint4 *slot = reinterpret_cast<uint4 *>(l2smem + L2B_WORDS * THREADS) +
                   slotq * ((threadIdx.x >> 5) * (32 >> tt.la1) + (lane >> tt.la1));
     for (uint32_t jb = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); jb < nrec;
@@ -2177,7 +2180,7 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
         const uint32_t i = i0 + (j >> la1), a1 = j & ((1u << la1) - 1u);
         const uint32_t t = valid ? list1[i] : 0u;
         const TileRec *rec = recs + t;
-        if (valid && (rec->nnodes <= 32 || stage_wide)) {  // uint2 rows, or nnodes uint4 rows
+        if (valid && (rec->nnodes <= 32 || rec->nnodes <= slotq)) {  // uint2 rows, or nnodes uint4 rows
             const uint4 *src = rec->rows;
             const int nq = rec->nnodes <= 32 ? 16 : rec->nnodes;
             for (int q = lane & ((1 << la1) - 1); q < nq; q += 1 << la1) slot[q] = src[q];
@@ -2198,9 +2201,9 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
                     nn <= 32
                         ? (pk ? l15_build<uint32_t, true>(tt, luts, rec, slot, a1, out, h, mine)
                               : l15_build<uint32_t, false>(tt, luts, rec, slot, a1, out, h, mine))
-                        : (pk ? l15_build<unsigned long long, true>(tt, luts, rec, stage_wide ? slot : rec->rows,
+                        : (pk ? l15_build<unsigned long long, true>(tt, luts, rec, nn <= slotq ? slot : rec->rows,
                                                                     a1, out, h, mine)
-                              : l15_build<unsigned long long, false>(tt, luts, rec, stage_wide ? slot : rec->rows,
+                              : l15_build<unsigned long long, false>(tt, luts, rec, nn <= slotq ? slot : rec->rows,
                                                                      a1, out, h, mine));
                 if (m < 0) {
                     atomicOr(fail, 1u);
@@ -4038,15 +4041,24 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     uint32_t i0v = i0, nbv = nb, s1 = stride1;
     const unsigned g1 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8, (nrec1 + THREADS - 1) / THREADS);
     const L15Lut *lutp = P->d_lut + mode;
-    static const int stage_wide = [] {
-        const char *e = std::getenv("TCG_L15_STAGE");
+    // row slot size (uint4 rows, 16..64; TCG_L15_STAGE=0 stages only <= 32-node tiles)
+    // and where the lookup tables live (global by default, measured 0.5 % faster
+    // than staging them; TCG_L15_LUTG=0 stages them in shared memory)
+    static const int slotq_env = [] {
+        const char *e = std::getenv("TCG_L15_SLOTQ");
+        const char *f = std::getenv("TCG_L15_STAGE");
+        if (f && std::atoi(f) == 0) return 16;
+        return e ? std::max(16, std::min(64, std::atoi(e))) : 64;
+    }();
+    static const int lutg_env = [] {
+        const char *e = std::getenv("TCG_L15_LUTG");
         return e ? std::atoi(e) : 1;
     }();
-    int sw = stage_wide;
+    int slotq = slotq_env, lut_smem = !lutg_env;
     void *ab[] = {&tt, &recs, &list1, &dup1, &mint1, &i0v, &nbv, &t0, &a, &b, &pool1, &s1,
-                  &hash1, &wts1, &poss1, &oldlist, &oldcount, &failp, &lutp, &sw};
-    const size_t smem1 = (size_t)L2B_WORDS * 4 * THREADS +
-                         (size_t)(THREADS / 32) * (32 >> T.la1) * (sw ? 1024 : L2B_SLOT);
+                  &hash1, &wts1, &poss1, &oldlist, &oldcount, &failp, &lutp, &slotq, &lut_smem};
+    const size_t smem1 = (size_t)L2B_WORDS * 4 * THREADS + (size_t)(THREADS / 32) * (32 >> T.la1) * slotq * 16 +
+                         (lut_smem ? sizeof(L15Lut) : 0);
     cudaEvent_t e0 = timing_begin(P);
     if (!cuda_ok(cudaLaunchKernel((void *)k_l15_build, dim3(g1), dim3(THREADS), ab, smem1, st), "l15 build"))
         return false;
