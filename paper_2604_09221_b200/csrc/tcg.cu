@@ -2374,6 +2374,9 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
 }
 
 // One thread per level-2 record: exact deduplication (hash, then word-by-word).
+#ifndef L2D_PRE
+#define L2D_PRE 8  // record words k_l2_dedup fetches before probing
+#endif
 __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *__restrict__ pool,
                                                       uint32_t stride, uint32_t nrec,
                                                       const unsigned long long *__restrict__ hashes,
@@ -2397,7 +2400,15 @@ __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *
             const unsigned long long h = hashes[j];
             const unsigned long long tag = (h >> 32) << 32;
             const unsigned long long *mine = pool + (size_t)j * stride;
+            // the record's first words, fetched with its length and alongside the
+            // first probe (a tag match -- every duplicate -- compares them); words
+            // past the record's end lie inside its slot (stride >= 5) and are unused
+            const int npre = min(L2D_PRE, (int)stride - 1);
             const unsigned long long m = mine[0];
+            unsigned long long pw[L2D_PRE];
+#pragma unroll
+            for (int q = 0; q < L2D_PRE; ++q) pw[q] = q < npre ? mine[1 + q] : 0ull;
+            const int nw = wps * (int)m;
             uint32_t at = (uint32_t)h & smask;
             while (true) {
                 unsigned long long cur = slots[at];
@@ -2415,8 +2426,11 @@ __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *
                     const uint32_t o = (uint32_t)cur;
                     const unsigned long long *ow = pool + (size_t)o * stride;
                     unsigned long long diff = ow[0] ^ m;
+#pragma unroll
+                    for (int q = 0; q < L2D_PRE; ++q)
+                        if (q < npre && q < nw) diff |= ow[1 + q] ^ pw[q];
 #pragma unroll 4
-                    for (int q = 1; q <= wps * (int)m; ++q) diff |= ow[q] ^ mine[q];
+                    for (int q = npre + 1; q <= nw; ++q) diff |= ow[q] ^ mine[q];
                     if (diff == 0ull) {
                         atomicAdd(&w2[o], wj);
                         atomicMin(&pos2[o], poss[j]);

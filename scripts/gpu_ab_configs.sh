@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" 2>&1 | tail -1
 for rep in 1 2; do for c in $CONFIGS; do
-  tag=$(echo "$c" | tr ':=' '__')
+  tag=$(echo "$c" | tr ':=/.' '____' | tail -c 60)
   env $(echo "$c" | tr ':' ' ') timeout 300 python bench.py --steps 8 --warmup 3 --no-cpu-baseline > gpurun_out/ab_$tag.json 2> gpurun_out/ab_$tag.err
   echo "$c $(grep -E 'kernel ms by kind' gpurun_out/ab_$tag.err | tail -1)"
   python -c "import json; d=json.load(open('gpurun_out/ab_$tag.json')); print('value', d['value'], d['parity'])"
