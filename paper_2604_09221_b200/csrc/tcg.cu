@@ -2816,7 +2816,16 @@ __global__ void __launch_bounds__(THREADS) k_large(LargeParams P, const uint64_t
             }
         }
         __syncthreads();
-        for (int v = threadIdx.x; v < nv; v += blockDim.x) p1[v] = lfind(p1, v);
+        // flatten in two phases: roots found read-only (into rid, free until the
+        // region ids below), then stored.  A halving find here could land a stale
+        // non-root ancestor in p1[v] after v's own thread stored the root.
+        for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+            int x = v;
+            while (p1[x] != x) x = p1[x];
+            rid[v] = x;
+        }
+        __syncthreads();
+        for (int v = threadIdx.x; v < nv; v += blockDim.x) p1[v] = rid[v];
         __syncthreads();
         if (threadIdx.x == 0) {
             // parity union-find over the antipodal pairs (components named by root vertex)
