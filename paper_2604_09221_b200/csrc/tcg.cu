@@ -4062,7 +4062,18 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     uint32_t *oldlist = P->d_oldlist + 1, *oldcount = P->d_oldlist;
     uint64_t t0 = tile0, a = lo, b = hi;
     uint32_t i0v = i0, nbv = nb, s1 = stride1;
-    const unsigned g1 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8, (nrec1 + THREADS - 1) / THREADS);
+    // grid sizes (CTAs per SM; measured, profiles/README.md): the stage-1 build
+    // runs one pass (a whole grid: its per-record work varies, and the block
+    // scheduler balances it better than a grid-stride loop), the stage-1 dedup 8,
+    // stage 2 3 (= resident CTAs)
+    auto env_grid = [](const char *name, uint64_t dflt) {
+        const char *e = std::getenv(name);
+        return e ? (uint64_t)std::max(1, std::atoi(e)) : dflt;
+    };
+    static const uint64_t gm1 = env_grid("TCG_L15_GRID", 1u << 20), gm1d = env_grid("TCG_L15D_GRID", 8),
+                          gm2 = env_grid("TCG_L2F_GRID", 3);
+    const unsigned g1 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * gm1, (nrec1 + THREADS - 1) / THREADS);
+    const unsigned g1d = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * gm1d, (nrec1 + THREADS - 1) / THREADS);
     const L15Lut *lutp = P->d_lut + mode;
     // row slot size (uint4 rows, 16..64; TCG_L15_STAGE=0 stages only <= 32-node tiles)
     // and where the lookup tables live (global by default, measured 0.5 % faster
@@ -4092,7 +4103,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     uint32_t nr1 = nrec1;
     void *ad[] = {&pool1, &s1, &nr1, &hash1, &wts1, &poss1, &slots1, &smask1, &w15, &pos15,
                   &list15, &count15, &wps2};
-    if (!cuda_ok(cudaLaunchKernel((void *)k_l2_dedup, dim3(g1), dim3(THREADS), ad, 0, st), "l15 dedup"))
+    if (!cuda_ok(cudaLaunchKernel((void *)k_l2_dedup, dim3(g1d), dim3(THREADS), ad, 0, st), "l15 dedup"))
         return false;
     uint32_t hostv[2] = {0, 0};  // count15, fail
     if (!cuda_ok(cudaMemcpyAsync(hostv, count15, 8, cudaMemcpyDeviceToHost, st), "copy") ||
@@ -4112,7 +4123,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     const uint32_t nrec = n15 << T.la2;
     uint32_t *wts = P->d_l2u32, *poss = wts + cap;
     unsigned long long *pool = P->d_l2pool, *hashes = P->d_l2hash;
-    const unsigned g2 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8, (nrec + THREADS - 1) / THREADS);
+    const unsigned g2 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * gm2, (nrec + THREADS - 1) / THREADS);
     uint32_t s2 = stride;
     void *a2[] = {&tt, &pool1, &s1, &list15, &count15, &w15, &pos15, &pool, &s2, &hashes, &wts,
                   &poss, &failp};
