@@ -4211,7 +4211,11 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
             if (rc2) return rc2;
             if (done) continue;
         }
-        const unsigned g12 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * 8,
+        static const uint64_t gmb = [] {  // CTAs per SM of the direct level-2 build
+            const char *e = std::getenv("TCG_L2B_GRID");
+            return e ? (uint64_t)std::max(1, std::atoi(e)) : (uint64_t)8;
+        }();
+        const unsigned g12 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * gmb,
                                                           (nrec + THREADS - 1) / THREADS);
         unsigned long long *pool = P->d_l2pool, *hashes = P->d_l2hash;
         uint32_t *wts = P->d_l2u32, *poss = wts + cap;
