@@ -4082,13 +4082,25 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
         const char *e = std::getenv("TCG_L15_SLOTQ");
         const char *f = std::getenv("TCG_L15_STAGE");
         if (f && std::atoi(f) == 0) return 16;
-        return e ? std::max(16, std::min(64, std::atoi(e))) : 64;
+        return e ? std::max(16, std::min(64, std::atoi(e))) : 0;  // 0: fit 4 CTAs per SM
     }();
     static const int lutg_env = [] {
         const char *e = std::getenv("TCG_L15_LUTG");
         return e ? std::atoi(e) : 1;
     }();
+    static const int l15_static = [] {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, (const void *)k_l15_build);
+        return (int)fa.sharedSizeBytes;
+    }();
     int slotq = slotq_env, lut_smem = !lutg_env;
+    if (slotq == 0) {  // the widest slot that keeps 4 CTAs (= the register limit) per SM:
+        // with the whole-grid launch 4 CTAs and 47-row slots beat 3 CTAs and 64 (profiles/README.md)
+        const int tiles = (THREADS / 32) * (32 >> T.la1);
+        const int budget = 228 * 1024 / 4 - 1024 - l15_static - L2B_WORDS * 4 * THREADS -
+                           (lut_smem ? (int)sizeof(L15Lut) : 0);
+        slotq = std::max(16, std::min(64, budget / (tiles * 16)));
+    }
     void *ab[] = {&tt, &recs, &list1, &dup1, &mint1, &i0v, &nbv, &t0, &a, &b, &pool1, &s1,
                   &hash1, &wts1, &poss1, &oldlist, &oldcount, &failp, &lutp, &slotq, &lut_smem};
     const size_t smem1 = (size_t)L2B_WORDS * 4 * THREADS + (size_t)(THREADS / 32) * (32 >> T.la1) * slotq * 16 +
