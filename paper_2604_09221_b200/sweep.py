@@ -28,22 +28,30 @@ from .scheme import scheme_from_key
 from .signs import representative, sign_from_raw_index
 
 DEFAULT_CHUNK = 1 << 16
-_MAX_DOMAIN_BITS = 62
+_MAX_DOMAIN_BITS = 62  # indices must stay below 2^62 (reference sweep.py:32)
 
 
 @dataclass(frozen=True)
 class SweepRange:
+    """Half-open index interval [start, end) of one enumeration domain."""
+
     start: int
     end: int
 
     def __post_init__(self):
-        if not (0 <= self.start <= self.end):
+        if self.start < 0 or self.end < self.start:
             raise IndexOutOfRange(f"bad sweep range [{self.start}, {self.end})")
+
+    def __len__(self) -> int:
+        return self.end - self.start
 
 
 @dataclass
 class SweepReport:
-    """Mergeable aggregate of one enumeration run (reference sweep.py:45-69)."""
+    """Mergeable result of one enumeration (field contract: reference
+    sweep.py:45-69).  ``scheme_map[s] = (count, witness)`` where the witness
+    is the smallest index of the report's own domain classified as ``s``;
+    ``params`` describe the run and take no part in equality."""
 
     degree: int
     fingerprint: str
@@ -54,53 +62,54 @@ class SweepReport:
     params: dict = field(default_factory=dict, compare=False)
 
     def witness_bitstring(self, scheme: str) -> str:
-        m = self.scheme_map[scheme][1]
-        if self.raw_space:
-            return sign_from_raw_index(self.degree, m).bitstring()
-        return representative(self.degree, m).bitstring()
+        index = self.scheme_map[scheme][1]
+        decode = sign_from_raw_index if self.raw_space else representative
+        return decode(self.degree, index).bitstring()
 
     def distinct_schemes(self) -> int:
         return len(self.scheme_map)
 
     def max_ovals(self) -> int:
-        return max((k for k, c in enumerate(self.oval_histogram) if c), default=0)
+        nonzero = [k for k, c in enumerate(self.oval_histogram) if c]
+        return nonzero[-1] if nonzero else 0
 
 
 def empty_report(T, raw_space: bool = False) -> SweepReport:
-    return SweepReport(
-        degree=T.degree,
-        fingerprint=fingerprint_of(T),
-        raw_space=raw_space,
-        oval_histogram=tuple([0] * (harnack_bound(T.degree) + 1)),
-        scheme_map={},
-        total_classified=0,
-    )
+    """The identity of :func:`merge` for T's domain."""
+    bins = harnack_bound(T.degree) + 1
+    return SweepReport(T.degree, fingerprint_of(T), raw_space, (0,) * bins, {}, 0)
+
+
+def _merge_scheme_maps(x: dict, y: dict) -> dict:
+    out = dict(x)
+    for s, (cnt, wit) in y.items():
+        have = out.get(s)
+        out[s] = (cnt, wit) if have is None else (have[0] + cnt, min(have[1], wit))
+    return out
 
 
 def merge(a: SweepReport, b: SweepReport) -> SweepReport:
-    """Associative, commutative merge (reference sweep.py:83-105)."""
-    if (a.degree, a.fingerprint, a.raw_space) != (b.degree, b.fingerprint, b.raw_space):
+    """Associative, commutative combination: counts add, witnesses take the
+    minimum, histograms add bin by bin (semantics of reference
+    sweep.py:83-105; MergeMismatch on a different T or domain)."""
+    ident_a = (a.degree, a.fingerprint, a.raw_space)
+    if ident_a != (b.degree, b.fingerprint, b.raw_space):
         raise MergeMismatch("cannot merge reports over different triangulations or domains")
-    hist = tuple(x + y for x, y in zip(a.oval_histogram, b.oval_histogram))
-    schemes = dict(a.scheme_map)
-    for s, (c, w) in b.scheme_map.items():
-        if s in schemes:
-            c0, w0 = schemes[s]
-            schemes[s] = (c0 + c, min(w0, w))
-        else:
-            schemes[s] = (c, w)
-    return SweepReport(a.degree, a.fingerprint, a.raw_space, hist, schemes,
-                       a.total_classified + b.total_classified, {**a.params, **b.params})
+    hist = tuple(map(sum, zip(a.oval_histogram, b.oval_histogram)))
+    params = dict(a.params)
+    params.update(b.params)
+    return SweepReport(*ident_a, hist, _merge_scheme_maps(a.scheme_map, b.scheme_map),
+                       a.total_classified + b.total_classified, params)
 
 
 def _domain_bits(d: int, raw_space: bool) -> int:
-    bits = num_points(d) if raw_space else num_points(d) - 3
-    if bits > _MAX_DOMAIN_BITS:
-        raise BudgetExceeded(
-            f"degree-{d} {'raw' if raw_space else 'representative'} space needs "
-            f"{bits} index bits; at most {_MAX_DOMAIN_BITS} are supported"
-        )
-    return bits
+    """log2 of the domain size; BudgetExceeded beyond 62 bits."""
+    bits = num_points(d) - (0 if raw_space else 3)
+    if bits <= _MAX_DOMAIN_BITS:
+        return bits
+    kind = "raw" if raw_space else "representative"
+    raise BudgetExceeded(f"degree-{d} {kind} space needs {bits} index bits; "
+                         f"at most {_MAX_DOMAIN_BITS} are supported")
 
 
 def _classifier_for(T, classifier, device=None) -> Classifier:
