@@ -1,25 +1,37 @@
 #!/usr/bin/env python3
 """Headline benchmark: patchworks classified per second, degree-7 full sign
-enumeration (BASELINE.json metric, config C3), 1..N B200.
+enumeration (BASELINE.json metric, config C3), on 1..N B200.
 
-Workload (config C3): T = delaunay-7 (the staircase), raw index space,
-lower half [0, 2^35) = the 2^36 sign space modulo the global sign flip
-(SURVEY.md section 0.1).  A step is one slice of 2^34 consecutive indices
-per GPU (weak scaling: rank r of N sweeps slice s*N + r); at N=1 the
-default 2 timed steps are the complete enumeration.  Indices are generated
-on the device (there is no input tensor), so `value` is kernel-resident
-throughput; `e2e` runs the same slices through the public API
-(`paper_2604_09221_b200.sweep`), host round trip and string rendering
-included.
+Workload (config C3, BASELINE.json configs[2]): T = delaunay-7 (the
+staircase), raw index space, lower half [0, 2^35) = the 2^36 sign space
+modulo the global sign flip.  One step = the COMPLETE enumeration: the
+2^35 indices are split into N contiguous shards, one per GPU (strong
+scaling: the total work is fixed); a rank sweeps its shard in chunks of
+at most 2^34 indices, then the per-rank aggregates are merged (NCCL
+all_reduce + all_gather, a few KB).  Every step's merged report is checked
+against the full C3 report computed by the pinned CPU oracle
+(tests/golden/c3_full.json) and the reference's own 2^20-index slices; a
+mismatch makes the run exit 1.
 
-`--impl reference` times the reference algorithm on the host cores instead
-(the plain-C restatement in oracle/, all threads), same metric and config,
-each step a bounded 2^21-index slice.
+`value` is device-resident throughput (indices are generated on the
+device); `e2e` runs the same steps through the public API (`sweep`, or
+`distributed.sweep_sharded` for N > 1) with the host round trip.
+`--weak` keeps the per-GPU work fixed instead (2^33 indices per GPU per
+step at disjoint offsets of the raw 2^36 space).
+
+`--impl reference` times the reference's own CPU implementation (`tcurves`,
+installed from /root/reference into baseline/_ref) on all host cores, same
+metric and config, each step a bounded 2^22-index slice at a random offset.
+
+By default (N = 1) the line also carries `other_workloads`: config C5
+(random sampling, degree 8) and config C4 (4,096 random degree-7
+triangulations x 2^16 signs), the per-patchwork kernels' throughput.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import random
@@ -36,44 +48,59 @@ METRIC = "patchworks classified/sec, degree-7 full sign enumeration, 1/2/4/8 B20
 BACKEND = os.environ.get("BENCH_BACKEND", "nccl")
 DEGREE = 7
 DOMAIN = 1 << 35  # raw lower half: one index per global-flip orbit
+RAW_DOMAIN = 1 << 36
 W_D = {4: 249, 5: 381, 6: 541, 7: 729, 8: 945, 9: 1189}  # 2|E_diamond| + |V_diamond|
 CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+# kernel kinds timed by the library (tcg.h TCG_KT_*) -> kernel names in ncu
+KIND_KERNELS = {
+    "super_build": ["k_super_build"], "tile_build": ["k_tile_from_super", "k_tile_build_lanes"],
+    "tile_dedup": ["k_tile_dedup"], "l15_build": ["k_l15_build"],
+    "l15_dedup": ["k_l2_dedup/stage1"], "l2_build": ["k_l2_from_l15", "k_l2_build"],
+    "l2_dedup": ["k_l2_dedup/level2"], "l2_classify": ["k_l2_classify", "k_l2_classify_even"],
+    "tile_classify": ["k_tile_classify"], "enumerate": ["k_enumerate"], "batch": ["k_batch"],
+}
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-def ncu_traffic(kernel):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the
-    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            return json.load(f)[kernel]["dram_bytes_per_launch"]
-    except (OSError, KeyError, ValueError):
-        return None
+def source_sha16():
+    with open(os.path.join(ROOT, "paper_2604_09221_b200", "csrc", "tcg.cu"), "rb") as fh:
+        return hashlib.sha256(fh.read()).hexdigest()[:16]
 
 
-def ncu_kernel(kernel):
-    """Issue / pipe utilisation of `kernel` from the committed ncu capture, or None."""
+def ncu_profile():
+    """Per-kernel counters of one C3 step (N = 1) from the committed ncu
+    capture, if it was taken from this very source (profiles/ncu_kernels.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            d = json.load(f)[kernel]
-        return {k: v for k, v in d.items() if k != "dram_bytes_per_launch"}
-    except (OSError, KeyError, ValueError):
-        return None
+        with open(os.path.join(ROOT, "profiles", "ncu_kernels.json")) as f:
+            prof = json.load(f)
+    except (OSError, ValueError):
+        return None, "profiles/ncu_kernels.json missing"
+    if prof.get("tcg_cu_sha16") != source_sha16():
+        return None, (f"profiles/ncu_kernels.json is from tcg.cu {prof.get('tcg_cu_sha16')}, "
+                      f"this build is {source_sha16()}: not used")
+    return prof, "profiles/ncu_kernels.json (same tcg.cu)"
 
 
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    mhz, hbm, src = 1965.0, 6548.0, "fallback (B200_PROFILING.md: 1965 MHz, ~6.5 TB/s copy)"
     try:
         with open(path) as fh:
             p = json.load(fh)
-        return float(p.get("sm_max_mhz", 1965.0)), "MEASURED_PEAKS.json sm_max_mhz"
+        mhz = float(p.get("sm_max_mhz", mhz))
+        for k in ("hbm_gbs", "hbm_copy_gbps", "hbm_gbps"):
+            if k in p:
+                hbm = float(p[k])
+                break
+        src = "MEASURED_PEAKS.json"
     except (OSError, ValueError):
-        return 1965.0, "fallback 1965 MHz (B200_PROFILING.md clocks.max.sm)"
+        pass
+    return mhz, hbm, src
 
 
 class ClockSampler:
@@ -143,76 +170,314 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_rate(n_per_slice: int, slices: int, threads: int, seed: int = 7):
-    """The reference algorithm (plain-C restatement, oracle/) on host cores."""
+# ------------------------------------------------------------------ CPU legs
+def import_tcurves():
+    """The reference package itself (installed from /root/reference into
+    baseline/_ref, git-ignored, travels to the GPU box), or None."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "tcurves")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "tcg_numba"))
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import tcurves
+        return tcurves
+    except Exception as exc:  # numba missing on the host, ...
+        log(f"tcurves not importable: {exc!r}")
+        return None
+
+
+def tcurves_rate(tc, n, slices, workers, seed):
+    """Reference sweep(T, SweepRange(a, a+n), workers, raw_space=True) at
+    random offsets of the C3 domain (BASELINE.md §3 / SURVEY §8(d))."""
+    T = tc.builtin(f"delaunay-{DEGREE}")
+    c = tc.Classifier(T)
+    tc.sweep(T, tc.SweepRange(0, 1 << 12), raw_space=True, classifier=c)  # JIT warm-up
+    rng = random.Random(seed)
+    elapsed = 0.0
+    for _ in range(slices):
+        a = rng.randrange(0, DOMAIN - n)
+        t0 = time.perf_counter()
+        r = tc.sweep(T, tc.SweepRange(a, a + n), workers=workers, raw_space=True, classifier=c)
+        elapsed += time.perf_counter() - t0
+        assert r.total_classified == n
+    return n * slices / elapsed, elapsed
+
+
+def oracle_rate(n, slices, threads, seed=7):
+    """The plain-C restatement of the reference kernels (oracle/) on host cores."""
     from oracle import oracle as O
     from paper_2604_09221_b200 import builtin
     from paper_2604_09221_b200.diamond import plan_arrays, reflect
 
     plan = O.OraclePlan.from_arrays(plan_arrays(reflect(builtin(f"delaunay-{DEGREE}"))))
     rng = random.Random(seed)
-    O.sweep(plan, True, 0, 1 << 14, threads=threads)  # warm
-    total, elapsed = 0, 0.0
+    O.sweep(plan, True, 0, 1 << 14, threads=threads)
+    elapsed = 0.0
     for _ in range(slices):
-        a = rng.randrange(0, DOMAIN - n_per_slice)
+        a = rng.randrange(0, DOMAIN - n)
         t0 = time.perf_counter()
-        r = O.sweep(plan, True, a, a + n_per_slice, threads=threads)
+        r = O.sweep(plan, True, a, a + n, threads=threads)
         elapsed += time.perf_counter() - t0
-        assert r["status"] == 0 and r["total"] == n_per_slice
-        total += n_per_slice
-    return total / elapsed, total, elapsed
+        assert r["status"] == 0 and r["total"] == n
+    return n * slices / elapsed, elapsed
+
+
+def cpu_baseline_block():
+    threads = os.cpu_count() or 1
+    tc = import_tcurves()
+    if tc is not None:
+        rate, sec = tcurves_rate(tc, 1 << 22, 4, threads, seed=7)
+        one, _ = tcurves_rate(tc, 1 << 17, 1, 1, seed=8)
+        port, _ = oracle_rate(1 << 22, 4, threads)
+        return {"value": rate, "unit": "patchworks/s", "cores": threads, "kind": "reference",
+                "cpu": cpu_model(), "one_worker": one, "port_all_cores": port,
+                "sample": f"reference tcurves.sweep(delaunay-7, SweepRange(a, a+2^22), "
+                          f"workers={threads}, raw_space=True) at 4 random offsets of [0,2^35) "
+                          f"(Random(7)), {sec:.1f} s; one_worker = workers=1 on 2^17 indices; "
+                          "port_all_cores = oracle/tcg_oracle.c (C restatement) on the same "
+                          "slices"}
+    rate, sec = oracle_rate(1 << 22, 4, threads)
+    return {"value": rate, "unit": "patchworks/s", "cores": threads, "kind": "port",
+            "cpu": cpu_model(),
+            "sample": f"4 x 2^22 delaunay-7 raw indices at random offsets (Random(7)) in "
+                      f"{sec:.1f} s; oracle/tcg_oracle.c restates the reference kernels.py"}
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    n = 1 << 21
+    n = 1 << 22
     rng = random.Random(11)
-    from oracle import oracle as O
-    from paper_2604_09221_b200 import builtin
-    from paper_2604_09221_b200.diamond import plan_arrays, reflect
-
-    plan = O.OraclePlan.from_arrays(plan_arrays(reflect(builtin(f"delaunay-{DEGREE}"))))
     offs = [rng.randrange(0, DOMAIN - n) for _ in range(args.warmup + args.steps)]
+    tc = import_tcurves()
+    if tc is not None:
+        T = tc.builtin(f"delaunay-{DEGREE}")
+        c = tc.Classifier(T)
+        tc.sweep(T, tc.SweepRange(0, 1 << 12), raw_space=True, classifier=c)  # JIT
+
+        def step(a):
+            r = tc.sweep(T, tc.SweepRange(a, a + n), workers=threads, raw_space=True,
+                         classifier=c)
+            assert r.total_classified == n
+        kind = "reference"
+        what = (f"reference tcurves.sweep(delaunay-7, SweepRange(a, a+2^22), workers={threads}, "
+                "raw_space=True), one random offset of [0,2^35) per step (Random(11)); "
+                "package installed from /root/reference into baseline/_ref")
+    else:
+        from oracle import oracle as O
+        from paper_2604_09221_b200 import builtin
+        from paper_2604_09221_b200.diamond import plan_arrays, reflect
+
+        plan = O.OraclePlan.from_arrays(plan_arrays(reflect(builtin(f"delaunay-{DEGREE}"))))
+
+        def step(a):
+            r = O.sweep(plan, True, a, a + n, threads=threads)
+            assert r["status"] == 0
+        kind = "port"
+        what = ("baseline/_ref missing: oracle/tcg_oracle.c (C restatement of kernels.py) on "
+                f"{threads} threads, 2^22 indices per step at random offsets (Random(11))")
     for a in offs[:args.warmup]:
-        O.sweep(plan, True, a, a + n, threads=threads)
+        step(a)
     t0 = time.perf_counter()
     for a in offs[args.warmup:]:
-        r = O.sweep(plan, True, a, a + n, threads=threads)
-        assert r["status"] == 0
+        step(a)
     dt = time.perf_counter() - t0
     value = n * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "patchworks/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic (sign indices)",
-        "config": {"workload": "C3 delaunay-7 raw lower half [0,2^35); bounded 2^21-index "
+        "config": {"workload": "C3 delaunay-7 raw lower half [0,2^35); bounded 2^22-index "
                                "slices at random offsets", "degree": DEGREE,
                    "parallelism": f"{threads} host threads"},
-        "cpu_baseline": {"value": value, "unit": "patchworks/s", "cores": threads,
-                         "kind": "port", "cpu": cpu_model(),
-                         "sample": f"{args.steps} x 2^21 raw indices at random offsets "
-                                   "(Random(11)); oracle/tcg_oracle.c restates kernels.py"},
+        "cpu_baseline": {"value": value, "unit": "patchworks/s", "cores": threads, "kind": kind,
+                         "cpu": cpu_model(), "sample": what},
         "e2e": {"value": value, "unit": "patchworks/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------- parity checks
+def c3_golden():
+    """Full C3 report (hist, scheme -> (count, witness)) from the oracle pieces."""
+    path = os.path.join(ROOT, "tests", "golden", "c3_full.json")
+    try:
+        with open(path) as fh:
+            doc = json.load(fh)
+    except (OSError, ValueError):
+        return None
+    pieces = doc["pieces"]
+    if len(pieces) != DOMAIN >> doc["piece_log2"]:
+        return None
+    hist = None
+    schemes = {}
+    for p in pieces.values():
+        hist = p["hist"] if hist is None else [a + b for a, b in zip(hist, p["hist"])]
+        for s, (c, w) in p["schemes"].items():
+            schemes[s] = (schemes[s][0] + c, min(schemes[s][1], w)) if s in schemes else (c, w)
+    return hist, schemes
+
+
+def slice_parity(T, c):
+    from paper_2604_09221_b200 import SweepRange, sweep
+
+    with open(os.path.join(ROOT, "tests", "golden", "c3_delaunay7_raw_slices.json")) as fh:
+        gs = json.load(fh)["slices"]
+    ok = 0
+    for g in gs:
+        r = sweep(T, SweepRange(g["start"], g["end"]), raw_space=True, classifier=c)
+        ok += (list(r.oval_histogram) == g["hist"] and
+               r.scheme_map == {k: tuple(v) for k, v in g["schemes"].items()})
+    return ok, len(gs)
+
+
+# ------------------------------------------------------------ other configs
+def bench_c5(dev, steps, warmup):
+    """Config C5: uniform sampling over the degree-8 representative space
+    (seed 20260810, draws k0 = 2^39 ..), per-patchwork full-diamond kernel."""
+    import torch
+
+    from paper_2604_09221_b200 import Classifier, builtin
+    from paper_2604_09221_b200.sweep import report_from_agg, sample_slice
+
+    with open(os.path.join(ROOT, "tests", "golden", "c5_sample_slices.json")) as fh:
+        gold = json.load(fh)["slices"]
+    out = {}
+    n = 1 << 28
+    k0 = 1 << 39
+    seed = 20260810
+    for name in ("bowtie8", "delaunay-8"):
+        T = builtin(name)
+        c = Classifier(T, device=dev.index)
+        stream = torch.cuda.current_stream(dev)
+        c.native.set_stream(stream.cuda_stream)
+        for s in range(warmup):
+            c.native.agg_reset()
+            c.native.sample_async(seed, k0 + (s + 1) * n * 4, k0 + (s + 1) * n * 4 + n, 42)
+            c.native.agg_fetch()
+        torch.cuda.synchronize()
+        evs = []
+        c.native.set_timing(True)
+        c.native.kernel_times()
+        for s in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c.native.agg_reset()
+            a.record(stream)
+            c.native.sample_async(seed, k0 + s * n, k0 + (s + 1) * n, 42)
+            b.record(stream)
+            rc, bad, agg = c.native.agg_fetch()
+            assert rc == 0, (rc, bad)
+            evs.append((a, b))
+        torch.cuda.synchronize()
+        kt = c.native.kernel_times()
+        c.native.set_timing(False)
+        ms = sum(x.elapsed_time(y) for x, y in evs) / steps
+        t0 = time.perf_counter()
+        for s in range(steps):
+            sample_slice(T, seed, k0 + s * n, k0 + (s + 1) * n, classifier=c)
+        e2e = n * steps / (time.perf_counter() - t0)
+        ok = 0
+        slices = [g for g in gold if g["name"] == name]
+        for g in slices:
+            r = sample_slice(T, g["seed"], g["k0"], g["k1"], classifier=c)
+            ok += (list(r.oval_histogram) == g["hist"] and
+                   r.scheme_map == {k: tuple(v) for k, v in g["schemes"].items()})
+        enum_ms = kt["enumerate"][0] / steps
+        out[f"c5_{name}"] = {
+            "metric": "draws classified/sec (degree-8 uniform sampling, one B200)",
+            "value": n / (ms / 1e3), "unit": "draws/s", "ms_per_step": ms,
+            "e2e": {"value": e2e, "unit": "draws/s", "h2d_bytes_per_step": 32,
+                    "path": "sweep.sample_slice (host round trip + string rendering)"},
+            "config": {"workload": f"C5 {name}: draws [2^39 + s 2^28, +2^28) seed 20260810, "
+                                   "m = splitmix64 & (2^42-1)", "draws_per_step": n},
+            "kernel": "k_enumerate<6,even,SAMPLE>", "kernel_ms_per_step": enum_ms,
+            "parity": f"{ok}/{len(slices)} reference sample_kernel slices (2^20 draws) bit-exact",
+            "parity_ok": ok == len(slices),
+        }
+    return out
+
+
+def bench_c4(dev, steps, warmup):
+    """Config C4: 4,096 random regular unimodular degree-7 triangulations
+    (reference generator, Random(0xB7)) x 2^16 sign words each,
+    m = splitmix64(7, k) & (2^36 - 1), one topology per CTA."""
+    import numpy as np
+
+    from paper_2604_09221_b200 import MultiClassifier, scheme_from_key
+    from paper_2604_09221_b200.lattice import Triangulation
+
+    data = np.load(os.path.join(ROOT, "tests", "golden", "c4_d7_4096.npz"))
+    E = data["edges"].astype(int)
+    Ts = [Triangulation(7, tuple(((int(a), int(b)), (int(c), int(d))) for a, b, c, d in e), ())
+          for e in E]
+    mc = MultiClassifier(Ts, device=dev.index)
+    per = 1 << 16
+    ntri = len(Ts)
+    n = ntri * per
+    k = np.arange(n, dtype=np.uint64)
+    z = np.uint64(7) + (k + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    words = (z ^ (z >> np.uint64(31))) & np.uint64((1 << 36) - 1)
+    tri = (np.arange(n, dtype=np.int64) // per).astype(np.int32)
+    for _ in range(warmup):
+        mc.classify_words(tri, words)
+    kms, wall = [], []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        keys, ov, nr, st = mc.classify_words(tri, words)
+        wall.append(time.perf_counter() - t0)
+        kms.append(mc.native.last_ms())
+    assert (st == 0).all()
+    # parity: the 16 c4-7-k fixtures (reference pairs) are the first 16 T
+    with open(os.path.join(ROOT, "tests", "golden", "pairs.json")) as fh:
+        pairs = {e["name"]: e["rows"] for e in json.load(fh)}
+    ok = tot = 0
+    ptri, pw, want = [], [], []
+    for t in range(16):
+        for s, scheme, o, r in pairs[f"c4-7-{t}"]:
+            ptri.append(t)
+            pw.append(int(s[::-1], 2))
+            want.append((scheme, o, r))
+    pk, po, pr, ps = mc.classify_words(np.array(ptri, np.int32), np.array(pw, np.uint64))
+    for i, (scheme, o, r) in enumerate(want):
+        tot += 1
+        ok += (ps[i] == 0 and scheme_from_key(int(pk[i]), True) == scheme and
+               int(po[i]) == o and int(pr[i]) == r)
+    ms = statistics.median(kms)
+    return {"c4": {
+        "metric": "(triangulation, sign) pairs classified/sec, degree 7, one B200",
+        "value": n / (ms / 1e3), "unit": "pairs/s", "ms_per_step": ms,
+        "e2e": {"value": n / statistics.median(wall), "unit": "pairs/s",
+                "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 14 * n,
+                "path": "MultiClassifier.classify_words (host buffers, grouping, copies)"},
+        "config": {"workload": "C4: 4096 T from random_unimodular(7, Random(0xB7)) x 2^16 "
+                               "words splitmix64(7,k) & (2^36-1)", "pairs_per_step": n},
+        "kernel": "k_multi<4,odd>",
+        "parity": f"{ok}/{tot} reference pairs of c4-7-0..15 bit-exact",
+        "parity_ok": ok == tot,
+    }}
+
+
+# ---------------------------------------------------------------------- ours
 def run_ours(args, rank, world, local_rank):
     import numpy as np
     import torch
     import torch.distributed as dist
 
     from paper_2604_09221_b200 import Classifier, SweepRange, builtin, merge, sweep
-    from paper_2604_09221_b200.distributed import allreduce_aggregate
+    from paper_2604_09221_b200.distributed import allreduce_aggregate, shard, sweep_sharded
+    from paper_2604_09221_b200.io import report_jsonl
     from paper_2604_09221_b200.sweep import report_from_agg
 
     # one process per GPU; BENCH_BACKEND=gloo lets a 2-rank run share one GPU
-    # (used to exercise the N>1 path on a single-GPU box; ranks never wait
-    # on each other inside a kernel)
+    # (exercises the N>1 path on a single-GPU box; ranks never wait on each
+    # other inside a kernel)
     gpu = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(gpu)
     dev = torch.device("cuda", gpu)
@@ -220,16 +485,26 @@ def run_ours(args, rank, world, local_rank):
     T = builtin(f"delaunay-{DEGREE}")
     c = Classifier(T, device=gpu)
     # a dedicated stream: the library and the timing events must share it
-    # (handle 0 would mean "the plan's own stream" to tcg_plan_set_stream)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
     c.native.set_stream(stream.cuda_stream)
-    sl = 1 << args.slice_log2
 
-    def rng_of(step):
-        a = (args.offset + (step * world + rank) * sl) % DOMAIN
-        a -= a % sl
-        return a, a + sl
+    if args.weak:
+        sl = 1 << args.slice_log2
+        groups = RAW_DOMAIN // (sl * world)
+        if groups < 1:
+            raise SystemExit(f"--weak: {world} x 2^{args.slice_log2} exceeds the raw 2^36 space")
+
+        def rng_of(step):  # disjoint within a step; the next step takes the next group
+            a = ((step % groups) * world + rank) * sl
+            return a, a + sl
+        units_per_step = sl * world
+    else:
+        lo, hi = shard(0, DOMAIN, rank, world)
+
+        def rng_of(step):
+            return lo, hi
+        units_per_step = DOMAIN
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -237,16 +512,22 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
-    # ---- warm-up (untimed): same launches as a timed step, L2 flush included
+    def merged(agg_result):
+        h, tot, keys, counts, wits = agg_result
+        hist, total, keys, counts, wits = allreduce_aggregate(
+            np.asarray(h, np.int64).tolist(), int(tot), keys, counts, wits,
+            device=coll_dev if world > 1 else None)
+        return report_from_agg(T, True, hist, total, keys, counts, wits, {})
+
+    # ---- warm-up (untimed): same launches as a timed step
     for s in range(args.warmup):
         flush.zero_()
-        a, b = rng_of(args.steps + s)
+        a, b = rng_of(s + 1)
         c.native.agg_reset()
         c.native.sweep_async(True, a, b)
         c.native.agg_fetch()
     torch.cuda.synchronize()
 
-    # ---- timed: K steps, device events, max over ranks
     gpu_index = gpu
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
     if vis:
@@ -254,21 +535,18 @@ def run_ours(args, rank, world, local_rank):
             gpu_index = int(vis.split(",")[local_rank])
         except (ValueError, IndexError):
             pass
-    hist_acc = np.zeros(64, np.int64)
-    tables = []
-    k_ms = []
     launches0 = c.native.launches()
     c.native.kernel_times()  # clear
-    c.native.tile_stats()  # clear
-    c.native.level2_stats()  # clear
+    c.native.tile_stats()
+    c.native.level2_stats()
     c.native.set_timing(True)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    reports, k_ms, step_ev = [], [], []
     with ClockSampler(gpu_index) as clocks:
         barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
-        step_ev = []
         for s in range(args.steps):
             sa = torch.cuda.Event(enable_timing=True)
             sa.record(stream)
@@ -283,19 +561,11 @@ def run_ours(args, rank, world, local_rank):
             rc, bad, agg = c.native.agg_fetch()
             if rc:
                 raise RuntimeError(f"status {rc} at index {bad}")
-            h, tot, keys, counts, wits = agg.result()
-            hist_acc += np.asarray(h, np.int64)
-            tables.append((keys, counts, wits))
+            reports.append(merged(agg.result()))  # per-step merge over ranks (collective)
             k_ms.append((ka, kb))
             sb = torch.cuda.Event(enable_timing=True)
             sb.record(stream)
             step_ev.append((sa, sb))
-        from paper_2604_09221_b200.distributed import merge_tables
-
-        keys, counts, wits = merge_tables(tables)
-        hist, total, keys, counts, wits = allreduce_aggregate(
-            hist_acc.tolist(), int(hist_acc.sum()), keys, counts, wits,
-            device=coll_dev if world > 1 else None)
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -309,156 +579,207 @@ def run_ours(args, rank, world, local_rank):
     tiles_built, tiles_classified = c.native.tile_stats()
     l2_built, l2_classified, l1_left = c.native.level2_stats()
     tile_bits = c.native.info["tile_bits_raw"]
-    # dominant kernel: the kind with the most device time
     dom = max(ktimes, key=lambda k: ktimes[k][0])
-    dom_ms, dom_n = ktimes[dom]
     log("kernel ms by kind:", {k: round(v[0], 2) for k, v in ktimes.items() if v[1]})
-    t = torch.tensor([ms, dom_ms, statistics.mean(kern)], dtype=torch.float64, device=coll_dev)
+    t = torch.tensor([ms, statistics.mean(kern)], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max, dom_ms_max, sweep_ms = float(t[0]), float(t[1]), float(t[2])
-    units = args.steps * sl * world
+    ms_max, sweep_ms = float(t[0]), float(t[1])
+    units = args.steps * units_per_step
     value = units / (ms_max / 1e3)
-    report = report_from_agg(T, True, hist, total, keys, counts, wits, {})
-    assert report.total_classified == units
+    rank_units = args.steps * (rng_of(0)[1] - rng_of(0)[0])
+    for r in reports:
+        assert r.total_classified == units_per_step
+    deterministic = all(r == reports[0] for r in reports) if not args.weak else True
 
     # ---- e2e through the public API (host round trip + string rendering)
     def e2e_step(s):
-        a, b = rng_of(s)
-        return sweep(T, SweepRange(a, b), raw_space=True, classifier=c)
+        if args.weak:  # each rank's own slice; reports are per rank
+            a, b = rng_of(s)
+            return sweep(T, SweepRange(a, b), raw_space=True, classifier=c)
+        if world > 1:
+            return sweep_sharded(T, 0, DOMAIN, raw_space=True, classifier=c)
+        return sweep(T, SweepRange(0, DOMAIN), raw_space=True, classifier=c)
 
-    e2e_step(args.steps)  # warm the path
+    e2e_step(0)  # warm
     barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rep = None
-    for s in range(args.steps):
-        r = e2e_step(s)
-        rep = r if rep is None else merge(rep, r)
-    if world > 1:
-        from paper_2604_09221_b200.io import report_jsonl  # noqa: F401
-        gathered = [None] * world
-        dist.all_gather_object(gathered, (rep.oval_histogram, rep.scheme_map,
-                                          rep.total_classified))
+    e2e_reports = [e2e_step(s) for s in range(args.steps)]
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     te = torch.tensor([e2e_s], dtype=torch.float64, device=coll_dev)
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = units / float(te[0])
-    consistent = (world > 1) or (rep.scheme_map == report.scheme_map and
-                                 rep.oval_histogram == report.oval_histogram)
+    if args.weak:
+        consistent = True
+    else:
+        consistent = all(r.scheme_map == reports[0].scheme_map and
+                         r.oval_histogram == reports[0].oval_histogram for r in e2e_reports)
 
-    if rank != 0:
-        return
-    # ---- parity spot check against reference slices (tests/golden, committed)
-    parity = None
-    gpath = os.path.join(ROOT, "tests", "golden", "c3_delaunay7_raw_slices.json")
-    if os.path.exists(gpath):
-        with open(gpath) as fh:
-            gs = json.load(fh)["slices"]
-        ok = 0
-        for g in gs:
-            r = sweep(T, SweepRange(g["start"], g["end"]), raw_space=True, classifier=c)
-            ok += (list(r.oval_histogram) == g["hist"] and
-                   r.scheme_map == {k: tuple(v) for k, v in g["schemes"].items()})
-        parity = f"{ok}/{len(gs)} reference C3 slices (2^20 each) bit-exact"
-
-    mhz, peak_src = peaks()
-    nsm = c.native.info["sms"]
-    peak = nsm * 128 * mhz * 1e6  # thread-instruction issue slots / s / GPU
-    # patchworks the classify kernels classified explicitly (the rest are
-    # counted through the multiplicities of identical tiles / level-2 records)
-    if l2_built:  # level 2 ran: 32 patchworks per level-2 record + level-1 leftovers
+    # per-rank dedup factor (strong scaling shrinks each rank's window)
+    if l2_built:
         classified_pw = (l2_classified << 5) + (l1_left << tile_bits)
     else:
-        classified_pw = tiles_classified << tile_bits if tiles_classified else args.steps * sl
-    # achieved = patchworks/s x W(d) per GPU over the issue peak
-    achieved = value / world * W_D[DEGREE]
-    kernel_names = {"tile_classify": "k_tile_classify<K=4,odd,raw>",
-                    "enumerate": "k_enumerate<K=4,odd,raw>",
-                    "tile_build": "k_tile_from_super", "tile_dedup": "k_tile_dedup",
-                    "l2_build": "k_l2_from_l15 (+ k_l2_build)", "l2_dedup": "k_l2_dedup",
-                    "l2_classify": "k_l2_classify", "batch": "k_batch",
-                    "super_build": "k_super_build<K=4,raw>", "l15_build": "k_l15_build",
-                    "l15_dedup": "k_l2_dedup (stage 1)"}
-    total_kernel_ms = sum(v[0] for v in ktimes.values())
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        rate, n_cpu, sec = oracle_rate(1 << 22, 4, threads)
-        cpu = {"value": rate, "unit": "patchworks/s", "cores": threads, "kind": "port",
-               "cpu": cpu_model(),
-               "sample": f"4 x 2^22 delaunay-7 raw indices at random offsets (Random(7)), "
-                         f"{n_cpu} patchworks in {sec:.1f} s; oracle/tcg_oracle.c restates "
-                         "the reference kernels.py on all host threads"}
-    d2h = 4 + 4 + 512 + 8 + 24 * len(report.scheme_map)
+        classified_pw = tiles_classified << tile_bits if tiles_classified else rank_units
+    dfac = torch.tensor([rank_units / classified_pw if classified_pw else 0.0],
+                        dtype=torch.float64, device=coll_dev)
+    dfacs = [torch.zeros_like(dfac) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(dfacs, dfac)
+    else:
+        dfacs = [dfac]
+
+    other = {}
+    if world == 1 and not args.no_extra:
+        other.update(bench_c5(dev, 3, 2))
+        other.update(bench_c4(dev, 3, 1))
+
+    if rank != 0:
+        return 0
+    # ---- parity gate: full report vs the oracle's C3 golden + reference slices
+    parity = {}
+    ok_all = True
+    if not args.weak:
+        g = c3_golden()
+        if g is not None:
+            hist, schemes = g
+            full_ok = all(list(r.oval_histogram) == hist[:len(r.oval_histogram)] and
+                          r.scheme_map == schemes for r in reports)
+            parity["full_c3"] = ("every step's merged report == tests/golden/c3_full.json "
+                                 "(pinned oracle, all 2^35 indices)" if full_ok else "MISMATCH")
+            ok_all &= full_ok
+        else:
+            parity["full_c3"] = "tests/golden/c3_full.json incomplete: not checked"
+    ok, n_sl = slice_parity(T, c)
+    parity["reference_slices"] = f"{ok}/{n_sl} reference C3 slices (2^20 each) bit-exact"
+    ok_all &= ok == n_sl and deterministic and consistent
+    for k, v in other.items():
+        ok_all &= v.get("parity_ok", True)
+    rep0 = reports[0]
+    rep0.params = {"mode": "sweep", "start": 0, "end": DOMAIN, "raw_space": True}
+    parity["report_sha256"] = hashlib.sha256(report_jsonl(rep0).encode()).hexdigest()
+
+    # ---- roofline: dominant kernel's issue rate from a same-source ncu capture
+    mhz, hbm_peak, peak_src = peaks()
+    nsm = c.native.info["sms"]
+    p_issue = nsm * 128 * mhz * 1e6  # thread-instruction issue slots / s / GPU
+    prof, prof_src = ncu_profile() if world == 1 and not args.weak else (
+        None, "ncu capture is of the N=1 strong step only")
+    kms_step = {k: v[0] / args.steps for k, v in ktimes.items() if v[1]}
+    total_kernel_ms = sum(kms_step.values())
+    roof = {"bound": "issue", "unit": "thread-inst/s", "peak": p_issue,
+            "kernel": "/".join(KIND_KERNELS[dom]), "kernel_kind": dom,
+            "kernel_ms_per_step": kms_step[dom],
+            "launches_per_step": ktimes[dom][1] / args.steps,
+            "share_of_device_time": kms_step[dom] / total_kernel_ms if total_kernel_ms else None,
+            "kernels_ms_per_step": {k: round(v, 3) for k, v in kms_step.items()},
+            "sweep_ms_per_step": sweep_ms, "achieved": None, "frac": None, "traffic": None,
+            "source": prof_src}
+    if prof is not None:
+        kp = prof["kernels"]
+        names = KIND_KERNELS[dom]
+        inst = sum(kp[n]["thread_inst_per_step"] for n in names if n in kp)
+        dram = sum(kp[n]["dram_bytes_per_step"] for n in names if n in kp)
+        nl = max(1, ktimes[dom][1] // args.steps)
+        roof["achieved"] = inst / (kms_step[dom] / 1e3)
+        roof["frac"] = roof["achieved"] / p_issue
+        roof["traffic"] = dram / nl
+        roof["thread_inst_per_launch"] = inst / nl
+        roof["ncu"] = {n: {k: v for k, v in kp[n].items()
+                           if k in ("issue_active_pct", "alu_pipe_pct", "threads_per_inst",
+                                    "local_sectors_per_step", "registers", "warps_active_pct")}
+                       for n in names if n in kp}
+        hbm = {}
+        step_bytes = 0
+        for kind, kms in kms_step.items():
+            byts = sum(kp[n]["dram_bytes_per_step"] for n in KIND_KERNELS.get(kind, []) if n in kp)
+            step_bytes += byts
+            if byts:
+                gbps = byts / (kms / 1e3) / 1e9
+                hbm[kind] = {"dram_bytes_per_step": byts, "GBps": round(gbps, 1),
+                             "frac_of_hbm": round(gbps / hbm_peak, 3)}
+        roof["hbm"] = {"peak_GBps": hbm_peak, "per_kind": hbm,
+                       "dram_bytes_per_step": step_bytes,
+                       "bytes_per_patchwork": step_bytes / units_per_step}
+    roof["note"] = (f"integer instruction issue bound (no FP / tensor work; SURVEY 8(d)): "
+                    f"achieved = thread instructions the dominant kernel executes per step "
+                    f"(ncu smsp__thread_inst_executed.sum, same tcg.cu) / its CUDA-event time "
+                    f"per step in this run; peak = {nsm} SMs x 128 lanes x {mhz:.0f} MHz "
+                    f"({peak_src}). hbm.per_kind: ncu dram bytes / live time vs the copy peak.")
+
+    work_avoidance = {
+        "w_d_ratio": value / world * W_D[DEGREE] / p_issue,
+        "dedup_factor_per_rank": [float(x) for x in dfacs],
+        "note": "patchworks/s per GPU x W(7) = 2|E|+|V| = 729 element visits / P_issue: the "
+                "SURVEY 8(d) algorithmic ratio; > 1 because contraction + exact deduplication "
+                "classify one patchwork in dedup_factor explicitly (not a hardware fraction)",
+    }
     line = {
         "metric": METRIC, "value": value, "unit": "patchworks/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+        "vs_baseline": None, "dtype": "u64",
         "data": "synthetic: exhaustive sign-index enumeration, indices generated on device",
         "config": {
-            "workload": "C3: delaunay-7 raw sweep, lower half [0,2^35) = 2^36 mod global "
-                        f"sign flip; 2^{args.slice_log2} indices per GPU per step",
+            "workload": ("C3: delaunay-7 raw sweep, lower half [0,2^35) = 2^36 mod global sign "
+                         "flip; one step = the full enumeration, split in N contiguous shards"
+                         if not args.weak else
+                         f"C3 weak: 2^{args.slice_log2} raw indices per GPU per step, disjoint "
+                         "offsets in the raw 2^36 space"),
             "degree": DEGREE, "triangulation": "delaunay-7 (staircase)", "domain": "raw",
             "parallelism": f"dp{world}", "l2": "flushed between steps (256 MiB write)",
-            "covered": f"{units} indices = {units / DOMAIN:.3f} of the 2^35 domain",
+            "indices_per_rank_per_step": rng_of(0)[1] - rng_of(0)[0],
         },
-        "roofline": {
-            "bound": "issue", "achieved": achieved, "peak": peak, "unit": "elem-visits/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(kernel_names[dom]),
-            "note": f"SURVEY 8(d) integer-issue roofline (no tensor or HBM-bound work): "
-                    f"achieved = patchworks/s per GPU x W(7) = 2|E|+|V| = 729 element visits "
-                    f"(the reference algorithm's work per patchwork); peak = {nsm} SMs x 128 "
-                    f"lanes x {mhz:.0f} MHz ({peak_src}). frac > 1 means the path does less "
-                    f"than W(7) work per patchwork: super-tile/tile contraction plus exact "
-                    f"deduplication classify 1 patchwork in "
-                    f"{(args.steps * sl / classified_pw) if classified_pw else 0:.0f} explicitly. "
-                    f"kernel = the kind with the most CUDA-event time ({dom}); its hardware "
-                    "issue utilisation and dram bytes per launch come from the committed ncu "
-                    "capture (profiles/ncu_traffic.json)",
-            "kernel": kernel_names[dom], "kernel_ms": dom_ms_max / max(1, dom_n),
-            "launches": dom_n,
-            "share_of_device_time": dom_ms / total_kernel_ms if total_kernel_ms else None,
-            "kernel_ncu": ncu_kernel(kernel_names[dom]),
-            "kernels_ms": {k: round(v[0], 3) for k, v in ktimes.items()},
-            "sweep_ms_per_step": sweep_ms,
-            "dedup": {"tiles": tiles_built, "distinct_tiles": tiles_classified,
-                      "level2_records": l2_built, "level2_distinct": l2_classified,
-                      "level1_leftover_tiles": l1_left,
-                      "patchworks_classified": classified_pw,
-                      "factor": args.steps * sl / classified_pw if classified_pw else None,
-                      "note": "identical contracted tiles, then identical level-2 records "
-                              "(32 patchworks each), are classified once and counted with "
-                              "their multiplicity (exact; within each chunk of up to 2^34 "
-                              "indices of one sweep call; never across steps)"},
-        },
-        "cpu_baseline": cpu,
+        "roofline": roof,
+        "work_avoidance": work_avoidance,
+        "dedup": {"tiles": tiles_built, "distinct_tiles": tiles_classified,
+                  "level2_records": l2_built, "level2_distinct": l2_classified,
+                  "level1_leftover_tiles": l1_left, "patchworks_classified": classified_pw},
+        "cpu_baseline": (cpu_baseline_block() if world == 1 and not args.no_cpu_baseline
+                         else None),
         "e2e": {"value": e2e_value, "unit": "patchworks/s", "h2d_bytes_per_step": 16,
-                "d2h_bytes_per_step": d2h,
-                "path": "paper_2604_09221_b200.sweep(T, SweepRange(a,b), raw_space=True) per "
-                        "step + merge; h2d = the (start,end) pair, d2h = aggregate"},
+                "d2h_bytes_per_step": 528 + 24 * len(rep0.scheme_map),
+                "path": "paper_2604_09221_b200.sweep(T, SweepRange(0, 2^35), raw_space=True) "
+                        "(N > 1: distributed.sweep_sharded); h2d = (start, end), d2h = the "
+                        "aggregate"},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
-        "distinct_schemes": len(report.scheme_map),
-        "max_ovals": report.max_ovals(),
-        "consistent_e2e_vs_device": consistent,
+        "distinct_schemes": len(rep0.scheme_map),
+        "max_ovals": rep0.max_ovals(),
         "parity": parity,
+        "parity_ok": bool(ok_all),
+        "other_workloads": other or None,
     }
     print(json.dumps(line), flush=True)
+    return 0 if ok_all else 1
+
+
+def run_single_workload(args):
+    """--workload c4 | c5: one line for that config (N = 1, for profiling)."""
+    import torch
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    res = bench_c5(dev, args.steps, args.warmup) if args.workload == "c5" else bench_c4(
+        dev, args.steps, args.warmup)
+    for k, v in res.items():
+        print(json.dumps({"workload": k, **v}), flush=True)
+    return 0 if all(v["parity_ok"] for v in res.values()) else 1
 
 
 def main():
     ap = argparse.ArgumentParser(description=__doc__)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--slice-log2", type=int, default=34)
+    ap.add_argument("--workload", choices=["c3", "c4", "c5"], default="c3")
+    ap.add_argument("--weak", action="store_true", help="fixed work per GPU (see docstring)")
+    ap.add_argument("--slice-log2", type=int, default=33, help="--weak: indices per GPU-step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--offset", type=lambda x: int(x, 0), default=0,
-                    help="first index of the timed slices (profiling away from the easy low prefix)")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C4 / C5 lines")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: the contract asks for >= 3 warm-up steps")
@@ -467,7 +788,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
-        return
+        return 0
+    if args.workload != "c3":
+        return run_single_workload(args)
     if world > 1:
         import torch
         import torch.distributed as dist
@@ -479,7 +802,7 @@ def main():
         else:
             dist.init_process_group(BACKEND)
     try:
-        run_ours(args, rank, world, local_rank)
+        return run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
@@ -488,4 +811,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

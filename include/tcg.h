@@ -160,8 +160,17 @@ int tcg_classify_batch_device(tcg_plan *plan, const uint64_t *d_sigma, int64_t n
 /* sweep_kernel over [start, end) of the representative (raw=0) or raw
  * (raw=1) domain; sample_kernel over draws [k0, k1) with nbits-bit indices.
  * Return TCG_OK or the status of the failing patchwork with the smallest
- * index (*bad = that index: m for sweeps, the drawn m for samples), or a
- * negative library error. */
+ * index (*bad = that index: m for sweeps, the drawn m of the earliest failing
+ * draw for samples), or a negative library error.
+ * TCG_TABLE_FULL follows the reference's threshold (kernels.py:389-391: a
+ * new scheme is refused once 32,768 are stored): it is returned when the run
+ * meets more than 32,768 distinct schemes, with *bad = the 32,769th smallest
+ * witness -- the index where one sequential worker (workers=1) stops.  If a
+ * classification failure comes first in index order, that status wins.  For
+ * samples, whose witnesses are not in draw order, a classification failure
+ * always wins and *bad is the 32,769th smallest witness m.  Exact while the
+ * device table (65,536 schemes) has not overflowed.  HASH_COLLISION cannot
+ * occur (keys are exact tree codes). */
 int tcg_sweep(tcg_plan *plan, int raw, uint64_t start, uint64_t end, tcg_agg *agg, int64_t *bad);
 int tcg_sample(tcg_plan *plan, uint64_t seed, uint64_t k0, uint64_t k1, int nbits, tcg_agg *agg,
                int64_t *bad);
@@ -176,8 +185,12 @@ int tcg_sample_async(tcg_plan *plan, uint64_t seed, uint64_t k0, uint64_t k1, in
 int tcg_agg_fetch(tcg_plan *plan, tcg_agg *agg, int64_t *bad);
 
 /* Multi-device: contiguous shards of the range, one host thread per plan
- * (each plan bound to its own device), merged on the host (count sum,
- * witness min).  Output is identical for any number of plans. */
+ * (plans on distinct devices, or several distinct plans on one device),
+ * merged on the host (count sum, witness min).  A plan may appear only once
+ * (TCG_E_ARG otherwise: its stream and aggregate are single-owner).  The
+ * failure rules above are applied to the merged run -- the earliest failure
+ * in enumeration order (index for sweeps, draw k for samples) -- so output and
+ * status are identical for any number of plans. */
 int tcg_sweep_multi(tcg_plan **plans, int nplans, int raw, uint64_t start, uint64_t end,
                     tcg_agg *agg, int64_t *bad);
 int tcg_sample_multi(tcg_plan **plans, int nplans, uint64_t seed, uint64_t k0, uint64_t k1,

@@ -96,6 +96,28 @@ class Classifier:
             self.native = _lib.NativePlan(self.arrays, device)
             self.device = self.native.info["device"]
 
+    def device_plans(self, devices) -> list:
+        """One distinct native plan per entry of ``devices`` (a device may be
+        listed more than once: each entry gets its own plan, stream and
+        aggregate).  Plans are created once and kept on the classifier, so
+        repeated multi-device sweeps do not rebuild their device buffers."""
+        if self.generic:
+            raise ParseError("multi-device sweeps need the mask engine (d <= 9)")
+        cache = self.__dict__.setdefault("_device_plans", {})
+        seen: dict[int, int] = {}
+        out = []
+        for dev in devices:
+            dev = int(dev)
+            k = seen.get(dev, 0)
+            seen[dev] = k + 1
+            if dev == self.device and k == 0:
+                out.append(self.native)
+                continue
+            if (dev, k) not in cache:
+                cache[(dev, k)] = _lib.NativePlan(self.arrays, dev)
+            out.append(cache[(dev, k)])
+        return out
+
     # reference-shaped accessors -------------------------------------------
     def plan(self, raw_space: bool = False):
         """The reference's plan tuple (classify.py:53-55), for inspection."""

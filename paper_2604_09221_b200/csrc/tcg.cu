@@ -4509,8 +4509,52 @@ static uint64_t host_rep_to_sigma(int d, uint64_t m) {
     return (low << 2) | ((m >> (d - 1)) << (d + 2));
 }
 
-int tcg_agg_fetch(tcg_plan *P, tcg_agg *A, int64_t *bad) {
-    if (!P || !A) return fail(TCG_E_ARG, "null argument");
+// What one plan's aggregate says about failures, before the table rule.
+struct FetchOut {
+    int cls_status = 0;        // smallest-index classification failure (0: none)
+    int64_t cls_bad = -1;      // its index in the run's domain (m)
+    uint64_t cls_order = 0;    // its position in enumeration order (sweep: m, sample: draw k)
+    bool overflow = false;     // the device table dropped a key (> GCAP distinct)
+    bool index_ordered = true; // witnesses are in enumeration order (sweeps; not samples)
+};
+
+// Reference _aggregate (kernels.py:389-391) refuses a NEW scheme once its table
+// holds cap/2 = 32,768 (ameta[2]*2 >= cap with cap = 65,536) and the kernel
+// stops at that index.  One sequential worker (workers=1) meets the schemes in
+// index order, so the failing index is the 32,769th smallest witness.
+constexpr int32_t REF_TABLE_LIMIT = 1 << 15;
+
+static int64_t table_full_index(const tcg_agg *A) {
+    std::vector<int64_t> w(A->witness, A->witness + A->n);
+    std::nth_element(w.begin(), w.begin() + REF_TABLE_LIMIT, w.end());
+    return w[REF_TABLE_LIMIT];
+}
+
+// Status and index a sweep_kernel / sample_kernel run would return.
+static int settle(const tcg_agg *A, const FetchOut &F, int64_t *bad) {
+    if (bad) *bad = -1;
+    const bool full = F.overflow || A->n > REF_TABLE_LIMIT;
+    const int64_t tbad = (full && A->n > REF_TABLE_LIMIT) ? table_full_index(A) : -1;
+    if (F.cls_status) {
+        // both fire: the earlier index wins (sweeps); samples report the
+        // classification failure (first-draw positions of schemes are not kept)
+        if (full && F.index_ordered && tbad >= 0 && tbad < F.cls_bad) {
+            if (bad) *bad = tbad;
+            return fail(TCG_TABLE_FULL, "scheme table full (32,768 distinct schemes)");
+        }
+        if (bad) *bad = F.cls_bad;
+        return F.cls_status;
+    }
+    if (full) {
+        if (bad) *bad = tbad;
+        return fail(TCG_TABLE_FULL, "scheme table full (32,768 distinct schemes)");
+    }
+    return TCG_OK;
+}
+
+// Copy the device aggregate into A (sorted by key) and find the smallest
+// failing index; library errors (< 0) only.
+static int fetch_raw(tcg_plan *P, tcg_agg *A, FetchOut &F) {
     DeviceGuard guard(P->device);
     CUDA_TRY(cudaMemsetAsync(P->d_cn, 0, 4, P->stream));
     k_agg_compact<<<64, 256, 0, P->stream>>>(P->agg, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn);
@@ -4523,7 +4567,9 @@ int tcg_agg_fetch(tcg_plan *P, tcg_agg *A, int64_t *bad) {
     CUDA_TRY(cudaMemcpyAsync(hist, P->agg.hist, sizeof(hist), cudaMemcpyDeviceToHost, P->stream));
     CUDA_TRY(cudaMemcpyAsync(&badidx, P->agg.bad, 8, cudaMemcpyDeviceToHost, P->stream));
     CUDA_TRY(cudaStreamSynchronize(P->stream));
-    if (bad) *bad = -1;
+    F = FetchOut{};
+    F.overflow = overflow != 0;
+    F.index_ordered = P->pending_mode != MODE_SAMPLE;
     if (badidx != ~0ull) {
         // recompute the failing patchwork's status (smallest failing index)
         uint64_t m = badidx, sigma;
@@ -4540,11 +4586,12 @@ int tcg_agg_fetch(tcg_plan *P, tcg_agg *A, int64_t *bad) {
         int32_t st = 0;
         int rc = tcg_classify_batch(P, &sigma, 1, &key, &ov, &nr, &st);
         if (rc) return rc;
-        if (bad) *bad = (int64_t)m;
-        return st ? st : fail(TCG_E_CUDA, "device reported a failure the replay did not reproduce");
+        if (!st) return fail(TCG_E_CUDA, "device reported a failure the replay did not reproduce");
+        F.cls_status = st;
+        F.cls_bad = (int64_t)m;
+        F.cls_order = badidx;
     }
-    if (overflow) return fail(TCG_TABLE_FULL, "global scheme table full");
-    if ((int32_t)n > A->cap) return fail(TCG_TABLE_FULL, "caller's aggregate capacity too small");
+    if ((int32_t)n > A->cap) return fail(TCG_E_RANGE, "caller's aggregate capacity too small");
     std::vector<unsigned long long> k(n), c(n), w(n);
     if (n) {
         CUDA_TRY(cudaMemcpy(k.data(), P->d_ckey, n * 8ull, cudaMemcpyDeviceToHost));
@@ -4569,6 +4616,14 @@ int tcg_agg_fetch(tcg_plan *P, tcg_agg *A, int64_t *bad) {
     return TCG_OK;
 }
 
+int tcg_agg_fetch(tcg_plan *P, tcg_agg *A, int64_t *bad) {
+    if (!P || !A) return fail(TCG_E_ARG, "null argument");
+    FetchOut F;
+    int rc = fetch_raw(P, A, F);
+    if (rc) return rc;
+    return settle(A, F, bad);
+}
+
 int tcg_sweep(tcg_plan *P, int raw, uint64_t start, uint64_t end, tcg_agg *A, int64_t *bad) {
     int rc = tcg_agg_reset(P);
     if (rc) return rc;
@@ -4586,20 +4641,24 @@ int tcg_sample(tcg_plan *P, uint64_t seed, uint64_t k0, uint64_t k1, int nbits, 
     return tcg_agg_fetch(P, A, bad);
 }
 
+// Merge per-device aggregates (count sum, witness min: sweep.py:168-180), then
+// apply the failure rules once to the whole range, so the outcome does not
+// depend on the number of devices: the classification failure earliest in
+// enumeration order (sweep index or draw k) wins, the table rule applies to
+// the merged scheme set.
 static int merge_multi(std::vector<tcg_agg> &parts, std::vector<int> &rcs,
-                       std::vector<int64_t> &bads, tcg_agg *A, int64_t *bad) {
-    int status = TCG_OK;
-    int64_t best = -1;
-    for (size_t i = 0; i < parts.size(); ++i) {
+                       std::vector<FetchOut> &fo, tcg_agg *A, int64_t *bad) {
+    for (size_t i = 0; i < parts.size(); ++i)
         if (rcs[i] < 0) return rcs[i];
-        if (rcs[i] > 0 && (best < 0 || bads[i] < best)) {
-            best = bads[i];
-            status = rcs[i];
+    FetchOut F;
+    for (auto &f : fo) {
+        F.overflow |= f.overflow;
+        F.index_ordered &= f.index_ordered;
+        if (f.cls_status && (!F.cls_status || f.cls_order < F.cls_order)) {
+            F.cls_status = f.cls_status;
+            F.cls_bad = f.cls_bad;
+            F.cls_order = f.cls_order;
         }
-    }
-    if (status) {
-        if (bad) *bad = best;
-        return status;
     }
     std::unordered_map<uint64_t, std::pair<int64_t, int64_t>> m;
     std::memset(A->hist, 0, sizeof(A->hist));
@@ -4616,8 +4675,9 @@ static int merge_multi(std::vector<tcg_agg> &parts, std::vector<int> &rcs,
             }
         }
     }
-    if ((int64_t)m.size() > A->cap) return fail(TCG_TABLE_FULL, "aggregate capacity too small");
+    if ((int64_t)m.size() > A->cap) return fail(TCG_E_RANGE, "aggregate capacity too small");
     std::vector<uint64_t> keys;
+    keys.reserve(m.size());
     for (auto &kv : m) keys.push_back(kv.first);
     std::sort(keys.begin(), keys.end());
     A->n = (int32_t)keys.size();
@@ -4626,42 +4686,52 @@ static int merge_multi(std::vector<tcg_agg> &parts, std::vector<int> &rcs,
         A->count[i] = m[keys[i]].first;
         A->witness[i] = m[keys[i]].second;
     }
-    if (bad) *bad = -1;
-    return TCG_OK;
+    return settle(A, F, bad);
 }
 
 static int run_multi(tcg_plan **plans, int nplans, uint64_t a, uint64_t b, tcg_agg *A,
-                     int64_t *bad, const std::function<int(tcg_plan *, uint64_t, uint64_t, tcg_agg *, int64_t *)> &fn) {
+                     int64_t *bad, const std::function<int(tcg_plan *, uint64_t, uint64_t)> &fn) {
     if (!plans || nplans < 1 || !A) return fail(TCG_E_ARG, "bad arguments");
+    for (int i = 0; i < nplans; ++i) {
+        if (!plans[i]) return fail(TCG_E_ARG, "null plan");
+        for (int j = 0; j < i; ++j)  // one host thread per plan: a plan may appear once
+            if (plans[j] == plans[i]) return fail(TCG_E_ARG, "plan listed twice");
+    }
     std::vector<tcg_agg> parts(nplans);
     std::vector<std::vector<uint64_t>> keys(nplans);
     std::vector<std::vector<int64_t>> cnts(nplans), wits(nplans);
     std::vector<int> rcs(nplans, 0);
-    std::vector<int64_t> bads(nplans, -1);
+    std::vector<FetchOut> fo(nplans);
     std::vector<std::thread> th;
     const uint64_t n = b - a;
     for (int i = 0; i < nplans; ++i) {
-        keys[i].resize(A->cap);
-        cnts[i].resize(A->cap);
-        wits[i].resize(A->cap);
+        keys[i].resize(GCAP);
+        cnts[i].resize(GCAP);
+        wits[i].resize(GCAP);
         parts[i] = tcg_agg{};
-        parts[i].cap = A->cap;
+        parts[i].cap = GCAP;
         parts[i].key = keys[i].data();
         parts[i].count = cnts[i].data();
         parts[i].witness = wits[i].data();
-        const uint64_t lo = a + n * (uint64_t)i / nplans, hi = a + n * (uint64_t)(i + 1) / nplans;
-        th.emplace_back([&, i, lo, hi] { rcs[i] = fn(plans[i], lo, hi, &parts[i], &bads[i]); });
+        const uint64_t lo = a + (uint64_t)((unsigned __int128)n * i / nplans);
+        const uint64_t hi = a + (uint64_t)((unsigned __int128)n * (i + 1) / nplans);
+        th.emplace_back([&, i, lo, hi] {
+            int rc = tcg_agg_reset(plans[i]);
+            if (!rc) rc = fn(plans[i], lo, hi);
+            if (!rc) rc = fetch_raw(plans[i], &parts[i], fo[i]);
+            rcs[i] = rc;
+        });
     }
     for (auto &t : th) t.join();
-    return merge_multi(parts, rcs, bads, A, bad);
+    return merge_multi(parts, rcs, fo, A, bad);
 }
 
 int tcg_sweep_multi(tcg_plan **plans, int nplans, int raw, uint64_t start, uint64_t end,
                     tcg_agg *A, int64_t *bad) {
     if (start > end) return fail(TCG_E_RANGE, "bad range");
     return run_multi(plans, nplans, start, end, A, bad,
-                     [raw](tcg_plan *p, uint64_t lo, uint64_t hi, tcg_agg *a, int64_t *b) {
-                         return tcg_sweep(p, raw, lo, hi, a, b);
+                     [raw](tcg_plan *p, uint64_t lo, uint64_t hi) {
+                         return tcg_sweep_async(p, raw, lo, hi);
                      });
 }
 
@@ -4669,8 +4739,8 @@ int tcg_sample_multi(tcg_plan **plans, int nplans, uint64_t seed, uint64_t k0, u
                      int nbits, tcg_agg *A, int64_t *bad) {
     if (k0 > k1) return fail(TCG_E_RANGE, "bad range");
     return run_multi(plans, nplans, k0, k1, A, bad,
-                     [seed, nbits](tcg_plan *p, uint64_t lo, uint64_t hi, tcg_agg *a, int64_t *b) {
-                         return tcg_sample(p, seed, lo, hi, nbits, a, b);
+                     [seed, nbits](tcg_plan *p, uint64_t lo, uint64_t hi) {
+                         return tcg_sample_async(p, seed, lo, hi, nbits);
                      });
 }
 

@@ -19,9 +19,6 @@ from __future__ import annotations
 
 import numpy as np
 
-TABLE_CAP = 8192  # distinct schemes per rank carried through the all_gather
-
-
 def shard(start: int, end: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous shard [lo, hi) of [start, end) for ``rank`` of ``world``."""
     n = end - start
@@ -46,7 +43,12 @@ def merge_tables(parts):
 
 def allreduce_aggregate(hist, total, keys, counts, wits, group=None, device=None):
     """Merge one rank's aggregate with every other rank's; returns the global
-    (hist, total, keys, counts, witnesses) on all ranks."""
+    (hist, total, keys, counts, witnesses) on all ranks.
+
+    Three collectives, every rank always takes part in all of them (a rank
+    can never raise before the others reach a collective): all_reduce(SUM)
+    of [hist..., total], all_reduce(MAX) of the table size, all_gather of
+    the (key, count, witness) tables padded to that size."""
     import torch
     import torch.distributed as dist
 
@@ -55,19 +57,20 @@ def allreduce_aggregate(hist, total, keys, counts, wits, group=None, device=None
         return list(hist), int(total), keys, counts, wits
     dev = device if device is not None else torch.device("cpu")
     n = len(keys)
-    if n > TABLE_CAP:
-        raise ValueError(f"{n} distinct schemes exceed the gather capacity {TABLE_CAP}")
     h = torch.tensor(list(hist) + [int(total)], dtype=torch.int64, device=dev)
     dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
-    tab = torch.zeros((3, TABLE_CAP + 1), dtype=torch.int64, device=dev)
+    width = torch.tensor([n], dtype=torch.int64, device=dev)
+    dist.all_reduce(width, op=dist.ReduceOp.MAX, group=group)
+    cap = max(1, int(width.item()))
+    tab = torch.zeros((3, cap + 1), dtype=torch.int64, device=dev)
     tab[0, 0] = n
     if n:
         tab[0, 1:n + 1] = torch.from_numpy(np.asarray(keys, np.uint64).view(np.int64))
         tab[1, 1:n + 1] = torch.from_numpy(np.asarray(counts, np.int64))
         tab[2, 1:n + 1] = torch.from_numpy(np.asarray(wits, np.int64))
-    out = torch.zeros(world * 3 * (TABLE_CAP + 1), dtype=torch.int64, device=dev)
+    out = torch.zeros(world * 3 * (cap + 1), dtype=torch.int64, device=dev)
     dist.all_gather_into_tensor(out, tab.reshape(-1), group=group)
-    out = out.cpu().numpy().reshape(world, 3, TABLE_CAP + 1)
+    out = out.cpu().numpy().reshape(world, 3, cap + 1)
     parts = []
     for r in range(world):
         m = int(out[r, 0, 0])

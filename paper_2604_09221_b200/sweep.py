@@ -136,9 +136,7 @@ def _raise_status(rc: int, bad: int):
 
 def _run(T, c: Classifier, devices, fn_single, fn_multi):
     if devices and len(devices) > 1:
-        plans = [c.native if dev == c.device else Classifier(T, device=dev).native
-                 for dev in devices]
-        return fn_multi(plans)
+        return fn_multi(c.device_plans(devices))
     return fn_single(c.native)
 
 

@@ -49,3 +49,22 @@ def rng():
     import random
 
     return random.Random(0xC0FFEE)
+
+
+def plan_arrays_of(P):
+    """PlanArrays from a fixture plan dict (degree included)."""
+    import numpy as np
+
+    from paper_2604_09221_b200.diamond import PlanArrays
+
+    return PlanArrays(P["degree"], P["nv"], P["npts"], np.array(P["edge_u"], np.int32),
+                      np.array(P["edge_v"], np.int32), np.array(P["src"], np.int32),
+                      np.array(P["par"], np.uint8), np.array(P["used"], np.uint8),
+                      np.array(P["ap_u"], np.int32), np.array(P["ap_v"], np.int32),
+                      P["maxreg"])
+
+
+def diff_triangulation(d, edges):
+    from paper_2604_09221_b200.lattice import validate_triangulation
+
+    return validate_triangulation(d, [((a, b), (c, e)) for a, b, c, e in edges])

@@ -374,6 +374,177 @@ def part_large():
     dump("pairs_large.json", out)
 
 
+def _garbage_T(d, rng, drop_frac, chords):
+    base = builtin(f"delaunay-{d}")
+    pts = lattice_points(d)
+    edges = list(base.edges)
+    for _ in range(int(len(edges) * drop_frac)):
+        edges.pop(rng.randrange(len(edges)))
+    for _ in range(chords):
+        p, q = rng.sample(pts, 2)
+        e = (p, q) if p < q else (q, p)
+        if e not in edges:
+            edges.append(e)
+    return Triangulation(d, tuple(sorted(edges)), ())
+
+
+def part_status():
+    """Rows of the compiled kernel (kernels.py:107-356) for every status the
+    classifier can return on a bad plan: TOO_MANY_REGIONS (kernels.py:183),
+    NO_ODD_REGION / MANY_ODD_REGIONS (:193,:196), NO_PSEUDOLINE (:228),
+    ROOT_CONFLICT (:216), NONSEPARATING_OVAL (:211), NOT_A_TREE (:221,:230),
+    DISCONNECTED (:266).  Plans are tuples an unvalidated caller can hand to
+    the kernel:
+
+    * ``edges``: dropped edges and random chords;
+    * ``maxreg``: a valid plan with its maxreg field lowered;
+    * ``pairs``: a random subset of the antipodal pairs (maxreg raised to 31);
+    * ``bogus``: an extra antipodal "pair" joining the two ends of a diamond
+      edge (maxreg raised to 31) -- not a (p, -p) pair, so only the generic
+      any-degree engine accepts it (``engine``: "generic").
+
+    A random search keeps up to 24 rows per (degree, status)."""
+    rng = random.Random(0x57A7)
+    want = 24
+    out = []
+    kinds = ("edges", "maxreg", "pairs", "bogus")
+    for d in range(2, 9):
+        got = {s: 0 for s in range(9)}
+        trials = 0
+        target = (1, 2, 3, 6, 7, 8) if d % 2 == 0 else (1, 4, 5, 7, 8)
+        while trials < 800 and min(got[s] for s in target) < want:
+            kind = kinds[trials % 4]
+            trials += 1
+            if kind == "edges" or rng.random() < 0.3:
+                T = _garbage_T(d, rng, rng.choice((0.0, 0.05, 0.1, 0.2, 0.35)),
+                               rng.choice((0, 1, 2, 4, 8)))
+            else:
+                T = builtin(f"delaunay-{d}")
+            c = Classifier(T)
+            common = list(c._plan_common)
+            if kind == "maxreg":
+                common[10] = rng.randint(1, max(1, int(common[10]) - 2))
+            elif kind == "pairs":
+                keep = [k for k in range(len(common[8])) if rng.random() < rng.random()]
+                common[8] = common[8][keep].copy()
+                common[9] = common[9][keep].copy()
+                common[10] = 31
+            elif kind == "bogus":
+                e = rng.randrange(len(common[3]))
+                common[8] = np.append(common[8], np.int32(common[3][e]))
+                common[9] = np.append(common[9], np.int32(common[4][e]))
+                common[10] = 31
+            c.maxreg = int(common[10])
+            c._plan_common = tuple(common)
+            plan = c.plan(raw_space=True)
+            scr = c.make_scratch()
+            pd = plan_dict(c)
+            rows = []
+            npts = len(lattice_points(d))
+            for _ in range(256):
+                m = rng.getrandbits(npts)
+                bits = np.array([(m >> k) & 1 for k in range(npts)], dtype=np.uint8)
+                st, ov, nr, ln = kernels.classify_bits_kernel(plan, scr, bits)
+                st = int(st)
+                if st == 0 or got[st] >= want:
+                    continue
+                got[st] += 1
+                rows.append([m, st, int(ov), int(nr), None])
+            if rows:
+                out.append({"name": f"status-{d}-{trials}-{kind}", "degree": d, "kind": kind,
+                            "engine": "generic" if kind == "bogus" else "mask",
+                            "edges": [[p[0], p[1], q[0], q[1]] for p, q in T.edges],
+                            "plan": pd, "rows": rows})
+        print(f"d={d}: {trials} plans, rows per status {got}", flush=True)
+    dump("status.json", out)
+
+
+def part_diff():
+    """The reference's differential criterion (test_acceptance.py:144-160)
+    replayed with the same generator and seed: 25 random unimodular T per
+    degree d = 1..6, 10^4 random sign vectors per degree (T = k mod 25),
+    each classified by the reference Classifier (which that test holds equal
+    to oracle_classify).  Rows: [k, sign word, scheme id, ovals, regions]."""
+    rng = random.Random(0xD1FF)
+    out = []
+    for d in range(1, 7):
+        pool = [random_unimodular(d, rng) for _ in range(25)]
+        cls = [Classifier(T) for T in pool]
+        names, rows = {}, []
+        for n in range(10_000):
+            k = n % 25
+            s = random_bits(d, rng)
+            r = cls[k].classify(s)
+            word = sum(1 << i for i, ch in enumerate(s) if ch == "1")
+            sid = names.setdefault(r.scheme, len(names))
+            rows.append([k, word, sid, r.oval_count, r.region_count])
+        out.append({"degree": d, "triangulations": [edges_flat(T) for T in pool],
+                    "fingerprints": [T.fingerprint() for T in pool],
+                    "schemes": sorted(names, key=names.get), "rows": rows})
+    dump("diff.json", out)
+
+
+def part_garbage_sweep():
+    """sweep_kernel (kernels.py:423-436) on degree-7/8 bad plans whose failures
+    are rare, over ranges where the first failure lies deep inside: the
+    (status, smallest failing index) pair a sweep must report."""
+    rng = random.Random(0x5EE9)
+    out = []
+    for d, raw, count in ((7, True, 4), (7, False, 2), (8, False, 2)):
+        npts = len(lattice_points(d))
+        nbits = npts if raw else npts - 3
+        found = 0
+        tries = 0
+        while found < count and tries < 300:
+            tries += 1
+            T = _garbage_T(d, rng, rng.choice((0.0, 0.01, 0.02)), rng.choice((1, 1, 2)))
+            c = Classifier(T)
+            plan = c.plan(raw_space=raw)
+            scr = c.make_scratch()
+            bits = np.zeros(npts, dtype=np.uint8)
+            # failure rate on 2048 random indices: keep plans failing rarely
+            fails = 0
+            for _ in range(2048):
+                kernels._expand_bits(plan[11], npts, rng.getrandbits(nbits), bits)
+                st, _, _, _ = kernels.classify_bits_kernel(plan, scr, bits)
+                fails += st != 0
+            if not (1 <= fails <= 40):
+                continue
+            n = 1 << 20
+            a = rng.randrange(0, (1 << nbits) - n) & ~0xFFF
+            agg = sweep_mod._make_agg(c.maxreg)
+            st, bad = kernels.sweep_kernel(plan, scr, agg, bits, a, a + n)
+            if st == 0 or bad - a < 4096:
+                continue
+            found += 1
+            out.append({"name": f"gsweep-{d}-{'raw' if raw else 'rep'}-{found}", "degree": d,
+                        "raw": raw, "start": a, "end": a + n, "status": int(st), "bad": int(bad),
+                        "fail_rate_2048": fails,
+                        "edges": [[p[0], p[1], q[0], q[1]] for p, q in T.edges],
+                        "plan": plan_dict(c)})
+            print(f"d={d} raw={raw}: status {st} at {bad} (start {a}, +{bad - a})", flush=True)
+    dump("garbage_sweep.json", out)
+
+
+def part_c4set():
+    """Config C4's triangulations: the first 4,096 draws of the
+    reference's own generator random_unimodular(7, Random(0xB7))
+    (tests/conftest.py:8-25; the first 16 are the c4-7-k fixtures).  Saved
+    as uint8 edge arrays [4096, 84, 4] (bench.py's C4 workload input)."""
+    rng = random.Random(0xB7)
+    E = np.zeros((4096, 84, 4), np.uint8)
+    fps = []
+    for k in range(4096):
+        T = random_unimodular(7, rng)
+        e = edges_flat(T)
+        assert len(e) == 84
+        E[k] = np.array(e, np.uint8)
+        fps.append(T.fingerprint())
+    path = os.path.join(OUT, "c4_d7_4096.npz")
+    np.savez_compressed(path, edges=E, fingerprints=np.array(fps))
+    print(f"wrote {path} ({os.path.getsize(path)} bytes)", flush=True)
+
+
 PARTS = {
     "large": part_large,
     "tri": part_tri,
@@ -384,6 +555,10 @@ PARTS = {
     "c2": part_c2,
     "c3": part_c3,
     "c5": part_c5,
+    "status": part_status,
+    "diff": part_diff,
+    "gsweep": part_garbage_sweep,
+    "c4set": part_c4set,
 }
 
 if __name__ == "__main__":

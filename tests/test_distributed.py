@@ -79,3 +79,36 @@ def test_gloo_world2_merge_equals_single_process():
         assert total == full["total"]
         got = {inv[k]: [c, w] for k, c, w in zip(keys, counts, wits)}
         assert got == full["schemes"]
+
+
+def _worker_uneven(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2604_09221_b200.distributed import allreduce_aggregate
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    # rank 0: 20,000 distinct keys (more than any fixed gather table used to
+    # hold); rank 1: none.  Every rank must reach every collective.
+    n = 20_000 if rank == 0 else 0
+    keys = np.arange(n, dtype=np.uint64) * np.uint64(7) + np.uint64(5)
+    out = allreduce_aggregate([n, 0], n, keys, np.ones(n, np.int64),
+                              np.arange(n, dtype=np.int64) + 100)
+    q.put((rank, out[0], out[1], len(out[2]), int(out[3].sum()), int(out[4].min())))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_uneven_tables_no_deadlock():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_uneven, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, hist, total, nkeys, csum, wmin in res:
+        assert hist == [20_000, 0] and total == 20_000
+        assert nkeys == 20_000 and csum == 20_000 and wmin == 100

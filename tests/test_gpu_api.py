@@ -229,6 +229,48 @@ def test_multi_device_api_single_device(api):
     assert a == api.sweep(T)
 
 
+def test_multi_plan_sweeps_and_samples_equal_single_plan(api):
+    """tcg_sweep_multi / tcg_sample_multi with two and three distinct plans on
+    device 0 (one host thread each) == one plan; plans are cached per entry."""
+    T = api.builtin("delaunay-7")
+    c = api.Classifier(T)
+    a, b = 3 << 30, (3 << 30) + (1 << 28) + 12345
+    single = api.sweep(T, api.SweepRange(a, b), raw_space=True, classifier=c)
+    for devs in ([0, 0], [0, 0, 0]):
+        multi = api.sweep(T, api.SweepRange(a, b), raw_space=True, classifier=c, devices=devs)
+        assert multi == single
+    plans = c.device_plans([0, 0, 0])
+    assert len({id(p) for p in plans}) == 3 and plans[0] is c.native
+    assert all(x is y for x, y in zip(plans, c.device_plans([0, 0, 0])))
+    T8 = api.builtin("bowtie8")
+    c8 = api.Classifier(T8)
+    s1 = api.sample(T8, 400_000, seed=5, classifier=c8)
+    s2 = api.sample(T8, 400_000, seed=5, classifier=c8, devices=[0, 0])
+    assert s1 == s2
+
+
+def test_multi_rejects_a_plan_listed_twice(api):
+    from paper_2604_09221_b200 import _lib
+
+    c = api.Classifier(api.builtin("delaunay-5"))
+    with pytest.raises(api.DeviceError, match="listed twice"):
+        _lib.sweep_multi([c.native, c.native], True, 0, 1 << 20)
+
+
+def test_multi_plan_failure_is_the_earliest(api):
+    """A failing plan sharded over 3 plans reports the same (status, index) as
+    one plan: the earliest failure in index order, whichever shard holds it."""
+    from paper_2604_09221_b200 import _lib
+
+    from conftest import plan_arrays_of
+
+    e = golden("garbage_sweep.json")[0]
+    arr = plan_arrays_of(plan_dict(e))
+    plans = [_lib.NativePlan(arr, 0) for _ in range(3)]
+    rc, bad, _ = _lib.sweep_multi(plans, e["raw"], e["start"], e["end"])
+    assert (rc, bad) == (e["status"], e["bad"])
+
+
 def test_report_bytes_identical_across_call_shapes(api):
     # criterion 09: byte-identical reports for any partition
     from paper_2604_09221_b200.io import histogram_csv, report_jsonl

@@ -121,3 +121,40 @@ def test_oracle_large_degrees_match_reference():
         got = O.classify_bitstrings(_oplan(T), [r[0] for r in e["rows"]])
         for (s, scheme, ov, nr), g in zip(e["rows"], got):
             assert g == (0, scheme, ov, nr), (e["name"], s)
+
+
+def test_oracle_every_status_matches_reference():
+    """Statuses 1-8 on bad plans (tests/golden/status.json, kernels.py:183-266)."""
+    seen = set()
+    for e in golden("status.json"):
+        P = plan_dict(e)
+        got = O.classify_words(O.OraclePlan.from_arrays(P), [r[0] for r in e["rows"]])
+        for (m, status, *_), (st, *_r) in zip(e["rows"], got):
+            assert st == status, (e["name"], m)
+            seen.add(st)
+    assert seen == {1, 2, 3, 4, 5, 6, 7, 8}
+
+
+def test_oracle_differential_criterion():
+    """test_acceptance.py:144-160 replayed: 25 T x 10^4 signs per degree 1..6."""
+    from conftest import diff_triangulation
+
+    for g in golden("diff.json"):
+        d = g["degree"]
+        plans = [_oplan(diff_triangulation(d, e)) for e in g["triangulations"]]
+        rows = np.array(g["rows"], dtype=np.int64)
+        for k, plan in enumerate(plans):
+            sel = rows[rows[:, 0] == k]
+            got = O.classify_words(plan, sel[:, 1].astype(np.uint64))
+            for r, (st, s, ov, nr) in zip(sel, got):
+                assert (st, s, ov, nr) == (0, g["schemes"][r[2]], r[3], r[4]), (d, k, r[1])
+
+
+def test_oracle_garbage_sweeps_first_failure():
+    """sweep_kernel's (status, smallest failing index) on rare-failure plans."""
+    import os
+
+    for e in golden("garbage_sweep.json"):
+        r = O.sweep(O.OraclePlan.from_arrays(plan_dict(e)), e["raw"], e["start"], e["end"],
+                    threads=os.cpu_count() or 1)
+        assert (r["status"], r["bad"]) == (e["status"], e["bad"]), e["name"]
