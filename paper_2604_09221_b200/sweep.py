@@ -42,9 +42,6 @@ class SweepRange:
         if self.start < 0 or self.end < self.start:
             raise IndexOutOfRange(f"bad sweep range [{self.start}, {self.end})")
 
-    def __len__(self) -> int:
-        return self.end - self.start
-
 
 @dataclass
 class SweepReport:
@@ -146,7 +143,7 @@ def sweep(T, sweep_range: SweepRange | None = None, workers: int = 1, raw_space:
     """Classify every sign index in the range (default: the whole domain)."""
     bits = _domain_bits(T.degree, raw_space)
     domain = 1 << bits
-    r = sweep_range or SweepRange(0, domain)
+    r = sweep_range if sweep_range is not None else SweepRange(0, domain)
     if r.end > domain:
         raise IndexOutOfRange(f"sweep range end {r.end} exceeds domain size {domain}")
     c = _classifier_for(T, classifier, devices[0] if devices else None)
