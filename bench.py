@@ -354,7 +354,8 @@ def bench_c5(dev, steps, warmup):
     for name in ("bowtie8", "delaunay-8"):
         T = builtin(name)
         c = Classifier(T, device=dev.index)
-        stream = torch.cuda.current_stream(dev)
+        stream = torch.cuda.Stream(device=dev)  # events and kernels on one stream
+        torch.cuda.set_stream(stream)
         c.native.set_stream(stream.cuda_stream)
         for s in range(warmup):
             c.native.agg_reset()

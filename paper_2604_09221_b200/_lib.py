@@ -213,10 +213,10 @@ class NativeMulti:
         n = len(w)
         if len(t) != n:
             raise ValueError("tri and words must have the same length")
-        key = np.zeros(n, np.uint64)
-        ov = np.zeros(n, np.uint8)
-        nr = np.zeros(n, np.uint8)
-        st = np.zeros(n, np.int32)
+        key = np.empty(n, np.uint64)
+        ov = np.empty(n, np.uint8)
+        nr = np.empty(n, np.uint8)
+        st = np.empty(n, np.int32)
         if n:
             _check(self._L.tcg_multi_classify(self.h, t.ctypes.data, w.ctypes.data, n,
                                               key.ctypes.data, ov.ctypes.data, nr.ctypes.data,
@@ -356,10 +356,10 @@ class NativePlan:
     def classify_words(self, words):
         w = np.ascontiguousarray(words, dtype=np.uint64)
         n = len(w)
-        key = np.zeros(n, np.uint64)
-        ov = np.zeros(n, np.uint8)
-        nr = np.zeros(n, np.uint8)
-        st = np.zeros(n, np.int32)
+        key = np.empty(n, np.uint64)
+        ov = np.empty(n, np.uint8)
+        nr = np.empty(n, np.uint8)
+        st = np.empty(n, np.int32)
         if n:
             _check(self._L.tcg_classify_batch(self.h, w.ctypes.data, n, key.ctypes.data,
                                               ov.ctypes.data, nr.ctypes.data, st.ctypes.data),

@@ -4851,20 +4851,29 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
     if (n <= 0) return TCG_OK;
     if (n > INT32_MAX) return fail(TCG_E_RANGE, "at most 2^31-1 pairs per call");
     DeviceGuard guard(M->device);
-    // counting sort of the pairs by triangulation; items of <= 2048 pairs
+    // pairs grouped by triangulation (a counting sort unless the caller's
+    // triangulation ids are already non-decreasing, e.g. config C4's layout);
+    // work items of <= 2048 pairs of one triangulation
     constexpr int ITEM = 2048;
     std::vector<int64_t> cnt(M->ntri + 1, 0);
+    bool grouped = true;
     for (int64_t i = 0; i < n; ++i) {
         if (tri[i] < 0 || tri[i] >= M->ntri) return fail(TCG_E_ARG, "triangulation index out of range");
         cnt[tri[i] + 1]++;
+        grouped &= i == 0 || tri[i] >= tri[i - 1];
     }
     for (int t = 0; t < M->ntri; ++t) cnt[t + 1] += cnt[t];
-    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1), order(n);
-    std::vector<uint64_t> ssig(n);
-    for (int64_t i = 0; i < n; ++i) {
-        const int64_t j = pos[tri[i]]++;
-        order[j] = i;
-        ssig[j] = sig[i];
+    std::vector<int64_t> order;
+    std::vector<uint64_t> ssig;
+    if (!grouped) {
+        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+        order.resize(n);
+        ssig.resize(n);
+        for (int64_t i = 0; i < n; ++i) {
+            const int64_t j = pos[tri[i]]++;
+            order[j] = i;
+            ssig[j] = sig[i];
+        }
     }
     std::vector<int4> items;
     for (int t = 0; t < M->ntri; ++t)
@@ -4890,7 +4899,8 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
         CUDA_TRY(cudaMalloc(&M->d_items, sizeof(int4) * items.size()));
         M->items_cap = (int64_t)items.size();
     }
-    CUDA_TRY(cudaMemcpyAsync(M->d_sig, ssig.data(), n * 8, cudaMemcpyHostToDevice, M->stream));
+    CUDA_TRY(cudaMemcpyAsync(M->d_sig, grouped ? sig : ssig.data(), n * 8, cudaMemcpyHostToDevice,
+                             M->stream));
     CUDA_TRY(cudaMemcpyAsync(M->d_items, items.data(), sizeof(int4) * items.size(),
                              cudaMemcpyHostToDevice, M->stream));
     void *fn = pick_multi(M->K, M->even);
@@ -4904,6 +4914,17 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
                               M->stream));
     cudaEventRecord(e1, M->stream);
     M->launches++;
+    if (grouped) {  // outputs are already in the caller's order
+        CUDA_TRY(cudaMemcpyAsync(key, M->d_key, n * 8, cudaMemcpyDeviceToHost, M->stream));
+        CUDA_TRY(cudaMemcpyAsync(ov, M->d_ov, n, cudaMemcpyDeviceToHost, M->stream));
+        CUDA_TRY(cudaMemcpyAsync(nr, M->d_nr, n, cudaMemcpyDeviceToHost, M->stream));
+        CUDA_TRY(cudaMemcpyAsync(st, M->d_st, n * 4, cudaMemcpyDeviceToHost, M->stream));
+        CUDA_TRY(cudaStreamSynchronize(M->stream));
+        cudaEventElapsedTime(&M->last_ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return TCG_OK;
+    }
     std::vector<uint64_t> k(n);
     std::vector<uint8_t> o(n), r(n);
     std::vector<int32_t> s(n);
