@@ -47,6 +47,17 @@
 
 #define TCG_VERSION "tcg 0.1.0 sm_100a"
 
+// Bounds-checked build (-DTCG_CHECKED, scripts/gpu_checked.sh): device
+// asserts on the computed indices into lane-private shared memory, row slots,
+// record pools and output lists.  compute-sanitizer is not available on this
+// GPU pool; this build, run over the GPU test suite, stands in for memcheck.
+#ifdef TCG_CHECKED
+#include <cassert>
+#define TCG_ASSERT(c) assert(c)
+#else
+#define TCG_ASSERT(c) ((void)0)
+#endif
+
 namespace {
 
 constexpr int MAXK = 6;        // 32-bit words per vertex mask (d <= 9)
@@ -243,6 +254,7 @@ __device__ __forceinline__ uint64_t tree_key(const uint32_t (&radj)[MAXR], int n
             const int s2 = __ffs(nb) - 1;
             nb &= nb - 1;
             parent[s2] = (uint8_t)r;
+            TCG_ASSERT(tail < MAXR && s2 < MAXR);
             order[tail++] = (uint8_t)s2;
         }
     }
@@ -685,6 +697,7 @@ struct CtaTable {  // 64-bit counts: a tiled launch covers up to 2^32 weighted p
                 h = (h + 1) & (TBL - 1);
             }
             const unsigned long long c = (unsigned long long)__popc(grp) * weight;
+            TCG_ASSERT(nreg >= 1 && nreg <= NHIST);
             atomicAdd(&hist[nreg - 1], c);
             if (slot >= 0) {
                 atomicAdd(&cnt[slot], c);
@@ -1443,6 +1456,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
             }
             const int v = __ffsll((long long)F) - 1;
             F &= F - 1ull;
+            TCG_ASSERT(v >= 0 && v < 64 && n < 64);
             lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)n;
             const unsigned long long nw = S->adj[v] & unv & same;
             unv ^= nw;
@@ -1468,7 +1482,10 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
                 const unsigned long long adj = ((unsigned long long)FB << n) | labels_of(CG & ~M);
                 const unsigned long long pl = labels_of(LK);
                 if (fcs)
-                    for (uint32_t y = FB; y; y &= y - 1u) FCs[(__ffs(y) - 1) * THREADS] |= 1u << c;
+                    for (uint32_t y = FB; y; y &= y - 1u) {
+                        TCG_ASSERT(__ffs(y) - 1 < nf && c < 32);
+                        FCs[(__ffs(y) - 1) * THREADS] |= 1u << c;
+                    }
                 store_row(rec, c, nn, adj, pl);
                 hs.row(adj, pl);
             };
@@ -1529,6 +1546,7 @@ __device__ __forceinline__ bool rec_equal(const TileRec *__restrict__ a,
                                           const TileRec *__restrict__ b) {
     if (a->n != b->n || a->nnodes != b->nnodes || a->sgn_fixed != b->sgn_fixed) return false;
     const int nn = a->nnodes;
+    TCG_ASSERT(nn >= 0 && nn <= 64);
     uint32_t diff = 0;
     if (nn <= 32) {  // uint2 rows: compare two per uint4, the last one by halves
         const uint4 *x = a->rows, *y = b->rows;
@@ -1585,6 +1603,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restric
                 }
                 if ((cur & 0xffffffff00000000ull) == tag) {
                     const uint32_t o = (uint32_t)cur;
+                    TCG_ASSERT(o < ntiles);
                     if (rec_equal(r, recs + o)) {
                         atomicAdd(&dup[o], 1u);
                         atomicMin(&mint[o], t);
@@ -1600,6 +1619,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restric
         uint32_t base = 0;
         if (lane == __ffs(bal) - 1) base = atomicAdd(count, (uint32_t)__popc(bal));
         base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
+        TCG_ASSERT(!rep || base + __popc(bal & ((1u << lane) - 1u)) < ntiles);
         if (rep) list[base + __popc(bal & ((1u << lane) - 1u))] = t;
     }
 }
@@ -1787,6 +1807,7 @@ __device__ __forceinline__ int l2_build_lbl(const TileTables &tt,
         while (f) {
             const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
             f &= f - one;
+            TCG_ASSERT(u >= 0 && u < 64 && m < 64);
             lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
             MT rx, ry;
             if constexpr (WIDE) {
@@ -1816,6 +1837,7 @@ __device__ __forceinline__ int l2_build_lbl(const TileTables &tt,
         for (uint32_t w = (uint32_t)x; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
         if constexpr (WIDE)
             for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) c |= 1u << label(31 + __ffs(w));
+        TCG_ASSERT(m < L2B_CS);
         cs[m * THREADS] = c;
         for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
         const uint32_t self = (cg & M) != (MT)0;
@@ -1879,6 +1901,7 @@ __device__ __forceinline__ int l2_build_even(const TileTables &tt,
         while (f) {
             const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
             f &= f - one;
+            TCG_ASSERT(u >= 0 && u < 64 && m < 64);
             lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
             MT rx, ry;
             if constexpr (WIDE) {
@@ -1916,6 +1939,7 @@ __device__ __forceinline__ int l2_build_even(const TileTables &tt,
         if constexpr (WIDE)
             for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) c |= 1u << label(31 + __ffs(w));
         const uint32_t self = (cg & M) != (MT)0;
+        TCG_ASSERT(m < L2B_CS);
         cs[m * THREADS] = c | self << 30 | (uint32_t)odd << 31;
         for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
         const unsigned long long w1 = cmp(p10) | cmp(p11) << nB | cmp(p00) << (2 * nB) |
@@ -2071,6 +2095,7 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
         while (f) {
             const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
             f &= f - one;
+            TCG_ASSERT(u >= 0 && u < 64 && m < 64);
             lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
             MT rx, ry;
             if constexpr (WIDE) {
@@ -2100,6 +2125,7 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
         if constexpr (WIDE)
             for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) c |= 1u << label(31 + __ffs(w));
         const uint32_t self = (cg & M) != (MT)0;
+        TCG_ASSERT(m < L2B_CS);
         cs[m * THREADS] = c | self << 31;
         for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
         const unsigned long long w1 = l15_compress(lut, (uint32_t)(pb >> n)) |
@@ -2294,6 +2320,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
             while (f) {
                 const int v = __ffs(f) - 1;
                 f &= f - 1u;
+                TCG_ASSERT(v >= 0 && v < 64 && m < 64);
                 lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)m;
                 uint32_t same, cross;
                 if (v < m1) {
@@ -2324,6 +2351,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
             }
             uint32_t c = 0;
             for (uint32_t w = cg & done; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
+            TCG_ASSERT(m < L2B_CS);
             cs[m * THREADS] = c;
             for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
             const uint32_t self = ((cg & M) != 0u) | selfany;
@@ -2424,6 +2452,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *
                 }
                 if ((cur & 0xffffffff00000000ull) == tag) {
                     const uint32_t o = (uint32_t)cur;
+                    TCG_ASSERT(o < nrec && at <= smask);
                     const unsigned long long *ow = pool + (size_t)o * stride;
                     unsigned long long diff = ow[0] ^ m;
 #pragma unroll
@@ -2445,6 +2474,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *
             uint32_t base = 0;
             if (lane == 0) base = atomicAdd(count2, (uint32_t)__popc(bal));
             base = __shfl_sync(0xffffffffu, base, 0);
+            TCG_ASSERT(!isnew || base + __popc(bal & ((1u << lane) - 1u)) < nrec);
             if (isnew) list2[base + __popc(bal & ((1u << lane) - 1u))] = j;
         }
     }
@@ -4097,7 +4127,13 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     if (slotq == 0) {  // the widest slot that keeps 4 CTAs (= the register limit) per SM:
         // with the whole-grid launch 4 CTAs and 47-row slots beat 3 CTAs and 64 (profiles/README.md)
         const int tiles = (THREADS / 32) * (32 >> T.la1);
-        const int budget = 228 * 1024 / 4 - 1024 - l15_static - L2B_WORDS * 4 * THREADS -
+        int sm_smem = 0;  // per-SM shared memory (228 KB on B200), queried
+        if (cudaDeviceGetAttribute(&sm_smem, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                   P->device) != cudaSuccess || sm_smem <= 0) {
+            cudaGetLastError();
+            sm_smem = 228 * 1024;
+        }
+        const int budget = sm_smem / 4 - 1024 - l15_static - L2B_WORDS * 4 * THREADS -
                            (lut_smem ? (int)sizeof(L15Lut) : 0);
         slotq = std::max(16, std::min(64, budget / (tiles * 16)));
     }
