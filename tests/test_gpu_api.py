@@ -545,3 +545,36 @@ def test_two_stage_level2_identical_to_direct():
         res[flag + "".join(extra)] = json.loads(p.stdout.strip().splitlines()[-1])
     # the third run forces stage-1 budget overflows: batches go back to the direct build
     assert res["0"] == res["1"] == res["1TCG_L15_MAXM"]
+
+
+def test_pipeline_deterministic_across_grid_shapes():
+    """Race canary (compute-sanitizer is unavailable on this GPU pool): the
+    d=7 and d=8 sweep pipelines give byte-identical reports whatever the
+    grid shapes of the two-stage kernels (CTAs per SM of the stage-1 build,
+    its dedup, stage 2, the direct level-2 build), run twice each."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import json,sys; sys.path.insert(0, %r)\n"
+        "from paper_2604_09221_b200 import builtin, sweep, SweepRange\n"
+        "from paper_2604_09221_b200.io import report_jsonl\n"
+        "out = []\n"
+        "for name, raw, a, n in (('delaunay-7', True, 0x5A5A5A5A0 + 3, (1 << 27) + 1001),\n"
+        "                        ('bowtie8', False, (1 << 38) + 17, 1 << 26)):\n"
+        "    for rep in range(2):\n"
+        "        out.append(report_jsonl(sweep(builtin(name), SweepRange(a, a + n), raw_space=raw)))\n"
+        "print(json.dumps(out))\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    res = []
+    for env in ({}, {"TCG_L15_GRID": "3", "TCG_L15D_GRID": "2", "TCG_L2F_GRID": "8",
+                     "TCG_L2B_GRID": "1"},
+                {"TCG_L15_GRID": "1", "TCG_L15D_GRID": "32", "TCG_L2F_GRID": "1",
+                 "TCG_L2B_GRID": "32"}):
+        p = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env),
+                           capture_output=True, text=True)
+        assert p.returncode == 0, p.stderr[-2000:]
+        res.append(json.loads(p.stdout.strip().splitlines()[-1]))
+    for r in res:
+        assert r[0] == r[1] == res[0][0] and r[2] == r[3] == res[0][2]
