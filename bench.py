@@ -6,8 +6,9 @@ Workload (config C3, BASELINE.json configs[2]): T = delaunay-7 (the
 staircase), raw index space, lower half [0, 2^35) = the 2^36 sign space
 modulo the global sign flip.  One step = the COMPLETE enumeration: the
 2^35 indices are split into N contiguous shards, one per GPU (strong
-scaling: the total work is fixed); a rank sweeps its shard in chunks of
-at most 2^34 indices, then the per-rank aggregates are merged (NCCL
+scaling: the total work is fixed); a rank sweeps its shard as one call
+(the library's deduplication window is up to 2^35 indices, so at N = 1 the
+whole domain is one window), then the per-rank aggregates are merged (NCCL
 all_reduce + all_gather, a few KB).  Every step's merged report is checked
 against the full C3 report computed by the pinned CPU oracle
 (tests/golden/c3_full.json) and the reference's own 2^20-index slices; a

@@ -797,7 +797,7 @@ constexpr int MAXF = 32;  // free vertices
 constexpr int MAXM = 24;  // mid vertices of a super-tile
 // level-1 list entries for a single A slice: tile | (a + 1) << slice_shift(la)
 // (a + 1 <= 2^la takes la + 1 bits; tile ids < 2^(31 - la), which the chunk
-// size guarantees: <= 2^34 indices = 2^(29 - la) tiles)
+// size guarantees: <= 2^35 indices = 2^(30 - la) tiles)
 __host__ __device__ constexpr int slice_shift(int la) { return 31 - la; }
 constexpr int SUPER_BITS_MAX = 6;
 
@@ -2246,6 +2246,11 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
 }
 
 // One lane per (distinct stage-1 record list15[i], A2 pattern): 4 per record.
+// NA: A2 nodes the per-record sameA / crossA rows are sized for.  NA <= 4
+// (d = 7 raw, 2^12-index tiles: nA2 = 3) keeps them in registers (static
+// indices); the general instance (16) keeps the dynamically indexed arrays,
+// which live in local memory.
+template <int NA>
 __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__restrict__ tt_g,
                                                          const unsigned long long *__restrict__ pool1,
                                                          uint32_t stride1,
@@ -2291,15 +2296,24 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
         const int m1 = (int)r1[0];
         const uint32_t SA2 = tt.a2sign[a2];
         // A2 rows toward the stage-1 super-nodes (same-sign or linked / crossed)
-        uint32_t sameA[16], crossA[16];
-        for (int k = 0; k < nA2; ++k) sameA[k] = crossA[k] = 0u;
+        uint32_t sameA[NA], crossA[NA];
+#pragma unroll
+        for (int k = 0; k < NA; ++k) sameA[k] = crossA[k] = 0u;
         for (int s = 0; s < m1; ++s) {
             const unsigned long long w1 = rw1(r1, s);
             const uint32_t pA = (uint32_t)(w1 >> nB) & a2m, mA = (uint32_t)(w1 >> (nF + nB)) & a2m,
                            lA = (uint32_t)(w1 >> (2 * nF + nB)) & a2m;
             const uint32_t same = (pA & SA2) | (mA & ~SA2) | lA, cross = (pA & ~SA2) | (mA & SA2);
-            for (uint32_t y = same; y; y &= y - 1u) sameA[__ffs(y) - 1] |= 1u << s;
-            for (uint32_t y = cross; y; y &= y - 1u) crossA[__ffs(y) - 1] |= 1u << s;
+            if constexpr (NA <= 4) {  // bits >= nA2 are zero (a2m)
+#pragma unroll
+                for (int k = 0; k < NA; ++k) {
+                    sameA[k] |= ((same >> k) & 1u) << s;
+                    crossA[k] |= ((cross >> k) & 1u) << s;
+                }
+            } else {
+                for (uint32_t y = same; y; y &= y - 1u) sameA[__ffs(y) - 1] |= 1u << s;
+                for (uint32_t y = cross; y; y &= y - 1u) crossA[__ffs(y) - 1] |= 1u << s;
+            }
         }
         const int nn = m1 + nA2;
         if (nn > 32) {  // 32-bit node masks: the host redoes the batch directly
@@ -2337,8 +2351,21 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
                 } else {
                     const int k = v - m1;
                     const uint32_t sk = (SA2 >> k) & 1u, own = sk ? SA2 : ~SA2;
-                    same = sameA[k] | (((tt.a2adjA2[k] & own) | tt.a2linkA2[k]) << m1);
-                    cross = crossA[k] | ((tt.a2adjA2[k] & ~own & a2m) << m1);
+                    uint32_t sAk, cAk;
+                    if constexpr (NA <= 4) {
+                        sAk = sameA[0];
+                        cAk = crossA[0];
+#pragma unroll
+                        for (int q = 1; q < NA; ++q) {
+                            sAk = k == q ? sameA[q] : sAk;
+                            cAk = k == q ? crossA[q] : cAk;
+                        }
+                    } else {
+                        sAk = sameA[k];
+                        cAk = crossA[k];
+                    }
+                    same = sAk | (((tt.a2adjA2[k] & own) | tt.a2linkA2[k]) << m1);
+                    cross = cAk | ((tt.a2adjA2[k] & ~own & a2m) << m1);
                     if (sk) pb |= tt.a2adjB[k];
                     else mb |= tt.a2adjB[k];
                     lk |= tt.a2linkB[k];
@@ -3228,13 +3255,16 @@ size_t cls_smem(int K) {
 // allocated on demand and only as large as the sweep needs, halved while it
 // would take more than a quarter of the free HBM).  TCG_CHUNK_LOG2 (14..24)
 // overrides.
-// indices per chunk (TCG_CHUNK_INDEX_LOG2, 32..34; default 2^34): larger chunks
-// deduplicate over a larger window (C3: 158x at 2^32, 244x at 2^33);
-// at most chunk_tiles() = 2^25 tiles
+// indices per chunk (TCG_CHUNK_INDEX_LOG2, 32..35; default 2^35): larger chunks
+// deduplicate over a larger window (C3 at 2^9-index tiles: 158x at 2^32,
+// 244x at 2^33, 379x at 2^34); 2^35 is the whole C3 domain in one window.
+// At most chunk_tiles() = 2^25 tiles; 2^35 indices = 2^(30 - la) tiles keeps
+// level-1 slice entries (tile < 2^(31 - la)) and level-2 positions
+// (tile << la < 2^30) in 32 bits.
 static uint64_t chunk_index_limit() {
     static const uint64_t c = [] {
-        int lg = 34;
-        if (const char *e = std::getenv("TCG_CHUNK_INDEX_LOG2")) lg = std::max(32, std::min(34, std::atoi(e)));
+        int lg = 35;
+        if (const char *e = std::getenv("TCG_CHUNK_INDEX_LOG2")) lg = std::max(32, std::min(35, std::atoi(e)));
         return 1ull << lg;
     }();
     return c;
@@ -3766,7 +3796,9 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
         if ((e = cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)L2B_SMEM)) != cudaSuccess)
             return bail(e, "l2 build smem");
-    if ((e = cudaFuncSetAttribute((void *)k_l2_from_l15, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((e = cudaFuncSetAttribute((void *)k_l2_from_l15<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)L2B_SMEM)) != cudaSuccess ||
+        (e = cudaFuncSetAttribute((void *)k_l2_from_l15<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)L2B_SMEM)) != cudaSuccess ||
         (e = cudaFuncSetAttribute((void *)k_l15_build, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)L15_SMEM_MAX)) != cudaSuccess)
@@ -4177,7 +4209,8 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
                   &poss, &failp};
     const size_t smem2 = (size_t)(L2B_WORDS + L2B_CS) * 4 * THREADS;  // + B-relation words
     cudaEvent_t e1 = timing_begin(P);
-    if (!cuda_ok(cudaLaunchKernel((void *)k_l2_from_l15, dim3(std::max(1u, g2)), dim3(THREADS), a2, smem2, st),
+    void *l2f = T.nA2 <= 4 ? (void *)k_l2_from_l15<4> : (void *)k_l2_from_l15<16>;
+    if (!cuda_ok(cudaLaunchKernel(l2f, dim3(std::max(1u, g2)), dim3(THREADS), a2, smem2, st),
                  "l2 from l15"))
         return false;
     if (!cuda_ok(cudaMemcpyAsync(hostv + 1, failp, 4, cudaMemcpyDeviceToHost, st), "copy") ||

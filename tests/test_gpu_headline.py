@@ -1,9 +1,9 @@
 """The bench's exact computation, pinned.
 
-bench.py times config C3 as two sweep calls over the 2^34-index chunks
-[0, 2^34) and [2^34, 2^35) of delaunay-7's raw space with the default
-pipeline (super-tiles, tile dedup, two-stage level 2).  These tests check
-those very calls:
+bench.py times config C3 as one sweep call over [0, 2^35) of delaunay-7's
+raw space with the default pipeline (super-tiles, tile dedup, two-stage
+level 2; one 2^35-index dedup window); N = 2 ranks sweep the 2^34-index
+halves.  These tests check those very calls:
 
 * against the per-patchwork full-diamond kernel (``TCG_NO_TILES=1``, the
   path the oracle pins pair by pair), in subprocesses, comparing the report
@@ -30,28 +30,35 @@ C3_FULL = os.path.join(GOLDEN, "c3_full.json")
 
 _SWEEP_CHUNKS = (
     "import json, sys; sys.path.insert(0, %r)\n"
-    "from paper_2604_09221_b200 import builtin, sweep, SweepRange, Classifier\n"
+    "from paper_2604_09221_b200 import builtin, sweep, SweepRange, Classifier, merge\n"
     "from paper_2604_09221_b200.io import report_jsonl, histogram_csv\n"
     "T = builtin('delaunay-7'); c = Classifier(T)\n"
-    "out = []\n"
-    "for a in (0, 1 << 34):\n"
-    "    r = sweep(T, SweepRange(a, a + (1 << 34)), raw_space=True, classifier=c)\n"
-    "    out.append([report_jsonl(r), histogram_csv(r), sorted(r.scheme_map.items())])\n"
+    "halves = [sweep(T, SweepRange(a, a + (1 << 34)), raw_space=True, classifier=c)\n"
+    "          for a in (0, 1 << 34)]\n"
+    "out = [[report_jsonl(r), histogram_csv(r), sorted(r.scheme_map.items())] for r in halves]\n"
+    "if len(sys.argv) > 1:  # the bench's call: the whole domain in one sweep\n"
+    "    r = sweep(T, SweepRange(0, 1 << 35), raw_space=True, classifier=c)\n"
+    "else:\n"
+    "    r = merge(*halves)\n"
+    "    r.params = {'mode': 'sweep', 'start': 0, 'end': 1 << 35, 'raw_space': True}\n"
+    "out.append([report_jsonl(r), histogram_csv(r), sorted(r.scheme_map.items())])\n"
     "print(json.dumps(out))\n" % ROOT)
 
 
-def _run(env_extra, timeout=900):
+def _run(env_extra, whole=False, timeout=900):
     env = dict(os.environ, **env_extra)
-    p = subprocess.run([sys.executable, "-c", _SWEEP_CHUNKS], env=env, capture_output=True,
-                       text=True, timeout=timeout)
+    p = subprocess.run([sys.executable, "-c", _SWEEP_CHUNKS] + (["whole"] if whole else []),
+                       env=env, capture_output=True, text=True, timeout=timeout)
     assert p.returncode == 0, p.stderr[-3000:]
     return json.loads(p.stdout.strip().splitlines()[-1])
 
 
 def test_bench_chunks_equal_per_patchwork_kernel():
-    default = _run({})
+    """The 2^34-index halves and the whole-domain sweep the bench times (one
+    2^35-index dedup window) vs the per-patchwork kernel's halves, merged."""
+    default = _run({}, whole=True)
     flat = _run({"TCG_NO_TILES": "1"})
-    for k in range(2):
+    for k in range(3):
         assert default[k][0] == flat[k][0]  # report JSONL bytes (witness strings included)
         assert default[k][1] == flat[k][1]  # histogram CSV bytes
         assert default[k][2] == flat[k][2]  # scheme -> (count, witness index)
@@ -108,5 +115,10 @@ def test_c3_bench_chunks_equal_oracle_golden():
         assert list(r.oval_histogram) == hist
         assert r.scheme_map == schemes
         done += 1
+    if done == 2:  # the bench's single whole-domain call
+        hist, schemes = _merge([pieces[i] for i in range(2 * per)])
+        r = sweep(T, SweepRange(0, 2 * CHUNK), raw_space=True, classifier=c)
+        assert list(r.oval_histogram) == hist
+        assert r.scheme_map == schemes
     if not done:
         pytest.skip("no complete 2^34 chunk in c3_full.json yet")
