@@ -126,7 +126,10 @@ int tcg_plan_info(const tcg_plan *plan, int32_t *info, int ninfo);
 #define TCG_KT_SUPER_BUILD 8   /* k_super_build: super-tile contraction */
 #define TCG_KT_L15_BUILD 9     /* k_l15_build: two-stage level 2, stage 1 */
 #define TCG_KT_L15_DEDUP 10    /* k_l2_dedup on the stage-1 records */
-#define TCG_NKINDS 11
+#define TCG_KT_SPLIT_BUILD 11  /* k_split_build: the sampler's component tables (once per plan) */
+#define TCG_KT_SAMPLE_SPLIT 12 /* k_sample_split: sampling on the separator-contracted graph */
+#define TCG_KT_SAMPLE_LIST 13  /* k_sample_list: draws the split sampler left to the flat classifier */
+#define TCG_NKINDS 14
 int tcg_plan_set_timing(tcg_plan *plan, int enable);
 int tcg_kernel_times(tcg_plan *plan, double *ms, int64_t *counts);
 /* Tile deduplication (exhaustive sweeps): tiles whose contracted records are
@@ -147,6 +150,20 @@ int tcg_tile_stats(tcg_plan *plan, int64_t *out);
  * graphs over 32 nodes, fallback tiles); all since the last call. */
 int tcg_plan_set_level2(tcg_plan *plan, int enable);
 int tcg_level2_stats(tcg_plan *plan, int64_t *out);
+/* Separator-split sampling (d >= 6, on by default; TCG_NO_SPLIT=1 or
+ * enable=0 samples with the flat kernel only -- results are identical).  At
+ * the first sample the plan picks a small vertex separator F of T's edge
+ * graph and tabulates, for every sign pattern of each side, the same-sign
+ * components of that side's diamond vertices (device memory, once); each draw
+ * is then classified on the graph of F's vertices plus the two sides'
+ * components.  Draws whose graph exceeds 64 nodes, or whose status is not OK,
+ * are re-classified by the flat kernel.  tcg_split_stats: out[0] = state
+ * (1 ready, -1 unavailable: flat sampling, 0 not built yet), out[1] = draws
+ * sampled through the split kernel, out[2] = of those, draws the flat kernel
+ * took, out[3] = separator vertices, out[4] = table bytes; counts since the
+ * last call (synchronises the plan's stream). */
+int tcg_plan_set_split(tcg_plan *plan, int enable);
+int tcg_split_stats(tcg_plan *plan, int64_t *out);
 
 /* classify_bits_kernel, batched.  sigma[t] bit k = sign of point k.
  * Outputs per patchwork: tree key, oval count, region count, status. */

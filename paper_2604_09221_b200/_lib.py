@@ -68,6 +68,8 @@ def load():
         L.tcg_tile_stats.argtypes = [P, C.c_void_p]
         L.tcg_plan_set_level2.argtypes = [P, C.c_int]
         L.tcg_level2_stats.argtypes = [P, C.c_void_p]
+        L.tcg_plan_set_split.argtypes = [P, C.c_int]
+        L.tcg_split_stats.argtypes = [P, C.c_void_p]
         L.tcg_classify_batch.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p]
         L.tcg_classify_batch_device.argtypes = L.tcg_classify_batch.argtypes
@@ -105,7 +107,7 @@ def load():
 EXPORTS = (
     "tcg_plan_create", "tcg_plan_destroy", "tcg_plan_set_stream", "tcg_plan_info",
     "tcg_plan_set_timing", "tcg_kernel_times", "tcg_plan_set_dedup", "tcg_tile_stats",
-    "tcg_plan_set_level2", "tcg_level2_stats",
+    "tcg_plan_set_level2", "tcg_level2_stats", "tcg_plan_set_split", "tcg_split_stats",
     "tcg_classify_batch", "tcg_classify_batch_device", "tcg_sweep", "tcg_sample",
     "tcg_agg_reset", "tcg_sweep_async", "tcg_sample_async", "tcg_agg_fetch",
     "tcg_sweep_multi", "tcg_sample_multi", "tcg_last_error", "tcg_device_count",
@@ -117,7 +119,8 @@ EXPORTS = (
 
 # tcg.h TCG_KT_* order (tcg_kernel_times)
 KERNEL_KINDS = ("tile_build", "tile_classify", "enumerate", "batch", "tile_dedup",
-                "l2_build", "l2_dedup", "l2_classify", "super_build", "l15_build", "l15_dedup")
+                "l2_build", "l2_dedup", "l2_classify", "super_build", "l15_build", "l15_dedup",
+                "split_build", "sample_split", "sample_list")
 
 
 def last_error() -> str:
@@ -346,6 +349,18 @@ class NativePlan:
         out = np.zeros(3, np.int64)
         _check(self._L.tcg_level2_stats(self.h, out.ctypes.data), "tcg_level2_stats")
         return int(out[0]), int(out[1]), int(out[2])
+
+    def set_split(self, enable: bool | None):
+        """Separator-split sampling on / off / None = default (see tcg.h)."""
+        flag = -1 if enable is None else int(bool(enable))
+        _check(self._L.tcg_plan_set_split(self.h, flag), "tcg_plan_set_split")
+
+    def split_stats(self):
+        """(state, draws through the split kernel, of those left to the flat
+        kernel, separator vertices, table bytes); counts since the last call."""
+        out = np.zeros(5, np.int64)
+        _check(self._L.tcg_split_stats(self.h, out.ctypes.data), "tcg_split_stats")
+        return tuple(int(x) for x in out)
 
     def tile_stats(self):
         """(tiles contracted, tiles classified) since the last call."""

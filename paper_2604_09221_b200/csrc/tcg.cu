@@ -3061,6 +3061,8 @@ __global__ void k_agg_compact(DevAgg g, unsigned long long *okey, unsigned long 
     }
 }
 
+#include "split.cuh"
+
 // ------------------------------------------------------------ error state
 thread_local std::string g_last_error;
 
@@ -3144,6 +3146,18 @@ struct tcg_plan {
     // split-phase bookkeeping: how to map a failing index back to its sign word
     int pending_mode = -1;
     uint64_t pending_seed = 0, pending_mask = 0;
+    // separator-split sampler (split.cuh), built at the first sample
+    int split = -1;                  // -1: TCG_NO_SPLIT decides, 0 off, 1 on
+    int split_state = 0;             // 0: not built, 1: ready, -1: unavailable
+    std::vector<int32_t> h_eu, h_ev, h_src, h_apu, h_apv, h_pos;  // descriptor copy
+    std::vector<uint8_t> h_par, h_used;
+    int h_nv = 0, h_npts = 0;
+    SplitParams split_sp{};
+    uint32_t *d_splitA = nullptr, *d_splitB = nullptr, *d_fbl = nullptr;
+    unsigned long long *d_pext = nullptr, *d_splitstats = nullptr;  // [0] list draws
+    int blocks_split = 0, blocks_list = 0;
+    int64_t split_draws = 0;
+    size_t split_bytes = 0;
 };
 
 namespace {
@@ -3658,6 +3672,8 @@ int build_host_plan(const tcg_desc *D, HostPlan &HP) {
     return TCG_OK;
 }
 
+#include "split_design.cuh"
+
 }  // namespace
 
 extern "C" {
@@ -3690,6 +3706,16 @@ int tcg_plan_create(const tcg_desc *D, int device, tcg_plan **out) {
     P->even = HP.even;
     P->maxreg = D->maxreg;
     P->nused = HP.nused;
+    P->h_nv = D->nv;
+    P->h_npts = D->npts;
+    P->h_eu.assign(D->edge_u, D->edge_u + D->ne);
+    P->h_ev.assign(D->edge_v, D->edge_v + D->ne);
+    P->h_src.assign(D->src, D->src + D->nv);
+    P->h_par.assign(D->par, D->par + D->nv);
+    P->h_used.assign(D->used, D->used + D->nv);
+    P->h_apu.assign(D->ap_u, D->ap_u + D->nap);
+    P->h_apv.assign(D->ap_v, D->ap_v + D->nap);
+    P->h_pos = HP.L.pos;
     KParams &kp = P->kp;
     kp = HP.kp;
     std::vector<uint32_t> &adj = HP.adj;
@@ -3865,7 +3891,8 @@ int tcg_plan_destroy(tcg_plan *P) {
     timing_resolve(P);
     void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_lut, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_l2slots, P->d_l15pool, P->d_l15hash, P->d_l15slots, P->d_l15u32, P->d_oldlist, P->d_ovf, P->d_super, P->d_hash, P->d_slots, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
-                    P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st};
+                    P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st, P->d_splitA, P->d_splitB,
+                    P->d_fbl, P->d_pext, P->d_splitstats};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 2; ++i) {
@@ -3937,6 +3964,30 @@ int tcg_level2_stats(tcg_plan *P, int64_t *out) {
     out[1] = (int64_t)c[0];
     out[2] = (int64_t)c[1];
     P->l2_built = 0;
+    return TCG_OK;
+}
+
+int tcg_plan_set_split(tcg_plan *P, int enable) {
+    if (!P) return fail(TCG_E_ARG, "null plan");
+    P->split = enable < 0 ? -1 : (enable ? 1 : 0);
+    return TCG_OK;
+}
+
+int tcg_split_stats(tcg_plan *P, int64_t *out) {
+    if (!P || !out) return fail(TCG_E_ARG, "null argument");
+    DeviceGuard guard(P->device);
+    unsigned long long fb = 0;
+    if (P->d_splitstats) {
+        CUDA_TRY(cudaStreamSynchronize(P->stream));
+        CUDA_TRY(cudaMemcpy(&fb, P->d_splitstats, 8, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemset(P->d_splitstats, 0, 8));
+    }
+    out[0] = P->split_state;
+    out[1] = P->split_draws;
+    out[2] = (int64_t)fb;
+    out[3] = P->split_state > 0 ? P->split_sp.nF : 0;
+    out[4] = (int64_t)P->split_bytes;
+    P->split_draws = 0;
     return TCG_OK;
 }
 
@@ -4372,6 +4423,117 @@ static bool dedup_enabled() {
     return on;
 }
 
+// TCG_NO_SPLIT=1 samples with the flat kernel only (A/B and debugging); results are identical.
+static bool split_enabled(const tcg_plan *P) {
+    if (P->split >= 0) return P->split != 0;
+    static const bool on = [] {
+        const char *e = std::getenv("TCG_NO_SPLIT");
+        return !(e && e[0] && e[0] != '0');
+    }();
+    return on;
+}
+
+// Design the separator and build the two component tables (once per plan,
+// at the first sample; d >= 6).  Leaves split_state = -1 (flat sampling)
+// when no separator fits the limits in split.cuh.
+static int ensure_split(tcg_plan *P) {
+    if (P->split_state) return TCG_OK;
+    P->split_state = -1;
+    if (P->d < 6) return TCG_OK;
+    tcg_desc D{};
+    D.degree = P->d;
+    D.nv = P->h_nv;
+    D.npts = P->h_npts;
+    D.ne = (int32_t)P->h_eu.size();
+    D.edge_u = P->h_eu.data();
+    D.edge_v = P->h_ev.data();
+    D.src = P->h_src.data();
+    D.par = P->h_par.data();
+    D.used = P->h_used.data();
+    D.nap = (int32_t)P->h_apu.size();
+    D.ap_u = P->h_apu.data();
+    D.ap_v = P->h_apv.data();
+    D.maxreg = P->maxreg;
+    Layout L;
+    L.d = P->d;
+    L.K = P->K;
+    L.H = 16 * P->K;
+    L.npts = P->h_npts;
+    L.pos = P->h_pos;
+    SplitDesign S;
+    if (!split_design(&D, L, S)) return TCG_OK;
+    const size_t na = (size_t)1 << S.pa.bits, nb = (size_t)1 << S.pb.bits;
+    const size_t ew = S.sp.stride;
+    CUDA_TRY(cudaMalloc(&P->d_splitA, na * ew * 4));
+    CUDA_TRY(cudaMalloc(&P->d_splitB, nb * ew * 4));
+    CUDA_TRY(cudaMalloc(&P->d_pext, S.pext.size() * 8));
+    CUDA_TRY(cudaMalloc(&P->d_fbl, (SPL_LAUNCH + 1) * 4));
+    CUDA_TRY(cudaMalloc(&P->d_splitstats, 8));
+    CUDA_TRY(cudaMemsetAsync(P->d_splitstats, 0, 8, P->stream));
+    CUDA_TRY(cudaMemcpyAsync(P->d_pext, S.pext.data(), S.pext.size() * 8, cudaMemcpyHostToDevice,
+                             P->stream));
+    P->split_bytes = (na + nb) * ew * 4;
+    void *fb = pick_split_build(P->K);
+    CUDA_TRY(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj_bytes(P->K)));
+    int bps = 0;
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fb, THREADS, adj_bytes(P->K)));
+    for (int t = 0; t < 2; ++t) {
+        SplitPart part = t ? S.pb : S.pa;
+        uint32_t *tab = t ? P->d_splitB : P->d_splitA;
+        uint32_t n = (uint32_t)(t ? nb : na);
+        const unsigned grid = (unsigned)std::min<uint64_t>((uint64_t)std::max(1, bps) * P->nsm,
+                                                           (n + THREADS - 1) / THREADS);
+        void *args[] = {&P->kp, &part, &tab, &n};
+        cudaEvent_t e0 = timing_begin(P);
+        CUDA_TRY(cudaLaunchKernel(fb, dim3(grid), dim3(THREADS), args, adj_bytes(P->K), P->stream));
+        timing_end(P, TCG_KT_SPLIT_BUILD, e0);
+        P->launches++;
+    }
+    S.sp.tabA = P->d_splitA;
+    S.sp.tabB = P->d_splitB;
+    S.sp.pext = P->d_pext;
+    P->split_sp = S.sp;
+    void *fs = pick_split(P->even);
+    CUDA_TRY(cudaFuncSetAttribute(fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SPLIT_SMEM));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fs, THREADS, SPLIT_SMEM));
+    P->blocks_split = std::max(1, bps) * P->nsm;
+    void *fl = pick_list(P->K, P->even);
+    CUDA_TRY(cudaFuncSetAttribute(fl, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P->smem_enum));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fl, THREADS, P->smem_enum));
+    P->blocks_list = std::max(1, bps) * P->nsm;
+    CUDA_TRY(cudaGetLastError());
+    P->split_state = 1;
+    return TCG_OK;
+}
+
+// Sampling through the split tables: launches of <= SPL_LAUNCH draws, each
+// followed by the flat classification of the draws it left.
+static int enqueue_split(tcg_plan *P, uint64_t k0, uint64_t k1, uint64_t seed, uint64_t mask) {
+    void *fs = pick_split(P->even);
+    void *fl = pick_list(P->K, P->even);
+    for (uint64_t a = k0; a < k1;) {
+        uint64_t count = std::min<uint64_t>(k1 - a, SPL_LAUNCH), base = a;
+        CUDA_TRY(cudaMemsetAsync(P->d_fbl, 0, 4, P->stream));
+        const uint64_t need = ((count + 31) / 32 * 32 + THREADS - 1) / THREADS;
+        const unsigned blocks = (unsigned)std::min<uint64_t>(P->blocks_split, std::max<uint64_t>(1, need));
+        uint32_t *fbl = P->d_fbl;
+        void *as[] = {&P->kp, &P->split_sp, &base, &count, &seed, &mask, &P->agg, &fbl};
+        cudaEvent_t e0 = timing_begin(P);
+        CUDA_TRY(cudaLaunchKernel(fs, dim3(blocks), dim3(THREADS), as, SPLIT_SMEM, P->stream));
+        timing_end(P, TCG_KT_SAMPLE_SPLIT, e0);
+        const uint32_t *cfbl = fbl;
+        unsigned long long *st = P->d_splitstats;
+        void *al[] = {&P->kp, &base, &seed, &mask, &P->agg, &cfbl, &st};
+        cudaEvent_t e1 = timing_begin(P);
+        CUDA_TRY(cudaLaunchKernel(fl, dim3(P->blocks_list), dim3(THREADS), al, P->smem_enum, P->stream));
+        timing_end(P, TCG_KT_SAMPLE_LIST, e1);
+        P->launches += 2;
+        P->split_draws += (int64_t)count;
+        a += count;
+    }
+    return TCG_OK;
+}
+
 static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t seed,
                    uint64_t mask) {
     if (P->pending_mode >= 0 && P->pending_mode != mode)
@@ -4528,6 +4690,11 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             P->launches += 2;
         }
         return TCG_OK;
+    }
+    if (mode == MODE_SAMPLE && end > start && split_enabled(P)) {
+        int rc = ensure_split(P);
+        if (rc) return rc;
+        if (P->split_state > 0) return enqueue_split(P, start, end, seed, mask);
     }
     void *fn = pick_enum(P->K, P->even, mode);
     for (uint64_t a = start; a < end;) {

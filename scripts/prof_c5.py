@@ -1,4 +1,6 @@
-"""C5 sampling launch for profiling: 2^24 draws at k0 = 2^39 (default bowtie8)."""
+"""C5 sampling launch for profiling: 2^24 draws at k0 = 2^39 (default bowtie8).
+The first slice builds the split tables (k_split_build) and warms the
+sampler; profile the second k_sample_split launch (ncu -k regex:k_sample -s 1)."""
 import os
 import sys
 
@@ -10,4 +12,4 @@ T = builtin(sys.argv[1] if len(sys.argv) > 1 else "bowtie8")
 c = Classifier(T)
 sample_slice(T, 20260810, 0, 1 << 20, classifier=c)
 r = sample_slice(T, 20260810, 1 << 39, (1 << 39) + (1 << 24), classifier=c)
-print(r.total_classified)
+print(r.total_classified, c.native.split_stats())
