@@ -188,24 +188,28 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
     };
     const uint4 *ca = reinterpret_cast<const uint4 *>(ea + 4 + nFp);
     const uint4 *cb = reinterpret_cast<const uint4 *>(eb + 4 + nFp);
-    seed();
-    for (int it = 0; it < nn; ++it) {
-        if (f == 0ull) {
-            close();
-            seed();
-        }
-        const int v = __ffsll((long long)f) - 1;
-        f &= f - 1ull;
+    const uint4 *fa = reinterpret_cast<const uint4 *>(ea + 4);
+    const uint4 *fb = reinterpret_cast<const uint4 *>(eb + 4);
+    // node row: F nodes take word v & 3 of two uint4s (the A and B entries'
+    // masks), components one uint4 of their entry; the loads are issued
+    // without branches so two nodes' loads are in flight together
+    auto load = [&](int v, uint4 &t1, uint4 &t2) {
+        const bool isF = v < nF, inA = v < sB;
+        const uint4 *pc = inA ? ca + (v - nF) : cb + (v - sB);
+        t1 = __ldg(isF ? fa + (v >> 2) : pc);
+        t2 = isF ? __ldg(fb + (v >> 2)) : make_uint4(0u, 0u, 0u, 0u);
+    };
+    auto expand = [&](int v, const uint4 &t1, const uint4 &t2) {
         u64 adj, link;
         if (v < nF) {
-            adj = (u64)fadj_s[v] | ((u64)__ldg(ea + 4 + v) << nF) | ((u64)__ldg(eb + 4 + v) << sB);
+            const uint32_t wa = (v & 2) ? ((v & 1) ? t1.w : t1.z) : ((v & 1) ? t1.y : t1.x);
+            const uint32_t wb = (v & 2) ? ((v & 1) ? t2.w : t2.z) : ((v & 1) ? t2.y : t2.x);
+            adj = (u64)fadj_s[v] | ((u64)wa << nF) | ((u64)wb << sB);
             link = flink_s[v];
         } else {
-            const bool inA = v < sB;
-            const int sh = inA ? nF : sB;
-            const uint4 t = __ldg((inA ? ca : cb) + (v - sh));
-            adj = (u64)t.x | ((u64)t.y << sh);
-            link = (u64)t.z << sh;
+            const int sh = v < sB ? nF : sB;
+            adj = (u64)t1.x | ((u64)t1.y << sh);
+            link = (u64)t1.z << sh;
         }
         const u64 sv = 0ull - ((sg >> v) & 1ull);
         const u64 o = sg ^ sv;  // nodes of the other sign
@@ -225,8 +229,27 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
             un ^= n;
             f |= n;
         }
+    };
+    // Two frontier nodes per step: their expansions run in order, so the
+    // result is the sequential pass's (a region's node set, crossed
+    // neighbourhood and parity verdict do not depend on the visit order).
+    seed();
+    while (true) {
+        if (f == 0ull) {
+            close();
+            if (un == 0ull) break;
+            seed();
+        }
+        const int v1 = __ffsll((long long)f) - 1;
+        f &= f - 1ull;
+        const int v2 = f ? __ffsll((long long)f) - 1 : v1;
+        f &= f - 1ull;  // no-op when f was a single node
+        uint4 a1, a2, b1, b2;
+        load(v1, a1, a2);
+        load(v2, b1, b2);
+        expand(v1, a1, a2);
+        if (v2 != v1) expand(v2, b1, b2);
     }
-    close();
     out.nreg = nreg;
     out.nedges = nedges;
     out.selfm = selfm;
@@ -376,8 +399,8 @@ constexpr size_t SPLIT_SMEM = SPLIT_SMEM_HEAD + TABLE_SMEM;
 // sign word -> (A pattern, B pattern, F bits) by byte tables -> contracted
 // classification.  fbl[0] counts the draws left to k_sample_list, fbl[1..]
 // their offsets from `base`.
-template <bool EVEN>
-__global__ void __launch_bounds__(THREADS) k_sample_split(KParams p, SplitParams sp, uint64_t base,
+template <bool EVEN, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_sample_split(KParams p, SplitParams sp, uint64_t base,
                                                           uint64_t count, uint64_t seed,
                                                           uint64_t nbmask, DevAgg g,
                                                           uint32_t *__restrict__ fbl) {
@@ -492,8 +515,14 @@ __global__ void __launch_bounds__(THREADS, K == 6 ? TCG_ENUM_MINB6 : 1)
 }
 
 
+// TCG_SPLIT_MINB: resident CTAs the register allocation targets (3 or 4)
 inline void *pick_split(bool even) {
-    return even ? (void *)k_sample_split<true> : (void *)k_sample_split<false>;
+    static const int minb = [] {
+        const char *e = std::getenv("TCG_SPLIT_MINB");
+        return e ? std::atoi(e) : 3;
+    }();
+    if (minb >= 4) return even ? (void *)k_sample_split<true, 4> : (void *)k_sample_split<false, 4>;
+    return even ? (void *)k_sample_split<true, 3> : (void *)k_sample_split<false, 3>;
 }
 
 inline void *pick_list(int K, bool even) {
