@@ -119,6 +119,24 @@ __global__ void __launch_bounds__(THREADS) k_split_build(KParams p, SplitPart sp
     }
 }
 
+// Table loads: read-only path, optionally with an L2 fetch-size hint (LD 1:
+// 128 B, 2: 256 B) so one DRAM trip brings in the neighbouring rows of the entry.
+template <int LD>
+__device__ __forceinline__ uint4 ldt(const uint4 *p) {
+    if constexpr (LD == 0) {
+        return __ldg(p);
+    } else {
+        uint4 r;
+        if constexpr (LD == 1)
+            asm("ld.global.nc.L2::128B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+        else
+            asm("ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
+                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+        return r;
+    }
+}
+
 // The region graph of one draw, built while the regions close.
 struct RegionGraph {
     uint32_t radj[MAXR];  // region adjacency (crossed edges), symmetric
@@ -135,7 +153,7 @@ struct RegionGraph {
 // already closed.  Each adjacent pair is met exactly once (at the later
 // region's close), so the region graph, its edge count and the status inputs
 // are complete when the pass ends.
-template <bool EVEN>
+template <bool EVEN, int LD>
 __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
                                            const uint32_t *__restrict__ flink_s,
                                            const uint32_t *__restrict__ ea,
@@ -196,8 +214,8 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
     auto load = [&](int v, uint4 &t1, uint4 &t2) {
         const bool isF = v < nF, inA = v < sB;
         const uint4 *pc = inA ? ca + (v - nF) : cb + (v - sB);
-        t1 = __ldg(isF ? fa + (v >> 2) : pc);
-        t2 = isF ? __ldg(fb + (v >> 2)) : make_uint4(0u, 0u, 0u, 0u);
+        t1 = ldt<LD>(isF ? fa + (v >> 2) : pc);
+        t2 = isF ? ldt<LD>(fb + (v >> 2)) : make_uint4(0u, 0u, 0u, 0u);
     };
     auto expand = [&](int v, const uint4 &t1, const uint4 &t2) {
         u64 adj, link;
@@ -399,8 +417,8 @@ constexpr size_t SPLIT_SMEM = SPLIT_SMEM_HEAD + TABLE_SMEM;
 // sign word -> (A pattern, B pattern, F bits) by byte tables -> contracted
 // classification.  fbl[0] counts the draws left to k_sample_list, fbl[1..]
 // their offsets from `base`.
-template <bool EVEN, int MINB>
-__global__ void __launch_bounds__(THREADS, MINB) k_sample_split(KParams p, SplitParams sp, uint64_t base,
+template <bool EVEN, int LD>
+__global__ void __launch_bounds__(THREADS, 3) k_sample_split(KParams p, SplitParams sp, uint64_t base,
                                                           uint64_t count, uint64_t seed,
                                                           uint64_t nbmask, DevAgg g,
                                                           uint32_t *__restrict__ fbl) {
@@ -447,8 +465,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sample_split(KParams p, Split
                 }
             }
         }
-        const uint2 ha = __ldg(reinterpret_cast<const uint2 *>(ea));
-        const uint2 hb = __ldg(reinterpret_cast<const uint2 *>(eb));
+        const uint4 ha = ldt<LD>(reinterpret_cast<const uint4 *>(ea));
+        const uint4 hb = ldt<LD>(reinterpret_cast<const uint4 *>(eb));
         const int sB = nF + (int)ha.x, nn = sB + (int)hb.x;
         const bool fits = valid && ha.x <= (uint32_t)SPL_CAPC && hb.x <= (uint32_t)SPL_CAPC &&
                           nn <= sp.maxnodes;
@@ -461,7 +479,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_sample_split(KParams p, Split
                                           ((unsigned long long)ha.y << nF) |
                                           ((unsigned long long)hb.y << sB);
             RegionGraph rg;
-            split_pass<EVEN>(fadj_s, flink_s, ea, eb, nF, sp.nFp, sB, nn, sg, rg);
+            split_pass<EVEN, LD>(fadj_s, flink_s, ea, eb, nF, sp.nFp, sB, nn, sg, rg);
             r = finish_graph<EVEN>(rg, p.maxreg);
         }
         uint64_t k = 0;
@@ -515,14 +533,15 @@ __global__ void __launch_bounds__(THREADS, K == 6 ? TCG_ENUM_MINB6 : 1)
 }
 
 
-// TCG_SPLIT_MINB: resident CTAs the register allocation targets (3 or 4)
+// TCG_SPLIT_LD: table-load flavour (0 plain, 1 / 2: L2 fetch size 128 / 256 B)
 inline void *pick_split(bool even) {
-    static const int minb = [] {
-        const char *e = std::getenv("TCG_SPLIT_MINB");
-        return e ? std::atoi(e) : 3;
+    static const int ld = [] {
+        const char *e = std::getenv("TCG_SPLIT_LD");
+        return e ? std::atoi(e) : 0;
     }();
-    if (minb >= 4) return even ? (void *)k_sample_split<true, 4> : (void *)k_sample_split<false, 4>;
-    return even ? (void *)k_sample_split<true, 3> : (void *)k_sample_split<false, 3>;
+    if (ld == 1) return even ? (void *)k_sample_split<true, 1> : (void *)k_sample_split<false, 1>;
+    if (ld == 2) return even ? (void *)k_sample_split<true, 2> : (void *)k_sample_split<false, 2>;
+    return even ? (void *)k_sample_split<true, 0> : (void *)k_sample_split<false, 0>;
 }
 
 inline void *pick_list(int K, bool even) {

@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -3116,6 +3117,8 @@ struct tcg_plan {
     int l2 = -1;                     // -1: TCG_NO_L2 decides
     int l2_stride = 0;               // u64 words per level-2 record
     size_t l2_cap = 0;               // level-2 records the buffers hold
+    size_t l2_sized_for = 0;         // largest request the pool was sized for
+    size_t l15_sized_for = 0, chunk_sized_for = 0;
     unsigned long long *d_l2pool = nullptr, *d_l2hash = nullptr;
     uint32_t *d_l2u32 = nullptr;     // wts | poss | w2 | pos2 | list2 | count2
     unsigned long long *d_l2slots = nullptr;  // [2 pow2(l2_cap)] tag << 32 | record
@@ -3174,6 +3177,21 @@ struct DeviceGuard {
         if (prev >= 0 && cur != prev) cudaSetDevice(prev);
     }
 };
+
+// TCG_HOST_TRACE=1: host timestamps (us since the previous mark) around the
+// pipeline's synchronisation points, to stderr (diagnostics only).
+static void host_mark(const char *what) {
+    static const bool on = [] {
+        const char *e = std::getenv("TCG_HOST_TRACE");
+        return e && e[0] && e[0] != '0';
+    }();
+    if (!on) return;
+    static auto prev = std::chrono::steady_clock::now();
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[tcg] %-22s +%9.1f us\n", what,
+                 std::chrono::duration<double, std::micro>(now - prev).count());
+    prev = now;
+}
 
 // Per-kernel timing: events bracket each launch on the plan's stream and are
 // resolved after the next synchronisation (tcg_agg_fetch / tcg_kernel_times).
@@ -4133,7 +4151,8 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
         if (e != cudaSuccess) rc = fail(TCG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
         return e == cudaSuccess;
     };
-    if (nrec1 > P->l15_cap) {
+    if (nrec1 > P->l15_cap && nrec1 > P->l15_sized_for) {
+        P->l15_sized_for = nrec1;
         size_t fr = 0, tot = 0;
         if (!cuda_ok(cudaStreamSynchronize(P->stream), "sync")) return false;
         if (!cuda_ok(cudaMemGetInfo(&fr, &tot), "meminfo")) return false;
@@ -4159,6 +4178,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
             return false;
         P->l15_cap = c;
     }
+    if (nrec1 > P->l15_cap) return false;  // sized before and did not fit: direct path
     const size_t c = P->l15_cap;
     uint32_t *wts1 = P->d_l15u32, *poss1 = wts1 + c, *w15 = poss1 + c, *pos15 = w15 + c,
              *list15 = pos15 + c, *count15 = list15 + c, *failp = count15 + 1, *saved = failp + 1;
@@ -4237,9 +4257,11 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     if (!cuda_ok(cudaLaunchKernel((void *)k_l2_dedup, dim3(g1d), dim3(THREADS), ad, 0, st), "l15 dedup"))
         return false;
     uint32_t hostv[2] = {0, 0};  // count15, fail
+    host_mark("l15 enqueued");
     if (!cuda_ok(cudaMemcpyAsync(hostv, count15, 8, cudaMemcpyDeviceToHost, st), "copy") ||
         !cuda_ok(cudaStreamSynchronize(st), "sync"))
         return false;
+    host_mark("l15 synced");
     timing_end(P, TCG_KT_L15_DEDUP, e0);
     P->l15_built += nrec1;
     P->launches += 2;
@@ -4264,9 +4286,11 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     if (!cuda_ok(cudaLaunchKernel(l2f, dim3(std::max(1u, g2)), dim3(THREADS), a2, smem2, st),
                  "l2 from l15"))
         return false;
+    host_mark("l2f enqueued");
     if (!cuda_ok(cudaMemcpyAsync(hostv + 1, failp, 4, cudaMemcpyDeviceToHost, st), "copy") ||
         !cuda_ok(cudaStreamSynchronize(st), "sync"))
         return false;
+    host_mark("l2f synced");
     timing_end(P, TCG_KT_L2_BUILD, e1);
     P->launches++;
     if (hostv[1]) return fallback();
@@ -4294,8 +4318,10 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
                       const uint32_t *mint1, uint64_t tile0, uint64_t lo, uint64_t hi) {
     const TileTables &T = P->h_tiles[mode];
     uint32_t n1 = 0;
+    host_mark("l1 enqueued");
     CUDA_TRY(cudaMemcpyAsync(&n1, count1, sizeof(n1), cudaMemcpyDeviceToHost, P->stream));
     CUDA_TRY(cudaStreamSynchronize(P->stream));
+    host_mark("l1 synced");
     P->reps1_host += n1;
     CUDA_TRY(cudaMemsetAsync(P->d_oldlist, 0, sizeof(uint32_t), P->stream));
     if (n1 == 0) return TCG_OK;
@@ -4306,8 +4332,12 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
     // that later sweeps never reallocate inside a timed region
     const size_t want = std::max((size_t)n1, (size_t)P->chunk_cap / 2) << la;
     const size_t per_rec = stride * 8 + 8 + 4 * 6 + 16;
-    if (want > P->l2_cap || (int)stride != P->l2_stride) {
+    // (re)size only when this want was not tried before: once the pool is as
+    // large as memory allows, later sweeps must not query the driver again
+    // (cudaMemGetInfo measured 2..90 ms on the box, inside the timed region)
+    if ((want > P->l2_cap && want > P->l2_sized_for) || (int)stride != P->l2_stride) {
         size_t fr = 0, tot = 0;
+        P->l2_sized_for = want;
         CUDA_TRY(cudaMemGetInfo(&fr, &tot));
         fr += P->l2_cap * per_rec;
         size_t cap = std::max<size_t>(want, P->l2_cap);
@@ -4556,7 +4586,8 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
         uint32_t chunk = (uint32_t)std::min<uint64_t>(chunk_tiles(), chunk_index_limit() >> bits);
         chunk = std::min<uint32_t>(chunk, next_pow2((uint32_t)std::min<uint64_t>(
                                               t_end - (start >> bits), 1u << 30)));
-        if (chunk > P->chunk_cap) {  // (re)allocate the contraction records + dedup table
+        if (chunk > P->chunk_cap && chunk > P->chunk_sized_for) {  // (re)allocate records + dedup table
+            P->chunk_sized_for = chunk;
             CUDA_TRY(cudaStreamSynchronize(P->stream));
             size_t fr = 0, tot = 0;
             CUDA_TRY(cudaMemGetInfo(&fr, &tot));
@@ -4792,6 +4823,7 @@ static int settle(const tcg_agg *A, const FetchOut &F, int64_t *bad) {
 // failing index; library errors (< 0) only.
 static int fetch_raw(tcg_plan *P, tcg_agg *A, FetchOut &F) {
     DeviceGuard guard(P->device);
+    host_mark("fetch");
     CUDA_TRY(cudaMemsetAsync(P->d_cn, 0, 4, P->stream));
     k_agg_compact<<<64, 256, 0, P->stream>>>(P->agg, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn);
     CUDA_TRY(cudaGetLastError());
@@ -4803,6 +4835,7 @@ static int fetch_raw(tcg_plan *P, tcg_agg *A, FetchOut &F) {
     CUDA_TRY(cudaMemcpyAsync(hist, P->agg.hist, sizeof(hist), cudaMemcpyDeviceToHost, P->stream));
     CUDA_TRY(cudaMemcpyAsync(&badidx, P->agg.bad, 8, cudaMemcpyDeviceToHost, P->stream));
     CUDA_TRY(cudaStreamSynchronize(P->stream));
+    host_mark("fetch synced");
     F = FetchOut{};
     F.overflow = overflow != 0;
     F.index_ordered = P->pending_mode != MODE_SAMPLE;
