@@ -340,7 +340,8 @@ def slice_parity(T, c):
 # ------------------------------------------------------------ other configs
 def bench_c5(dev, steps, warmup):
     """Config C5: uniform sampling over the degree-8 representative space
-    (seed 20260810, draws k0 = 2^39 ..), per-patchwork full-diamond kernel."""
+    (seed 20260810, draws k0 = 2^39 ..): the separator-split sampler
+    (k_sample_split, csrc/split.cuh; draws it leaves go to k_sample_list)."""
     import torch
 
     from paper_2604_09221_b200 import Classifier, builtin
@@ -358,11 +359,14 @@ def bench_c5(dev, steps, warmup):
         stream = torch.cuda.Stream(device=dev)  # events and kernels on one stream
         torch.cuda.set_stream(stream)
         c.native.set_stream(stream.cuda_stream)
-        for s in range(warmup):
+        c.native.set_timing(True)
+        for s in range(warmup):  # the first one builds the split tables
             c.native.agg_reset()
             c.native.sample_async(seed, k0 + (s + 1) * n * 4, k0 + (s + 1) * n * 4 + n, 42)
             c.native.agg_fetch()
         torch.cuda.synchronize()
+        build_ms = c.native.kernel_times()["split_build"][0]
+        c.native.split_stats()
         evs = []
         c.native.set_timing(True)
         c.native.kernel_times()
@@ -378,6 +382,7 @@ def bench_c5(dev, steps, warmup):
         torch.cuda.synchronize()
         kt = c.native.kernel_times()
         c.native.set_timing(False)
+        sst = c.native.split_stats()  # state, draws, left to the flat kernel, F vertices, bytes
         ms = sum(x.elapsed_time(y) for x, y in evs) / steps
         t0 = time.perf_counter()
         for s in range(steps):
@@ -389,7 +394,8 @@ def bench_c5(dev, steps, warmup):
             r = sample_slice(T, g["seed"], g["k0"], g["k1"], classifier=c)
             ok += (list(r.oval_histogram) == g["hist"] and
                    r.scheme_map == {k: tuple(v) for k, v in g["schemes"].items()})
-        enum_ms = kt["enumerate"][0] / steps
+        split = sst[0] == 1
+        kern_ms = (kt["sample_split"][0] + kt["sample_list"][0] if split else kt["enumerate"][0]) / steps
         out[f"c5_{name}"] = {
             "metric": "draws classified/sec (degree-8 uniform sampling, one B200)",
             "value": n / (ms / 1e3), "unit": "draws/s", "ms_per_step": ms,
@@ -397,7 +403,14 @@ def bench_c5(dev, steps, warmup):
                     "path": "sweep.sample_slice (host round trip + string rendering)"},
             "config": {"workload": f"C5 {name}: draws [2^39 + s 2^28, +2^28) seed 20260810, "
                                    "m = splitmix64 & (2^42-1)", "draws_per_step": n},
-            "kernel": "k_enumerate<6,even,SAMPLE>", "kernel_ms_per_step": enum_ms,
+            "kernel": ("k_sample_split<even> + k_sample_list<6,even>" if split
+                       else "k_enumerate<6,even,SAMPLE>"),
+            "kernel_ms_per_step": kern_ms,
+            "split": {"separator_vertices": sst[3], "table_bytes": sst[4],
+                      "table_build_ms": build_ms,
+                      "flat_fallback_fraction": sst[2] / sst[1] if sst[1] else None,
+                      "sample_split_ms_per_step": kt["sample_split"][0] / steps,
+                      "sample_list_ms_per_step": kt["sample_list"][0] / steps} if split else None,
             "parity": f"{ok}/{len(slices)} reference sample_kernel slices (2^20 draws) bit-exact",
             "parity_ok": ok == len(slices),
         }

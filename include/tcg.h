@@ -150,9 +150,10 @@ int tcg_tile_stats(tcg_plan *plan, int64_t *out);
  * graphs over 32 nodes, fallback tiles); all since the last call. */
 int tcg_plan_set_level2(tcg_plan *plan, int enable);
 int tcg_level2_stats(tcg_plan *plan, int64_t *out);
-/* Separator-split sampling (d >= 6, on by default; TCG_NO_SPLIT=1 or
- * enable=0 samples with the flat kernel only -- results are identical).  At
- * the first sample the plan picks a small vertex separator F of T's edge
+/* Separator-split sampling (d >= 6; on by default for samples of >= 2^22
+ * draws, and for any sample once the tables exist; enable=1 forces it,
+ * TCG_NO_SPLIT=1 or enable=0 samples with the flat kernel only -- results are
+ * identical).  At the first such sample the plan picks a small vertex separator F of T's edge
  * graph and tabulates, for every sign pattern of each side, the same-sign
  * components of that side's diamond vertices (device memory, once); each draw
  * is then classified on the graph of F's vertices plus the two sides'

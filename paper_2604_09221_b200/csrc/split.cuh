@@ -60,7 +60,12 @@ template <int K>
 __global__ void __launch_bounds__(THREADS) k_split_build(KParams p, SplitPart sp,
                                                          uint32_t *__restrict__ tab, uint32_t n) {
     extern __shared__ __align__(16) uint32_t smem[];
+    int8_t *fidx = reinterpret_cast<int8_t *>(smem + 32 * K * K);  // layout position -> F vertex
     stage_adj<K>(p, smem);
+    for (int i = threadIdx.x; i < 32 * K; i += blockDim.x) fidx[i] = -1;
+    __syncthreads();
+    for (int f = threadIdx.x; f < sp.nF; f += blockDim.x)
+        fidx[32 * sp.fword[f] + __ffs(sp.fbit[f]) - 1] = (int8_t)f;
     __syncthreads();
     for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < n; x += gridDim.x * blockDim.x) {
         uint64_t sigma = 0;
@@ -80,37 +85,40 @@ __global__ void __launch_bounds__(THREADS) k_split_build(KParams p, SplitPart sp
             e[0] = 0xffffu;
             continue;
         }
-        uint32_t fm[SPL_MAXF];
-        for (int f = 0; f < SPL_MAXF; ++f) fm[f] = 0u;
+        // component label of every part vertex, then each component's
+        // neighbourhoods are read through the labels (O(|X|), not O(nc^2))
+        uint8_t lab[32 * K];
         uint32_t sgn = 0;
         for (int c = 0; c < nc; ++c) {
-            uint32_t X[K], R[K], P[K];
+            uint32_t s = 0;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                X[k] = comps.X[c][k];
-                R[k] = comps.R[c][k];
+                const uint32_t r = comps.R[c][k];
+                s |= r & SG[k];
+                for (uint32_t w = r; w; w &= w - 1u) lab[32 * k + __ffs(w) - 1] = (uint8_t)c;
             }
-#pragma unroll
-            for (int k = 0; k < K; ++k) P[k] = R[(k + K / 2) % K] & p.bd[(k + K / 2) % K];
-            uint32_t adjP = 0, linkP = 0, adjF = 0, s = 0;
-            for (int c2 = 0; c2 < nc; ++c2) {
-                uint32_t a = 0, q = 0;
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    a |= X[k] & comps.R[c2][k];
-                    q |= P[k] & comps.R[c2][k];
-                }
-                if (a && c2 != c) adjP |= 1u << c2;
-                if (q) linkP |= 1u << c2;
-            }
-            for (int f = 0; f < sp.nF; ++f)
-                if (sel<K>(X, sp.fword[f]) & sp.fbit[f]) {
-                    adjF |= 1u << f;
-                    fm[f] |= 1u << c;
-                }
-#pragma unroll
-            for (int k = 0; k < K; ++k) s |= R[k] & SG[k];
             if (s) sgn |= 1u << c;
+        }
+        uint32_t fm[SPL_MAXF];
+        for (int f = 0; f < SPL_MAXF; ++f) fm[f] = 0u;
+        for (int c = 0; c < nc; ++c) {
+            uint32_t adjP = 0, linkP = 0, adjF = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const uint32_t xk = comps.X[c][k];
+                const int ks = (k + K / 2) % K;  // antipodal partners: swap of halves
+                const uint32_t pk = comps.R[c][ks] & p.bd[ks];
+                for (uint32_t w = xk & pm[k]; w; w &= w - 1u) adjP |= 1u << lab[32 * k + __ffs(w) - 1];
+                for (uint32_t w = pk & pm[k]; w; w &= w - 1u) linkP |= 1u << lab[32 * k + __ffs(w) - 1];
+                for (uint32_t w = xk & ~pm[k]; w; w &= w - 1u) {
+                    const int f = fidx[32 * k + __ffs(w) - 1];
+                    if (f >= 0) {
+                        adjF |= 1u << f;
+                        fm[f] |= 1u << c;
+                    }
+                }
+            }
+            adjP &= ~(1u << c);
             reinterpret_cast<uint4 *>(e + 4 + sp.nFp)[c] = make_uint4(adjF, adjP, linkP, 0u);
         }
         e[0] = (uint32_t)nc;

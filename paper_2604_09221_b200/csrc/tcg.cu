@@ -4453,6 +4453,8 @@ static bool dedup_enabled() {
     return on;
 }
 
+constexpr uint64_t SPLIT_MIN_DRAWS = 1ull << 22;
+
 // TCG_NO_SPLIT=1 samples with the flat kernel only (A/B and debugging); results are identical.
 static bool split_enabled(const tcg_plan *P) {
     if (P->split >= 0) return P->split != 0;
@@ -4504,9 +4506,10 @@ static int ensure_split(tcg_plan *P) {
                              P->stream));
     P->split_bytes = (na + nb) * ew * 4;
     void *fb = pick_split_build(P->K);
-    CUDA_TRY(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)adj_bytes(P->K)));
+    const size_t bsm = adj_bytes(P->K) + 32 * P->K;  // + F index per layout position
+    CUDA_TRY(cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsm));
     int bps = 0;
-    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fb, THREADS, adj_bytes(P->K)));
+    CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, fb, THREADS, bsm));
     for (int t = 0; t < 2; ++t) {
         SplitPart part = t ? S.pb : S.pa;
         uint32_t *tab = t ? P->d_splitB : P->d_splitA;
@@ -4515,7 +4518,7 @@ static int ensure_split(tcg_plan *P) {
                                                            (n + THREADS - 1) / THREADS);
         void *args[] = {&P->kp, &part, &tab, &n};
         cudaEvent_t e0 = timing_begin(P);
-        CUDA_TRY(cudaLaunchKernel(fb, dim3(grid), dim3(THREADS), args, adj_bytes(P->K), P->stream));
+        CUDA_TRY(cudaLaunchKernel(fb, dim3(grid), dim3(THREADS), args, bsm, P->stream));
         timing_end(P, TCG_KT_SPLIT_BUILD, e0);
         P->launches++;
     }
@@ -4722,7 +4725,11 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
         }
         return TCG_OK;
     }
-    if (mode == MODE_SAMPLE && end > start && split_enabled(P)) {
+    // the split tables (0.1-2.5 GB, built once per plan) pay off for large
+    // samples; smaller ones use the flat kernel unless the tables exist or
+    // the caller asked for the split path (tcg_plan_set_split(plan, 1))
+    if (mode == MODE_SAMPLE && end > start && split_enabled(P) &&
+        (P->split == 1 || P->split_state == 1 || end - start >= SPLIT_MIN_DRAWS)) {
         int rc = ensure_split(P);
         if (rc) return rc;
         if (P->split_state > 0) return enqueue_split(P, start, end, seed, mask);
