@@ -69,8 +69,14 @@ def log(*a):
 
 
 def source_sha16():
-    with open(os.path.join(ROOT, "paper_2604_09221_b200", "csrc", "tcg.cu"), "rb") as fh:
-        return hashlib.sha256(fh.read()).hexdigest()[:16]
+    """sha256 of the CUDA sources (csrc/*.cu, *.cuh in name order), 16 hex digits."""
+    d = os.path.join(ROOT, "paper_2604_09221_b200", "csrc")
+    h = hashlib.sha256()
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh")):
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(fh.read())
+    return h.hexdigest()[:16]
 
 
 def ncu_profile():
@@ -82,9 +88,9 @@ def ncu_profile():
     except (OSError, ValueError):
         return None, "profiles/ncu_kernels.json missing"
     if prof.get("tcg_cu_sha16") != source_sha16():
-        return None, (f"profiles/ncu_kernels.json is from tcg.cu {prof.get('tcg_cu_sha16')}, "
+        return None, (f"profiles/ncu_kernels.json is from CUDA sources {prof.get('tcg_cu_sha16')}, "
                       f"this build is {source_sha16()}: not used")
-    return prof, "profiles/ncu_kernels.json (same tcg.cu)"
+    return prof, "profiles/ncu_kernels.json (same CUDA sources)"
 
 
 def peaks():
@@ -720,7 +726,7 @@ def run_ours(args, rank, world, local_rank):
                        "bytes_per_patchwork": step_bytes / units_per_step}
     roof["note"] = (f"integer instruction issue bound (no FP / tensor work; SURVEY 8(d)): "
                     f"achieved = thread instructions the dominant kernel executes per step "
-                    f"(ncu smsp__thread_inst_executed.sum, same tcg.cu) / its CUDA-event time "
+                    f"(ncu smsp__thread_inst_executed.sum, same CUDA sources) / its CUDA-event time "
                     f"per step in this run; peak = {nsm} SMs x 128 lanes x {mhz:.0f} MHz "
                     f"({peak_src}). hbm.per_kind: ncu dram bytes / live time vs the copy peak.")
 

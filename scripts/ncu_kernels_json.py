@@ -74,8 +74,13 @@ def main(path, out_path, desc):
     for a in acc.values():
         for lab, (s, t) in a.pop("_w").items():
             a[lab] = round(s / t, 3) if t else None
-    with open(os.path.join(ROOT, "paper_2604_09221_b200", "csrc", "tcg.cu"), "rb") as fh:
-        sha = hashlib.sha256(fh.read()).hexdigest()[:16]
+    d = os.path.join(ROOT, "paper_2604_09221_b200", "csrc")
+    h = hashlib.sha256()
+    for f in sorted(os.listdir(d)):  # same digest as bench.py source_sha16
+        if f.endswith((".cu", ".cuh")):
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(fh.read())
+    sha = h.hexdigest()[:16]
     doc = {"tcg_cu_sha16": sha, "capture": desc, "report": os.path.basename(path),
            "kernels": acc}
     with open(out_path, "w") as fh:
