@@ -4362,39 +4362,51 @@ static int run_level2(tcg_plan *P, int mode, const TileTables *tt, const TileRec
         }
     }
     const size_t cap = P->l2_cap;
-    const uint32_t nbmax = (uint32_t)(cap >> la);
+    // Batches of level-1 representatives.  The direct build writes 2^la records
+    // per tile into the level-2 pool, so its batches hold cap >> la tiles; the
+    // two-stage path writes 2^la1 stage-1 records per tile into its own pool
+    // and only the distinct ones' 2^la2 records into the level-2 pool, so it
+    // takes every representative of the chunk in one batch -- one stage-1
+    // deduplication window (C3: 2 -> 1 batch per step).  A batch the two-stage
+    // path declines runs the direct path in cap >> la sub-batches.
+    const uint32_t nbdir = (uint32_t)(cap >> la);
+    const bool ts = T.ts && l2_twostage_enabled();
+    const uint32_t nbmax = ts ? n1 : nbdir;
     for (uint32_t i0 = 0; i0 < n1; i0 += nbmax) {
-        uint32_t nb = std::min(nbmax, n1 - i0);
-        uint32_t nrec = nb << la;
-        if (T.ts && l2_twostage_enabled()) {
+        const uint32_t nbb = std::min(nbmax, n1 - i0);
+        if (ts) {
             int rc2 = 0;
-            const bool done = run_two_stage(P, mode, tt, recs, list1, dup1, mint1, i0, nb, tile0,
+            const bool done = run_two_stage(P, mode, tt, recs, list1, dup1, mint1, i0, nbb, tile0,
                                             lo, hi, cap, stride, rc2);
             if (rc2) return rc2;
             if (done) continue;
         }
-        static const uint64_t gmb = [] {  // CTAs per SM of the direct level-2 build
-            const char *e = std::getenv("TCG_L2B_GRID");
-            return e ? (uint64_t)std::max(1, std::atoi(e)) : (uint64_t)8;
-        }();
-        const unsigned g12 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * gmb,
-                                                          (nrec + THREADS - 1) / THREADS);
-        unsigned long long *pool = P->d_l2pool, *hashes = P->d_l2hash;
-        uint32_t *wts = P->d_l2u32, *poss = wts + cap;
-        uint32_t *oldlist = P->d_oldlist + 1, *oldcount = P->d_oldlist;
-        uint64_t t0 = tile0, a = lo, b = hi;
-        void *a1[] = {&tt, &recs, &list1, &dup1, &mint1, &i0, &nb, &t0, &a, &b, &pool,
-                      (void *)&stride, &hashes, &wts, &poss, &oldlist, &oldcount};
-        cudaEvent_t e0 = timing_begin(P);
-        const size_t l2b_smem = (size_t)L2B_WORDS * 4 * THREADS +
-                                (size_t)(THREADS / 32) * (32 >> std::min(la, 5)) * L2B_SLOT;
-        void *kb = T.l2even ? (void *)k_l2_build<true> : (void *)k_l2_build<false>;
-        CUDA_TRY(cudaLaunchKernel(kb, dim3(g12), dim3(THREADS), a1, l2b_smem,
-                                  P->stream));
-        timing_end(P, TCG_KT_L2_BUILD, e0);
-        P->launches++;
-        const int rc = l2_tail(P, T, tt, nrec, stride, tile0);
-        if (rc) return rc;
+        for (uint32_t j0 = i0; j0 < i0 + nbb; j0 += nbdir) {
+            uint32_t nb = std::min(nbdir, i0 + nbb - j0);
+            uint32_t jv = j0;
+            uint32_t nrec = nb << la;
+            static const uint64_t gmb = [] {  // CTAs per SM of the direct level-2 build
+                const char *e = std::getenv("TCG_L2B_GRID");
+                return e ? (uint64_t)std::max(1, std::atoi(e)) : (uint64_t)8;
+            }();
+            const unsigned g12 = (unsigned)std::min<uint64_t>((uint64_t)P->nsm * gmb,
+                                                              (nrec + THREADS - 1) / THREADS);
+            unsigned long long *pool = P->d_l2pool, *hashes = P->d_l2hash;
+            uint32_t *wts = P->d_l2u32, *poss = wts + cap;
+            uint32_t *oldlist = P->d_oldlist + 1, *oldcount = P->d_oldlist;
+            uint64_t t0 = tile0, a = lo, b = hi;
+            void *a1[] = {&tt, &recs, &list1, &dup1, &mint1, &jv, &nb, &t0, &a, &b, &pool,
+                          (void *)&stride, &hashes, &wts, &poss, &oldlist, &oldcount};
+            cudaEvent_t e0 = timing_begin(P);
+            const size_t l2b_smem = (size_t)L2B_WORDS * 4 * THREADS +
+                                    (size_t)(THREADS / 32) * (32 >> std::min(la, 5)) * L2B_SLOT;
+            void *kb = T.l2even ? (void *)k_l2_build<true> : (void *)k_l2_build<false>;
+            CUDA_TRY(cudaLaunchKernel(kb, dim3(g12), dim3(THREADS), a1, l2b_smem, P->stream));
+            timing_end(P, TCG_KT_L2_BUILD, e0);
+            P->launches++;
+            const int rc = l2_tail(P, T, tt, nrec, stride, tile0);
+            if (rc) return rc;
+        }
     }
     return TCG_OK;
 }
