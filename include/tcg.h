@@ -217,8 +217,10 @@ int tcg_sample_multi(tcg_plan **plans, int nplans, uint64_t seed, uint64_t k0, u
 /* Many triangulations of one degree on one device (config C4, SURVEY
  * section 8f row 2): pairs (tri[t], sigma[t]) are grouped by triangulation
  * and every CTA classifies one group on its own topology.  Host buffers;
- * outputs in the input order.  tcg_multi_last_ms = device time of the last
- * classification kernel (CUDA events). */
+ * outputs in the input order; the call pipelines chunks of 2^22 pairs
+ * through pinned staging (host threads copy in and out while the GPU copies
+ * and classifies the neighbouring chunks).  tcg_multi_last_ms = device time
+ * of the last call's classification kernels (CUDA events, summed). */
 typedef struct tcg_multi tcg_multi;
 int tcg_multi_create(const tcg_desc *descs, int32_t ntri, int device, tcg_multi **out);
 int tcg_multi_destroy(tcg_multi *m);

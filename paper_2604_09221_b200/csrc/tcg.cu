@@ -5048,7 +5048,33 @@ struct tcg_multi {
     int64_t items_cap = 0;
     float last_ms = 0.f;
     int64_t launches = 0;
+    // host-buffer pipeline: two slots of pinned staging, one stream each
+    cudaStream_t sst[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2][2] = {};       // kernel start / stop per slot
+    uint8_t *h_stage[2] = {nullptr, nullptr};  // [MULTI_CHUNK] sig | key | st | ov | nr
 };
+
+static constexpr int64_t MULTI_CHUNK = 1 << 22;  // pairs per pipeline chunk
+static constexpr size_t MULTI_STAGE = (size_t)MULTI_CHUNK * (8 + 8 + 4 + 1 + 1);
+
+// Host copies of the pipeline split over a few threads (one memcpy stream is
+// ~10 GB/s; the box has >= 16 cores).
+static void par_for(int64_t n, const std::function<void(int64_t, int64_t)> &fn) {
+    static const int nth = [] {
+        const char *e = std::getenv("TCG_HOST_THREADS");
+        const int hw = (int)std::thread::hardware_concurrency();
+        return e ? std::max(1, std::atoi(e)) : std::max(1, std::min(8, hw / 2));
+    }();
+    const int t = (int)std::min<int64_t>(nth, std::max<int64_t>(1, n >> 16));
+    if (t <= 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int i = 1; i < t; ++i) th.emplace_back(fn, n * i / t, n * (i + 1) / t);
+    fn(0, n / t);
+    for (auto &x : th) x.join();
+}
 
 static void *pick_multi(int K, bool even) {
     if (K == 2) return even ? (void *)k_multi<2, true> : (void *)k_multi<2, false>;
@@ -5064,6 +5090,15 @@ int tcg_multi_destroy(tcg_multi *M) {
                     M->d_st, M->d_items};
     for (void *q : ptrs)
         if (q) cudaFree(q);
+    for (int i = 0; i < 2; ++i) {
+        if (M->sst[i]) {
+            cudaStreamSynchronize(M->sst[i]);
+            cudaStreamDestroy(M->sst[i]);
+        }
+        for (int j = 0; j < 2; ++j)
+            if (M->ev[i][j]) cudaEventDestroy(M->ev[i][j]);
+        if (M->h_stage[i]) cudaFreeHost(M->h_stage[i]);
+    }
     if (M->stream) cudaStreamDestroy(M->stream);
     delete M;
     return TCG_OK;
@@ -5143,13 +5178,32 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
     // triangulation ids are already non-decreasing, e.g. config C4's layout);
     // work items of <= 2048 pairs of one triangulation
     constexpr int ITEM = 2048;
+    host_mark("multi start");
     std::vector<int64_t> cnt(M->ntri + 1, 0);
-    bool grouped = true;
-    for (int64_t i = 0; i < n; ++i) {
-        if (tri[i] < 0 || tri[i] >= M->ntri) return fail(TCG_E_ARG, "triangulation index out of range");
-        cnt[tri[i] + 1]++;
-        grouped &= i == 0 || tri[i] >= tri[i - 1];
+    {  // validate, count and test the order in parallel slices
+        std::mutex mu;
+        std::atomic<bool> bad{false}, unordered{false};
+        par_for(n, [&](int64_t lo, int64_t hi) {
+            std::vector<int64_t> c(M->ntri + 1, 0);
+            bool ord = lo == 0 || (tri[lo] >= tri[lo - 1]);
+            for (int64_t i = lo; i < hi; ++i) {
+                const int32_t t = tri[i];
+                if (t < 0 || t >= M->ntri) {
+                    bad = true;
+                    return;
+                }
+                c[t + 1]++;
+                ord &= i == lo || t >= tri[i - 1];
+            }
+            if (!ord) unordered = true;
+            std::lock_guard<std::mutex> g(mu);
+            for (int t = 0; t <= M->ntri; ++t) cnt[t] += c[t];
+        });
+        if (bad) return fail(TCG_E_ARG, "triangulation index out of range");
+        if (unordered) cnt[0] = -1;  // marker
     }
+    const bool grouped = cnt[0] == 0;
+    cnt[0] = 0;
     for (int t = 0; t < M->ntri; ++t) cnt[t + 1] += cnt[t];
     std::vector<int64_t> order;
     std::vector<uint64_t> ssig;
@@ -5163,10 +5217,12 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
             ssig[j] = sig[i];
         }
     }
+    const uint64_t *gsig = grouped ? sig : ssig.data();
     std::vector<int4> items;
     for (int t = 0; t < M->ntri; ++t)
         for (int64_t a = cnt[t]; a < cnt[t + 1]; a += ITEM)
             items.push_back(make_int4(t, (int)a, (int)std::min<int64_t>(ITEM, cnt[t + 1] - a), 0));
+    host_mark("multi grouped");
     if (n > M->cap) {
         void *ptrs[] = {M->d_sig, M->d_key, M->d_ov, M->d_nr, M->d_st};
         for (void *q : ptrs)
@@ -5187,50 +5243,93 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
         CUDA_TRY(cudaMalloc(&M->d_items, sizeof(int4) * items.size()));
         M->items_cap = (int64_t)items.size();
     }
-    CUDA_TRY(cudaMemcpyAsync(M->d_sig, grouped ? sig : ssig.data(), n * 8, cudaMemcpyHostToDevice,
-                             M->stream));
-    CUDA_TRY(cudaMemcpyAsync(M->d_items, items.data(), sizeof(int4) * items.size(),
-                             cudaMemcpyHostToDevice, M->stream));
+    for (int i = 0; i < 2; ++i) {
+        if (!M->sst[i]) CUDA_TRY(cudaStreamCreateWithFlags(&M->sst[i], cudaStreamNonBlocking));
+        for (int j = 0; j < 2; ++j)
+            if (!M->ev[i][j]) CUDA_TRY(cudaEventCreate(&M->ev[i][j]));
+        if (!M->h_stage[i]) CUDA_TRY(cudaHostAlloc((void **)&M->h_stage[i], MULTI_STAGE, cudaHostAllocDefault));
+    }
+    CUDA_TRY(cudaMemcpy(M->d_items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
     void *fn = pick_multi(M->K, M->even);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M->smem);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, M->stream);
-    void *args[] = {&M->d_kp, &M->d_items, &M->d_sig, &M->d_key, &M->d_ov, &M->d_nr, &M->d_st};
-    CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)items.size()), dim3(THREADS), args, M->smem,
-                              M->stream));
-    cudaEventRecord(e1, M->stream);
-    M->launches++;
-    if (grouped) {  // outputs are already in the caller's order
-        CUDA_TRY(cudaMemcpyAsync(key, M->d_key, n * 8, cudaMemcpyDeviceToHost, M->stream));
-        CUDA_TRY(cudaMemcpyAsync(ov, M->d_ov, n, cudaMemcpyDeviceToHost, M->stream));
-        CUDA_TRY(cudaMemcpyAsync(nr, M->d_nr, n, cudaMemcpyDeviceToHost, M->stream));
-        CUDA_TRY(cudaMemcpyAsync(st, M->d_st, n * 4, cudaMemcpyDeviceToHost, M->stream));
-        CUDA_TRY(cudaStreamSynchronize(M->stream));
-        cudaEventElapsedTime(&M->last_ms, e0, e1);
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
+    // Pipeline over chunks of whole items (<= MULTI_CHUNK pairs): slot c & 1
+    // stages chunk c's signs into pinned memory (host threads), copies them up,
+    // classifies, copies the results down on its stream; chunk c-2's results
+    // leave the slot (host threads, scattered back if the input was regrouped)
+    // before it is reused, so host copies, PCIe both ways and the kernel overlap.
+    struct Chunk { int64_t ib, ie, p0, p1; };
+    std::vector<Chunk> chunks;
+    for (int64_t ib = 0; ib < (int64_t)items.size();) {
+        int64_t ie = ib, p0 = items[ib].y, p1 = p0;
+        while (ie < (int64_t)items.size() && items[ie].y + items[ie].z - p0 <= MULTI_CHUNK) {
+            p1 = items[ie].y + items[ie].z;
+            ++ie;
+        }
+        chunks.push_back({ib, ie, p0, p1});
+        ib = ie;
+    }
+    auto stage = [&](int sl) {
+        uint8_t *h = M->h_stage[sl];
+        return std::make_tuple(reinterpret_cast<uint64_t *>(h),
+                               reinterpret_cast<uint64_t *>(h + 8 * MULTI_CHUNK),
+                               reinterpret_cast<int32_t *>(h + 16 * MULTI_CHUNK),
+                               h + 20 * MULTI_CHUNK, h + 21 * MULTI_CHUNK);
+    };
+    float kms = 0.f;
+    auto drain = [&](size_t c) -> int {
+        const int sl = (int)(c & 1);
+        const Chunk &C = chunks[c];
+        CUDA_TRY(cudaStreamSynchronize(M->sst[sl]));
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, M->ev[sl][0], M->ev[sl][1]);
+        kms += ms;
+        auto [hs, hk, hst, hov, hnr] = stage(sl);
+        (void)hs;
+        const int64_t len = C.p1 - C.p0;
+        par_for(len, [&](int64_t lo, int64_t hi) {
+            if (grouped) {
+                std::memcpy(key + C.p0 + lo, hk + lo, (hi - lo) * 8);
+                std::memcpy(st + C.p0 + lo, hst + lo, (hi - lo) * 4);
+                std::memcpy(ov + C.p0 + lo, hov + lo, hi - lo);
+                std::memcpy(nr + C.p0 + lo, hnr + lo, hi - lo);
+            } else {
+                for (int64_t j = lo; j < hi; ++j) {
+                    const int64_t i = order[C.p0 + j];
+                    key[i] = hk[j];
+                    st[i] = hst[j];
+                    ov[i] = hov[j];
+                    nr[i] = hnr[j];
+                }
+            }
+        });
         return TCG_OK;
+    };
+    for (size_t c = 0; c < chunks.size() + 2; ++c) {
+        if (c >= 2) {
+            int rc = drain(c - 2);
+            if (rc) return rc;
+        }
+        if (c >= chunks.size()) continue;
+        const int sl = (int)(c & 1);
+        const Chunk &C = chunks[c];
+        const int64_t len = C.p1 - C.p0;
+        cudaStream_t s = M->sst[sl];
+        auto [hs, hk, hst, hov, hnr] = stage(sl);
+        par_for(len, [&](int64_t lo, int64_t hi) { std::memcpy(hs + lo, gsig + C.p0 + lo, (hi - lo) * 8); });
+        CUDA_TRY(cudaMemcpyAsync(M->d_sig + C.p0, hs, len * 8, cudaMemcpyHostToDevice, s));
+        const int4 *it = M->d_items + C.ib;
+        void *args[] = {&M->d_kp, &it, &M->d_sig, &M->d_key, &M->d_ov, &M->d_nr, &M->d_st};
+        cudaEventRecord(M->ev[sl][0], s);
+        CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)(C.ie - C.ib)), dim3(THREADS), args, M->smem, s));
+        cudaEventRecord(M->ev[sl][1], s);
+        M->launches++;
+        CUDA_TRY(cudaMemcpyAsync(hk, M->d_key + C.p0, len * 8, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(hst, M->d_st + C.p0, len * 4, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(hov, M->d_ov + C.p0, len, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(hnr, M->d_nr + C.p0, len, cudaMemcpyDeviceToHost, s));
     }
-    std::vector<uint64_t> k(n);
-    std::vector<uint8_t> o(n), r(n);
-    std::vector<int32_t> s(n);
-    CUDA_TRY(cudaMemcpyAsync(k.data(), M->d_key, n * 8, cudaMemcpyDeviceToHost, M->stream));
-    CUDA_TRY(cudaMemcpyAsync(o.data(), M->d_ov, n, cudaMemcpyDeviceToHost, M->stream));
-    CUDA_TRY(cudaMemcpyAsync(r.data(), M->d_nr, n, cudaMemcpyDeviceToHost, M->stream));
-    CUDA_TRY(cudaMemcpyAsync(s.data(), M->d_st, n * 4, cudaMemcpyDeviceToHost, M->stream));
-    CUDA_TRY(cudaStreamSynchronize(M->stream));
-    cudaEventElapsedTime(&M->last_ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    for (int64_t j = 0; j < n; ++j) {
-        const int64_t i = order[j];
-        key[i] = k[j];
-        ov[i] = o[j];
-        nr[i] = r[j];
-        st[i] = s[j];
-    }
+    host_mark("multi done");
+    M->last_ms = kms;
     return TCG_OK;
 }
 
