@@ -476,7 +476,7 @@ def bench_c4(dev, steps, warmup):
         "value": n / (ms / 1e3), "unit": "pairs/s", "ms_per_step": ms,
         "e2e": {"value": n / statistics.median(wall), "unit": "pairs/s",
                 "h2d_bytes_per_step": 12 * n, "d2h_bytes_per_step": 14 * n,
-                "path": "MultiClassifier.classify_words (host buffers, grouping, copies)"},
+                "path": "MultiClassifier.classify_words (host buffers; validation, grouping, pinned-staging pipeline of 2^23-pair chunks)"},
         "config": {"workload": "C4: 4096 T from random_unimodular(7, Random(0xB7)) x 2^16 "
                                "words splitmix64(7,k) & (2^36-1)", "pairs_per_step": n},
         "kernel": "k_multi<4,odd>",

@@ -5054,8 +5054,14 @@ struct tcg_multi {
     uint8_t *h_stage[2] = {nullptr, nullptr};  // [MULTI_CHUNK] sig | key | st | ov | nr
 };
 
-static constexpr int64_t MULTI_CHUNK = 1 << 22;  // pairs per pipeline chunk
-static constexpr size_t MULTI_STAGE = (size_t)MULTI_CHUNK * (8 + 8 + 4 + 1 + 1);
+// pairs per pipeline chunk (TCG_MULTI_CHUNK_LOG2, 18..26)
+static int64_t multi_chunk() {
+    static const int64_t c = [] {
+        const char *e = std::getenv("TCG_MULTI_CHUNK_LOG2");
+        return (int64_t)1 << (e ? std::max(18, std::min(26, std::atoi(e))) : 23);
+    }();
+    return c;
+}
 
 // Host copies of the pipeline split over a few threads (one memcpy stream is
 // ~10 GB/s; the box has >= 16 cores).
@@ -5247,7 +5253,8 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
         if (!M->sst[i]) CUDA_TRY(cudaStreamCreateWithFlags(&M->sst[i], cudaStreamNonBlocking));
         for (int j = 0; j < 2; ++j)
             if (!M->ev[i][j]) CUDA_TRY(cudaEventCreate(&M->ev[i][j]));
-        if (!M->h_stage[i]) CUDA_TRY(cudaHostAlloc((void **)&M->h_stage[i], MULTI_STAGE, cudaHostAllocDefault));
+        if (!M->h_stage[i])
+            CUDA_TRY(cudaHostAlloc((void **)&M->h_stage[i], (size_t)multi_chunk() * 22, cudaHostAllocDefault));
     }
     CUDA_TRY(cudaMemcpy(M->d_items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
     void *fn = pick_multi(M->K, M->even);
@@ -5257,6 +5264,7 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
     // classifies, copies the results down on its stream; chunk c-2's results
     // leave the slot (host threads, scattered back if the input was regrouped)
     // before it is reused, so host copies, PCIe both ways and the kernel overlap.
+    const int64_t MULTI_CHUNK = multi_chunk();
     struct Chunk { int64_t ib, ie, p0, p1; };
     std::vector<Chunk> chunks;
     for (int64_t ib = 0; ib < (int64_t)items.size();) {
@@ -5268,12 +5276,16 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
         chunks.push_back({ib, ie, p0, p1});
         ib = ie;
     }
+    struct Stage {
+        uint64_t *sig, *key;
+        int32_t *st;
+        uint8_t *ov, *nr;
+    };
     auto stage = [&](int sl) {
         uint8_t *h = M->h_stage[sl];
-        return std::make_tuple(reinterpret_cast<uint64_t *>(h),
-                               reinterpret_cast<uint64_t *>(h + 8 * MULTI_CHUNK),
-                               reinterpret_cast<int32_t *>(h + 16 * MULTI_CHUNK),
-                               h + 20 * MULTI_CHUNK, h + 21 * MULTI_CHUNK);
+        return Stage{reinterpret_cast<uint64_t *>(h), reinterpret_cast<uint64_t *>(h + 8 * MULTI_CHUNK),
+                     reinterpret_cast<int32_t *>(h + 16 * MULTI_CHUNK), h + 20 * MULTI_CHUNK,
+                     h + 21 * MULTI_CHUNK};
     };
     float kms = 0.f;
     auto drain = [&](size_t c) -> int {
@@ -5283,8 +5295,10 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
         float ms = 0.f;
         cudaEventElapsedTime(&ms, M->ev[sl][0], M->ev[sl][1]);
         kms += ms;
-        auto [hs, hk, hst, hov, hnr] = stage(sl);
-        (void)hs;
+        const Stage S = stage(sl);
+        const uint64_t *hk = S.key;
+        const int32_t *hst = S.st;
+        const uint8_t *hov = S.ov, *hnr = S.nr;
         const int64_t len = C.p1 - C.p0;
         par_for(len, [&](int64_t lo, int64_t hi) {
             if (grouped) {
@@ -5314,7 +5328,10 @@ int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, in
         const Chunk &C = chunks[c];
         const int64_t len = C.p1 - C.p0;
         cudaStream_t s = M->sst[sl];
-        auto [hs, hk, hst, hov, hnr] = stage(sl);
+        const Stage S = stage(sl);
+        uint64_t *hs = S.sig, *hk = S.key;
+        int32_t *hst = S.st;
+        uint8_t *hov = S.ov, *hnr = S.nr;
         par_for(len, [&](int64_t lo, int64_t hi) { std::memcpy(hs + lo, gsig + C.p0 + lo, (hi - lo) * 8); });
         CUDA_TRY(cudaMemcpyAsync(M->d_sig + C.p0, hs, len * 8, cudaMemcpyHostToDevice, s));
         const int4 *it = M->d_items + C.ib;
