@@ -25,8 +25,10 @@ installed from /root/reference into baseline/_ref) on all host cores, same
 metric and config, each step a bounded 2^22-index slice at a random offset.
 
 By default (N = 1) the line also carries `other_workloads`: config C5
-(random sampling, degree 8) and config C4 (4,096 random degree-7
-triangulations x 2^16 signs), the per-patchwork kernels' throughput.
+(random sampling, degree 8: bowtie8, delaunay-8, fig2-middle8, fig2-right8,
+through the separator-split sampler, with the reference's own sampler on the
+host cores as cpu_baseline) and config C4 (4,096 random degree-7
+triangulations x 2^16 signs, the per-patchwork full-diamond kernel).
 """
 
 from __future__ import annotations
@@ -359,7 +361,9 @@ def bench_c5(dev, steps, warmup):
     n = 1 << 28
     k0 = 1 << 39
     seed = 20260810
-    for name in ("bowtie8", "delaunay-8"):
+    tc = import_tcurves()
+    threads = os.cpu_count() or 1
+    for name in ("bowtie8", "delaunay-8", "fig2-middle8", "fig2-right8"):
         T = builtin(name)
         c = Classifier(T, device=dev.index)
         stream = torch.cuda.Stream(device=dev)  # events and kernels on one stream
@@ -401,6 +405,20 @@ def bench_c5(dev, steps, warmup):
             ok += (list(r.oval_histogram) == g["hist"] and
                    r.scheme_map == {k: tuple(v) for k, v in g["schemes"].items()})
         split = sst[0] == 1
+        # CPU baseline: the reference's own sampler on all host cores
+        cpu = None
+        if tc is not None:
+            tT = tc.builtin(name)
+            tcl = tc.Classifier(tT)
+            tc.sample(tT, 1 << 12, seed, workers=threads, classifier=tcl)  # JIT
+            ncpu = 1 << 20
+            t0 = time.perf_counter()
+            r = tc.sample(tT, ncpu, seed, workers=threads, classifier=tcl)
+            sec = time.perf_counter() - t0
+            assert r.total_classified == ncpu
+            cpu = {"value": ncpu / sec, "unit": "draws/s", "cores": threads, "kind": "reference",
+                   "sample": f"tcurves.sample({name}, 2^20, seed {seed}, workers={threads}), "
+                             f"{sec:.1f} s"}
         kern_ms = (kt["sample_split"][0] + kt["sample_list"][0] if split else kt["enumerate"][0]) / steps
         out[f"c5_{name}"] = {
             "metric": "draws classified/sec (degree-8 uniform sampling, one B200)",
@@ -419,6 +437,7 @@ def bench_c5(dev, steps, warmup):
                       "sample_list_ms_per_step": kt["sample_list"][0] / steps} if split else None,
             "parity": f"{ok}/{len(slices)} reference sample_kernel slices (2^20 draws) bit-exact",
             "parity_ok": ok == len(slices),
+            "cpu_baseline": cpu,
         }
     return out
 

@@ -155,7 +155,7 @@ static bool split_design(const tcg_desc *D, const Layout &L, SplitDesign &S) {
     std::sort(cands.begin(), cands.end(), [](const Cand &x, const Cand &y) {
         return x.cost != y.cost ? x.cost < y.cost : x.maxbits < y.maxbits;
     });
-    if (cands.size() > 24) cands.resize(24);
+    if (cands.size() > 96) cands.resize(96);
     // score by simulation: same-sign components of each part (union-find)
     std::vector<int> uf(nv);
     std::function<int(int)> find = [&](int x) {
@@ -164,7 +164,7 @@ static bool split_design(const tcg_desc *D, const Layout &L, SplitDesign &S) {
     };
     double best = 1e30;
     int bi = -1;
-    const int NS = 96;
+    const int NS = 128;
     for (int ci = 0; ci < (int)cands.size(); ++ci) {
         const Cand &c = cands[ci];
         double tot = 0, over = 0;
@@ -193,6 +193,11 @@ static bool split_design(const tcg_desc *D, const Layout &L, SplitDesign &S) {
         }
     }
     const Cand &c = cands[bi];
+    if (const char *e = std::getenv("TCG_SPLIT_DEBUG"))
+        if (e[0] && e[0] != '0')
+            std::fprintf(stderr, "[tcg split] %zu candidates; F = %d points / %d vertices, "
+                         "mean contracted graph %.1f nodes, score %.1f\n",
+                         cands.size(), popc(c.F), c.cost, S.mean_nodes, best);
     // F vertices in layout order; part vertex masks; index ranks
     std::vector<std::pair<int, int>> fv;
     SplitPart *parts[2] = {&S.pa, &S.pb};
