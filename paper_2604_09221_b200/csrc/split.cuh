@@ -127,24 +127,6 @@ __global__ void __launch_bounds__(THREADS) k_split_build(KParams p, SplitPart sp
     }
 }
 
-// Table loads: read-only path, optionally with an L2 fetch-size hint (LD 1:
-// 128 B, 2: 256 B) so one DRAM trip brings in the neighbouring rows of the entry.
-template <int LD>
-__device__ __forceinline__ uint4 ldt(const uint4 *p) {
-    if constexpr (LD == 0) {
-        return __ldg(p);
-    } else {
-        uint4 r;
-        if constexpr (LD == 1)
-            asm("ld.global.nc.L2::128B.v4.u32 {%0, %1, %2, %3}, [%4];"
-                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-        else
-            asm("ld.global.nc.L2::256B.v4.u32 {%0, %1, %2, %3}, [%4];"
-                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
-        return r;
-    }
-}
-
 // The region graph of one draw, built while the regions close.
 struct RegionGraph {
     uint32_t radj[MAXR];  // region adjacency (crossed edges), symmetric
@@ -161,7 +143,7 @@ struct RegionGraph {
 // already closed.  Each adjacent pair is met exactly once (at the later
 // region's close), so the region graph, its edge count and the status inputs
 // are complete when the pass ends.
-template <bool EVEN, int LD>
+template <bool EVEN, int V>
 __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
                                            const uint32_t *__restrict__ flink_s,
                                            const uint32_t *__restrict__ ea,
@@ -182,27 +164,36 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
         if (EVEN) q = 0ull;
         odd = false;
     };
+    // V = 1: a closing region only records its crossed neighbours among the
+    // closed nodes; the label lookups run after the pass (out of the divergent
+    // close branch)
+    u64 xs[V ? MAXR : 1];
+    auto adjacency = [&](int rr, u64 w) {
+        uint32_t A = 0;
+        while (w) {
+            const int n = __ffsll((long long)w) - 1;
+            const int l = (int)((lab0 >> n) & 1ull) | (int)((lab1 >> n) & 1ull) << 1 |
+                          (int)((lab2 >> n) & 1ull) << 2 | (int)((lab3 >> n) & 1ull) << 3 |
+                          (int)((lab4 >> n) & 1ull) << 4;
+            A |= 1u << l;
+            const u64 m = (l & 1 ? lab0 : ~lab0) & (l & 2 ? lab1 : ~lab1) & (l & 4 ? lab2 : ~lab2) &
+                          (l & 8 ? lab3 : ~lab3) & (l & 16 ? lab4 : ~lab4);
+            w &= ~m;
+        }
+        out.radj[rr] = A;
+        nedges += __popc(A);
+        for (uint32_t a = A; a; a &= a - 1u) out.radj[__ffs(a) - 1] |= 1u << rr;
+    };
     auto close = [&]() {
         if (nreg < MAXR) {
             const u64 rs = r ^ un;
             if (x & rs) selfm |= 1u << nreg;
             if (EVEN && odd) oddmask |= 1u << nreg;
-            // earlier regions across crossed edges: one label lookup per region
-            u64 w = x & closed;
-            uint32_t A = 0;
-            while (w) {
-                const int n = __ffsll((long long)w) - 1;
-                const int l = (int)((lab0 >> n) & 1ull) | (int)((lab1 >> n) & 1ull) << 1 |
-                              (int)((lab2 >> n) & 1ull) << 2 | (int)((lab3 >> n) & 1ull) << 3 |
-                              (int)((lab4 >> n) & 1ull) << 4;
-                A |= 1u << l;
-                const u64 m = (l & 1 ? lab0 : ~lab0) & (l & 2 ? lab1 : ~lab1) & (l & 4 ? lab2 : ~lab2) &
-                              (l & 8 ? lab3 : ~lab3) & (l & 16 ? lab4 : ~lab4);
-                w &= ~m;
+            if (V) {
+                xs[nreg] = x & closed;
+            } else {
+                adjacency(nreg, x & closed);
             }
-            out.radj[nreg] = A;
-            nedges += __popc(A);
-            for (uint32_t a = A; a; a &= a - 1u) out.radj[__ffs(a) - 1] |= 1u << nreg;
             closed |= rs;
             if (nreg & 1) lab0 |= rs;
             if (nreg & 2) lab1 |= rs;
@@ -222,8 +213,8 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
     auto load = [&](int v, uint4 &t1, uint4 &t2) {
         const bool isF = v < nF, inA = v < sB;
         const uint4 *pc = inA ? ca + (v - nF) : cb + (v - sB);
-        t1 = ldt<LD>(isF ? fa + (v >> 2) : pc);
-        t2 = isF ? ldt<LD>(fb + (v >> 2)) : make_uint4(0u, 0u, 0u, 0u);
+        t1 = __ldg(isF ? fa + (v >> 2) : pc);
+        t2 = isF ? __ldg(fb + (v >> 2)) : make_uint4(0u, 0u, 0u, 0u);
     };
     auto expand = [&](int v, const uint4 &t1, const uint4 &t2) {
         u64 adj, link;
@@ -276,6 +267,8 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
         expand(v1, a1, a2);
         if (v2 != v1) expand(v2, b1, b2);
     }
+    if (V)
+        for (int rr = 0; rr < nreg && rr < MAXR; ++rr) adjacency(rr, xs[rr]);
     out.nreg = nreg;
     out.nedges = nedges;
     out.selfm = selfm;
@@ -425,7 +418,7 @@ constexpr size_t SPLIT_SMEM = SPLIT_SMEM_HEAD + TABLE_SMEM;
 // sign word -> (A pattern, B pattern, F bits) by byte tables -> contracted
 // classification.  fbl[0] counts the draws left to k_sample_list, fbl[1..]
 // their offsets from `base`.
-template <bool EVEN, int LD>
+template <bool EVEN, int V>
 __global__ void __launch_bounds__(THREADS, 3) k_sample_split(KParams p, SplitParams sp, uint64_t base,
                                                           uint64_t count, uint64_t seed,
                                                           uint64_t nbmask, DevAgg g,
@@ -473,8 +466,8 @@ __global__ void __launch_bounds__(THREADS, 3) k_sample_split(KParams p, SplitPar
                 }
             }
         }
-        const uint4 ha = ldt<LD>(reinterpret_cast<const uint4 *>(ea));
-        const uint4 hb = ldt<LD>(reinterpret_cast<const uint4 *>(eb));
+        const uint4 ha = __ldg(reinterpret_cast<const uint4 *>(ea));
+        const uint4 hb = __ldg(reinterpret_cast<const uint4 *>(eb));
         const int sB = nF + (int)ha.x, nn = sB + (int)hb.x;
         const bool fits = valid && ha.x <= (uint32_t)SPL_CAPC && hb.x <= (uint32_t)SPL_CAPC &&
                           nn <= sp.maxnodes;
@@ -487,7 +480,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_sample_split(KParams p, SplitPar
                                           ((unsigned long long)ha.y << nF) |
                                           ((unsigned long long)hb.y << sB);
             RegionGraph rg;
-            split_pass<EVEN, LD>(fadj_s, flink_s, ea, eb, nF, sp.nFp, sB, nn, sg, rg);
+            split_pass<EVEN, V>(fadj_s, flink_s, ea, eb, nF, sp.nFp, sB, nn, sg, rg);
             r = finish_graph<EVEN>(rg, p.maxreg);
         }
         uint64_t k = 0;
@@ -541,14 +534,14 @@ __global__ void __launch_bounds__(THREADS, K == 6 ? TCG_ENUM_MINB6 : 1)
 }
 
 
-// TCG_SPLIT_LD: table-load flavour (0 plain, 1 / 2: L2 fetch size 128 / 256 B)
+// TCG_SPLIT_V: 1 region adjacency after the pass (default; +6 % on bowtie8),
+// 0 at each region close
 inline void *pick_split(bool even) {
-    static const int ld = [] {
-        const char *e = std::getenv("TCG_SPLIT_LD");
-        return e ? std::atoi(e) : 0;
+    static const int v = [] {
+        const char *e = std::getenv("TCG_SPLIT_V");
+        return e ? std::atoi(e) : 1;
     }();
-    if (ld == 1) return even ? (void *)k_sample_split<true, 1> : (void *)k_sample_split<false, 1>;
-    if (ld == 2) return even ? (void *)k_sample_split<true, 2> : (void *)k_sample_split<false, 2>;
+    if (v == 1) return even ? (void *)k_sample_split<true, 1> : (void *)k_sample_split<false, 1>;
     return even ? (void *)k_sample_split<true, 0> : (void *)k_sample_split<false, 0>;
 }
 
