@@ -167,6 +167,7 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
     // V = 1: a closing region only records its crossed neighbours among the
     // closed nodes; the label lookups run after the pass (out of the divergent
     // close branch)
+    constexpr int NSTEP = V >= 3 ? 4 : (V == 2 ? 3 : 2);  // frontier nodes per step
     u64 xs[V ? MAXR : 1];
     auto adjacency = [&](int rr, u64 w) {
         uint32_t A = 0;
@@ -247,9 +248,6 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
             f |= n;
         }
     };
-    // Two frontier nodes per step: their expansions run in order, so the
-    // result is the sequential pass's (a region's node set, crossed
-    // neighbourhood and parity verdict do not depend on the visit order).
     seed();
     while (true) {
         if (f == 0ull) {
@@ -257,15 +255,23 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
             if (un == 0ull) break;
             seed();
         }
-        const int v1 = __ffsll((long long)f) - 1;
-        f &= f - 1ull;
-        const int v2 = f ? __ffsll((long long)f) - 1 : v1;
-        f &= f - 1ull;  // no-op when f was a single node
-        uint4 a1, a2, b1, b2;
-        load(v1, a1, a2);
-        load(v2, b1, b2);
-        expand(v1, a1, a2);
-        if (v2 != v1) expand(v2, b1, b2);
+        // NSTEP frontier nodes per step: their row loads are issued together,
+        // the expansions then run in order (the result is the sequential
+        // pass's: a region's node set, crossed neighbourhood and parity verdict
+        // do not depend on the visit order); missing nodes repeat v[0]
+        int vs[NSTEP];
+        uint4 t1[NSTEP], t2[NSTEP];
+#pragma unroll
+        for (int i = 0; i < NSTEP; ++i) {
+            vs[i] = f ? __ffsll((long long)f) - 1 : vs[0];
+            f &= f - 1ull;
+        }
+#pragma unroll
+        for (int i = 0; i < NSTEP; ++i) load(vs[i], t1[i], t2[i]);
+        expand(vs[0], t1[0], t2[0]);
+#pragma unroll
+        for (int i = 1; i < NSTEP; ++i)
+            if (vs[i] != vs[0]) expand(vs[i], t1[i], t2[i]);
     }
     if (V)
         for (int rr = 0; rr < nreg && rr < MAXR; ++rr) adjacency(rr, xs[rr]);
@@ -542,6 +548,8 @@ inline void *pick_split(bool even) {
         return e ? std::atoi(e) : 1;
     }();
     if (v == 1) return even ? (void *)k_sample_split<true, 1> : (void *)k_sample_split<false, 1>;
+    if (v == 2) return even ? (void *)k_sample_split<true, 2> : (void *)k_sample_split<false, 2>;
+    if (v == 3) return even ? (void *)k_sample_split<true, 3> : (void *)k_sample_split<false, 3>;
     return even ? (void *)k_sample_split<true, 0> : (void *)k_sample_split<false, 0>;
 }
 
