@@ -165,6 +165,12 @@ int tcg_level2_stats(tcg_plan *plan, int64_t *out);
  * last call (synchronises the plan's stream). */
 int tcg_plan_set_split(tcg_plan *plan, int enable);
 int tcg_split_stats(tcg_plan *plan, int64_t *out);
+/* The separator design for a descriptor, on the host (no device needed):
+ * out[0] = 1 if the split sampler applies, out[1] = separator vertices,
+ * out[2] / out[3] = index bits of the two tables, out[4..6] = lattice-point
+ * masks of the separator F and the two sides A, B, out[7] = estimated mean
+ * contracted-graph size x 1000, out[8] = table bytes. */
+int tcg_split_design(const tcg_desc *desc, int64_t *out);
 
 /* classify_bits_kernel, batched.  sigma[t] bit k = sign of point k.
  * Outputs per patchwork: tree key, oval count, region count, status. */

@@ -70,6 +70,7 @@ def load():
         L.tcg_level2_stats.argtypes = [P, C.c_void_p]
         L.tcg_plan_set_split.argtypes = [P, C.c_int]
         L.tcg_split_stats.argtypes = [P, C.c_void_p]
+        L.tcg_split_design.argtypes = [C.POINTER(TcgDesc), C.c_void_p]
         L.tcg_classify_batch.argtypes = [P, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                          C.c_void_p, C.c_void_p]
         L.tcg_classify_batch_device.argtypes = L.tcg_classify_batch.argtypes
@@ -107,7 +108,7 @@ def load():
 EXPORTS = (
     "tcg_plan_create", "tcg_plan_destroy", "tcg_plan_set_stream", "tcg_plan_info",
     "tcg_plan_set_timing", "tcg_kernel_times", "tcg_plan_set_dedup", "tcg_tile_stats",
-    "tcg_plan_set_level2", "tcg_level2_stats", "tcg_plan_set_split", "tcg_split_stats",
+    "tcg_plan_set_level2", "tcg_level2_stats", "tcg_plan_set_split", "tcg_split_stats", "tcg_split_design",
     "tcg_classify_batch", "tcg_classify_batch_device", "tcg_sweep", "tcg_sample",
     "tcg_agg_reset", "tcg_sweep_async", "tcg_sample_async", "tcg_agg_fetch",
     "tcg_sweep_multi", "tcg_sample_multi", "tcg_last_error", "tcg_device_count",
@@ -183,6 +184,21 @@ def _desc(arrays, keep):
     return TcgDesc(arrays.degree, arrays.nv, arrays.npts, len(eu), eu.ctypes.data,
                    ev.ctypes.data, src.ctypes.data, par.ctypes.data, used.ctypes.data,
                    len(apu), apu.ctypes.data, apv.ctypes.data, arrays.maxreg)
+
+
+def split_design(arrays):
+    """The split sampler's separator for a plan, computed on the host (no GPU):
+    None if it does not apply, else a dict (tcg.h tcg_split_design)."""
+    L = load()
+    keep = []
+    d = _desc(arrays, keep)
+    out = np.zeros(9, np.int64)
+    _check(L.tcg_split_design(C.byref(d), out.ctypes.data), "tcg_split_design")
+    if not out[0]:
+        return None
+    u = [int(x) & ((1 << 64) - 1) for x in out]
+    return {"separator_vertices": u[1], "bits_a": u[2], "bits_b": u[3], "F": u[4], "A": u[5],
+            "B": u[6], "mean_nodes": u[7] / 1000.0, "table_bytes": u[8]}
 
 
 class NativeMulti:

@@ -8,6 +8,7 @@ struct SplitDesign {
     SplitPart pa{}, pb{};
     std::vector<unsigned long long> pext;  // [nbytes * 256]
     int nfpts = 0;                         // separator points
+    unsigned long long Fm = 0, Am = 0, Bm = 0;  // point masks of F and the two sides
     double mean_nodes = 0;                 // estimated contracted-graph size
 };
 
@@ -254,6 +255,9 @@ static bool split_design(const tcg_desc *D, const Layout &L, SplitDesign &S) {
         if (t < 2) parts[t]->pt[rank[p]] = (uint8_t)p;
     }
     S.nfpts = popc(c.F);
+    S.Fm = c.F;
+    S.Am = c.A;
+    S.Bm = c.B;
     uint32_t parm = 0, cm[SPL_MAXFB] = {};
     for (int f = 0; f < nF; ++f) {
         const int v = fv[f].second, p = D->src[v];

@@ -3985,6 +3985,29 @@ int tcg_level2_stats(tcg_plan *P, int64_t *out) {
     return TCG_OK;
 }
 
+int tcg_split_design(const tcg_desc *D, int64_t *out) {
+    // host only (no device): the separator the sampler would use for D
+    if (!D || !out) return fail(TCG_E_ARG, "null argument");
+    HostPlan HP;
+    int rc = build_host_plan(D, HP);
+    if (rc) return rc;
+    SplitDesign S;
+    if (!split_design(D, HP.L, S)) {
+        out[0] = 0;
+        return TCG_OK;
+    }
+    out[0] = 1;
+    out[1] = S.sp.nF;
+    out[2] = S.pa.bits;
+    out[3] = S.pb.bits;
+    out[4] = (int64_t)S.Fm;
+    out[5] = (int64_t)S.Am;
+    out[6] = (int64_t)S.Bm;
+    out[7] = (int64_t)(S.mean_nodes * 1000.0);
+    out[8] = (int64_t)S.sp.stride * 4 * ((1ll << S.pa.bits) + (1ll << S.pb.bits));
+    return TCG_OK;
+}
+
 int tcg_plan_set_split(tcg_plan *P, int enable) {
     if (!P) return fail(TCG_E_ARG, "null plan");
     P->split = enable < 0 ? -1 : (enable ? 1 : 0);
