@@ -28,6 +28,20 @@
 //   5. sweep / sample kernels aggregate keys in a per-CTA shared-memory
 //      hash table (warp-aggregated with __match_any_sync), flushed to a
 //      global table: count sum, witness min (kernels.py:379-420).
+//
+// Source layout (one compilation unit; the .cuh files are included below):
+//   classify.cuh     full-diamond classifier, batch / C4 / enumeration kernels,
+//                    per-CTA scheme tables
+//   tiles.cuh        sweep tiles: super-tiles, tile records, dedup, tile classify
+//   level2.cuh       level-2 and two-stage records, their dedup and classifiers
+//   large.cuh        any-degree kernel (d > 9)
+//   split.cuh        separator-split sampler (C5) kernels
+//   host_plan.cuh    plan-side host helpers: layout, tile tables, host plan
+//   split_design.cuh the sampler's separator design and tables (host)
+//   tcg.cu           plan lifetime, sweep / sample pipelines, aggregation fetch,
+//                    multi-plan runs (the C ABI of include/tcg.h)
+//   api_multi.cuh    C ABI of the many-triangulation engine
+//   api_large.cuh    C ABI of the any-degree engine
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -104,2935 +118,13 @@ struct Result {
     uint64_t key;
 };
 
-// ------------------------------------------------------------------ helpers
-template <int K>
-__device__ __forceinline__ uint32_t sel(const uint32_t (&x)[K], int w) {
-    uint32_t r = x[0];
-#pragma unroll
-    for (int k = 1; k < K; ++k) r = (w == k) ? x[k] : r;
-    return r;
-}
+#include "classify.cuh"
 
-template <int K>
-__device__ __forceinline__ bool any(const uint32_t (&x)[K]) {
-    uint32_t r = 0;
-#pragma unroll
-    for (int k = 0; k < K; ++k) r |= x[k];
-    return r != 0;
-}
+#include "tiles.cuh"
 
-// lowest set bit of a K-word mask: returns word index and bit; caller
-// guarantees the mask is non-zero.
-template <int K>
-__device__ __forceinline__ void lowest(const uint32_t (&x)[K], int &w, int &b) {
-    uint32_t word = x[K - 1];
-    int wi = K - 1;
-#pragma unroll
-    for (int k = K - 2; k >= 0; --k) {
-        const bool nz = x[k] != 0;
-        word = nz ? x[k] : word;
-        wi = nz ? k : wi;
-    }
-    w = wi;
-    b = __ffs(word) - 1;
-}
+#include "level2.cuh"
 
-// Row v of a node table: K adjacency words (+ K partner words if ROWS, which
-// are OR-ed into PL).  Vectorised shared-memory loads.
-template <int K, bool ROWS>
-__device__ __forceinline__ void load_row(const uint32_t *__restrict__ base, int v, uint32_t (&a)[K],
-                                         uint32_t (&PL)[K]) {
-    if constexpr (ROWS) {
-        static_assert(K == 2, "contracted graphs use 64-node masks");
-        const uint4 t = reinterpret_cast<const uint4 *>(base)[v];
-        a[0] = t.x; a[1] = t.y;
-        PL[0] |= t.z; PL[1] |= t.w;
-    } else if constexpr (K == 2) {
-        const uint2 t = reinterpret_cast<const uint2 *>(base)[v];
-        a[0] = t.x; a[1] = t.y;
-    } else if constexpr (K == 4) {
-        const uint4 t = reinterpret_cast<const uint4 *>(base)[v];
-        a[0] = t.x; a[1] = t.y; a[2] = t.z; a[3] = t.w;
-    } else {
-        const uint2 *r = reinterpret_cast<const uint2 *>(base) + 3 * v;
-        const uint2 t0 = r[0], t1 = r[1], t2 = r[2];
-        a[0] = t0.x; a[1] = t0.y; a[2] = t1.x; a[3] = t1.y; a[4] = t2.x; a[5] = t2.y;
-    }
-}
-
-__device__ __forceinline__ uint64_t splitmix64(uint64_t seed, uint64_t k) {
-    // kernels.py:439-444
-    uint64_t z = seed + (k + 1ull) * 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
-
-__device__ __forceinline__ uint64_t rep_to_sigma(int d, uint64_t m) {
-    // free positions ascending take the bits of m (signs.py:188-206):
-    // pinned set {0, 1, d+1} -> two shifted runs
-    const uint64_t low = m & ((1ull << (d - 1)) - 1ull);
-    return (low << 2) | ((m >> (d - 1)) << (d + 2));
-}
-
-// sign of every vertex, in the half-swap layout (see plan construction)
-template <int K>
-__device__ __forceinline__ void sign_words(const KParams &p, uint64_t sigma, uint32_t (&SG)[K]) {
-    uint64_t q4 = 0;
-#pragma unroll
-    for (int r = 0; r < NQ4; ++r) {
-        if (r < p.nq4)
-            q4 |= ((sigma >> p.q4src[r]) & ((1ull << p.q4len[r]) - 1ull)) << p.q4dst[r];
-    }
-    const int sh = p.npts - 1;  // 2..54
-    uint64_t lo = (sigma >> 1) | (q4 << sh);
-    uint64_t hi = q4 >> (64 - sh);
-    const uint64_t c = sigma & 1ull;
-    if (p.center < 64) lo |= c << p.center;
-    else hi |= c << (p.center - 64);
-    const uint32_t w[3] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi};
-#pragma unroll
-    for (int k = 0; k < K / 2; ++k) {
-        SG[k] = w[k] ^ p.jodd[k];
-        SG[K / 2 + k] = SG[k] ^ p.parP[k];
-    }
-}
-
-// Exact replay of kernels.py:199-230 (edge order) for the rare inputs where
-// two order-dependent failures coexist.  Returns the status it produces.
-template <int K, bool EVEN>
-__device__ __noinline__ int ordered_scan(const KParams &p, const uint32_t (&SG)[K],
-                                         const uint32_t (*regR)[K], int nreg, int root) {
-    uint32_t sg[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) sg[k] = SG[k];
-    uint32_t seen[MAXR];
-    for (int r = 0; r < MAXR; ++r) seen[r] = 0;
-    int nedges = 0;
-    for (int e = 0; e < p.ne; ++e) {
-        const uint32_t pk = p.edges[e];
-        const int u = pk & 0xffff, v = pk >> 16;
-        const int su = (sg[u >> 5] >> (u & 31)) & 1, sv = (sg[v >> 5] >> (v & 31)) & 1;
-        if (su == sv) continue;
-        int a = -1, b = -1;
-        for (int r = 0; r < nreg && r < MAXR; ++r) {
-            if ((regR[r][u >> 5] >> (u & 31)) & 1) a = r;
-            if ((regR[r][v >> 5] >> (v & 31)) & 1) b = r;
-        }
-        if (a == b) {
-            if (EVEN) return TCG_NONSEPARATING_OVAL;
-            if (root < 0) root = a;
-            else if (root != a) return TCG_ROOT_CONFLICT;
-            continue;
-        }
-        if (a > b) { const int t = a; a = b; b = t; }
-        if (!((seen[a] >> b) & 1u)) {
-            seen[a] |= 1u << b;
-            if (nedges >= nreg - 1) return TCG_NOT_A_TREE;
-            ++nedges;
-        }
-    }
-    return TCG_NOT_A_TREE;  // unreachable for the inputs routed here
-}
-
-// Rooted BFS over the region tree, then the AHU canonical key bottom-up:
-// code(v) = 1 . sorted child codes . 0, children ordered by sentinel key
-// (length first), leaves (key 0b110) emitted as one run; the root contributes
-// only its child sequence.  Sets status (OK or DISCONNECTED).
-__device__ __forceinline__ uint64_t tree_key(const uint32_t (&radj)[MAXR], int nreg, int root,
-                                             int &status) {
-    // rooted BFS over the region tree
-    uint8_t order[MAXR], parent[MAXR];
-    order[0] = (uint8_t)root;
-    parent[root] = (uint8_t)root;
-    uint32_t vis = 1u << root;
-    int head = 0, tail = 1;
-    while (head < tail) {
-        const int r = order[head++];
-        uint32_t nb = radj[r] & ~vis;
-        vis |= nb;
-        while (nb) {
-            const int s2 = __ffs(nb) - 1;
-            nb &= nb - 1;
-            parent[s2] = (uint8_t)r;
-            TCG_ASSERT(tail < MAXR && s2 < MAXR);
-            order[tail++] = (uint8_t)s2;
-        }
-    }
-    if (tail != nreg) { status = TCG_DISCONNECTED; return 0ull; }
-
-    // AHU canonical key, bottom-up (children before parents)
-    uint64_t skey[MAXR];
-    uint64_t acc = 1;
-    for (int k = nreg - 1; k >= 0; --k) {
-        const int v = order[k];
-        uint32_t ch = radj[v];
-        if (k > 0) ch &= ~(1u << parent[v]);
-        int nleaf = 0, h = 0;
-        uint64_t buf[MAXR];
-        while (ch) {
-            const int c = __ffs(ch) - 1;
-            ch &= ch - 1;
-            const uint64_t ck = skey[c];
-            if (ck == 6ull) {
-                ++nleaf;
-            } else {
-                int j = h++;
-                while (j > 0 && buf[j - 1] > ck) { buf[j] = buf[j - 1]; --j; }
-                buf[j] = ck;
-            }
-        }
-        acc = 1;
-        if (nleaf) {
-            const int nb2 = 2 * nleaf;
-            acc = (1ull << nb2) | (0xAAAAAAAAAAAAAAAAull & ((1ull << nb2) - 1ull));
-        }
-        for (int i = 0; i < h; ++i) {
-            const uint64_t c = buf[i];
-            const int ln = 63 - __clzll(c);
-            acc = (acc << ln) | (c ^ (1ull << ln));
-        }
-        if (k > 0) {
-            const int il = 63 - __clzll(acc);
-            skey[v] = (acc << 1) | (1ull << (il + 2));
-        }
-    }
-    status = TCG_OK;
-    return acc;
-}
-
-// ------------------------------------------------------------- classify one
-// Regions of one patchwork as vertex (or node) masks.
-template <int K, int CAP = MAXR>
-struct Regions {
-    uint32_t R[CAP][K];  // region vertex sets
-    uint32_t X[CAP][K];  // crossed-edge neighbourhoods (COMPS mode: all neighbours)
-    uint32_t oddmask;     // regions closing an orientation-reversing cycle
-    int nreg;
-};
-
-// One breadth-first pass over the used vertices that labels regions.
-//  * inside a layer all vertices share one sign (non-crossed edges join equal
-//    signs), so `same` is a per-layer mask and a visited vertex costs
-//    new = adj & unvS; unvS ^= new; F |= new; NB |= adj   (4 ops per word);
-//  * a layer ends when its frontier empties; the next layer is seeded by the
-//    antipodal partners of the layer (ROWS=false: swap of mask halves;
-//    ROWS=true: per-node partner rows, for contracted graphs).  Partners have
-//    the same sign in even degree and the opposite sign in odd degree;
-//  * layers alternate orientation parity: a partner link between two nodes of
-//    equal layer parity closes an odd cycle (the reference's parity
-//    union-find, kernels.py:151-174).
-// rows: per node K words of adjacency (+ K words of partner links if ROWS).
-// COMPS: no antipodal jumps, so every "region" is one same-sign component and
-// X collects all of its neighbours (used to contract a tile's fixed part).
-template <int K, bool EVEN, bool ROWS, bool COMPS = false, int CAP = MAXR>
-__device__ __forceinline__ void region_pass(const uint32_t *__restrict__ rows,
-                                            const uint32_t (&SG)[K], const uint32_t (&USED)[K],
-                                            const uint32_t (&BD)[K], int nused,
-                                            Regions<K, CAP> &out) {
-    constexpr int HK = K / 2;
-    uint32_t unvS[K], unvO[K], F[K], NB[K], XB[K], regS[K], LS[K], SAME[K], PL[K];
-    uint32_t Ec[EVEN ? K : 1], Eo[EVEN ? K : 1];
-    int nreg = 0;
-    uint32_t oddmask = 0;
-    bool odd = false;
-
-    auto seed = [&](const uint32_t (&unv)[K]) {
-        int w, b;
-        lowest<K>(unv, w, b);
-        const uint32_t nm = ((sel<K>(SG, w) >> b) & 1u) - 1u;  // seed sign s: s ? 0 : ~0
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            SAME[k] = SG[k] ^ nm;
-            unvS[k] = unv[k] & SAME[k];
-            unvO[k] = unv[k] & ~SAME[k];
-            regS[k] = unv[k];
-            LS[k] = unvS[k];
-            F[k] = (k == w) ? (1u << b) : 0u;
-            unvS[k] ^= F[k];
-            XB[k] = 0u;
-            NB[k] = 0u;
-            PL[k] = 0u;
-            if (EVEN) { Ec[k] = 0u; Eo[k] = 0u; }
-        }
-        odd = false;
-    };
-
-    auto layer_end = [&](bool more) {
-        uint32_t L[K], unv[K], P[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            XB[k] |= COMPS ? NB[k] : (NB[k] & ~SAME[k]);
-            NB[k] = 0u;
-            L[k] = LS[k] ^ unvS[k];
-            unv[k] = unvS[k] | unvO[k];
-        }
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (COMPS) {
-                P[k] = 0u;
-            } else if (ROWS) {
-                P[k] = PL[k];
-                PL[k] = 0u;
-            } else {
-                const int ks = (k + HK) % K;  // antipodal map = swap of halves
-                P[k] = L[ks] & BD[ks];
-            }
-        }
-        if (EVEN) {
-            uint32_t hit = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                Ec[k] |= L[k];
-                hit |= P[k] & Ec[k];
-            }
-            odd |= hit != 0u;
-        }
-        uint32_t anyp = 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            P[k] &= unv[k];
-            anyp |= P[k];
-        }
-        if (anyp) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                if (!EVEN) {  // partners carry the opposite sign in odd degree
-                    SAME[k] = ~SAME[k];
-                    unvS[k] = unv[k] & SAME[k];
-                    unvO[k] = unv[k] & ~SAME[k];
-                }
-                LS[k] = unvS[k];
-                F[k] = P[k];
-                unvS[k] ^= P[k];
-                if (EVEN) {
-                    const uint32_t t = Ec[k];
-                    Ec[k] = Eo[k];
-                    Eo[k] = t;
-                }
-            }
-            return;
-        }
-        // region complete
-        if (nreg < CAP) {
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                out.R[nreg][k] = regS[k] ^ unv[k];
-                out.X[nreg][k] = XB[k];
-            }
-            if (EVEN && odd) oddmask |= 1u << nreg;
-        }
-        ++nreg;
-        if (more) seed(unv);
-    };
-
-    seed(USED);
-    for (int it = 0; it < nused; ++it) {
-        if (!any<K>(F)) layer_end(true);
-        int w, b;
-        lowest<K>(F, w, b);
-        const int v = 32 * w + b;
-        const uint32_t bit = 1u << b;
-        uint32_t a[K];
-        load_row<K, ROWS>(rows, v, a, PL);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const uint32_t nw = a[k] & unvS[k];
-            unvS[k] ^= nw;
-            F[k] = (F[k] ^ ((k == w) ? bit : 0u)) | nw;
-            NB[k] |= a[k];
-        }
-    }
-    layer_end(false);
-    out.nreg = nreg;
-    out.oddmask = oddmask;
-}
-
-// Region graph -> status (reference precedence) -> rooted tree -> AHU key.
-// EXACT: replay the two order-dependent status collisions in edge order
-// (only meaningful for the flat diamond layout); otherwise report a failure
-// and let the host recompute the exact status through the flat kernel.
-template <int K, bool EVEN, bool EXACT>
-__device__ __forceinline__ Result finish(const KParams &p, const uint32_t (&SG)[K],
-                                         const Regions<K> &rg, int maxreg) {
-    Result res;
-    const int nreg = rg.nreg;
-    res.nreg = nreg;
-    res.key = 0;
-    if (nreg > maxreg || nreg > MAXR) {  // kernels.py:182: ids 0..maxreg-1 allowed
-        res.status = TCG_TOO_MANY_REGIONS;
-        return res;
-    }
-    int root = -1;
-    if (EVEN) {
-        const int c = __popc(rg.oddmask);
-        if (c == 0) { res.status = TCG_NO_ODD_REGION; return res; }
-        if (c > 1) { res.status = TCG_MANY_ODD_REGIONS; return res; }
-        root = __ffs(rg.oddmask) - 1;
-    } else {
-        // the pseudoline region: the first region with a crossed edge inside
-        for (int r = 0; r < nreg; ++r) {
-            uint32_t t = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) t |= rg.X[r][k] & rg.R[r][k];
-            if (t) { root = r; break; }
-        }
-    }
-    // Fast path, flat trees (92 % of degree-7 patchworks): every other
-    // region touches only the root across crossed edges.  Then the region
-    // graph is the star at the root -- nreg-1 edges, connected, no crossed
-    // edge inside a non-root region -- so no status can fire and the key is
-    // the root with nreg-1 leaf children.  Anything else takes the general
-    // path below (which also settles every status exactly).
-    if (root >= 0) {
-        bool flat = true;
-        uint32_t rroot[K];
-#pragma unroll
-        for (int k = 0; k < K; ++k) rroot[k] = rg.R[root][k];
-        if (EVEN) {
-            uint32_t t = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) t |= rg.X[root][k] & rroot[k];
-            flat = t == 0u;
-        }
-        for (int r = 0; r < nreg && flat; ++r) {
-            if (r == root) continue;
-            uint32_t out = 0, in = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                out |= rg.X[r][k] & ~rroot[k];
-                in |= rg.X[r][k];
-            }
-            flat = out == 0u && in != 0u;
-        }
-        if (flat) {
-            const int nb2 = 2 * (nreg - 1);
-            res.status = TCG_OK;
-            res.key = (1ull << nb2) | (0xAAAAAAAAAAAAAAAAull & ((1ull << nb2) - 1ull));
-            return res;
-        }
-    }
-    // region graph from crossed-edge neighbourhoods
-    uint32_t radj[MAXR];
-    uint32_t selfm = 0;
-    int nedges = 0;
-    for (int r = 0; r < nreg; ++r) radj[r] = 0u;
-    for (int r = 0; r < nreg; ++r) {
-        uint32_t x[K];
-        uint32_t t = 0;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            x[k] = rg.X[r][k];
-            t |= x[k] & rg.R[r][k];
-        }
-        if (t) selfm |= 1u << r;
-        for (int r2 = r + 1; r2 < nreg; ++r2) {
-            uint32_t u = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) u |= x[k] & rg.R[r2][k];
-            if (u) {
-                radj[r] |= 1u << r2;
-                radj[r2] |= 1u << r;
-                ++nedges;
-            }
-        }
-    }
-    const bool toomany = nedges > nreg - 1;  // mid-loop NOT_A_TREE will fire
-    if (EVEN) {
-        if (toomany && selfm) {
-            if constexpr (EXACT) res.status = ordered_scan<K, EVEN>(p, SG, rg.R, nreg, root);
-            else res.status = TCG_NOT_A_TREE;
-            return res;
-        }
-        if (toomany) { res.status = TCG_NOT_A_TREE; return res; }
-        if (selfm) { res.status = TCG_NONSEPARATING_OVAL; return res; }
-    } else {
-        const bool conflict = __popc(selfm) >= 2;
-        if (toomany && conflict) {
-            if constexpr (EXACT) res.status = ordered_scan<K, EVEN>(p, SG, rg.R, nreg, -1);
-            else res.status = TCG_NOT_A_TREE;
-            return res;
-        }
-        if (toomany) { res.status = TCG_NOT_A_TREE; return res; }
-        if (conflict) { res.status = TCG_ROOT_CONFLICT; return res; }
-        if (!selfm) { res.status = TCG_NO_PSEUDOLINE; return res; }
-        root = __ffs(selfm) - 1;
-    }
-    if (nedges != nreg - 1) { res.status = TCG_NOT_A_TREE; return res; }
-    // a tree on nreg <= 3 nodes is connected; its key is closed-form:
-    // 1 = <no oval>, 0b110 = one oval, 0b11010 = two leaves under the root,
-    // 0b11100 = a chain (one oval inside another)
-    if (nreg <= 3) {
-        res.status = TCG_OK;
-        res.key = nreg == 1 ? 1ull : (nreg == 2 ? 6ull : (__popc(radj[root]) == 2 ? 26ull : 28ull));
-        return res;
-    }
-    res.key = tree_key(radj, nreg, root, res.status);
-    return res;
-}
-
-template <int K, bool EVEN>
-__device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__restrict__ adj,
-                                           uint64_t sigma) {
-    uint32_t SG[K];
-    sign_words<K>(p, sigma, SG);
-    uint32_t used[K], bd[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        used[k] = p.used[k];
-        bd[k] = p.bd[k];
-    }
-    Regions<K> rg;
-    region_pass<K, EVEN, false>(adj, SG, used, bd, p.nused, rg);
-    return finish<K, EVEN, true>(p, SG, rg, p.maxreg);
-}
-
-// ------------------------------------------------------------------ kernels
-template <int K>
-__device__ __forceinline__ void stage_adj(const KParams &p, uint32_t *adj_s) {
-    const int n = 32 * K * K;  // 2H rows of K words, H = 16K
-    for (int i = threadIdx.x; i < n; i += blockDim.x) adj_s[i] = p.adj[i];
-}
-
-template <int K, bool EVEN>
-__global__ void __launch_bounds__(THREADS) k_batch(KParams p, const uint64_t *__restrict__ sig,
-                                                   int64_t n, uint64_t *__restrict__ key,
-                                                   uint8_t *__restrict__ ovals,
-                                                   uint8_t *__restrict__ nreg,
-                                                   int32_t *__restrict__ status) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    stage_adj<K>(p, smem);
-    __syncthreads();
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n; t += stride) {
-        const Result r = classify<K, EVEN>(p, smem, sig[t]);
-        key[t] = r.status == TCG_OK ? r.key : 0ull;
-        ovals[t] = r.status == TCG_OK ? (uint8_t)(r.nreg - 1) : 0xff;
-        nreg[t] = (uint8_t)min(r.nreg, 255);
-        status[t] = r.status;
-    }
-}
-
-// Many triangulations of one degree (config C4): a work item is
-// (triangulation, first pair, pair count) over pairs sorted by triangulation;
-// each CTA stages its item's descriptor and adjacency rows in shared memory,
-// so consecutive CTAs classify on different topologies.
-template <int K, bool EVEN>
-__global__ void __launch_bounds__(THREADS) k_multi(const KParams *__restrict__ kps,
-                                                   const int4 *__restrict__ items,
-                                                   const uint64_t *__restrict__ sig,
-                                                   uint64_t *__restrict__ key,
-                                                   uint8_t *__restrict__ ovals,
-                                                   uint8_t *__restrict__ nreg,
-                                                   int32_t *__restrict__ status) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    __shared__ KParams kp_s;
-    const int4 it = items[blockIdx.x];  // x = triangulation, y = first, z = count
-    if (threadIdx.x == 0) kp_s = kps[it.x];
-    __syncthreads();
-    stage_adj<K>(kp_s, smem);
-    __syncthreads();
-    for (int t = threadIdx.x; t < it.z; t += blockDim.x) {
-        const int64_t i = (int64_t)it.y + t;
-        const Result r = classify<K, EVEN>(kp_s, smem, sig[i]);
-        key[i] = r.status == TCG_OK ? r.key : 0ull;
-        ovals[i] = r.status == TCG_OK ? (uint8_t)(r.nreg - 1) : 0xff;
-        nreg[i] = (uint8_t)min(r.nreg, 255);
-        status[i] = r.status;
-    }
-}
-
-__device__ __forceinline__ uint32_t hash_slot(uint64_t key, int bits) {
-    return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> (64 - bits));
-}
-
-__device__ void global_insert(const DevAgg &g, uint64_t key, uint64_t cnt, uint64_t wit) {
-    uint32_t h = hash_slot(key, GCAP_BITS);
-    for (int probe = 0; probe < GCAP; ++probe) {
-        const unsigned long long prev = atomicCAS(&g.keys[h], 0ull, (unsigned long long)key);
-        if (prev == 0ull || prev == key) {
-            atomicAdd(&g.cnt[h], (unsigned long long)cnt);
-            atomicMin(&g.wit[h], (unsigned long long)wit);
-            return;
-        }
-        h = (h + 1) & (GCAP - 1);
-    }
-    atomicOr(g.overflow, 1u);
-}
-
-// Per-CTA scheme table in shared memory (flushed to the global table).
-struct CtaTable {  // 64-bit counts: a tiled launch covers up to 2^32 weighted patchworks
-    unsigned long long *key, *wit;
-    unsigned long long *cnt, *hist;
-
-    __device__ void init() {
-        for (int i = threadIdx.x; i < TBL; i += blockDim.x) {
-            key[i] = 0ull;
-            wit[i] = ~0ull;
-            cnt[i] = 0ull;
-        }
-        for (int i = threadIdx.x; i < NHIST; i += blockDim.x) hist[i] = 0ull;
-    }
-
-    // Warp-aggregated insert of one result per lane (all 32 lanes call).
-    // WITNESS_BY_LEADER: lanes are in increasing index order, so the group
-    // leader holds the group's minimal index (sweeps); otherwise every lane
-    // offers its own index (random draws).
-    template <bool WITNESS_BY_LEADER>
-    __device__ __forceinline__ void add(const DevAgg &g, uint64_t k, int nreg, uint64_t m,
-                                        uint32_t weight = 1u) {
-        const int lane = threadIdx.x & 31;
-        const unsigned grp = __match_any_sync(0xffffffffu, k);
-        if (k == 0ull) return;
-        const int leader = __ffs(grp) - 1;
-        int slot = -1;
-        if (lane == leader) {
-            uint32_t h = hash_slot(k, TBL_BITS);
-            for (int probe = 0; probe < TBL_PROBES; ++probe) {
-                const unsigned long long cur = key[h];
-                if (cur == k) { slot = (int)h; break; }
-                if (cur == 0ull) {
-                    const unsigned long long prev = atomicCAS(&key[h], 0ull, k);
-                    if (prev == 0ull || prev == k) { slot = (int)h; break; }
-                }
-                h = (h + 1) & (TBL - 1);
-            }
-            const unsigned long long c = (unsigned long long)__popc(grp) * weight;
-            TCG_ASSERT(nreg >= 1 && nreg <= NHIST);
-            atomicAdd(&hist[nreg - 1], c);
-            if (slot >= 0) {
-                atomicAdd(&cnt[slot], c);
-                if (WITNESS_BY_LEADER) atomicMin(&wit[slot], (unsigned long long)m);
-            } else {  // table saturated: straight to the global table
-                global_insert(g, k, c, WITNESS_BY_LEADER ? m : ~0ull);
-            }
-        }
-        if (!WITNESS_BY_LEADER) {
-            slot = __shfl_sync(grp, slot, leader);
-            if (slot >= 0) atomicMin(&wit[slot], (unsigned long long)m);
-            else global_insert(g, k, 0ull, m);
-        }
-    }
-
-    __device__ void flush(const DevAgg &g) {
-        for (int i = threadIdx.x; i < TBL; i += blockDim.x) {
-            const unsigned long long kk = key[i];
-            if (kk != 0ull) global_insert(g, kk, cnt[i], wit[i]);
-        }
-        for (int i = threadIdx.x; i < NHIST; i += blockDim.x)
-            if (hist[i]) atomicAdd(&g.hist[i], hist[i]);
-    }
-};
-
-constexpr size_t TABLE_SMEM = TBL * 3 * sizeof(unsigned long long) +
-                              NHIST * sizeof(unsigned long long);
-
-__device__ __forceinline__ CtaTable carve_table(void *at) {
-    CtaTable t;
-    t.key = reinterpret_cast<unsigned long long *>(at);
-    t.wit = t.key + TBL;
-    t.cnt = t.wit + TBL;
-    t.hist = t.cnt + TBL;
-    return t;
-}
-
-// Enumeration kernel: raw / representative sweep or counter-based sample.
-// Persistent grid; each warp walks 32 consecutive indices per step.
-template <int K, bool EVEN, int MODE>
-#ifndef TCG_ENUM_MINB6
-#define TCG_ENUM_MINB6 3  // d = 8, 9: cap registers for 3 resident CTAs (measured +14 % on bowtie8)
-#endif
-__global__ void __launch_bounds__(THREADS, K == 6 ? TCG_ENUM_MINB6 : 1) k_enumerate(KParams p, uint64_t base, uint64_t count,
-                                                       uint64_t seed, uint64_t nbmask, DevAgg g) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t *adj_s = smem;
-    CtaTable tab = carve_table(smem + 32 * K * K);
-    stage_adj<K>(p, adj_s);
-    tab.init();
-    __syncthreads();
-
-    const int lane = threadIdx.x & 31;
-    const uint64_t warp = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t wstride = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t wb = warp * 32ull; wb < count; wb += wstride * 32ull) {
-        const uint64_t idx = wb + lane;
-        const bool valid = idx < count;
-        const uint64_t gidx = base + idx;  // m (sweeps) or draw number k (sample)
-        uint64_t m, sigma;
-        if (MODE == MODE_SAMPLE) {
-            m = splitmix64(seed, gidx) & nbmask;
-            sigma = rep_to_sigma(p.d, m);
-        } else if (MODE == MODE_REP) {
-            m = gidx;
-            sigma = rep_to_sigma(p.d, m);
-        } else {
-            m = gidx;
-            sigma = m;
-        }
-        const Result r = classify<K, EVEN>(p, adj_s, valid ? sigma : 0ull);
-        uint64_t k = 0;
-        if (valid) {
-            if (r.status == TCG_OK) k = r.key;
-            else atomicMin(g.bad, (unsigned long long)gidx);
-        }
-        tab.add<MODE != MODE_SAMPLE>(g, k, r.nreg, m);
-    }
-    __syncthreads();
-    tab.flush(g);
-}
-
-// ---------------------------------------------------------- tile contraction
-// A sweep tile is 2^TILE_BITS consecutive indices aligned to its size: every
-// index in it shares all sign bits except those of a few "free" lattice
-// points (raw: points 0..9, i.e. the j-axis and two more; representative:
-// the first 10 free positions).  Their diamond copies are the free vertices.
-// Once per tile, warp 0 labels the same-sign components of the remaining
-// (fixed) vertices and contracts each to one node; every lane then
-// classifies its patchwork on the contracted graph -- at most 64 nodes
-// (components + free vertices), one 64-bit mask per set -- with the same
-// region pass (ROWS mode: per-node adjacency and antipodal-link rows).
-// Any tile whose contraction does not fit falls back to the flat kernel.
-constexpr int TILE_BITS_MAX = 12;
-constexpr int MAXC = 48;  // fixed components per tile
-constexpr int MAXF = 32;  // free vertices
-constexpr int MAXM = 24;  // mid vertices of a super-tile
-// level-1 list entries for a single A slice: tile | (a + 1) << slice_shift(la)
-// (a + 1 <= 2^la takes la + 1 bits; tile ids < 2^(31 - la), which the chunk
-// size guarantees: <= 2^35 indices = 2^(30 - la) tiles)
-__host__ __device__ constexpr int slice_shift(int la) { return 31 - la; }
-constexpr int SUPER_BITS_MAX = 6;
-
-struct alignas(16) TileTables {  // per plan and domain (raw / representative), device memory
-    int nf, nfixed, bits, maxnodes;  // maxnodes: contraction size limit (64; lower only in tests)
-    uint32_t fixed[MAXK];                  // used and not free (layout mask)
-    uint32_t fword[MAXF], fbit[MAXF];      // layout word / bit of free node f
-    unsigned long long fadj[MAXF];         // free-free adjacency (bit g = free node g)
-    unsigned long long fpl[MAXF];          // free-free antipodal links
-    unsigned long long fcopy[TILE_BITS_MAX];  // free nodes whose sign is index bit i
-    unsigned long long fpar;               // sign-extension parity of the free nodes
-    // free-node sign words for the tile-local index: fsign[0][low & 63] ^
-    // fsign[1][(low >> 6) & 63] (parity folded into fsign[0])
-    unsigned long long fsign[2][64];
-    // level-2 contraction (odd degree): index bits 0..4 are the B points (one
-    // per lane), bits 5..bits-1 the A points fixed per level-2 record
-    int l2, nB, NA, la;                     // enabled, B nodes, A patterns = 2^la
-    int l2shift, l2even;                    // B nodes = free nodes l2shift .. +nB-1 (or -1)
-    // two-stage level 2 (odd degree, 4 A bits): stage 1 fixes A1 = tile bits 5,6,
-    // stage 2 the A2 = bits 7,8.  F space (stage-1 free nodes) = B nodes 0..nB-1,
-    // then A2 nodes nB..nB+nA2-1.
-    int ts, nA2;
-    uint32_t fa1, fa2;                      // free-node masks of A1 / A2 nodes
-    int8_t l15F[MAXF];                      // free node -> F index (or -1)
-    uint32_t a2sign[16];                    // A2-node signs (A2 index space) per A2 pattern
-    int la1, la2;                           // A1 = tile bits 5 .. 4+la1, A2 = the la2 = la - la1 above
-    int l15max;                             // stage-1 super-node budget (TCG_L15_MAXM tests the fallback)
-    uint32_t a2adjA2[16], a2linkA2[16];     // A2-A2 adjacency / links (A2 space)
-    uint32_t a2adjB[16], a2linkB[16];       // A2-B adjacency / links (B space)
-    uint32_t fa, fbm;                       // free-node masks of A and B nodes
-    int8_t l2j[MAXF];                       // free node -> B index (or -1)
-    uint32_t l2adjB[16], l2linkB[16];       // B-B adjacency / links (B index space)
-    uint32_t l2bsign[32];                   // B-node signs for tile-local bits 0..4
-    uint32_t freem[MAXK];                   // free vertices (layout mask)
-    int8_t vfree[32 * MAXK];                // layout position -> free node (or -1)
-    // super-tiles (k_super_build / k_tile_from_super): 2^sh consecutive tiles share
-    // every sign except those of the "mid" points (tile-index bits 0..sh-1)
-    int sh, nm, nsfixed, pad2;              // sh = 0: off
-    uint32_t sfixed[MAXK];                  // fixed vertices that are not mid vertices
-    uint16_t mpos[MAXM];                    // layout positions of the mid vertices, ascending
-    uint32_t msign[1 << SUPER_BITS_MAX];    // mid-vertex signs (bit j) for mid pattern x
-};
-
-// Contracted tile, written by k_tile_build and staged into shared memory by
-// k_tile_classify.
-struct TileRec {
-    uint4 rows[64];  // per node: adjacency (x, y), antipodal links (z, w)
-    unsigned long long sgn_fixed;
-    int n, nnodes, fallback, pad;
-};
-
-// Graphs of <= 32 nodes (all of d = 6, 99 % of d = 7) store only the low
-// adjacency and link words, packed as uint2 at the start of rows[]: a quarter
-// of the bytes to write, deduplicate and stage.
-__device__ __forceinline__ const uint2 *rows2(const TileRec *r) {
-    return reinterpret_cast<const uint2 *>(r->rows);
-}
-
-__device__ __forceinline__ void store_row(TileRec *rec, int node, int nn, unsigned long long adj,
-                                          unsigned long long pl) {
-    if (nn <= 32)
-        reinterpret_cast<uint2 *>(rec->rows)[node] = make_uint2((uint32_t)adj, (uint32_t)pl);
-    else
-        rec->rows[node] = make_uint4((uint32_t)adj, (uint32_t)(adj >> 32), (uint32_t)pl,
-                                     (uint32_t)(pl >> 32));
-}
-
-// Record hash, accumulated by the builders as they write the rows (the
-// deduplication only uses it to find candidates; equality is decided by
-// comparing the records word by word).
-__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
-
-struct RecHash {
-    uint32_t h1 = 0x243F6A88u, h2 = 0x85A308D3u;
-    __device__ __forceinline__ void row(unsigned long long adj, unsigned long long pl) {
-        const uint32_t ah = (uint32_t)(adj >> 32), ph = (uint32_t)(pl >> 32);
-        h1 = (h1 ^ (uint32_t)adj ^ __funnelshift_l(ah, ah, 16)) * 0x9E3779B1u;
-        h1 ^= h1 >> 15;
-        h2 = (h2 ^ (uint32_t)pl ^ __funnelshift_l(ph, ph, 16)) * 0x85EBCA77u;
-        h2 ^= h2 >> 13;
-    }
-    __device__ __forceinline__ unsigned long long fin(unsigned long long sgn, int n, int nn) const {
-        return mix64(((unsigned long long)h1 << 32 | h2) ^
-                     mix64(sgn ^ ((unsigned long long)nn << 56) ^ ((unsigned long long)n << 48)));
-    }
-};
-
-// Region pass over a contracted graph (<= 64 nodes, one u64 per set) without
-// layers: antipodal links are followed in the same step as edges, so a lane
-// only branches when a region ends.  Each popped node v uses its own sign:
-//   new = unvisited & ((adj & same_v) | links_v);   XB |= adj & ~same_v.
-// Even degree: orientation parity is tracked per node (edges keep it, links
-// flip it); any edge or link whose ends violate the 2-colouring closes an odd
-// cycle (the reference's parity union-find, kernels.py:151-174).
-template <bool EVEN>
-__device__ __forceinline__ void node_pass(const uint4 *__restrict__ rows, uint32_t sg0,
-                                          uint32_t sg1, uint32_t u0, uint32_t u1, int nn,
-                                          Regions<2> &out) {
-    // two 32-bit halves per node set: lo = nodes 0..31, hi = nodes 32..63
-    uint32_t un0 = u0, un1 = u1, f0 = 0, f1 = 0, x0 = 0, x1 = 0, q0 = 0, q1 = 0, r0 = 0, r1 = 0;
-    bool odd = false;
-    int nreg = 0;
-    uint32_t oddmask = 0;
-    auto seed = [&]() {
-        const bool lo = un0 != 0u;
-        const uint32_t w = lo ? un0 : un1;
-        const uint32_t low = w & (0u - w);
-        r0 = un0;
-        r1 = un1;
-        f0 = lo ? low : 0u;
-        f1 = lo ? 0u : low;
-        un0 ^= f0;
-        un1 ^= f1;
-        x0 = x1 = 0u;
-        if (EVEN) q0 = q1 = 0u;
-        odd = false;
-    };
-    auto close = [&]() {
-        if (nreg < MAXR) {
-            out.R[nreg][0] = r0 ^ un0;
-            out.R[nreg][1] = r1 ^ un1;
-            out.X[nreg][0] = x0;
-            out.X[nreg][1] = x1;
-            if (EVEN && odd) oddmask |= 1u << nreg;
-        }
-        ++nreg;
-    };
-    seed();
-    for (int it = 0; it < nn; ++it) {
-        if ((f0 | f1) == 0u) {
-            close();
-            seed();
-        }
-        const bool lo = f0 != 0u;
-        const uint32_t w = lo ? f0 : f1;
-        const int b = __ffs(w) - 1;
-        const uint32_t rest = w & (w - 1u);
-        f0 = lo ? rest : f0;
-        f1 = lo ? f1 : rest;
-        const int v = lo ? b : b + 32;
-        const uint4 row = rows[v];
-        // opp = nodes whose sign differs from v's: SG ^ (s_v ? ~0 : 0)
-        const uint32_t sv = (uint32_t)((int32_t)((lo ? sg0 : sg1) << (31 - b)) >> 31);
-        const uint32_t o0 = sg0 ^ sv, o1 = sg1 ^ sv;
-        x0 |= row.x & o0;
-        x1 |= row.y & o1;
-        if (EVEN) {
-            // parity of v (equal-parity mask pv): edges keep it, links flip it
-            const uint32_t pv = (uint32_t)((int32_t)((lo ? q0 : q1) << (31 - b)) >> 31);
-            const uint32_t te0 = row.x & ~o0, te1 = row.y & ~o1;
-            const uint32_t nt0 = te0 & un0, nt1 = te1 & un1;
-            const uint32_t np0 = row.z & un0, np1 = row.w & un1;
-            const uint32_t eq0 = ~(q0 ^ pv), eq1 = ~(q1 ^ pv);
-            const uint32_t bad = (nt0 & np0) | (nt1 & np1) | (te0 & ~un0 & ~eq0) |
-                                 (te1 & ~un1 & ~eq1) | (row.z & ~un0 & eq0) | (row.w & ~un1 & eq1);
-            odd |= bad != 0u;
-            q0 |= (nt0 & pv) | (np0 & ~pv);
-            q1 |= (nt1 & pv) | (np1 & ~pv);
-            const uint32_t n0 = nt0 | np0, n1 = nt1 | np1;
-            un0 ^= n0;
-            un1 ^= n1;
-            f0 |= n0;
-            f1 |= n1;
-        } else {
-            const uint32_t n0 = ((row.x & ~o0) | row.z) & un0;
-            const uint32_t n1 = ((row.y & ~o1) | row.w) & un1;
-            un0 ^= n0;
-            un1 ^= n1;
-            f0 |= n0;
-            f1 |= n1;
-        }
-    }
-    close();
-    out.nreg = nreg;
-    out.oddmask = oddmask;
-}
-
-// node_pass for contracted graphs of at most 32 nodes: one 32-bit word per set.
-template <bool EVEN>
-__device__ __forceinline__ void node_pass1(const uint4 *__restrict__ rows, uint32_t sg,
-                                           uint32_t used, int nn, Regions<1> &out) {
-    uint32_t un = used, f = 0, x = 0, q = 0, r = 0;
-    bool odd = false;
-    int nreg = 0;
-    uint32_t oddmask = 0;
-    auto seed = [&]() {
-        f = un & (0u - un);
-        r = un;
-        un ^= f;
-        x = 0u;
-        if (EVEN) q = 0u;
-        odd = false;
-    };
-    auto close = [&]() {
-        if (nreg < MAXR) {
-            out.R[nreg][0] = r ^ un;
-            out.X[nreg][0] = x;
-            if (EVEN && odd) oddmask |= 1u << nreg;
-        }
-        ++nreg;
-    };
-    seed();
-    for (int it = 0; it < nn; ++it) {
-        if (f == 0u) {
-            close();
-            seed();
-        }
-        const int v = __ffs(f) - 1;
-        f &= f - 1u;
-        const uint4 row = rows[v];
-        const uint32_t sv = (uint32_t)((int32_t)(sg << (31 - v)) >> 31);
-        const uint32_t o = sg ^ sv;  // nodes of the other sign
-        x |= row.x & o;
-        if (EVEN) {
-            const uint32_t pv = (uint32_t)((int32_t)(q << (31 - v)) >> 31);
-            const uint32_t te = row.x & ~o, nt = te & un, np = row.z & un;
-            const uint32_t eq = ~(q ^ pv);
-            odd |= ((nt & np) | (te & ~un & ~eq) | (row.z & ~un & eq)) != 0u;
-            q |= (nt & pv) | (np & ~pv);
-            const uint32_t n = nt | np;
-            un ^= n;
-            f |= n;
-        } else {
-            const uint32_t n = ((row.x & ~o) | row.z) & un;
-            un ^= n;
-            f |= n;
-        }
-    }
-    close();
-    out.nreg = nreg;
-    out.oddmask = oddmask;
-}
-
-// Two independent patchworks of one tile per thread, stepped in lock-step:
-// the region opens/closes stay branches, but both shared-memory row loads
-// and both expansions sit in one basic block, so their latencies overlap.
-template <bool EVEN>
-struct NP1 {
-    uint32_t un, f, x, q, r, oddmask;
-    bool odd;
-    int nreg;
-    __device__ __forceinline__ void start(uint32_t used) {
-        un = used;
-        nreg = 0;
-        oddmask = 0u;
-        seed();
-    }
-    __device__ __forceinline__ void seed() {
-        f = un & (0u - un);
-        r = un;
-        un ^= f;
-        x = 0u;
-        if (EVEN) q = 0u;
-        odd = false;
-    }
-    __device__ __forceinline__ void close(Regions<1> &out) {
-        if (nreg < MAXR) {
-            out.R[nreg][0] = r ^ un;
-            out.X[nreg][0] = x;
-            if (EVEN && odd) oddmask |= 1u << nreg;
-        }
-        ++nreg;
-    }
-    __device__ __forceinline__ void expand(const uint32_t rx, const uint32_t rz, int v,
-                                           uint32_t sg) {
-        const uint32_t sv = (uint32_t)((int32_t)(sg << (31 - v)) >> 31);
-        const uint32_t o = sg ^ sv;
-        x |= rx & o;
-        if (EVEN) {
-            const uint32_t pv = (uint32_t)((int32_t)(q << (31 - v)) >> 31);
-            const uint32_t te = rx & ~o, nt = te & un, np = rz & un;
-            const uint32_t eq = ~(q ^ pv);
-            odd |= ((nt & np) | (te & ~un & ~eq) | (rz & ~un & eq)) != 0u;
-            q |= (nt & pv) | (np & ~pv);
-            const uint32_t n = nt | np;
-            un ^= n;
-            f |= n;
-        } else {
-            const uint32_t n = ((rx & ~o) | rz) & un;
-            un ^= n;
-            f |= n;
-        }
-    }
-    __device__ __forceinline__ void finish(Regions<1> &out) {
-        close(out);
-        out.nreg = nreg;
-        out.oddmask = oddmask;
-    }
-};
-
-template <bool EVEN>
-__device__ __forceinline__ void node_pass1x2(const uint32_t *__restrict__ ax,
-                                             const uint32_t *__restrict__ az, uint32_t sga,
-                                             uint32_t sgb, uint32_t used, int nn,
-                                             Regions<1> &oa, Regions<1> &ob) {
-    NP1<EVEN> a, b;
-    a.start(used);
-    b.start(used);
-    for (int it = 0; it < nn; ++it) {
-        if (a.f == 0u) {
-            a.close(oa);
-            a.seed();
-        }
-        if (b.f == 0u) {
-            b.close(ob);
-            b.seed();
-        }
-        const int va = __ffs(a.f) - 1, vb = __ffs(b.f) - 1;
-        a.f &= a.f - 1u;
-        b.f &= b.f - 1u;
-        const uint32_t xa = ax[va], xb = ax[vb], za = az[va], zb = az[vb];
-        a.expand(xa, za, va, sga);
-        b.expand(xb, zb, vb, sgb);
-    }
-    a.finish(oa);
-    b.finish(ob);
-}
-
-template <bool EVEN>
-__device__ __forceinline__ Result classify_tile(const KParams &p, const TileTables &tt,
-                                                const uint4 *rows,
-                                                unsigned long long sgn_fixed, int n, int nn,
-                                                uint32_t low) {
-    // signs of the free nodes: two table lookups on the tile-local index
-    const unsigned long long fs = tt.fsign[0][low & 63u] ^ tt.fsign[1][(low >> 6) & 63u];
-    const unsigned long long sg = sgn_fixed | (fs << n);
-    const unsigned long long used = nn >= 64 ? ~0ull : ((1ull << nn) - 1ull);
-    if (nn <= 32) {  // tile-uniform: a warp owns the tile
-        Regions<1> r1;
-        node_pass1<EVEN>(rows, (uint32_t)sg, (uint32_t)used, nn, r1);
-        const uint32_t SG1[1] = {(uint32_t)sg};
-        return finish<1, EVEN, false>(p, SG1, r1, p.maxreg);
-    }
-    Regions<2> rg;
-    node_pass<EVEN>(rows, (uint32_t)sg, (uint32_t)(sg >> 32), (uint32_t)used,
-                    (uint32_t)(used >> 32), nn, rg);
-    const uint32_t SG[2] = {(uint32_t)sg, (uint32_t)(sg >> 32)};
-    return finish<2, EVEN, false>(p, SG, rg, p.maxreg);
-}
-
-template <int K, int MODE>
-__device__ __forceinline__ void build_lane(const KParams &p, const uint32_t *__restrict__ adj_s,
-                                           const TileTables &tt_r, uint64_t tile0, uint32_t t,
-                                           TileRec *__restrict__ recs,
-                                           unsigned long long *__restrict__ hashes) {
-    RecHash hs;
-    const TileTables *tt = &tt_r;
-    const uint64_t base = (tile0 + t) << tt->bits;
-    const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, base) : base;
-    uint32_t SG[K], fixed[K], zero[K];
-    sign_words<K>(p, sigma, SG);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-        fixed[k] = tt->fixed[k];
-        zero[k] = 0u;
-    }
-    Regions<K, MAXC> comps;
-    region_pass<K, false, false, true, MAXC>(adj_s, SG, fixed, zero, tt->nfixed, comps);
-    const int n = comps.nreg, nf = tt->nf, nn = n + nf;
-    TileRec *rec = recs + t;
-    const bool fits = n <= MAXC && nn <= tt->maxnodes;
-    unsigned long long sbits = 0;
-    if (fits) {
-        unsigned long long fadj_c[MAXF];  // free node f -> comps adjacent to it
-        for (int f = 0; f < nf; ++f) fadj_c[f] = 0ull;
-        for (int c = 0; c < n; ++c) {
-            uint32_t X[K], R[K], P[K];
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                X[k] = comps.X[c][k];
-                R[k] = comps.R[c][k];
-            }
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int ks = (k + K / 2) % K;
-                P[k] = R[ks] & p.bd[ks];
-            }
-            unsigned long long adj = 0, pl = 0;
-            for (int c2 = 0; c2 < n; ++c2) {
-                uint32_t a = 0, q = 0;
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    a |= X[k] & comps.R[c2][k];
-                    q |= P[k] & comps.R[c2][k];
-                }
-                if (a && c2 != c) adj |= 1ull << c2;
-                if (q) pl |= 1ull << c2;
-            }
-            for (int f = 0; f < nf; ++f)
-                if (sel<K>(X, tt->fword[f]) & tt->fbit[f]) {
-                    adj |= 1ull << (n + f);
-                    fadj_c[f] |= 1ull << c;
-                }
-            uint32_t sg = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) sg |= R[k] & SG[k];
-            if (sg) sbits |= 1ull << c;
-            store_row(rec, c, nn, adj, pl);
-            hs.row(adj, pl);
-        }
-        for (int f = 0; f < nf; ++f) {
-            const unsigned long long adj = (tt->fadj[f] << n) | fadj_c[f];
-            const unsigned long long pl = tt->fpl[f] << n;
-            store_row(rec, n + f, nn, adj, pl);
-            hs.row(adj, pl);
-        }
-    }
-    hashes[t] = hs.fin(sbits, n, nn);
-    rec->sgn_fixed = sbits;
-    rec->n = n;
-    rec->nnodes = nn;
-    rec->fallback = fits ? 0 : 1;
-}
-// list != nullptr: only the tiles list[0 .. *count) (the ones k_tile_from_super
-// left: super-tiles whose contraction does not fit), grid-stride.
-template <int K, int MODE>
-__global__ void __launch_bounds__(THREADS) k_tile_build_lanes(KParams p,
-                                                              const TileTables *__restrict__ tt_g,
-                                                              uint64_t tile0, uint32_t ntiles,
-                                                              TileRec *__restrict__ recs,
-                                                              unsigned long long *__restrict__ hashes,
-                                                              const uint32_t *__restrict__ list,
-                                                              const uint32_t *__restrict__ count) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t *adj_s = smem;
-    TileTables *tt = reinterpret_cast<TileTables *>(smem + 32 * K * K);
-    stage_adj<K>(p, adj_s);
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    __syncthreads();
-    const uint32_t nwork = list ? *count : ntiles;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nwork;
-         i += gridDim.x * blockDim.x)
-        build_lane<K, MODE>(p, adj_s, *tt, tile0, list ? list[i] : i, recs, hashes);
-}
-
-
-// ------------------------------------------------------------ super-tiles
-// A super-tile is 2^sh consecutive tiles: they share the signs of every
-// fixed vertex except the "mid" vertices (copies of the points of tile-index
-// bits 0..sh-1).  k_super_build contracts the remaining ("super-fixed")
-// vertices once per super-tile, exactly as k_tile_build_lanes contracts a
-// tile, and keeps the mid vertices as single nodes: SN nodes = super
-// components + mid vertices, ordered by their lowest layout position.
-// k_tile_from_super then gives each tile (one per lane) its mid signs and
-// merges same-sign SN neighbours -- a breadth-first pass over <= 64 nodes
-// instead of ~100 vertices -- and emits the tile record.  Components come out
-// ordered by their lowest vertex, as in k_tile_build_lanes, so the records
-// are byte-identical to the direct contraction (tested: dedup counts and
-// reports agree with TCG_BUILD_GENERIC=1).
-struct SuperRec {
-    unsigned long long adj[64];   // SN-node adjacency (no self bit)
-    unsigned long long link[64];  // SN-node antipodal links (self bit: pair inside the node)
-    unsigned long long fsn[MAXF]; // free node -> adjacent SN nodes
-    uint32_t fadj[64];            // SN node -> adjacent free nodes
-    unsigned long long sgn;       // signs of the component nodes (mid nodes: 0)
-    uint8_t msn[MAXM];            // SN index of mid vertex j
-    int nsn, fallback;
-};
-
-template <int K, int MODE>
-__global__ void __launch_bounds__(THREADS) k_super_build(KParams p,
-                                                         const TileTables *__restrict__ tt_g,
-                                                         uint64_t s0, uint32_t nsup,
-                                                         SuperRec *__restrict__ srecs) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t *adj_s = smem;
-    TileTables *tt = reinterpret_cast<TileTables *>(smem + 32 * K * K);
-    stage_adj<K>(p, adj_s);
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    __syncthreads();
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nsup;
-         i += gridDim.x * blockDim.x) {
-        const uint64_t base = ((s0 + i) << tt->sh) << tt->bits;
-        const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, base) : base;
-        uint32_t SG[K], sf[K], zero[K];
-        sign_words<K>(p, sigma, SG);
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            sf[k] = tt->sfixed[k];
-            zero[k] = 0u;
-        }
-        Regions<K, MAXC> comps;
-        region_pass<K, false, false, true, MAXC>(adj_s, SG, sf, zero, tt->nsfixed, comps);
-        SuperRec *S = srecs + i;
-        const int n = comps.nreg, nm = tt->nm, nsn = n + nm;
-        if (n > MAXC || nsn > 64) {
-            S->nsn = nsn;
-            S->fallback = 1;
-            continue;
-        }
-        // SN order: merge the components (ascending lowest vertex) with the mid vertices
-        uint8_t ord[64];  // c, or 64 + j for mid vertex j
-        {
-            int ci = 0, mj = 0;
-            for (int q = 0; q < nsn; ++q) {
-                bool takec = ci < n;
-                if (takec && mj < nm) {
-                    int w, b;
-                    uint32_t R[K];
-#pragma unroll
-                    for (int k = 0; k < K; ++k) R[k] = comps.R[ci][k];
-                    lowest<K>(R, w, b);
-                    takec = 32 * w + b < (int)tt->mpos[mj];
-                }
-                ord[q] = takec ? (uint8_t)ci++ : (uint8_t)(64 + mj++);
-            }
-        }
-        auto node = [&](int q, uint32_t (&R)[K], uint32_t (&NB)[K]) {
-            const int o = ord[q];
-            if (o < 64) {
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    R[k] = comps.R[o][k];
-                    NB[k] = comps.X[o][k];
-                }
-            } else {
-                const int pos = tt->mpos[o - 64];
-                uint32_t dummy[K];
-                load_row<K, false>(adj_s, pos, NB, dummy);
-#pragma unroll
-                for (int k = 0; k < K; ++k) R[k] = (k == (pos >> 5)) ? (1u << (pos & 31)) : 0u;
-            }
-        };
-        unsigned long long sgn = 0;
-        unsigned long long fsn[MAXF];
-        for (int f = 0; f < tt->nf; ++f) fsn[f] = 0ull;
-        for (int q = 0; q < nsn; ++q) {
-            uint32_t R[K], NB[K], P[K];
-            node(q, R, NB);
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                const int ks = (k + K / 2) % K;
-                P[k] = R[ks] & p.bd[ks];
-            }
-            unsigned long long adj = 0, pl = 0;
-            for (int q2 = 0; q2 < nsn; ++q2) {
-                uint32_t R2[K], NB2[K];
-                const int o2 = ord[q2];
-                if (o2 < 64) {
-#pragma unroll
-                    for (int k = 0; k < K; ++k) R2[k] = comps.R[o2][k];
-                } else {
-                    const int pos = tt->mpos[o2 - 64];
-#pragma unroll
-                    for (int k = 0; k < K; ++k)
-                        R2[k] = (k == (pos >> 5)) ? (1u << (pos & 31)) : 0u;
-                }
-                (void)NB2;
-                uint32_t a = 0, l = 0;
-#pragma unroll
-                for (int k = 0; k < K; ++k) {
-                    a |= NB[k] & R2[k];
-                    l |= P[k] & R2[k];
-                }
-                if (a && q2 != q) adj |= 1ull << q2;
-                if (l) pl |= 1ull << q2;
-            }
-            uint32_t fb = 0;
-#pragma unroll
-            for (int k = 0; k < K; ++k) {
-                uint32_t x = NB[k] & tt->freem[k];
-                while (x) {
-                    const int f = tt->vfree[32 * k + __ffs(x) - 1];
-                    x &= x - 1u;
-                    fb |= 1u << f;
-                    fsn[f] |= 1ull << q;
-                }
-            }
-            S->adj[q] = adj;
-            S->link[q] = pl;
-            S->fadj[q] = fb;
-            const int o = ord[q];
-            if (o < 64) {
-                uint32_t sg = 0;
-#pragma unroll
-                for (int k = 0; k < K; ++k) sg |= R[k] & SG[k];
-                if (sg) sgn |= 1ull << q;
-            } else {
-                S->msn[o - 64] = (uint8_t)q;
-            }
-        }
-        for (int f = 0; f < tt->nf; ++f) S->fsn[f] = fsn[f];
-        S->sgn = sgn;
-        S->nsn = nsn;
-        S->fallback = 0;
-    }
-}
-
-// One tile per lane: mid signs, merge same-sign SN neighbours (labels are
-// lane-private bytes in shared memory, bank = lane), then one more pass per
-// component to collect its neighbours, links and free neighbours and write
-// the row.  Tiles of fallback super-tiles are listed in ovf for
-// k_tile_build_lanes.
-constexpr size_t FROM_SUPER_SMEM = sizeof(TileTables) + (16 + MAXF) * 4 * THREADS;  // max
-inline size_t from_super_smem(int nf) { return sizeof(TileTables) + (size_t)(16 + nf) * 4 * THREADS; }
-
-__global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *__restrict__ tt_g,
-                                                             const SuperRec *__restrict__ srecs,
-                                                             uint64_t tile0, uint32_t ntiles,
-                                                             TileRec *__restrict__ recs,
-                                                             unsigned long long *__restrict__ hashes,
-                                                             uint32_t *__restrict__ ovf) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    TileTables *tt = reinterpret_cast<TileTables *>(smem);
-    uint8_t *lb = reinterpret_cast<uint8_t *>(smem + sizeof(TileTables) / 4 + threadIdx.x);
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    __syncthreads();
-    const int h = tt->sh, nf = tt->nf, nm = tt->nm;
-    const uint64_t sbase = tile0 >> h;
-    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
-    // labels of the SN nodes in x, as a node mask (one lookup per set bit;
-    // 32-bit halves: __ffs is cheaper than __ffsll)
-    auto labels_of = [&](unsigned long long x) -> unsigned long long {
-        unsigned long long r = 0;
-        for (uint32_t w = (uint32_t)x; w; w &= w - 1u) r |= 1ull << label(__ffs(w) - 1);
-        for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) r |= 1ull << label(31 + __ffs(w));
-        return r;
-    };
-    uint32_t *FCs = smem + sizeof(TileTables) / 4 + 16 * THREADS + threadIdx.x;  // [nf] lane-private
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles;
-         t += gridDim.x * blockDim.x) {
-        const uint64_t gt = tile0 + t;
-        const SuperRec *S = srecs + ((gt >> h) - sbase);
-        TileRec *rec = recs + t;
-        if (S->fallback) {
-            ovf[1 + atomicAdd(ovf, 1u)] = t;
-            continue;
-        }
-        const int nsn = S->nsn;
-        const uint32_t ms = tt->msign[gt & ((1u << h) - 1u)];
-        unsigned long long sg = S->sgn;
-        for (int j = 0; j < nm; ++j) sg |= (unsigned long long)((ms >> j) & 1u) << S->msn[j];
-        const unsigned long long all = nsn >= 64 ? ~0ull : ((1ull << nsn) - 1ull);
-        // pass 1: label the merged components.  One flat loop of nsn pops (every
-        // lane of a warp shares the super record, so the trip count is uniform);
-        // a component closes when its frontier empties.
-        unsigned long long unv = all, seeds = 0, sbits = 0, F = 0, same = 0;
-        int n = -1;
-        for (int it = 0; it < nsn; ++it) {
-            if (F == 0ull) {
-                const unsigned long long seed = unv & (0ull - unv);
-                const bool s1 = (sg & seed) != 0ull;
-                same = s1 ? sg : ~sg;
-                F = seed;
-                unv ^= seed;
-                seeds |= seed;
-                ++n;
-                if (s1) sbits |= 1ull << n;
-            }
-            const int v = __ffsll((long long)F) - 1;
-            F &= F - 1ull;
-            TCG_ASSERT(v >= 0 && v < 64 && n < 64);
-            lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)n;
-            const unsigned long long nw = S->adj[v] & unv & same;
-            unv ^= nw;
-            F |= nw;
-        }
-        ++n;
-        const int nn = n + nf;
-        const bool fits = n <= MAXC && nn <= tt->maxnodes;
-        RecHash hs;
-        if (fits) {
-            // pass 2: the same traversal again, collecting each component's
-            // neighbours / links / free neighbours; rows are written as the
-            // components close
-            unsigned long long sd = seeds, M = 0, CG = 0, LK = 0;
-            uint32_t FB = 0;
-            unv = all;
-            F = 0;
-            int c = -1;
-            const bool fcs = n <= 32;  // free rows by scattering the components' free bits
-            if (fcs)
-                for (int f = 0; f < nf; ++f) FCs[f * THREADS] = 0u;
-            auto close = [&]() {
-                const unsigned long long adj = ((unsigned long long)FB << n) | labels_of(CG & ~M);
-                const unsigned long long pl = labels_of(LK);
-                if (fcs)
-                    for (uint32_t y = FB; y; y &= y - 1u) {
-                        TCG_ASSERT(__ffs(y) - 1 < nf && c < 32);
-                        FCs[(__ffs(y) - 1) * THREADS] |= 1u << c;
-                    }
-                store_row(rec, c, nn, adj, pl);
-                hs.row(adj, pl);
-            };
-            for (int it = 0; it < nsn; ++it) {
-                if (F == 0ull) {
-                    if (c >= 0) close();
-                    const unsigned long long seed = sd & (0ull - sd);
-                    sd ^= seed;
-                    same = (sg & seed) ? sg : ~sg;
-                    F = seed;
-                    unv ^= seed;
-                    M = CG = LK = 0ull;
-                    FB = 0u;
-                    ++c;
-                }
-                const int v = __ffsll((long long)F) - 1;
-                F &= F - 1ull;
-                M |= 1ull << v;
-                const unsigned long long a = S->adj[v];
-                CG |= a;
-                LK |= S->link[v];
-                FB |= S->fadj[v];
-                const unsigned long long nw = a & unv & same;
-                unv ^= nw;
-                F |= nw;
-            }
-            close();
-            for (int f = 0; f < nf; ++f) {
-                const unsigned long long fc = fcs ? (unsigned long long)FCs[f * THREADS]
-                                                  : labels_of(S->fsn[f]);
-                const unsigned long long adj = (tt->fadj[f] << n) | fc, pl = tt->fpl[f] << n;
-                store_row(rec, n + f, nn, adj, pl);
-                hs.row(adj, pl);
-            }
-        }
-        const unsigned long long sgf = fits ? sbits : 0ull;
-        hashes[t] = hs.fin(sgf, n, nn);
-        rec->sgn_fixed = sgf;
-        rec->n = n;
-        rec->nnodes = nn;
-        rec->fallback = fits ? 0 : 1;
-    }
-}
-
-// Tile deduplication.  A tile's classification depends only on its contracted
-// record (rows, fixed signs, sizes) and the tile-local index, so tiles with
-// byte-identical records produce identical results index by index.  One
-// thread per tile probes an open-addressing table keyed by the record hash
-// the builder computed (slot = hash tag << 32 | tile); a slot whose tag
-// matches is compared word by word (never by hash alone) and an equal record
-// absorbs the tile: dup[rep] += 1, mint[rep] = min tile id (the witness of
-// every scheme in the group is the smallest index, which lies in the group's
-// smallest tile).  Representatives are appended to list[] (warp-aggregated);
-// partial tiles (range ends) and fallback tiles are never merged.
-constexpr unsigned long long SLOT_EMPTY = ~0ull;
-
-__device__ __forceinline__ bool rec_equal(const TileRec *__restrict__ a,
-                                          const TileRec *__restrict__ b) {
-    if (a->n != b->n || a->nnodes != b->nnodes || a->sgn_fixed != b->sgn_fixed) return false;
-    const int nn = a->nnodes;
-    TCG_ASSERT(nn >= 0 && nn <= 64);
-    uint32_t diff = 0;
-    if (nn <= 32) {  // uint2 rows: compare two per uint4, the last one by halves
-        const uint4 *x = a->rows, *y = b->rows;
-        const int full = nn >> 1;
-#pragma unroll 4
-        for (int i = 0; i < full; ++i) {
-            const uint4 p = x[i], q = y[i];
-            diff |= (p.x ^ q.x) | (p.y ^ q.y) | (p.z ^ q.z) | (p.w ^ q.w);
-        }
-        if (nn & 1) {
-            const uint2 p = rows2(a)[nn - 1], q = rows2(b)[nn - 1];
-            diff |= (p.x ^ q.x) | (p.y ^ q.y);
-        }
-    } else {
-#pragma unroll 4
-        for (int i = 0; i < nn; ++i) {
-            const uint4 p = a->rows[i], q = b->rows[i];
-            diff |= (p.x ^ q.x) | (p.y ^ q.y) | (p.z ^ q.z) | (p.w ^ q.w);
-        }
-    }
-    return diff == 0u;
-}
-
-__global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restrict__ recs,
-                                                        const unsigned long long *__restrict__ hashes,
-                                                        uint32_t ntiles, uint64_t tile0, int bits,
-                                                        uint64_t start, uint64_t end,
-                                                        unsigned long long *__restrict__ slots,
-                                                        uint32_t smask, uint32_t *__restrict__ dup,
-                                                        uint32_t *__restrict__ mint,
-                                                        uint32_t *__restrict__ list,
-                                                        uint32_t *__restrict__ count) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    bool rep = false;
-    if (t < ntiles) {
-        const TileRec *r = recs + t;
-        const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
-        if (r->fallback || b0 < start || b1 > end) {
-            rep = true;
-        } else {
-            const unsigned long long h = hashes[t];
-            const unsigned long long tag = (h >> 32) << 32;
-            uint32_t at = (uint32_t)h & smask;
-            while (true) {
-                unsigned long long cur = slots[at];
-                if (cur == SLOT_EMPTY) {
-                    const unsigned long long prev = atomicCAS(&slots[at], SLOT_EMPTY, tag | t);
-                    if (prev == SLOT_EMPTY) {
-                        rep = true;
-                        break;
-                    }
-                    cur = prev;
-                }
-                if ((cur & 0xffffffff00000000ull) == tag) {
-                    const uint32_t o = (uint32_t)cur;
-                    TCG_ASSERT(o < ntiles);
-                    if (rec_equal(r, recs + o)) {
-                        atomicAdd(&dup[o], 1u);
-                        atomicMin(&mint[o], t);
-                        break;
-                    }
-                }
-                at = (at + 1) & smask;
-            }
-        }
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, rep);
-    if (bal) {
-        uint32_t base = 0;
-        if (lane == __ffs(bal) - 1) base = atomicAdd(count, (uint32_t)__popc(bal));
-        base = __shfl_sync(0xffffffffu, base, __ffs(bal) - 1);
-        TCG_ASSERT(!rep || base + __popc(bal & ((1u << lane) - 1u)) < ntiles);
-        if (rep) list[base + __popc(bal & ((1u << lane) - 1u))] = t;
-    }
-}
-
-// Classify every index of [start, end) that falls in tiles tile0 .. tile0+ntiles-1.
-// One warp owns a whole tile at a time (its contracted graph staged in a
-// per-warp shared-memory slot), so warps never wait on each other.
-constexpr int CLS_WARPS = THREADS / 32;
-
-
-template <int K, bool EVEN, int MODE>
-__global__ void __launch_bounds__(THREADS) k_tile_classify(KParams p,
-                                                           const TileTables *__restrict__ tt_g,
-                                                           const TileRec *__restrict__ recs,
-                                                           uint64_t tile0, uint32_t ntiles,
-                                                           uint64_t start, uint64_t end,
-                                                           DevAgg g, const uint32_t *__restrict__ list,
-                                                           const uint32_t *__restrict__ count,
-                                                           const uint32_t *__restrict__ dup,
-                                                           const uint32_t *__restrict__ mint,
-                                                           unsigned long long *__restrict__ tstats) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t *adj_s = smem;
-    CtaTable tab = carve_table(smem + 32 * K * K);
-    TileTables *tt = reinterpret_cast<TileTables *>(
-        reinterpret_cast<char *>(smem) + 32 * K * K * 4 + TABLE_SMEM);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    TileRec *rec = reinterpret_cast<TileRec *>(tt + 1) + w;
-    stage_adj<K>(p, adj_s);
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    tab.init();
-    __syncthreads();
-    const int bits = tt->bits;
-    const uint32_t tsize = 1u << bits;
-    // list != nullptr: classify only the representatives, each with the weight
-    // of its duplicate group and the group's smallest tile as the witness base
-    const uint32_t nwork = list ? *count : ntiles;
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(tstats, (unsigned long long)nwork);
-    for (uint32_t i = blockIdx.x * CLS_WARPS + w; i < nwork; i += gridDim.x * CLS_WARPS) {
-        // list entries: tile, or tile | (a + 1) << 24 for the 32-index slice of
-        // A pattern a only (a slice the level-2 path could not take)
-        const uint32_t e = list ? list[i] : i;
-        const int ssh = slice_shift(tt->la);
-        const uint32_t t = e & ((1u << ssh) - 1u), sub = e >> ssh;
-        const uint32_t lo0 = sub ? (sub - 1u) << 5 : 0u, lo1 = sub ? lo0 + 32u : tsize;
-        const uint32_t weight = list ? 1u + dup[t] : 1u;
-        const uint32_t tw = list ? min(t, mint[t]) : t;
-        const TileRec *src = recs + t;
-        const int nn = src->nnodes;
-        const bool fb = src->fallback != 0;
-        // nn <= 32: the node pass reads only the low adjacency and link words;
-        // stage them as two 32-word arrays (one bank per node: no conflicts)
-        uint32_t *ax = reinterpret_cast<uint32_t *>(rec->rows), *az = ax + 32;
-        if (!fb && nn <= 32) {
-            if (lane < nn) {
-                const uint2 row = rows2(src)[lane];
-                ax[lane] = row.x;
-                az[lane] = row.y;
-            }
-        } else {
-            if (lane < nn) rec->rows[lane] = src->rows[lane];
-            if (lane + 32 < nn) rec->rows[lane + 32] = src->rows[lane + 32];
-        }
-        const int n = src->n;
-        const unsigned long long sgf = src->sgn_fixed;
-        __syncwarp();
-        const uint64_t base = (tile0 + tw) << bits;
-        if (!fb && nn <= 32 && !sub) {  // two patchworks per thread (tile sizes are >= 64)
-            const uint32_t used = nn >= 32 ? ~0u : ((1u << nn) - 1u);
-            for (uint32_t low = lane; low < tsize; low += 64) {
-                const unsigned long long fa =
-                    tt->fsign[0][low & 63u] ^ tt->fsign[1][(low >> 6) & 63u];
-                const unsigned long long fb2 =
-                    tt->fsign[0][(low + 32) & 63u] ^ tt->fsign[1][((low + 32) >> 6) & 63u];
-                const uint32_t sga = (uint32_t)(sgf | (fa << n));
-                const uint32_t sgb = (uint32_t)(sgf | (fb2 << n));
-                Regions<1> ra, rb;
-                node_pass1x2<EVEN>(ax, az, sga, sgb, used, nn, ra, rb);
-#pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
-                    const uint64_t m = base + low + 32u * h;
-                    const bool valid = m >= start && m < end;
-                    const uint32_t SG1[1] = {h ? sgb : sga};
-                    const Result r = finish<1, EVEN, false>(p, SG1, h ? rb : ra, p.maxreg);
-                    uint64_t k = 0;
-                    if (valid) {
-                        if (r.status == TCG_OK) k = r.key;
-                        else atomicMin(g.bad, (unsigned long long)m);
-                    }
-                    tab.add<true>(g, k, r.nreg, m, weight);
-                }
-            }
-            __syncwarp();
-            continue;
-        }
-        for (uint32_t low = lo0 + lane; low < lo1; low += 32) {
-            const uint64_t m = base + low;
-            const bool valid = m >= start && m < end;
-            Result r;
-            if (fb) {
-                const uint64_t sigma = MODE == MODE_REP ? rep_to_sigma(p.d, m) : m;
-                r = classify<K, EVEN>(p, adj_s, valid ? sigma : 0ull);
-            } else {
-                r = classify_tile<EVEN>(p, *tt, rec->rows, sgf, n, nn, low);
-            }
-            uint64_t k = 0;
-            if (valid) {
-                if (r.status == TCG_OK) k = r.key;
-                else atomicMin(g.bad, (unsigned long long)m);
-            }
-            tab.add<true>(g, k, r.nreg, m, weight);
-        }
-        __syncwarp();
-    }
-    __syncthreads();
-    tab.flush(g);
-}
-
-// ------------------------------------------------------------ level 2
-// Level-2 contraction of a representative tile (odd degree, <= 64 nodes).
-// Fix the signs of the A points (tile-local index bits 5..bits-1) as well:
-// the fixed components and the A nodes then merge, through same-sign edges
-// and antipodal links, into "super-nodes" -- subsets of regions whatever
-// the B signs (bits 0..4) are.  A super-node mixes signs, so its edges to a
-// B node are recorded by the sign of the member they leave from (plusB /
-// minusB); edges between two super-nodes are always crossed (a same-sign
-// edge would have merged them).  One record (header + one u64 per
-// super-node) describes 32 patchworks, one per lane.  Records built from
-// different tiles coincide far more often than level-1 records do, and are
-// deduplicated the same way (exact comparison, weights add, witness = the
-// smallest (tile, A) position of the group).
-//   word[s] = crossS | (plusB | minusB << nB | linkB << 2nB | self << 3nB) << 32
-
-__device__ __forceinline__ uint32_t l2_compress(const TileTables &tt, uint32_t freemask) {
-    if (tt.l2shift >= 0) return (freemask >> tt.l2shift) & ((1u << tt.nB) - 1u);
-    uint32_t r = 0;
-    while (freemask) {
-        const int f = __ffs(freemask) - 1;
-        freemask &= freemask - 1u;
-        r |= 1u << tt.l2j[f];
-    }
-    return r;
-}
-
-// <= 32-node records (98 % at d=7): the same super-node BFS without
-// per-super-node arrays in local memory.  Node labels (bytes) and the
-// cross-adjacency words cs[q] are lane-private shared memory (bank = lane);
-// when super-node q closes, its crossed neighbours that are already labelled
-// (earlier super-nodes) set cs[q] and cs[q2] -- every pair is met once, from
-// its later end -- and the record's high half (B-node words, self flag) is
-// written immediately; the low halves (cs) follow at the end.
-constexpr int L2B_CS = 24;          // super-nodes per level-2 record (also <= 32 - nB)
-constexpr int L2B_WORDS = 16 + L2B_CS;  // labels (64 nodes, 4 per word) | cs[L2B_CS]
-constexpr int L2B_SLOT = 256;       // staged rows per tile: 32 x uint2 (wider tiles read global)
-// level 2 needs tile bits >= 6 (la >= 1): at most 16 tiles per warp
-constexpr size_t L2B_SMEM = (size_t)L2B_WORDS * 4 * THREADS + (THREADS / 32) * 16 * L2B_SLOT;
-
-template <typename MT>
-__device__ __forceinline__ int l2_build_lbl(const TileTables &tt,
-                                            const TileRec *__restrict__ rec,
-                                            const uint4 *__restrict__ R4, uint32_t a, int mmax,
-                                            unsigned long long *out, unsigned long long &hout,
-                                            uint32_t *mine) {
-    constexpr bool WIDE = sizeof(MT) == 8;
-    const int n = rec->n, nB = tt.nB;
-    uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
-    uint32_t *cs = mine + 16 * THREADS;
-    const uint32_t lowA = a << 5;
-    const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
-    const MT one = 1;
-    const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa) << n);
-    const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa << n);
-    const MT FBn = (MT)tt.fbm << n;
-    uint32_t *out32 = reinterpret_cast<uint32_t *>(out);
-    MT unv = G, done = 0;
-    uint32_t hh = 0x9E3779B9u;
-    int m = 0;
-    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
-    while (unv) {
-        if (m == mmax) return -1;
-        MT f = unv & ((MT)0 - unv);
-        unv ^= f;
-        MT M = f, cg = 0, pb = 0, mb = 0, lk = 0;
-        while (f) {
-            const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
-            f &= f - one;
-            TCG_ASSERT(u >= 0 && u < 64 && m < 64);
-            lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
-            MT rx, ry;
-            if constexpr (WIDE) {
-                const uint4 r = R4[u];
-                rx = (MT)r.x | ((MT)r.y << 32);
-                ry = (MT)r.z | ((MT)r.w << 32);
-            } else {
-                const uint2 r = reinterpret_cast<const uint2 *>(R4)[u];
-                rx = r.x;
-                ry = r.y;
-            }
-            const MT s = (sg1 >> u) & one;
-            const MT diff = sg1 ^ ((MT)0 - s);  // nodes of the other sign
-            const MT nw = ((rx & ~diff) | ry) & unv;
-            unv ^= nw;
-            f |= nw;
-            M |= nw;
-            cg |= rx & G & diff;
-            const MT bp = rx & FBn;
-            pb |= s ? bp : (MT)0;
-            mb |= s ? (MT)0 : bp;
-            lk |= ry & FBn;
-        }
-        // crossed neighbours in earlier super-nodes (labelled): both ends' cs words
-        uint32_t c = 0;
-        const MT x = cg & done;
-        for (uint32_t w = (uint32_t)x; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
-        if constexpr (WIDE)
-            for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) c |= 1u << label(31 + __ffs(w));
-        TCG_ASSERT(m < L2B_CS);
-        cs[m * THREADS] = c;
-        for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
-        const uint32_t self = (cg & M) != (MT)0;
-        const uint32_t hi = l2_compress(tt, (uint32_t)(pb >> n)) |
-                            l2_compress(tt, (uint32_t)(mb >> n)) << nB |
-                            l2_compress(tt, (uint32_t)(lk >> n)) << (2 * nB) | self << (3 * nB);
-        out32[2 * (1 + m) + 1] = hi;
-        hh = (hh ^ hi) * 0x85EBCA77u;
-        hh ^= hh >> 13;
-        done |= M;
-        ++m;
-    }
-    out[0] = (unsigned long long)m;
-    uint32_t hl = 0xC2B2AE3Du;
-    for (int q = 0; q < m; ++q) {
-        const uint32_t c = cs[q * THREADS];
-        out32[2 * (1 + q)] = c;
-        hl = (hl ^ c) * 0x9E3779B1u;
-        hl ^= hl >> 15;
-    }
-    hout = mix64(((unsigned long long)hh << 32 | hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
-    return m;
-}
-
-// Level 2 in even degree.  Antipodal partners carry the same sign, and a
-// region's orientation matters (the root is its unique region with an
-// orientation-reversing cycle), so a super-node keeps each member's parity
-// relative to its seed (same-sign edges keep it, links flip it) and an odd
-// flag (a member reached with both parities).  Its record is two words:
-//   word0 = cs | self << 30 | odd << 31
-//   word1 = P10 | P11 << nB | P00 << 2nB | P01 << 3nB | LK0 << 4nB | LK1 << 5nB
-// where Psp = B nodes adjacent to members of sign s and parity p, LKp = B
-// nodes linked to members of parity p.
-template <typename MT>
-__device__ __forceinline__ int l2_build_even(const TileTables &tt,
-                                             const TileRec *__restrict__ rec,
-                                             const uint4 *__restrict__ R4, uint32_t a, int mmax,
-                                             unsigned long long *out, unsigned long long &hout,
-                                             uint32_t *mine) {
-    constexpr bool WIDE = sizeof(MT) == 8;
-    const int n = rec->n, nB = tt.nB;
-    uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
-    uint32_t *cs = mine + 16 * THREADS;
-    const uint32_t lowA = a << 5;
-    const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
-    const MT one = 1;
-    const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa) << n);
-    const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa << n);
-    const MT FBn = (MT)tt.fbm << n;
-    MT unv = G, done = 0, q = 0;  // q: parity-1 nodes (relative to their super-node's seed)
-    unsigned long long hh = 0x9E3779B97F4A7C15ull;
-    int m = 0;
-    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
-    auto cmp = [&](MT x) -> unsigned long long { return l2_compress(tt, (uint32_t)(x >> n)); };
-    while (unv) {
-        if (m == mmax) return -1;
-        MT f = unv & ((MT)0 - unv);
-        unv ^= f;
-        MT M = f, cg = 0, p10 = 0, p11 = 0, p00 = 0, p01 = 0, lk0 = 0, lk1 = 0;
-        bool odd = false;
-        while (f) {
-            const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
-            f &= f - one;
-            TCG_ASSERT(u >= 0 && u < 64 && m < 64);
-            lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
-            MT rx, ry;
-            if constexpr (WIDE) {
-                const uint4 r = R4[u];
-                rx = (MT)r.x | ((MT)r.y << 32);
-                ry = (MT)r.z | ((MT)r.w << 32);
-            } else {
-                const uint2 r = reinterpret_cast<const uint2 *>(R4)[u];
-                rx = r.x;
-                ry = r.y;
-            }
-            const MT s = (sg1 >> u) & one, pu = (q >> u) & one;
-            const MT diff = sg1 ^ ((MT)0 - s);        // nodes of the other sign
-            const MT eqm = pu ? q : ~q;                 // nodes with u's parity
-            const MT te = rx & ~diff & G, tl = ry & G;  // same-sign edges keep, links flip
-            const MT nt = te & unv, np = tl & unv;
-            odd |= ((nt & np) | (te & ~unv & ~eqm) | (tl & ~unv & eqm)) != (MT)0;
-            q |= pu ? nt : np;
-            const MT nw = nt | np;
-            unv ^= nw;
-            f |= nw;
-            M |= nw;
-            cg |= rx & G & diff;
-            const MT bp = rx & FBn, bl = ry & FBn;
-            if (s) {
-                if (pu) p11 |= bp; else p10 |= bp;
-            } else {
-                if (pu) p01 |= bp; else p00 |= bp;
-            }
-            if (pu) lk1 |= bl; else lk0 |= bl;
-        }
-        uint32_t c = 0;
-        const MT x = cg & done;
-        for (uint32_t w = (uint32_t)x; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
-        if constexpr (WIDE)
-            for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) c |= 1u << label(31 + __ffs(w));
-        const uint32_t self = (cg & M) != (MT)0;
-        TCG_ASSERT(m < L2B_CS);
-        cs[m * THREADS] = c | self << 30 | (uint32_t)odd << 31;
-        for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
-        const unsigned long long w1 = cmp(p10) | cmp(p11) << nB | cmp(p00) << (2 * nB) |
-                                      cmp(p01) << (3 * nB) | cmp(lk0) << (4 * nB) |
-                                      cmp(lk1) << (5 * nB);
-        out[2 + 2 * m] = w1;
-        hh = mix64(hh ^ w1);
-        done |= M;
-        ++m;
-    }
-    out[0] = (unsigned long long)m;
-    uint32_t hl = 0xC2B2AE3Du;
-    for (int k = 0; k < m; ++k) {
-        const uint32_t c = cs[k * THREADS];
-        out[1 + 2 * k] = c;
-        hl = (hl ^ c) * 0x9E3779B1u;
-        hl ^= hl >> 15;
-    }
-    hout = mix64((hh ^ hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
-    return m;
-}
-
-// One thread per (representative tile, A pattern) of list1[i0 .. i0+nb).
-// Tiles the level-2 path cannot take go to oldlist for the level-1
-// classifier: whole tiles (entry = tile: range ends, fallback) or single A
-// slices whose super-node graph is too large (entry = tile | (a + 1) << 24).
-template <bool EVEN>
-__global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restrict__ tt_g,
-                                                      const TileRec *__restrict__ recs,
-                                                      const uint32_t *__restrict__ list1,
-                                                      const uint32_t *__restrict__ dup1,
-                                                      const uint32_t *__restrict__ mint1,
-                                                      uint32_t i0, uint32_t nb, uint64_t tile0,
-                                                      uint64_t start, uint64_t end,
-                                                      unsigned long long *__restrict__ pool,
-                                                      uint32_t stride,
-                                                      unsigned long long *__restrict__ hashes,
-                                                      uint32_t *__restrict__ wts,
-                                                      uint32_t *__restrict__ poss,
-                                                      uint32_t *__restrict__ oldlist,
-                                                      uint32_t *__restrict__ oldcount) {
-    __shared__ TileTables tts;
-    extern __shared__ __align__(16) uint32_t l2smem[];
-    uint32_t *mine = l2smem + threadIdx.x;
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    __syncthreads();
-    const TileTables &tt = tts;
-    const int la = tt.la, bits = tt.bits;
-    const int mmax = min(32 - tt.nB, L2B_CS);
-    const uint32_t nrec = nb << la;
-    // the 2^la lanes of one tile stage its (<= 32-node) rows in shared memory
-    // first: the breadth-first pass then reads rows at shared-memory latency
-    const int lane = threadIdx.x & 31, lpt = la < 5 ? la : 5;
-    uint4 *slot = reinterpret_cast<uint4 *>(l2smem + L2B_WORDS * THREADS) +
-                  (L2B_SLOT / 16) * ((threadIdx.x >> 5) * (32 >> lpt) + (lane >> lpt));
-    for (uint32_t jb = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); jb < nrec;
-         jb += gridDim.x * blockDim.x) {  // warp-uniform
-        const uint32_t j = jb + lane;
-        const bool valid = j < nrec;
-        const uint32_t i = i0 + (j >> la), a = j & ((1u << la) - 1u);
-        const uint32_t t = valid ? list1[i] : 0u;
-        const TileRec *rec = recs + t;
-        if (valid && rec->nnodes <= 32) {  // 256 bytes of uint2 rows
-            const uint4 *src = rec->rows;
-            for (int q = lane & ((1 << lpt) - 1); q < 16; q += 1 << lpt) slot[q] = src[q];
-        }
-        __syncwarp();
-        if (valid) {
-            const int nn = rec->nnodes;
-            const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
-            if (rec->fallback || b0 < start || b1 > end) {
-                if (a == 0) oldlist[atomicAdd(oldcount, 1u)] = t;
-                wts[j] = 0u;
-            } else {
-                unsigned long long *out = pool + (size_t)j * stride;
-                unsigned long long h = 0;
-                int m;
-                if constexpr (EVEN)
-                    m = nn <= 32 ? l2_build_even<uint32_t>(tt, rec, slot, a, mmax, out, h, mine)
-                                 : l2_build_even<unsigned long long>(tt, rec, rec->rows, a, mmax, out,
-                                                                     h, mine);
-                else
-                    m = nn <= 32 ? l2_build_lbl<uint32_t>(tt, rec, slot, a, mmax, out, h, mine)
-                                 : l2_build_lbl<unsigned long long>(tt, rec, rec->rows, a, mmax, out,
-                                                                    h, mine);
-                if (m < 0) {
-                    oldlist[atomicAdd(oldcount, 1u)] = t | ((a + 1u) << slice_shift(la));
-                    wts[j] = 0u;
-                } else {
-                    hashes[j] = h;
-                    wts[j] = 1u + dup1[t];
-                    poss[j] = (min(t, mint1[t]) << la) | a;
-                }
-            }
-        }
-        __syncwarp();
-    }
-}
-
-// ---------------------------------------------------- two-stage level 2
-// Stage 1 (k_l15_build, one lane per (representative tile, A1 pattern)):
-// fix the A1 nodes (tile bits 5, 6) and merge components + A1 nodes into
-// super-nodes, keeping their relations to the F nodes (B and A2) by member
-// sign; records are two words per super-node,
-//   word0 = cs | self << 31,   word1 = plusF | minusF << nF | linkF << 2nF,
-// and are deduplicated like level-2 records.  Stage 2 (k_l2_from_l15, one
-// lane per (distinct stage-1 record, A2 pattern)) fixes the A2 nodes and
-// merges again, emitting ordinary level-2 records (same format and hash as
-// k_l2_build, so the rest of the pipeline is unchanged).  Either stage sets
-// *fail when a record would exceed its super-node budget; the host then
-// redoes the batch on the direct path.
-// dynamic shared memory of k_l15_build: labels | cs, then one 1 KB row slot
-// per tile of each warp (at least 2 A1 bits: <= 8 tiles per warp)
-constexpr size_t L15_SMEM_MAX = (size_t)L2B_WORDS * 4 * THREADS + (THREADS / 32) * 8 * 1024 + 4096;
-constexpr int L15_MAXM = L2B_CS;  // stage-1 super-nodes (cs bit 31 is the self flag)
-
-// F-space compression by byte lookup tables (k_l15_build stages them in shared memory)
-struct L15Lut {
-    uint32_t b[4][256];  // byte k of a free-node mask -> its F bits
-};
-
-__device__ __forceinline__ unsigned long long l15_compress(const L15Lut &L, uint32_t fm) {
-    return (unsigned long long)(L.b[0][fm & 0xffu] | L.b[1][(fm >> 8) & 0xffu] |
-                                L.b[2][(fm >> 16) & 0xffu] | L.b[3][fm >> 24]);
-}
-
-template <typename MT, bool PACK>
-__device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut,
-                                         const TileRec *__restrict__ rec,
-                                         const uint4 *__restrict__ R4, uint32_t a1,
-                                         unsigned long long *out, unsigned long long &hout,
-                                         uint32_t *mine) {
-    constexpr bool WIDE = sizeof(MT) == 8;
-    const int n = rec->n, nF = tt.nB + tt.nA2;
-    uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
-    uint32_t *cs = mine + 16 * THREADS;
-    const uint32_t lowA = a1 << 5;
-    const unsigned long long fsA = tt.fsign[0][lowA & 63u] ^ tt.fsign[1][(lowA >> 6) & 63u];
-    const MT one = 1;
-    const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa1) << n);
-    const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa1 << n);
-    const MT FBn = (MT)(tt.fbm | tt.fa2) << n;
-    MT unv = G, done = 0;
-    unsigned long long hh = 0x9E3779B97F4A7C15ull;
-    int m = 0;
-    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
-    while (unv) {
-        if (m == tt.l15max) return -1;
-        MT f = unv & ((MT)0 - unv);
-        unv ^= f;
-        MT M = f, cg = 0, pb = 0, mb = 0, lk = 0;
-        while (f) {
-            const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
-            f &= f - one;
-            TCG_ASSERT(u >= 0 && u < 64 && m < 64);
-            lb[(u >> 2) * (4 * THREADS) + (u & 3)] = (uint8_t)m;
-            MT rx, ry;
-            if constexpr (WIDE) {
-                const uint4 r = R4[u];
-                rx = (MT)r.x | ((MT)r.y << 32);
-                ry = (MT)r.z | ((MT)r.w << 32);
-            } else {
-                const uint2 r = reinterpret_cast<const uint2 *>(R4)[u];
-                rx = r.x;
-                ry = r.y;
-            }
-            const MT s = (sg1 >> u) & one;
-            const MT diff = sg1 ^ ((MT)0 - s);
-            const MT nw = ((rx & ~diff) | ry) & unv;
-            unv ^= nw;
-            f |= nw;
-            M |= nw;
-            cg |= rx & G & diff;
-            const MT bp = rx & FBn;
-            pb |= s ? bp : (MT)0;
-            mb |= s ? (MT)0 : bp;
-            lk |= ry & FBn;
-        }
-        uint32_t c = 0;
-        const MT x = cg & done;
-        for (uint32_t w = (uint32_t)x; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
-        if constexpr (WIDE)
-            for (uint32_t w = (uint32_t)(x >> 32); w; w &= w - 1u) c |= 1u << label(31 + __ffs(w));
-        const uint32_t self = (cg & M) != (MT)0;
-        TCG_ASSERT(m < L2B_CS);
-        cs[m * THREADS] = c | self << 31;
-        for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
-        const unsigned long long w1 = l15_compress(lut, (uint32_t)(pb >> n)) |
-                                      l15_compress(lut, (uint32_t)(mb >> n)) << nF |
-                                      l15_compress(lut, (uint32_t)(lk >> n)) << (2 * nF);
-        if (PACK) {  // low half now; the high half (w1 >> 32, cs, self) at the end
-            reinterpret_cast<uint32_t *>(out)[2 * (1 + m)] = (uint32_t)w1;
-            cs[m * THREADS] |= (uint32_t)(w1 >> 32) << 24;  // <= 7 bits: 3 nF <= 39
-        } else {
-            out[2 + 2 * m] = w1;
-        }
-        hh = mix64(hh ^ w1);
-        done |= M;
-        ++m;
-    }
-    out[0] = (unsigned long long)m;
-    uint32_t hl = 0xC2B2AE3Du;
-    for (int k = 0; k < m; ++k) {
-        const uint32_t c = cs[k * THREADS];
-        if (PACK)  // word bits 32..: w1 >> 32, then cs (24 bits) and self from bit 3 nF
-            reinterpret_cast<uint32_t *>(out)[2 * (1 + k) + 1] =
-                ((c >> 24) & 0x7fu) | ((c & 0xffffffu) << (3 * nF - 32)) |
-                ((c >> 31) << (3 * nF - 32 + 24));
-        else
-            out[1 + 2 * k] = c;
-        hl = (hl ^ c) * 0x9E3779B1u;
-        hl ^= hl >> 15;
-    }
-    hout = mix64((hh ^ hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
-    return m;
-}
-
-// One lane per (representative tile, A1 pattern) of list1[i0 .. i0+nb): 4 per tile.
-__global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restrict__ tt_g,
-                                                       const TileRec *__restrict__ recs,
-                                                       const uint32_t *__restrict__ list1,
-                                                       const uint32_t *__restrict__ dup1,
-                                                       const uint32_t *__restrict__ mint1,
-                                                       uint32_t i0, uint32_t nb, uint64_t tile0,
-                                                       uint64_t start, uint64_t end,
-                                                       unsigned long long *__restrict__ pool,
-                                                       uint32_t stride,
-                                                       unsigned long long *__restrict__ hashes,
-                                                       uint32_t *__restrict__ wts,
-                                                       uint32_t *__restrict__ poss,
-                                                       uint32_t *__restrict__ oldlist,
-                                                       uint32_t *__restrict__ oldcount,
-                                                       uint32_t *__restrict__ fail,
-                                                       const L15Lut *__restrict__ lut_g,
-                                                       int slotq, int lut_smem) {
-    __shared__ TileTables tts;
-    extern __shared__ __align__(16) uint32_t l2smem[];
-    uint32_t *mine = l2smem + threadIdx.x;
-    // dynamic shared memory: labels | cs (lane-private), one row slot of
-    // slotq uint4 rows per tile of each warp, then (lut_smem) the lookup tables
-    const int nslot = (THREADS / 32) * (32 >> tt_g->la1);
-    uint32_t *lutsm = l2smem + L2B_WORDS * THREADS + nslot * slotq * 4;
-    const L15Lut &luts = lut_smem ? *reinterpret_cast<const L15Lut *>(lutsm) : *lut_g;
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    for (int i = threadIdx.x; i < (int)(sizeof(L15Lut) / 4); i += blockDim.x)
-        if (lut_smem) lutsm[i] = reinterpret_cast<const uint32_t *>(lut_g)[i];
-    __syncthreads();
-    const TileTables &tt = tts;
-    const int bits = tt.bits;
-    const int la1 = tt.la1;
-    const uint32_t nrec = nb << la1;
-    const int lane = threadIdx.x & 31;
-    // one row slot per tile of the warp: 16 uint4 hold <= 32-node rows (uint2);
-    // tiles of 33..slotq nodes (all of d = 7 at 2^12-index tiles have > 32)
-    // are staged too, wider ones read their rows from global memory
-    uint4 *slot = reinterpret_cast<uint4 *>(l2smem + L2B_WORDS * THREADS) +
-                  slotq * ((threadIdx.x >> 5) * (32 >> tt.la1) + (lane >> tt.la1));
-    for (uint32_t jb = blockIdx.x * blockDim.x + (threadIdx.x & ~31u); jb < nrec;
-         jb += gridDim.x * blockDim.x) {  // warp-uniform
-        const uint32_t j = jb + lane;
-        const bool valid = j < nrec;
-        const uint32_t i = i0 + (j >> la1), a1 = j & ((1u << la1) - 1u);
-        const uint32_t t = valid ? list1[i] : 0u;
-        const TileRec *rec = recs + t;
-        if (valid && (rec->nnodes <= 32 || rec->nnodes <= slotq)) {  // uint2 rows, or nnodes uint4 rows
-            const uint4 *src = rec->rows;
-            const int nq = rec->nnodes <= 32 ? 16 : rec->nnodes;
-            for (int q = lane & ((1 << la1) - 1); q < nq; q += 1 << la1) slot[q] = src[q];
-        }
-        __syncwarp();
-        if (valid) {
-            const int nn = rec->nnodes;
-            const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
-            if (rec->fallback || b0 < start || b1 > end) {
-                if (a1 == 0) oldlist[atomicAdd(oldcount, 1u)] = t;
-                wts[j] = 0u;
-            } else {
-                unsigned long long *out = pool + (size_t)j * stride;
-                unsigned long long h = 0;
-                const int nF = tt.nB + tt.nA2;
-                const bool pk = nF >= 11 && nF <= 13;  // one word per super-node
-                const int m =
-                    nn <= 32
-                        ? (pk ? l15_build<uint32_t, true>(tt, luts, rec, slot, a1, out, h, mine)
-                              : l15_build<uint32_t, false>(tt, luts, rec, slot, a1, out, h, mine))
-                        : (pk ? l15_build<unsigned long long, true>(tt, luts, rec, nn <= slotq ? slot : rec->rows,
-                                                                    a1, out, h, mine)
-                              : l15_build<unsigned long long, false>(tt, luts, rec, nn <= slotq ? slot : rec->rows,
-                                                                     a1, out, h, mine));
-                if (m < 0) {
-                    atomicOr(fail, 1u);
-                    wts[j] = 0u;
-                } else {
-                    hashes[j] = h;
-                    wts[j] = 1u + dup1[t];
-                    poss[j] = (min(t, mint1[t]) << la1) | a1;
-                }
-            }
-        }
-        __syncwarp();
-    }
-}
-
-// One lane per (distinct stage-1 record list15[i], A2 pattern): 4 per record.
-// NA: A2 nodes the per-record sameA / crossA rows are sized for.  NA <= 4
-// (d = 7 raw, 2^12-index tiles: nA2 = 3) keeps them in registers (static
-// indices); the general instance (16) keeps the dynamically indexed arrays,
-// which live in local memory.
-template <int NA>
-__global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__restrict__ tt_g,
-                                                         const unsigned long long *__restrict__ pool1,
-                                                         uint32_t stride1,
-                                                         const uint32_t *__restrict__ list15,
-                                                         const uint32_t *__restrict__ count15,
-                                                         const uint32_t *__restrict__ w15,
-                                                         const uint32_t *__restrict__ pos15,
-                                                         unsigned long long *__restrict__ pool,
-                                                         uint32_t stride,
-                                                         unsigned long long *__restrict__ hashes,
-                                                         uint32_t *__restrict__ wts,
-                                                         uint32_t *__restrict__ poss,
-                                                         uint32_t *__restrict__ fail) {
-    __shared__ TileTables tts;
-    extern __shared__ __align__(16) uint32_t l2smem[];
-    uint32_t *mine = l2smem + threadIdx.x;
-    uint8_t *lb = reinterpret_cast<uint8_t *>(mine);
-    uint32_t *cs = mine + 16 * THREADS, *hw = cs + L2B_CS * THREADS;
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(&tts)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    __syncthreads();
-    const TileTables &tt = tts;
-    const int nB = tt.nB, nA2 = tt.nA2, nF = nB + nA2;
-    const uint32_t bm = (1u << nB) - 1u, a2m = (1u << nA2) - 1u;
-    const unsigned long long fm = (1ull << nF) - 1ull;
-    const int mmax = min(32 - nB, L2B_CS);
-    const int la2 = tt.la2;
-    const uint32_t nrec = *count15 << la2;
-    const bool pk = nF >= 11 && nF <= 13;  // stage-1 records packed one word per super-node
-    // stage-1 super-node s: w1 = F relations, w0 = cs | self << 31
-    auto rw1 = [&](const unsigned long long *r1, int s2) -> unsigned long long {
-        return pk ? (r1[1 + s2] & ((1ull << (3 * nF)) - 1ull)) : r1[2 + 2 * s2];
-    };
-    auto rw0 = [&](const unsigned long long *r1, int s2) -> uint32_t {
-        if (!pk) return (uint32_t)r1[1 + 2 * s2];
-        const uint32_t x = (uint32_t)(r1[1 + s2] >> (3 * nF));
-        return (x & 0xffffffu) | ((x >> 24) & 1u) << 31;
-    };
-    auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nrec; j += gridDim.x * blockDim.x) {
-        const uint32_t j1 = list15[j >> la2], a2 = j & ((1u << la2) - 1u);
-        const unsigned long long *r1 = pool1 + (size_t)j1 * stride1;
-        const int m1 = (int)r1[0];
-        const uint32_t SA2 = tt.a2sign[a2];
-        // A2 rows toward the stage-1 super-nodes (same-sign or linked / crossed)
-        uint32_t sameA[NA], crossA[NA];
-#pragma unroll
-        for (int k = 0; k < NA; ++k) sameA[k] = crossA[k] = 0u;
-        for (int s = 0; s < m1; ++s) {
-            const unsigned long long w1 = rw1(r1, s);
-            const uint32_t pA = (uint32_t)(w1 >> nB) & a2m, mA = (uint32_t)(w1 >> (nF + nB)) & a2m,
-                           lA = (uint32_t)(w1 >> (2 * nF + nB)) & a2m;
-            const uint32_t same = (pA & SA2) | (mA & ~SA2) | lA, cross = (pA & ~SA2) | (mA & SA2);
-            if constexpr (NA <= 4) {  // bits >= nA2 are zero (a2m)
-#pragma unroll
-                for (int k = 0; k < NA; ++k) {
-                    sameA[k] |= ((same >> k) & 1u) << s;
-                    crossA[k] |= ((cross >> k) & 1u) << s;
-                }
-            } else {
-                for (uint32_t y = same; y; y &= y - 1u) sameA[__ffs(y) - 1] |= 1u << s;
-                for (uint32_t y = cross; y; y &= y - 1u) crossA[__ffs(y) - 1] |= 1u << s;
-            }
-        }
-        const int nn = m1 + nA2;
-        if (nn > 32) {  // 32-bit node masks: the host redoes the batch directly
-            atomicOr(fail, 1u);
-            wts[j] = 0u;
-            continue;
-        }
-        const uint32_t G = nn >= 32 ? ~0u : ((1u << nn) - 1u);
-        uint32_t unv = G, done = 0, hh = 0x9E3779B9u;
-        unsigned long long *out = pool + (size_t)j * stride;
-        int m = 0;
-        bool bad = false;
-        while (unv) {
-            if (m == mmax) { bad = true; break; }
-            uint32_t f = unv & (0u - unv);
-            unv ^= f;
-            uint32_t M = f, cg = 0, pb = 0, mb = 0, lk = 0, selfany = 0;
-            while (f) {
-                const int v = __ffs(f) - 1;
-                f &= f - 1u;
-                TCG_ASSERT(v >= 0 && v < 64 && m < 64);
-                lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)m;
-                uint32_t same, cross;
-                if (v < m1) {
-                    const unsigned long long w0 = rw0(r1, v), w1 = rw1(r1, v);
-                    const uint32_t pA = (uint32_t)(w1 >> nB) & a2m,
-                                   mA = (uint32_t)(w1 >> (nF + nB)) & a2m,
-                                   lA = (uint32_t)(w1 >> (2 * nF + nB)) & a2m;
-                    same = ((pA & SA2) | (mA & ~SA2) | lA) << m1;
-                    cross = ((uint32_t)w0 & 0x7fffffffu) | (((pA & ~SA2) | (mA & SA2)) << m1);
-                    selfany |= (uint32_t)w0 >> 31;
-                    pb |= (uint32_t)(w1 & fm) & bm;
-                    mb |= (uint32_t)((w1 >> nF) & fm) & bm;
-                    lk |= (uint32_t)((w1 >> (2 * nF)) & fm) & bm;
-                } else {
-                    const int k = v - m1;
-                    const uint32_t sk = (SA2 >> k) & 1u, own = sk ? SA2 : ~SA2;
-                    uint32_t sAk, cAk;
-                    if constexpr (NA <= 4) {
-                        sAk = sameA[0];
-                        cAk = crossA[0];
-#pragma unroll
-                        for (int q = 1; q < NA; ++q) {
-                            sAk = k == q ? sameA[q] : sAk;
-                            cAk = k == q ? crossA[q] : cAk;
-                        }
-                    } else {
-                        sAk = sameA[k];
-                        cAk = crossA[k];
-                    }
-                    same = sAk | (((tt.a2adjA2[k] & own) | tt.a2linkA2[k]) << m1);
-                    cross = cAk | ((tt.a2adjA2[k] & ~own & a2m) << m1);
-                    if (sk) pb |= tt.a2adjB[k];
-                    else mb |= tt.a2adjB[k];
-                    lk |= tt.a2linkB[k];
-                }
-                const uint32_t nw = same & unv;
-                unv ^= nw;
-                f |= nw;
-                M |= nw;
-                cg |= cross;
-            }
-            uint32_t c = 0;
-            for (uint32_t w = cg & done; w; w &= w - 1u) c |= 1u << label(__ffs(w) - 1);
-            TCG_ASSERT(m < L2B_CS);
-            cs[m * THREADS] = c;
-            for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
-            const uint32_t self = ((cg & M) != 0u) | selfany;
-            hw[m * THREADS] = pb | mb << nB | lk << (2 * nB) | self << (3 * nB);
-            done |= M;
-            ++m;
-        }
-        if (bad) {
-            atomicOr(fail, 1u);
-            wts[j] = 0u;
-            continue;
-        }
-        // canonical order: super-nodes sorted by their B-relation word (stable),
-        // so that equal graphs reached through different node numberings give
-        // equal records (the classification is invariant under relabelling)
-        // rank of super-node q in label slot q, the inverse in slot 32 + rank
-        // (lane-private bytes: slot v at (v >> 2) * 4 * THREADS + (v & 3))
-        auto slot8 = [&](int v) -> uint8_t & { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
-        for (int q = 0; q < m; ++q) {
-            const uint32_t hq = hw[q * THREADS];
-            int r = 0;
-            for (int q2 = 0; q2 < m; ++q2) {
-                const uint32_t h2 = hw[q2 * THREADS];
-                r += (h2 < hq) || (h2 == hq && q2 < q);
-            }
-            slot8(q) = (uint8_t)r;
-            slot8(32 + r) = (uint8_t)q;
-        }
-        out[0] = (unsigned long long)m;
-        uint32_t hl = 0xC2B2AE3Du;
-        for (int r = 0; r < m; ++r) {
-            const int q = slot8(32 + r);
-            uint32_t c = 0;
-            for (uint32_t y = cs[q * THREADS]; y; y &= y - 1u) c |= 1u << slot8(__ffs(y) - 1);
-            const uint32_t hi = hw[q * THREADS];
-            out[1 + r] = (unsigned long long)c | (unsigned long long)hi << 32;
-            hh = (hh ^ hi) * 0x85EBCA77u;
-            hh ^= hh >> 13;
-            hl = (hl ^ c) * 0x9E3779B1u;
-            hl ^= hl >> 15;
-        }
-        hashes[j] = mix64(((unsigned long long)hh << 32 | hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
-        wts[j] = w15[j1];
-        const uint32_t p1 = pos15[j1];
-        const int la1 = tt.la1;
-        poss[j] = ((p1 >> la1) << (la1 + la2)) | (a2 << la1) | (p1 & ((1u << la1) - 1u));
-    }
-}
-
-// One thread per level-2 record: exact deduplication (hash, then word-by-word).
-#ifndef L2D_PRE
-#define L2D_PRE 8  // record words k_l2_dedup fetches before probing
-#endif
-__global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *__restrict__ pool,
-                                                      uint32_t stride, uint32_t nrec,
-                                                      const unsigned long long *__restrict__ hashes,
-                                                      const uint32_t *__restrict__ wts,
-                                                      const uint32_t *__restrict__ poss,
-                                                      unsigned long long *__restrict__ slots,
-                                                      uint32_t smask,
-                                                      uint32_t *__restrict__ w2,
-                                                      uint32_t *__restrict__ pos2,
-                                                      uint32_t *__restrict__ list2,
-                                                      uint32_t *__restrict__ count2, int wps) {
-    // slot = hash tag << 32 | record; a tag match is confirmed word by word
-    // (wps = record words per super-node: 1 odd degree, 2 even)
-    const int lane = threadIdx.x & 31;
-    const uint32_t tot = gridDim.x * blockDim.x;
-    const uint32_t jmax = (nrec + 31u) & ~31u;  // whole warps iterate together
-    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < jmax; j += tot) {
-        bool isnew = false;
-        const uint32_t wj = j < nrec ? wts[j] : 0u;
-        if (wj) {
-            const unsigned long long h = hashes[j];
-            const unsigned long long tag = (h >> 32) << 32;
-            const unsigned long long *mine = pool + (size_t)j * stride;
-            // the record's first words, fetched with its length and alongside the
-            // first probe (a tag match -- every duplicate -- compares them); words
-            // past the record's end lie inside its slot (stride >= 5) and are unused
-            const int npre = min(L2D_PRE, (int)stride - 1);
-            const unsigned long long m = mine[0];
-            unsigned long long pw[L2D_PRE];
-#pragma unroll
-            for (int q = 0; q < L2D_PRE; ++q) pw[q] = q < npre ? mine[1 + q] : 0ull;
-            const int nw = wps * (int)m;
-            uint32_t at = (uint32_t)h & smask;
-            while (true) {
-                unsigned long long cur = slots[at];
-                if (cur == SLOT_EMPTY) {
-                    const unsigned long long prev = atomicCAS(&slots[at], SLOT_EMPTY, tag | j);
-                    if (prev == SLOT_EMPTY) {
-                        isnew = true;
-                        atomicAdd(&w2[j], wj);
-                        atomicMin(&pos2[j], poss[j]);
-                        break;
-                    }
-                    cur = prev;
-                }
-                if ((cur & 0xffffffff00000000ull) == tag) {
-                    const uint32_t o = (uint32_t)cur;
-                    TCG_ASSERT(o < nrec && at <= smask);
-                    const unsigned long long *ow = pool + (size_t)o * stride;
-                    unsigned long long diff = ow[0] ^ m;
-#pragma unroll
-                    for (int q = 0; q < L2D_PRE; ++q)
-                        if (q < npre && q < nw) diff |= ow[1 + q] ^ pw[q];
-#pragma unroll 4
-                    for (int q = npre + 1; q <= nw; ++q) diff |= ow[q] ^ mine[q];
-                    if (diff == 0ull) {
-                        atomicAdd(&w2[o], wj);
-                        atomicMin(&pos2[o], poss[j]);
-                        break;
-                    }
-                }
-                at = (at + 1) & smask;
-            }
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, isnew);
-        if (bal) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(count2, (uint32_t)__popc(bal));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            TCG_ASSERT(!isnew || base + __popc(bal & ((1u << lane) - 1u)) < nrec);
-            if (isnew) list2[base + __popc(bal & ((1u << lane) - 1u))] = j;
-        }
-    }
-}
-
-// Level-2 node pass.  Node rows (shared memory, SoA by node):
-//   same  = (A & ~T) | (B & T) | (s_v ? Cp : Cm) | L
-//   cross = (A &  T) | (B & ~T) | (s_v ? Cm : Cp) | X,   T = S ^ (s_v ? ~0 : 0)
-// super-node: A = minusB, B = plusB, Cp = Cm = 0, L = linkB, X = crossS | self
-// B node:     A = adjB, B = 0, Cp = plusS, Cm = minusS, L = linkBB | linkS, X = 0
-// (S = the lane's B-node signs; super-nodes carry sign 0).
-struct L2Rows {
-    uint32_t A[32], B[32], Cp[32], Cm[32], L[32], X[32];
-    unsigned long long W[32];
-};
-
-__device__ __forceinline__ void l2_node_pass(const L2Rows &rw, uint32_t S, int nn,
-                                             Regions<1> &out) {
-    uint32_t un = nn >= 32 ? ~0u : ((1u << nn) - 1u), f = 0, x = 0, r = 0;
-    int nreg = 0;
-    auto seed = [&]() {
-        f = un & (0u - un);
-        r = un;
-        un ^= f;
-        x = 0u;
-    };
-    seed();
-    for (int it = 0; it < nn; ++it) {
-        if (f == 0u) {
-            if (nreg < MAXR) {
-                out.R[nreg][0] = r ^ un;
-                out.X[nreg][0] = x;
-            }
-            ++nreg;
-            seed();
-        }
-        const int v = __ffs(f) - 1;
-        f &= f - 1u;
-        const uint32_t sv = (S >> v) & 1u;
-        const uint32_t T = S ^ (0u - sv);
-        const uint32_t a = rw.A[v], b = rw.B[v], cp = rw.Cp[v], cm = rw.Cm[v];
-        const uint32_t same = (a & ~T) | (b & T) | (sv ? cp : cm) | rw.L[v];
-        x |= (a & T) | (b & ~T) | (sv ? cm : cp) | rw.X[v];
-        const uint32_t nw = same & un;
-        un ^= nw;
-        f |= nw;
-    }
-    if (nreg < MAXR) {
-        out.R[nreg][0] = r ^ un;
-        out.X[nreg][0] = x;
-    }
-    out.nreg = nreg + 1;
-    out.oddmask = 0u;
-}
-
-constexpr size_t L2_CLS_SMEM = TABLE_SMEM + sizeof(TileTables) + CLS_WARPS * sizeof(L2Rows);
-
-// One warp per representative level-2 record; lane b classifies B pattern b.
-__global__ void __launch_bounds__(THREADS) k_l2_classify(KParams p,
-                                                         const TileTables *__restrict__ tt_g,
-                                                         const unsigned long long *__restrict__ pool,
-                                                         uint32_t stride,
-                                                         const uint32_t *__restrict__ list2,
-                                                         const uint32_t *__restrict__ count2,
-                                                         const uint32_t *__restrict__ w2,
-                                                         const uint32_t *__restrict__ pos2,
-                                                         uint64_t tile0, DevAgg g,
-                                                         unsigned long long *__restrict__ tstats) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    CtaTable tab = carve_table(smem);
-    TileTables *tt = reinterpret_cast<TileTables *>(reinterpret_cast<char *>(smem) + TABLE_SMEM);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    L2Rows *rw = reinterpret_cast<L2Rows *>(tt + 1) + w;
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    tab.init();
-    __syncthreads();
-    const int nB = tt->nB, bits = tt->bits;
-    const uint32_t bm = (1u << nB) - 1u;
-    const uint32_t n2 = *count2;
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(tstats, (unsigned long long)n2);
-    const uint32_t Sb = tt->l2bsign[lane];
-    for (uint32_t i = blockIdx.x * CLS_WARPS + w; i < n2; i += gridDim.x * CLS_WARPS) {
-        const uint32_t j = list2[i];
-        const unsigned long long *rec = pool + (size_t)j * stride;
-        const int m = (int)rec[0];
-        if (lane < m) rw->W[lane] = rec[1 + lane];
-        __syncwarp();
-        if (lane < m) {
-            const unsigned long long wd = rw->W[lane];
-            const uint32_t hi = (uint32_t)(wd >> 32);
-            rw->A[lane] = ((hi >> nB) & bm) << m;
-            rw->B[lane] = (hi & bm) << m;
-            rw->Cp[lane] = 0u;
-            rw->Cm[lane] = 0u;
-            rw->L[lane] = ((hi >> (2 * nB)) & bm) << m;
-            rw->X[lane] = (uint32_t)wd | (((hi >> (3 * nB)) & 1u) << lane);
-        }
-        if (lane < nB) {
-            uint32_t ps = 0, ms = 0, ls = 0;
-            for (int q = 0; q < m; ++q) {
-                const uint32_t hi = (uint32_t)(rw->W[q] >> 32);
-                ps |= ((hi >> lane) & 1u) << q;
-                ms |= ((hi >> (nB + lane)) & 1u) << q;
-                ls |= ((hi >> (2 * nB + lane)) & 1u) << q;
-            }
-            const int v = m + lane;
-            rw->A[v] = tt->l2adjB[lane] << m;
-            rw->B[v] = 0u;
-            rw->Cp[v] = ps;
-            rw->Cm[v] = ms;
-            rw->L[v] = (tt->l2linkB[lane] << m) | ls;
-            rw->X[v] = 0u;
-        }
-        __syncwarp();
-        Regions<1> rg;
-        l2_node_pass(*rw, Sb << m, m + nB, rg);
-        const uint32_t SG1[1] = {0u};
-        const Result r = finish<1, false, false>(p, SG1, rg, p.maxreg);
-        const uint64_t mw = (tile0 << bits) + ((uint64_t)pos2[j] << 5) + lane;
-        uint64_t k = 0;
-        if (r.status == TCG_OK) k = r.key;
-        else atomicMin(g.bad, (unsigned long long)mw);
-        tab.add<true>(g, k, r.nreg, mw, w2[j]);
-        __syncwarp();
-    }
-    __syncthreads();
-    tab.flush(g);
-}
-
-// Even-degree level-2 classification.  Rows per node v (super-nodes 0..m-1,
-// B nodes m..m+nB-1), with T = the lane's B-sign mask S for a super-node
-// and all-ones / all-zeros by the B node's own sign:
-//   E0 = T&F0 | ~T&F2 | F5 | AB&~(S^T)    neighbours at the same parity
-//   E1 = T&F1 | ~T&F3 | F4 | LB           neighbours at the other parity
-//   X  = T&(F2|F3) | ~T&(F0|F1) | CS | AB&(S^T)   crossed neighbours
-// F0..F5 = P10, P11, P00, P01, LK0, LK1 (super-nodes: B masks; B nodes: the
-// transposed super-node masks), AB / LB = static B-B adjacency / links, CS =
-// super-node crossed adjacency (+ self bit), ODD = odd super-nodes.
-struct L2RowsE {
-    uint32_t F[6][32], AB[32], LB[32], CS[32];
-    unsigned long long W0[32], W1[32];
-};
-
-__device__ __forceinline__ void l2_node_pass_even(const L2RowsE &rw, uint32_t S, uint32_t oddn,
-                                                  int m, int nn, Regions<1> &out) {
-    uint32_t un = nn >= 32 ? ~0u : ((1u << nn) - 1u), f = 0, x = 0, r = 0, q = 0, oddmask = 0;
-    bool odd = false;
-    int nreg = 0;
-    auto seed = [&]() {
-        f = un & (0u - un);
-        r = un;
-        un ^= f;
-        x = 0u;
-        odd = false;
-    };
-    auto close = [&]() {
-        if (nreg < MAXR) {
-            out.R[nreg][0] = r ^ un;
-            out.X[nreg][0] = x;
-            if (odd) oddmask |= 1u << nreg;
-        }
-        ++nreg;
-    };
-    seed();
-    for (int it = 0; it < nn; ++it) {
-        if (f == 0u) {
-            close();
-            seed();
-        }
-        const int v = __ffs(f) - 1;
-        f &= f - 1u;
-        const uint32_t T = v < m ? S : (0u - ((S >> v) & 1u));
-        const uint32_t f0 = rw.F[0][v], f1 = rw.F[1][v], f2 = rw.F[2][v], f3 = rw.F[3][v];
-        const uint32_t ab = rw.AB[v];
-        const uint32_t e0 = (T & f0) | (~T & f2) | rw.F[5][v] | (ab & ~(S ^ T));
-        const uint32_t e1 = (T & f1) | (~T & f3) | rw.F[4][v] | rw.LB[v];
-        x |= (T & (f2 | f3)) | (~T & (f0 | f1)) | rw.CS[v] | (ab & (S ^ T));
-        const uint32_t pv = (q >> v) & 1u;
-        const uint32_t eqm = pv ? q : ~q;
-        const uint32_t nt = e0 & un, np = e1 & un;
-        odd |= ((nt & np) | (e0 & ~un & ~eqm) | (e1 & ~un & eqm) | (oddn & (1u << v))) != 0u;
-        q |= pv ? nt : np;
-        un ^= nt | np;
-        f |= nt | np;
-    }
-    close();
-    out.nreg = nreg;
-    out.oddmask = oddmask;
-}
-
-constexpr size_t L2E_CLS_SMEM = TABLE_SMEM + sizeof(TileTables) + CLS_WARPS * sizeof(L2RowsE);
-
-__global__ void __launch_bounds__(THREADS) k_l2_classify_even(KParams p,
-                                                              const TileTables *__restrict__ tt_g,
-                                                              const unsigned long long *__restrict__ pool,
-                                                              uint32_t stride,
-                                                              const uint32_t *__restrict__ list2,
-                                                              const uint32_t *__restrict__ count2,
-                                                              const uint32_t *__restrict__ w2,
-                                                              const uint32_t *__restrict__ pos2,
-                                                              uint64_t tile0, DevAgg g,
-                                                              unsigned long long *__restrict__ tstats) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    CtaTable tab = carve_table(smem);
-    TileTables *tt = reinterpret_cast<TileTables *>(reinterpret_cast<char *>(smem) + TABLE_SMEM);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    L2RowsE *rw = reinterpret_cast<L2RowsE *>(tt + 1) + w;
-    for (int i = threadIdx.x; i < (int)(sizeof(TileTables) / 4); i += blockDim.x)
-        reinterpret_cast<uint32_t *>(tt)[i] = reinterpret_cast<const uint32_t *>(tt_g)[i];
-    tab.init();
-    __syncthreads();
-    const int nB = tt->nB, bits = tt->bits;
-    const uint32_t bm = (1u << nB) - 1u;
-    const uint32_t n2 = *count2;
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(tstats, (unsigned long long)n2);
-    const uint32_t Sb = tt->l2bsign[lane];
-    for (uint32_t i = blockIdx.x * CLS_WARPS + w; i < n2; i += gridDim.x * CLS_WARPS) {
-        const uint32_t j = list2[i];
-        const unsigned long long *rec = pool + (size_t)j * stride;
-        const int m = (int)rec[0];
-        if (lane < m) {
-            rw->W0[lane] = rec[1 + 2 * lane];
-            rw->W1[lane] = rec[2 + 2 * lane];
-        }
-        __syncwarp();
-        uint32_t oddn = 0;
-        {
-            const bool od = lane < m && ((uint32_t)rw->W0[lane] >> 31);
-            oddn = __ballot_sync(0xffffffffu, od);
-        }
-        if (lane < m) {
-            const uint32_t c = (uint32_t)rw->W0[lane];
-            const unsigned long long w1 = rw->W1[lane];
-#pragma unroll
-            for (int k = 0; k < 6; ++k) rw->F[k][lane] = (uint32_t)((w1 >> (k * nB)) & bm) << m;
-            rw->AB[lane] = 0u;
-            rw->LB[lane] = 0u;
-            rw->CS[lane] = (c & 0x3fffffffu) | (((c >> 30) & 1u) << lane);
-        }
-        if (lane < nB) {
-            uint32_t t[6] = {0u, 0u, 0u, 0u, 0u, 0u};
-            for (int s = 0; s < m; ++s) {
-                const unsigned long long w1 = rw->W1[s];
-#pragma unroll
-                for (int k = 0; k < 6; ++k) t[k] |= (uint32_t)((w1 >> (k * nB + lane)) & 1u) << s;
-            }
-            const int v = m + lane;
-#pragma unroll
-            for (int k = 0; k < 6; ++k) rw->F[k][v] = t[k];
-            rw->AB[v] = tt->l2adjB[lane] << m;
-            rw->LB[v] = tt->l2linkB[lane] << m;
-            rw->CS[v] = 0u;
-        }
-        __syncwarp();
-        Regions<1> rg;
-        l2_node_pass_even(*rw, Sb << m, oddn, m, m + nB, rg);
-        const uint32_t SG1[1] = {0u};
-        const Result r = finish<1, true, false>(p, SG1, rg, p.maxreg);
-        const uint64_t mw = (tile0 << bits) + ((uint64_t)pos2[j] << 5) + lane;
-        uint64_t k = 0;
-        if (r.status == TCG_OK) k = r.key;
-        else atomicMin(g.bad, (unsigned long long)mw);
-        tab.add<true>(g, k, r.nreg, mw, w2[j]);
-        __syncwarp();
-    }
-    __syncthreads();
-    tab.flush(g);
-}
-
-// ------------------------------------------------------------ any degree
-// Generic path for degrees the bit-mask layout does not cover (d > 9; any d
-// works): one CTA per patchwork, state in shared memory, vertex numbering
-// and edge order exactly the reference's.  Components by a lock-free
-// union-find over the non-crossed edges (CAS hooking of the larger root onto
-// the smaller, path halving); the parity union-find over the 2d antipodal
-// pairs, region ids, odd flags and any status collision are replayed by one
-// thread in the reference's order (kernels.py:151-230); the crossed-edge
-// region pairs are deduplicated in a shared hash set; the rooted tree comes
-// back as a parent array for the host to render.
-struct LargeParams {
-    int d, nv, ne, nap, npts, maxreg, words;  // words = u64 per sign row
-    const int32_t *eu, *ev, *src, *apu, *apv;
-    const uint8_t *par, *used;
-};
-
-constexpr int LHASH = 8192;  // region-pair hash set (pairs <= maxreg - 1 on valid input)
-
-__device__ __forceinline__ int lfind(int *p, int x) {
-    while (true) {
-        const int px = p[x];
-        if (px == x) return x;
-        const int ppx = p[px];
-        if (ppx != px) p[x] = ppx;  // path halving (benign race: only shortens paths)
-        x = px;
-    }
-}
-
-__device__ int lfind2(int *p2, uint8_t *par2, int x, int &parity) {
-    int root = x, pp = 0;
-    while (p2[root] != root) {
-        pp ^= par2[root];
-        root = p2[root];
-    }
-    int v = x, acc = pp;
-    while (p2[v] != v) {
-        const int nxt = p2[v];
-        const int step = par2[v];
-        p2[v] = root;
-        par2[v] = (uint8_t)acc;
-        acc ^= step;
-        v = nxt;
-    }
-    parity = pp;
-    return root;
-}
-
-// insert (a, b) into the pair set; returns true if it was new
-__device__ __forceinline__ bool pair_insert(uint32_t *hs, uint32_t key) {
-    uint32_t h = (key * 2654435761u) & (LHASH - 1);
-    for (int probe = 0; probe < LHASH; ++probe) {
-        const uint32_t prev = atomicCAS(&hs[h], 0xffffffffu, key);
-        if (prev == 0xffffffffu) return true;
-        if (prev == key) return false;
-        h = (h + 1) & (LHASH - 1);
-    }
-    return false;
-}
-
-__global__ void __launch_bounds__(THREADS) k_large(LargeParams P, const uint64_t *__restrict__ sig,
-                                                   int64_t n, int32_t *__restrict__ status,
-                                                   int32_t *__restrict__ nreg_out,
-                                                   int32_t *__restrict__ parent_out) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    const int nv = P.nv;
-    int *p1 = reinterpret_cast<int *>(smem);       // [nv] component union-find
-    int *rid = p1 + nv;                            // [nv] region id per vertex
-    int *p2 = rid + nv;                            // [nv] parity union-find (by vertex id)
-    uint32_t *hs = reinterpret_cast<uint32_t *>(p2 + nv);  // [LHASH]
-    int *deg = reinterpret_cast<int *>(hs + LHASH);        // [maxreg + 1] CSR offsets
-    int *adjl = deg + P.maxreg + 1;                        // [2 * maxreg]
-    int *bfs = adjl + 2 * P.maxreg;                        // [maxreg]
-    int *rpar = bfs + P.maxreg;                            // [maxreg]
-    uint8_t *sg = reinterpret_cast<uint8_t *>(rpar + P.maxreg);  // [nv]
-    uint8_t *par2 = sg + nv;                                     // [nv]
-    uint8_t *odd2 = par2 + nv;                                   // [nv]
-    __shared__ int s_nreg, s_status, s_root, s_nedges, s_selfm, s_self1, s_self2;
-    for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
-        const uint64_t *row = sig + t * P.words;
-        for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-            const int k = P.src[v];
-            sg[v] = (uint8_t)(((row[k >> 6] >> (k & 63)) & 1ull) ^ P.par[v]);
-            p1[v] = v;
-            p2[v] = v;
-            par2[v] = 0;
-            odd2[v] = 0;
-        }
-        for (int i = threadIdx.x; i < LHASH; i += blockDim.x) hs[i] = 0xffffffffu;
-        __syncthreads();
-        for (int e = threadIdx.x; e < P.ne; e += blockDim.x) {
-            int u = P.eu[e], v = P.ev[e];
-            if (sg[u] != sg[v]) continue;
-            while (true) {
-                u = lfind(p1, u);
-                v = lfind(p1, v);
-                if (u == v) break;
-                if (u < v) { const int tmp = u; u = v; v = tmp; }
-                if (atomicCAS(&p1[u], u, v) == u) break;
-            }
-        }
-        __syncthreads();
-        // flatten in two phases: roots found read-only (into rid, free until the
-        // region ids below), then stored.  A halving find here could land a stale
-        // non-root ancestor in p1[v] after v's own thread stored the root.
-        for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-            int x = v;
-            while (p1[x] != x) x = p1[x];
-            rid[v] = x;
-        }
-        __syncthreads();
-        for (int v = threadIdx.x; v < nv; v += blockDim.x) p1[v] = rid[v];
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            // parity union-find over the antipodal pairs (components named by root vertex)
-            for (int a = 0; a < P.nap; ++a) {
-                const int cu = p1[P.apu[a]], cv = p1[P.apv[a]];
-                int pu, pv;
-                int ru = lfind2(p2, par2, cu, pu), rv = lfind2(p2, par2, cv, pv);
-                if (ru == rv) {
-                    if (pu == pv) odd2[ru] = 1;
-                } else {
-                    // deterministic: hook the larger root onto the smaller
-                    if (ru > rv) { const int tmp = ru; ru = rv; rv = tmp; const int tp = pu; pu = pv; pv = tp; }
-                    p2[rv] = ru;
-                    par2[rv] = (uint8_t)(pu ^ pv ^ 1);
-                    if (odd2[rv]) odd2[ru] = 1;
-                }
-            }
-            // dense region ids in vertex order (the reference's first-occurrence order)
-            int nreg = 0, nodd = 0, oddr = -1, st = TCG_OK;
-            for (int v = 0; v < nv; ++v) {
-                if (!P.used[v] || p1[v] != v) continue;
-                int pp;
-                const int r = lfind2(p2, par2, v, pp);
-                if (r == v) {
-                    if (nreg >= P.maxreg) { st = TCG_TOO_MANY_REGIONS; break; }
-                    rid[v] = nreg;
-                    if (odd2[v]) { ++nodd; oddr = nreg; }
-                    ++nreg;
-                }
-            }
-            if (st == TCG_OK) {
-                for (int v = 0; v < nv; ++v) {
-                    if (!P.used[v] || p1[v] != v) continue;
-                    int pp;
-                    const int r = lfind2(p2, par2, v, pp);
-                    rid[v] = rid[r];
-                }
-            }
-            if (st == TCG_OK && P.d % 2 == 0) {
-                if (nodd == 0) st = TCG_NO_ODD_REGION;
-                else if (nodd > 1) st = TCG_MANY_ODD_REGIONS;
-            }
-            s_nreg = nreg;
-            s_status = st;
-            s_root = P.d % 2 == 0 ? oddr : -1;
-            s_nedges = 0;
-            s_selfm = 0;
-            s_self1 = -1;
-            s_self2 = -1;
-        }
-        __syncthreads();
-        for (int v = threadIdx.x; v < nv; v += blockDim.x)
-            if (P.used[v]) rid[v] = rid[p1[v]];
-        __syncthreads();
-        if (s_status == TCG_OK) {
-            for (int e = threadIdx.x; e < P.ne; e += blockDim.x) {
-                const int u = P.eu[e], v = P.ev[e];
-                if (sg[u] == sg[v]) continue;
-                int a = rid[u], b = rid[v];
-                if (a == b) {
-                    atomicAdd(&s_selfm, 1);
-                    if (atomicCAS(&s_self1, -1, a) != -1 && s_self1 != a) atomicExch(&s_self2, a);
-                    continue;
-                }
-                if (a > b) { const int tmp = a; a = b; b = tmp; }
-                if (pair_insert(hs, ((uint32_t)a << 16) | (uint32_t)b)) atomicAdd(&s_nedges, 1);
-            }
-        }
-        __syncthreads();
-        if (threadIdx.x == 0 && s_status == TCG_OK) {
-            const int nreg = s_nreg;
-            const bool even = P.d % 2 == 0;
-            const bool toomany = s_nedges > nreg - 1;
-            const bool anomaly = toomany || (even && s_selfm) || (!even && s_self2 >= 0);
-            int st = TCG_OK, root = s_root;
-            if (anomaly) {
-                // exact replay in the reference's edge order (kernels.py:199-230)
-                for (int i = 0; i < LHASH; ++i) hs[i] = 0xffffffffu;
-                int ne2 = 0;
-                root = even ? s_root : -1;
-                for (int e = 0; e < P.ne && st == TCG_OK; ++e) {
-                    const int u = P.eu[e], v = P.ev[e];
-                    if (sg[u] == sg[v]) continue;
-                    int a = rid[u], b = rid[v];
-                    if (a == b) {
-                        if (even) st = TCG_NONSEPARATING_OVAL;
-                        else if (root < 0) root = a;
-                        else if (root != a) st = TCG_ROOT_CONFLICT;
-                        continue;
-                    }
-                    if (a > b) { const int tmp = a; a = b; b = tmp; }
-                    if (pair_insert(hs, ((uint32_t)a << 16) | (uint32_t)b)) {
-                        if (ne2 >= nreg - 1) st = TCG_NOT_A_TREE;
-                        ++ne2;
-                    }
-                }
-                if (st == TCG_OK) st = TCG_NOT_A_TREE;  // unreachable for anomalous inputs
-            } else if (!even) {
-                if (s_self1 < 0) st = TCG_NO_PSEUDOLINE;
-                root = s_self1;
-            }
-            if (st == TCG_OK && s_nedges != nreg - 1) st = TCG_NOT_A_TREE;
-            if (st == TCG_OK) {
-                // CSR over the deduplicated pairs, BFS from the root
-                for (int r = 0; r <= nreg; ++r) deg[r] = 0;
-                for (int i = 0; i < LHASH; ++i) {
-                    const uint32_t k = hs[i];
-                    if (k == 0xffffffffu) continue;
-                    deg[(k >> 16) + 1]++;
-                    deg[(k & 0xffff) + 1]++;
-                }
-                for (int r = 0; r < nreg; ++r) deg[r + 1] += deg[r];
-                for (int r = 0; r < nreg; ++r) rpar[r] = deg[r];
-                for (int i = 0; i < LHASH; ++i) {
-                    const uint32_t k = hs[i];
-                    if (k == 0xffffffffu) continue;
-                    const int a = (int)(k >> 16), b = (int)(k & 0xffff);
-                    adjl[rpar[a]++] = b;
-                    adjl[rpar[b]++] = a;
-                }
-                for (int r = 0; r < nreg; ++r) rpar[r] = -1;
-                int head = 0, tail = 1;
-                bfs[0] = root;
-                rpar[root] = root;
-                while (head < tail) {
-                    const int r = bfs[head++];
-                    for (int k = deg[r]; k < deg[r + 1]; ++k) {
-                        const int s2 = adjl[k];
-                        if (rpar[s2] < 0) {
-                            rpar[s2] = r;
-                            bfs[tail++] = s2;
-                        }
-                    }
-                }
-                if (tail != nreg) st = TCG_DISCONNECTED;
-            }
-            s_status = st;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            status[t] = s_status;
-            nreg_out[t] = s_nreg;
-        }
-        if (s_status == TCG_OK)
-            for (int r = threadIdx.x; r < s_nreg; r += blockDim.x)
-                parent_out[t * P.maxreg + r] = rpar[r];
-        __syncthreads();
-    }
-}
+#include "large.cuh"
 
 __global__ void k_agg_clear(DevAgg g) {
     const int stride = gridDim.x * blockDim.x;
@@ -3164,531 +256,7 @@ struct tcg_plan {
 };
 
 namespace {
-
-struct DeviceGuard {
-    int prev = -1;
-    explicit DeviceGuard(int dev) {
-        cudaGetDevice(&prev);
-        if (prev != dev) cudaSetDevice(dev);
-    }
-    ~DeviceGuard() {
-        int cur = -1;
-        cudaGetDevice(&cur);
-        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
-    }
-};
-
-// TCG_HOST_TRACE=1: host timestamps (us since the previous mark) around the
-// pipeline's synchronisation points, to stderr (diagnostics only).
-static void host_mark(const char *what) {
-    static const bool on = [] {
-        const char *e = std::getenv("TCG_HOST_TRACE");
-        return e && e[0] && e[0] != '0';
-    }();
-    if (!on) return;
-    static auto prev = std::chrono::steady_clock::now();
-    const auto now = std::chrono::steady_clock::now();
-    std::fprintf(stderr, "[tcg] %-22s +%9.1f us\n", what,
-                 std::chrono::duration<double, std::micro>(now - prev).count());
-    prev = now;
-}
-
-// Per-kernel timing: events bracket each launch on the plan's stream and are
-// resolved after the next synchronisation (tcg_agg_fetch / tcg_kernel_times).
-cudaEvent_t timing_begin(tcg_plan *P, cudaStream_t st = nullptr) {
-    if (!P->timing) return nullptr;
-    cudaEvent_t a;
-    cudaEventCreate(&a);
-    cudaEventRecord(a, st ? st : P->stream);
-    return a;
-}
-
-void timing_end(tcg_plan *P, int kind, cudaEvent_t a, cudaStream_t st = nullptr) {
-    if (!P->timing || !a) return;
-    cudaEvent_t b;
-    cudaEventCreate(&b);
-    cudaEventRecord(b, st ? st : P->stream);
-    P->tev.push_back({kind, {a, b}});
-}
-
-void timing_resolve(tcg_plan *P) {
-    for (auto &t : P->tev) {
-        float ms = 0.f;
-        cudaEventSynchronize(t.second.second);
-        cudaEventElapsedTime(&ms, t.second.first, t.second.second);
-        P->t_ms[t.first] += ms;
-        P->t_n[t.first] += 1;
-        cudaEventDestroy(t.second.first);
-        cudaEventDestroy(t.second.second);
-    }
-    P->tev.clear();
-}
-
-template <int K, bool EVEN>
-void *enum_fn(int mode) {
-    switch (mode) {
-        case MODE_RAW: return (void *)k_enumerate<K, EVEN, MODE_RAW>;
-        case MODE_REP: return (void *)k_enumerate<K, EVEN, MODE_REP>;
-        default: return (void *)k_enumerate<K, EVEN, MODE_SAMPLE>;
-    }
-}
-
-void *pick_enum(int K, bool even, int mode) {
-    if (K == 2) return even ? enum_fn<2, true>(mode) : enum_fn<2, false>(mode);
-    if (K == 4) return even ? enum_fn<4, true>(mode) : enum_fn<4, false>(mode);
-    return even ? enum_fn<6, true>(mode) : enum_fn<6, false>(mode);
-}
-
-template <int K>
-void *build_fn(int mode) {
-    return mode == MODE_RAW ? (void *)k_tile_build_lanes<K, MODE_RAW>
-                            : (void *)k_tile_build_lanes<K, MODE_REP>;
-}
-
-
-template <int K>
-void *super_fn(int mode) {
-    return mode == MODE_RAW ? (void *)k_super_build<K, MODE_RAW> : (void *)k_super_build<K, MODE_REP>;
-}
-
-void *pick_super(int K, int mode) {
-    if (K == 2) return super_fn<2>(mode);
-    if (K == 4) return super_fn<4>(mode);
-    return super_fn<6>(mode);
-}
-
-void *pick_build(int K, int mode) {
-    if (K == 2) return build_fn<2>(mode);
-    if (K == 4) return build_fn<4>(mode);
-    return build_fn<6>(mode);
-}
-
-template <int K, bool EVEN>
-void *cls_fn(int mode) {
-    return mode == MODE_RAW ? (void *)k_tile_classify<K, EVEN, MODE_RAW>
-                            : (void *)k_tile_classify<K, EVEN, MODE_REP>;
-}
-
-void *pick_cls(int K, bool even, int mode) {
-    if (K == 2) return even ? cls_fn<2, true>(mode) : cls_fn<2, false>(mode);
-    if (K == 4) return even ? cls_fn<4, true>(mode) : cls_fn<4, false>(mode);
-    return even ? cls_fn<6, true>(mode) : cls_fn<6, false>(mode);
-}
-
-size_t build_smem(int K) { return (size_t)32 * K * K * 4 + sizeof(TileTables); }
-
-size_t cls_smem(int K) {
-    return (size_t)32 * K * K * 4 + TABLE_SMEM + sizeof(TileTables) + CLS_WARPS * sizeof(TileRec);
-}
-
-// Tiles per contraction chunk (records: 1 KiB each).  Deduplication works
-// within a chunk, and larger chunks find many more duplicates (C3: 1.6x at
-// 2^20 tiles, 2.4x at 2^23), so the default is 2^24 tiles (18 GB of records,
-// allocated on demand and only as large as the sweep needs, halved while it
-// would take more than a quarter of the free HBM).  TCG_CHUNK_LOG2 (14..24)
-// overrides.
-// indices per chunk (TCG_CHUNK_INDEX_LOG2, 32..35; default 2^35): larger chunks
-// deduplicate over a larger window (C3 at 2^9-index tiles: 158x at 2^32,
-// 244x at 2^33, 379x at 2^34); 2^35 is the whole C3 domain in one window.
-// At most chunk_tiles() = 2^25 tiles; 2^35 indices = 2^(30 - la) tiles keeps
-// level-1 slice entries (tile < 2^(31 - la)) and level-2 positions
-// (tile << la < 2^30) in 32 bits.
-static uint64_t chunk_index_limit() {
-    static const uint64_t c = [] {
-        int lg = 35;
-        if (const char *e = std::getenv("TCG_CHUNK_INDEX_LOG2")) lg = std::max(32, std::min(35, std::atoi(e)));
-        return 1ull << lg;
-    }();
-    return c;
-}
-
-static uint32_t chunk_tiles() {
-    static const uint32_t c = [] {
-        int lg = 25;
-        if (const char *e = std::getenv("TCG_CHUNK_LOG2")) lg = std::max(14, std::min(25, std::atoi(e)));
-        return 1u << lg;
-    }();
-    return c;
-}
-
-static uint32_t next_pow2(uint32_t x) {
-    uint32_t p = 1;
-    while (p < x) p <<= 1;
-    return p;
-}
-
-void *pick_batch(int K, bool even) {
-    if (K == 2) return even ? (void *)k_batch<2, true> : (void *)k_batch<2, false>;
-    if (K == 4) return even ? (void *)k_batch<4, true> : (void *)k_batch<4, false>;
-    return even ? (void *)k_batch<6, true> : (void *)k_batch<6, false>;
-}
-
-size_t adj_bytes(int K) { return (size_t)32 * K * K * sizeof(uint32_t); }
-
-size_t enum_smem(int K) { return adj_bytes(K) + TABLE_SMEM; }
-
-// Vertex layout.  H = 16K bits per half.  P-half (points p > -p
-// lexicographically, i.e. i > 0 or (i == 0 and j > 0)):
-//   bits [0, npts-1)      : first-quadrant points except the origin, in
-//                           A(d) index order (bit = index - 1), so their
-//                           signs are sigma >> 1;
-//   bits [npts-1, d^2+d)  : mirrored quadrant (i > 0, j < 0), in A(d) order
-//                           of (i, |j|); signs = compressed sigma ^ (j odd);
-//   bit d^2+d             : the origin.
-// N-half: bit H + b holds the antipode of P-half bit b, whose sign is the
-// P-half sign ^ ((|i|+|j|) & 1).  The antipodal map is therefore a swap of
-// the two halves.
-struct Layout {
-    int d, K, H, npts;
-    std::vector<int> pos;  // lex vertex -> bit position
-};
-
-int point_index(int d, int i, int j) { return i * (d + 1) - i * (i - 1) / 2 + j; }
-
-int build_layout(const tcg_desc *D, Layout &L) {
-    const int d = D->degree;
-    L.d = d;
-    L.npts = (d + 1) * (d + 2) / 2;
-    const int half = d * d + d + 1;  // P-half incl. the origin
-    L.K = half <= 32 ? 2 : (half <= 64 ? 4 : 6);
-    L.H = 16 * L.K;
-    // q4 rank of (i, j), i > 0, j > 0
-    std::vector<int> q4rank(L.npts, -1);
-    int r = 0;
-    for (int i = 1; i <= d; ++i)
-        for (int j = 1; j <= d - i; ++j) q4rank[point_index(d, i, j)] = r++;
-    // lexicographic diamond points
-    std::vector<std::pair<int, int>> pts;
-    for (int i = -d; i <= d; ++i) {
-        const int a = d - std::abs(i);
-        for (int j = -a; j <= a; ++j) pts.emplace_back(i, j);
-    }
-    if ((int)pts.size() != D->nv) return fail(TCG_E_ARG, "nv does not match the degree");
-    auto ppos = [&](int i, int j) -> int {  // P-half position of a P-half point
-        if (j >= 0) return point_index(d, i, j) - 1;
-        return (L.npts - 1) + q4rank[point_index(d, i, -j)];
-    };
-    L.pos.assign(D->nv, -1);
-    for (int v = 0; v < D->nv; ++v) {
-        const int i = pts[v].first, j = pts[v].second;
-        if (i == 0 && j == 0) L.pos[v] = d * d + d;
-        else if (i > 0 || (i == 0 && j > 0)) L.pos[v] = ppos(i, j);
-        else L.pos[v] = L.H + ppos(-i, -j);
-    }
-    return TCG_OK;
-}
-
-
-// Free vertices of a tile (index bits 0..bits-1) and the fixed mask.
-bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, TileTables &T) {
-    const int d = D->degree;
-    const int npts = D->npts;
-    const int dom_bits = mode == MODE_RAW ? npts : npts - 3;
-    if (d < 5 || bits > TILE_BITS_MAX || dom_bits < bits + 2) return false;
-    std::memset(&T, 0, sizeof(T));
-    std::memset(T.vfree, 0xff, sizeof(T.vfree));
-    T.bits = bits;
-    T.maxnodes = 64;
-    if (const char *e = std::getenv("TCG_TILE_MAXNODES")) T.maxnodes = std::max(0, std::min(64, std::atoi(e)));
-    int sbit[TILE_BITS_MAX];
-    for (int i = 0; i < bits; ++i)
-        sbit[i] = mode == MODE_RAW ? i : (i < d - 1 ? i + 2 : i - (d - 1) + d + 2);
-    std::vector<int> fnode(D->nv, -1);
-    int nf = 0;
-    for (int v = 0; v < D->nv; ++v) {
-        if (!D->used[v]) continue;
-        int bit = -1;
-        for (int i = 0; i < bits; ++i)
-            if (sbit[i] == D->src[v]) bit = i;
-        const int pos = L.pos[v];
-        if (bit < 0) {
-            T.fixed[pos >> 5] |= 1u << (pos & 31);
-            ++T.nfixed;
-            continue;
-        }
-        if (nf >= MAXF) return false;
-        fnode[v] = nf;
-        T.fword[nf] = (uint32_t)(pos >> 5);
-        T.fbit[nf] = 1u << (pos & 31);
-        T.freem[pos >> 5] |= 1u << (pos & 31);
-        T.vfree[pos] = (int8_t)nf;
-        T.fpar |= (unsigned long long)(D->par[v] & 1) << nf;
-        T.fcopy[bit] |= 1ull << nf;
-        ++nf;
-    }
-    T.nf = nf;
-    for (int h = 0; h < 2; ++h)
-        for (int x = 0; x < 64; ++x) {
-            unsigned long long w = h == 0 ? T.fpar : 0ull;
-            for (int i = 0; i < 6; ++i)
-                if (((x >> i) & 1) && 6 * h + i < bits) w ^= T.fcopy[6 * h + i];
-            T.fsign[h][x] = w;
-        }
-    for (int e = 0; e < D->ne; ++e) {
-        const int fu = fnode[D->edge_u[e]], fv = fnode[D->edge_v[e]];
-        if (fu >= 0 && fv >= 0) {
-            T.fadj[fu] |= 1ull << fv;
-            T.fadj[fv] |= 1ull << fu;
-        }
-    }
-    // level-2 tables (filled after fadj / fpl below)
-    auto l2_tables = [&]() {
-        T.l2 = 0;
-        if (bits < 6 || bits > 12 || nf > 32) return;
-        T.l2even = d % 2 == 0;
-        uint32_t fb = 0, fa = 0;
-        for (int i = 0; i < bits; ++i) (i < 5 ? fb : fa) |= (uint32_t)T.fcopy[i];
-        const int nB = __builtin_popcount(fb);
-        if (nB > 10 || nB == 0) return;
-        T.fbm = fb;
-        T.fa = fa;
-        T.nB = nB;
-        T.la = bits - 5;
-        T.NA = 1 << T.la;
-        int j = 0;
-        int fj[32];
-        for (int f = 0; f < MAXF; ++f) T.l2j[f] = -1;
-        for (int f = 0; f < nf; ++f)
-            if ((fb >> f) & 1u) {
-                T.l2j[f] = (int8_t)j;
-                fj[j++] = f;
-            }
-        auto comp = [&](unsigned long long x) {
-            uint32_t r = 0;
-            for (int f = 0; f < nf; ++f)
-                if (((x >> f) & 1ull) && T.l2j[f] >= 0) r |= 1u << T.l2j[f];
-            return r;
-        };
-        for (int q = 0; q < nB; ++q) {
-            T.l2adjB[q] = comp(T.fadj[fj[q]] & fb);
-            T.l2linkB[q] = comp(T.fpl[fj[q]] & fb);
-        }
-        for (int b = 0; b < 32; ++b) T.l2bsign[b] = comp(T.fsign[0][b] & fb);
-        T.l2shift = -1;
-        if (fb >> __builtin_ctz(fb) == (1u << nB) - 1u) T.l2shift = __builtin_ctz(fb);
-        T.l2 = 1;
-        // two-stage tables
-        T.ts = 0;
-        // A1 = the fewest low A bits (>= 2) that leave an F space of <= 21 nodes
-        int la1 = 2;
-        uint32_t fa1 = 0, fa2 = 0;
-        int nA2 = 0;
-        for (; la1 <= T.la - 1; ++la1) {
-            fa1 = fa2 = 0;
-            for (int i = 5; i < bits; ++i) (i < 5 + la1 ? fa1 : fa2) |= (uint32_t)T.fcopy[i];
-            nA2 = __builtin_popcount(fa2);
-            if (nA2 <= 16 && nB + nA2 <= 21) break;
-        }
-        if (!T.l2even && T.la >= 4 && la1 <= 4 && la1 < T.la && nA2 > 0 && nA2 <= 16 &&
-            nB + nA2 <= 21) {
-            T.la1 = la1;
-            T.la2 = T.la - la1;
-            T.l15max = L15_MAXM;
-            if (const char *e = std::getenv("TCG_L15_MAXM"))
-                T.l15max = std::max(1, std::min(L15_MAXM, std::atoi(e)));
-            T.fa1 = fa1;
-            T.fa2 = fa2;
-            T.nA2 = nA2;
-            int a2j[MAXF], a2f[16], k = 0;
-            for (int f = 0; f < MAXF; ++f) { T.l15F[f] = -1; a2j[f] = -1; }
-            for (int f = 0; f < nf; ++f) {
-                if (T.l2j[f] >= 0) T.l15F[f] = T.l2j[f];
-                if ((fa2 >> f) & 1u) {
-                    a2j[f] = k;
-                    a2f[k] = f;
-                    T.l15F[f] = (int8_t)(nB + k);
-                    ++k;
-                }
-            }
-            auto compA2 = [&](unsigned long long x) {
-                uint32_t r = 0;
-                for (int f = 0; f < nf; ++f)
-                    if (((x >> f) & 1ull) && a2j[f] >= 0) r |= 1u << a2j[f];
-                return r;
-            };
-            for (int q = 0; q < nA2; ++q) {
-                const int f = a2f[q];
-                T.a2adjA2[q] = compA2(T.fadj[f] & fa2);
-                T.a2linkA2[q] = compA2(T.fpl[f] & fa2);
-                T.a2adjB[q] = comp(T.fadj[f] & fb);
-                T.a2linkB[q] = comp(T.fpl[f] & fb);
-            }
-            for (int x = 0; x < (1 << T.la2); ++x) {  // tile-local index of the A2 bits
-                const uint32_t low = (uint32_t)x << (5 + la1);
-                T.a2sign[x] = compA2((T.fsign[0][low & 63u] ^ T.fsign[1][(low >> 6) & 63u]) & fa2);
-            }
-            T.ts = 1;
-        }
-    };
-    for (int a = 0; a < D->nap; ++a) {
-        const int fu = fnode[D->ap_u[a]], fv = fnode[D->ap_v[a]];
-        if ((fu >= 0) != (fv >= 0)) return false;  // cannot happen: p and -p share src
-        if (fu >= 0) {
-            T.fpl[fu] |= 1ull << fv;
-            T.fpl[fv] |= 1ull << fu;
-        }
-    }
-    l2_tables();
-    // super-tiles: mid points = index bits bits .. bits+sh-1; the largest sh <= 6
-    // (TCG_SUPER_BITS) whose mid vertices fit MAXM
-    T.sh = 0;
-    int hmax = SUPER_BITS_MAX;
-    if (const char *e = std::getenv("TCG_SUPER_BITS")) hmax = std::atoi(e);
-    if (const char *e = std::getenv("TCG_BUILD_GENERIC"))
-        if (e[0] && e[0] != '0') hmax = 0;
-    for (int h = std::max(0, std::min(hmax, SUPER_BITS_MAX)); h > 0 && T.sh == 0; --h) {
-        if (dom_bits >= bits + h + 1) {
-            auto point_of = [&](int ib) {  // index bit -> lattice point
-                return mode == MODE_RAW ? ib : (ib < d - 1 ? ib + 2 : ib - (d - 1) + d + 2);
-            };
-            std::vector<std::pair<int, int>> mids;  // (layout position, vertex)
-            std::vector<int> mbit(D->nv, -1);
-            for (int v = 0; v < D->nv; ++v) {
-                if (!D->used[v] || fnode[v] >= 0) continue;
-                for (int i = 0; i < h; ++i)
-                    if (point_of(bits + i) == D->src[v]) mbit[v] = i;
-                if (mbit[v] >= 0) mids.push_back({L.pos[v], v});
-            }
-            std::sort(mids.begin(), mids.end());
-            if ((int)mids.size() <= MAXM && !mids.empty()) {
-                T.sh = h;
-                T.nm = (int)mids.size();
-                for (int k = 0; k < MAXK; ++k) T.sfixed[k] = T.fixed[k];
-                for (int j = 0; j < T.nm; ++j) {
-                    const int pos = mids[j].first, v = mids[j].second;
-                    T.mpos[j] = (uint16_t)pos;
-                    T.sfixed[pos >> 5] &= ~(1u << (pos & 31));
-                    for (int x = 0; x < (1 << h); ++x)
-                        T.msign[x] |= (uint32_t)(((x >> mbit[v]) & 1) ^ (D->par[v] & 1)) << j;
-                }
-                T.nsfixed = T.nfixed - T.nm;
-            }
-        }
-    }
-    return T.nfixed > 0 && nf > 0;
-}
-
-// Tile size: 2^bits indices.  Larger tiles amortise the contraction but add
-// free vertices (lane work); since contraction runs one tile per lane it is
-// cheap, so the default picks the largest tile whose contracted graph
-// (free vertices + the fixed part's components) usually fits one 32-bit
-// word: at most 16 free vertices (d=7 raw: 2^8 indices, the j-axis).
-// Degree 8-9 graphs exceed 32 nodes anyway, so they take 2^10.
-// TCG_TILE_BITS overrides.
-// Odd degrees up to 7 run the two-stage level 2 (which also takes 33..64-node
-// tiles), so they allow 29 free vertices: d=7 raw tiles are 2^12 indices
-// (measured on C3: 7.48e11 patchworks/s vs 7.11e11 at 2^11, 5.07e11 at 2^10,
-// 3.49e11 at 2^9; with the direct level 2, 2^9 had been best).
-bool build_tiles(const tcg_desc *D, const Layout &L, int mode, TileTables &T) {
-    int want = D->degree >= 8 ? 10 : 12;
-    int fmax = D->degree >= 8 ? 28 : (D->degree % 2 ? 29 : 16);
-    if (const char *e = std::getenv("TCG_TILE_BITS")) {
-        want = std::atoi(e);
-        fmax = MAXF;
-    }
-    for (int bits = std::min(want, TILE_BITS_MAX); bits >= 6; --bits)
-        if (build_tiles_bits(D, L, mode, bits, T) && T.nf <= fmax) return true;
-    return false;
-}
-
-// Host-side plan: layout, masks, adjacency rows and edge list of one
-// triangulation, validated against the reference's sign-extension tables.
-struct HostPlan {
-    int d = 0, K = 0, even = 0, nused = 0;
-    KParams kp{};
-    Layout L;
-    std::vector<uint32_t> adj, edges;
-};
-
-int build_host_plan(const tcg_desc *D, HostPlan &HP) {
-    if (!D) return fail(TCG_E_ARG, "null descriptor");
-    const int d = D->degree;
-    if (d < 1) return fail(TCG_E_ARG, "degree must be >= 1");
-    if (d > 9)
-        return fail(TCG_E_UNSUPPORTED,
-                    "degree > 9 exceeds the 64-bit sign word / 96-bit half-mask layout");
-    if (D->nv != 2 * d * d + 2 * d + 1) return fail(TCG_E_ARG, "nv != 2d^2+2d+1");
-    if (D->npts != (d + 1) * (d + 2) / 2) return fail(TCG_E_ARG, "npts mismatch");
-    if (D->maxreg < 1 || D->maxreg > MAXR) return fail(TCG_E_UNSUPPORTED, "maxreg out of range");
-    if (D->ne < 1) return fail(TCG_E_ARG, "empty edge list");
-    Layout &L = HP.L;
-    int rc = build_layout(D, L);
-    if (rc) return rc;
-    const int K = L.K, H = L.H;
-    HP.d = d;
-    HP.K = K;
-    HP.even = (d % 2 == 0);
-    KParams &kp = HP.kp;
-    kp = KParams{};
-    kp.d = d;
-    kp.npts = D->npts;
-    kp.maxreg = D->maxreg;
-    kp.center = d * d + d;
-    kp.ne = D->ne;
-    std::vector<std::pair<int, int>> pts;
-    for (int i = -d; i <= d; ++i) {
-        const int a = d - std::abs(i);
-        for (int j = -a; j <= a; ++j) pts.emplace_back(i, j);
-    }
-    auto setbit = [&](uint32_t *m, int pos) { m[pos >> 5] |= 1u << (pos & 31); };
-    int nused = 0;
-    for (int v = 0; v < D->nv; ++v)
-        if (D->used[v]) {
-            setbit(kp.used, L.pos[v]);
-            ++nused;
-        }
-    kp.nused = nused;
-    HP.nused = nused;
-    for (int a = 0; a < D->nap; ++a) {
-        const int u = D->ap_u[a], v = D->ap_v[a];
-        if (u < 0 || u >= D->nv || v < 0 || v >= D->nv)
-            return fail(TCG_E_ARG, "antipodal pair out of range");
-        const int pu = L.pos[u], pv = L.pos[v];
-        if (std::abs(pu - pv) != H) return fail(TCG_E_ARG, "antipodal pair is not (p, -p)");
-        if (std::abs(pts[u].first) + std::abs(pts[u].second) != d)
-            return fail(TCG_E_ARG, "antipodal pair off the diamond boundary");
-        setbit(kp.bd, pu);
-        setbit(kp.bd, pv);
-    }
-    // sign-extension tables -> P-half masks; verify they are the reference's
-    for (int v = 0; v < D->nv; ++v) {
-        const int i = pts[v].first, j = pts[v].second;
-        const int want_src = point_index(d, std::abs(i), std::abs(j));
-        const int want_par = ((i < 0 ? -i : 0) + (j < 0 ? -j : 0)) & 1;
-        if (D->src[v] != want_src || D->par[v] != want_par)
-            return fail(TCG_E_ARG, "src/par tables differ from the reflected sign extension");
-        const int pos = L.pos[v];
-        if (pos < H && !(i == 0 && j == 0)) {
-            if (((std::abs(i) + std::abs(j)) & 1) != 0) kp.parP[pos >> 5] |= 1u << (pos & 31);
-            if (j < 0 && ((-j) & 1)) kp.jodd[pos >> 5] |= 1u << (pos & 31);
-        }
-    }
-    // mirrored-quadrant compress runs: row i contributes (i,1..d-i)
-    {
-        int nq = 0, dst = 0;
-        for (int i = 1; i <= d - 1; ++i) {
-            kp.q4src[nq] = (uint8_t)point_index(d, i, 1);
-            kp.q4len[nq] = (uint8_t)(d - i);
-            kp.q4dst[nq] = (uint8_t)dst;
-            dst += d - i;
-            ++nq;
-        }
-        kp.nq4 = nq;
-    }
-    // adjacency rows and edge list in layout positions
-    HP.adj.assign((size_t)2 * H * K, 0u);
-    HP.edges.assign(D->ne, 0u);
-    for (int e = 0; e < D->ne; ++e) {
-        const int u = D->edge_u[e], v = D->edge_v[e];
-        if (u < 0 || u >= D->nv || v < 0 || v >= D->nv || u == v)
-            return fail(TCG_E_ARG, "edge endpoint out of range");
-        const int pu = L.pos[u], pv = L.pos[v];
-        HP.adj[(size_t)pu * K + (pv >> 5)] |= 1u << (pv & 31);
-        HP.adj[(size_t)pv * K + (pu >> 5)] |= 1u << (pu & 31);
-        HP.edges[e] = (uint32_t)pu | ((uint32_t)pv << 16);
-    }
-    return TCG_OK;
-}
+#include "host_plan.cuh"
 
 #include "split_design.cuh"
 
@@ -5056,472 +1624,8 @@ int tcg_sample_multi(tcg_plan **plans, int nplans, uint64_t seed, uint64_t k0, u
 }
 
 
-// ------------------------------------------------------------ many triangulations
-struct tcg_multi {
-    int device = 0, d = 0, K = 0, even = 0, ntri = 0;
-    KParams *d_kp = nullptr;
-    uint32_t *d_adj = nullptr, *d_edges = nullptr;
-    size_t smem = 0;
-    cudaStream_t stream = nullptr;
-    int64_t cap = 0;
-    uint64_t *d_sig = nullptr, *d_key = nullptr;
-    uint8_t *d_ov = nullptr, *d_nr = nullptr;
-    int32_t *d_st = nullptr;
-    int4 *d_items = nullptr;
-    int64_t items_cap = 0;
-    float last_ms = 0.f;
-    int64_t launches = 0;
-    // host-buffer pipeline: two slots of pinned staging, one stream each
-    cudaStream_t sst[2] = {nullptr, nullptr};
-    cudaEvent_t ev[2][2] = {};       // kernel start / stop per slot
-    uint8_t *h_stage[2] = {nullptr, nullptr};  // [MULTI_CHUNK] sig | key | st | ov | nr
-};
+#include "api_multi.cuh"
 
-// pairs per pipeline chunk (TCG_MULTI_CHUNK_LOG2, 18..26)
-static int64_t multi_chunk() {
-    static const int64_t c = [] {
-        const char *e = std::getenv("TCG_MULTI_CHUNK_LOG2");
-        return (int64_t)1 << (e ? std::max(18, std::min(26, std::atoi(e))) : 23);
-    }();
-    return c;
-}
-
-// Host copies of the pipeline split over a few threads (one memcpy stream is
-// ~10 GB/s; the box has >= 16 cores).
-static void par_for(int64_t n, const std::function<void(int64_t, int64_t)> &fn) {
-    static const int nth = [] {
-        const char *e = std::getenv("TCG_HOST_THREADS");
-        const int hw = (int)std::thread::hardware_concurrency();
-        return e ? std::max(1, std::atoi(e)) : std::max(1, std::min(8, hw / 2));
-    }();
-    const int t = (int)std::min<int64_t>(nth, std::max<int64_t>(1, n >> 16));
-    if (t <= 1) {
-        fn(0, n);
-        return;
-    }
-    std::vector<std::thread> th;
-    for (int i = 1; i < t; ++i) th.emplace_back(fn, n * i / t, n * (i + 1) / t);
-    fn(0, n / t);
-    for (auto &x : th) x.join();
-}
-
-static void *pick_multi(int K, bool even) {
-    if (K == 2) return even ? (void *)k_multi<2, true> : (void *)k_multi<2, false>;
-    if (K == 4) return even ? (void *)k_multi<4, true> : (void *)k_multi<4, false>;
-    return even ? (void *)k_multi<6, true> : (void *)k_multi<6, false>;
-}
-
-int tcg_multi_destroy(tcg_multi *M) {
-    if (!M) return TCG_OK;
-    DeviceGuard guard(M->device);
-    if (M->stream) cudaStreamSynchronize(M->stream);
-    void *ptrs[] = {M->d_kp, M->d_adj, M->d_edges, M->d_sig, M->d_key, M->d_ov, M->d_nr,
-                    M->d_st, M->d_items};
-    for (void *q : ptrs)
-        if (q) cudaFree(q);
-    for (int i = 0; i < 2; ++i) {
-        if (M->sst[i]) {
-            cudaStreamSynchronize(M->sst[i]);
-            cudaStreamDestroy(M->sst[i]);
-        }
-        for (int j = 0; j < 2; ++j)
-            if (M->ev[i][j]) cudaEventDestroy(M->ev[i][j]);
-        if (M->h_stage[i]) cudaFreeHost(M->h_stage[i]);
-    }
-    if (M->stream) cudaStreamDestroy(M->stream);
-    delete M;
-    return TCG_OK;
-}
-
-int tcg_multi_create(const tcg_desc *descs, int32_t ntri, int device, tcg_multi **out) {
-    if (!descs || !out || ntri < 1) return fail(TCG_E_ARG, "bad arguments");
-    *out = nullptr;
-    std::vector<HostPlan> hps(ntri);
-    for (int t = 0; t < ntri; ++t) {
-        int rc = build_host_plan(descs + t, hps[t]);
-        if (rc) return rc;
-        if (hps[t].d != hps[0].d) return fail(TCG_E_ARG, "all triangulations must share one degree");
-    }
-    const int K = hps[0].K;
-    const size_t arow = (size_t)32 * K * K;
-    size_t ne_tot = 0;
-    for (auto &h : hps) ne_tot += h.edges.size();
-    if (device < 0 && cudaGetDevice(&device) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(TCG_E_CUDA, "no CUDA device");
-    }
-    tcg_multi *M = new tcg_multi();
-    M->device = device;
-    M->d = hps[0].d;
-    M->K = K;
-    M->even = hps[0].even;
-    M->ntri = ntri;
-    DeviceGuard guard(device);
-    auto bail = [&](cudaError_t e, const char *what) {
-        std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
-        tcg_multi_destroy(M);
-        return fail(TCG_E_CUDA, msg);
-    };
-    cudaError_t e;
-    cudaDeviceProp prop;
-    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return bail(e, "props");
-    if (prop.major < 10) {
-        tcg_multi_destroy(M);
-        return fail(TCG_E_UNSUPPORTED, "libtcg is built for sm_100a (Blackwell B200)");
-    }
-    if ((e = cudaStreamCreateWithFlags(&M->stream, cudaStreamNonBlocking)) != cudaSuccess)
-        return bail(e, "stream");
-    if ((e = cudaMalloc(&M->d_kp, sizeof(KParams) * ntri)) != cudaSuccess) return bail(e, "malloc");
-    if ((e = cudaMalloc(&M->d_adj, 4 * arow * ntri)) != cudaSuccess) return bail(e, "malloc");
-    if ((e = cudaMalloc(&M->d_edges, 4 * std::max<size_t>(1, ne_tot))) != cudaSuccess)
-        return bail(e, "malloc");
-    std::vector<KParams> kps(ntri);
-    std::vector<uint32_t> adj(arow * ntri), edges(std::max<size_t>(1, ne_tot));
-    size_t eo = 0;
-    for (int t = 0; t < ntri; ++t) {
-        kps[t] = hps[t].kp;
-        kps[t].adj = M->d_adj + arow * t;
-        kps[t].edges = M->d_edges + eo;
-        std::copy(hps[t].adj.begin(), hps[t].adj.end(), adj.begin() + arow * t);
-        std::copy(hps[t].edges.begin(), hps[t].edges.end(), edges.begin() + eo);
-        eo += hps[t].edges.size();
-    }
-    cudaMemcpy(M->d_kp, kps.data(), sizeof(KParams) * ntri, cudaMemcpyHostToDevice);
-    cudaMemcpy(M->d_adj, adj.data(), 4 * adj.size(), cudaMemcpyHostToDevice);
-    if ((e = cudaMemcpy(M->d_edges, edges.data(), 4 * edges.size(), cudaMemcpyHostToDevice)) !=
-        cudaSuccess)
-        return bail(e, "upload");
-    M->smem = 4 * arow;
-    *out = M;
-    return TCG_OK;
-}
-
-int tcg_multi_classify(tcg_multi *M, const int32_t *tri, const uint64_t *sig, int64_t n,
-                       uint64_t *key, uint8_t *ov, uint8_t *nr, int32_t *st) {
-    if (!M || (n > 0 && (!tri || !sig || !key || !ov || !nr || !st)))
-        return fail(TCG_E_ARG, "null argument");
-    if (n <= 0) return TCG_OK;
-    if (n > INT32_MAX) return fail(TCG_E_RANGE, "at most 2^31-1 pairs per call");
-    DeviceGuard guard(M->device);
-    // pairs grouped by triangulation (a counting sort unless the caller's
-    // triangulation ids are already non-decreasing, e.g. config C4's layout);
-    // work items of <= 2048 pairs of one triangulation
-    constexpr int ITEM = 2048;
-    host_mark("multi start");
-    std::vector<int64_t> cnt(M->ntri + 1, 0);
-    {  // validate, count and test the order in parallel slices
-        std::mutex mu;
-        std::atomic<bool> bad{false}, unordered{false};
-        par_for(n, [&](int64_t lo, int64_t hi) {
-            std::vector<int64_t> c(M->ntri + 1, 0);
-            bool ord = lo == 0 || (tri[lo] >= tri[lo - 1]);
-            for (int64_t i = lo; i < hi; ++i) {
-                const int32_t t = tri[i];
-                if (t < 0 || t >= M->ntri) {
-                    bad = true;
-                    return;
-                }
-                c[t + 1]++;
-                ord &= i == lo || t >= tri[i - 1];
-            }
-            if (!ord) unordered = true;
-            std::lock_guard<std::mutex> g(mu);
-            for (int t = 0; t <= M->ntri; ++t) cnt[t] += c[t];
-        });
-        if (bad) return fail(TCG_E_ARG, "triangulation index out of range");
-        if (unordered) cnt[0] = -1;  // marker
-    }
-    const bool grouped = cnt[0] == 0;
-    cnt[0] = 0;
-    for (int t = 0; t < M->ntri; ++t) cnt[t + 1] += cnt[t];
-    std::vector<int64_t> order;
-    std::vector<uint64_t> ssig;
-    if (!grouped) {
-        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
-        order.resize(n);
-        ssig.resize(n);
-        for (int64_t i = 0; i < n; ++i) {
-            const int64_t j = pos[tri[i]]++;
-            order[j] = i;
-            ssig[j] = sig[i];
-        }
-    }
-    const uint64_t *gsig = grouped ? sig : ssig.data();
-    std::vector<int4> items;
-    for (int t = 0; t < M->ntri; ++t)
-        for (int64_t a = cnt[t]; a < cnt[t + 1]; a += ITEM)
-            items.push_back(make_int4(t, (int)a, (int)std::min<int64_t>(ITEM, cnt[t + 1] - a), 0));
-    host_mark("multi grouped");
-    if (n > M->cap) {
-        void *ptrs[] = {M->d_sig, M->d_key, M->d_ov, M->d_nr, M->d_st};
-        for (void *q : ptrs)
-            if (q) cudaFree(q);
-        M->cap = 0;
-        const int64_t cap = std::max<int64_t>(n, 1 << 16);
-        CUDA_TRY(cudaMalloc(&M->d_sig, cap * 8));
-        CUDA_TRY(cudaMalloc(&M->d_key, cap * 8));
-        CUDA_TRY(cudaMalloc(&M->d_ov, cap));
-        CUDA_TRY(cudaMalloc(&M->d_nr, cap));
-        CUDA_TRY(cudaMalloc(&M->d_st, cap * 4));
-        M->cap = cap;
-    }
-    if ((int64_t)items.size() > M->items_cap) {
-        if (M->d_items) cudaFree(M->d_items);
-        M->d_items = nullptr;
-        M->items_cap = 0;
-        CUDA_TRY(cudaMalloc(&M->d_items, sizeof(int4) * items.size()));
-        M->items_cap = (int64_t)items.size();
-    }
-    for (int i = 0; i < 2; ++i) {
-        if (!M->sst[i]) CUDA_TRY(cudaStreamCreateWithFlags(&M->sst[i], cudaStreamNonBlocking));
-        for (int j = 0; j < 2; ++j)
-            if (!M->ev[i][j]) CUDA_TRY(cudaEventCreate(&M->ev[i][j]));
-        if (!M->h_stage[i])
-            CUDA_TRY(cudaHostAlloc((void **)&M->h_stage[i], (size_t)multi_chunk() * 22, cudaHostAllocDefault));
-    }
-    CUDA_TRY(cudaMemcpy(M->d_items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
-    void *fn = pick_multi(M->K, M->even);
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)M->smem);
-    // Pipeline over chunks of whole items (<= MULTI_CHUNK pairs): slot c & 1
-    // stages chunk c's signs into pinned memory (host threads), copies them up,
-    // classifies, copies the results down on its stream; chunk c-2's results
-    // leave the slot (host threads, scattered back if the input was regrouped)
-    // before it is reused, so host copies, PCIe both ways and the kernel overlap.
-    const int64_t MULTI_CHUNK = multi_chunk();
-    struct Chunk { int64_t ib, ie, p0, p1; };
-    std::vector<Chunk> chunks;
-    for (int64_t ib = 0; ib < (int64_t)items.size();) {
-        int64_t ie = ib, p0 = items[ib].y, p1 = p0;
-        while (ie < (int64_t)items.size() && items[ie].y + items[ie].z - p0 <= MULTI_CHUNK) {
-            p1 = items[ie].y + items[ie].z;
-            ++ie;
-        }
-        chunks.push_back({ib, ie, p0, p1});
-        ib = ie;
-    }
-    struct Stage {
-        uint64_t *sig, *key;
-        int32_t *st;
-        uint8_t *ov, *nr;
-    };
-    auto stage = [&](int sl) {
-        uint8_t *h = M->h_stage[sl];
-        return Stage{reinterpret_cast<uint64_t *>(h), reinterpret_cast<uint64_t *>(h + 8 * MULTI_CHUNK),
-                     reinterpret_cast<int32_t *>(h + 16 * MULTI_CHUNK), h + 20 * MULTI_CHUNK,
-                     h + 21 * MULTI_CHUNK};
-    };
-    float kms = 0.f;
-    auto drain = [&](size_t c) -> int {
-        const int sl = (int)(c & 1);
-        const Chunk &C = chunks[c];
-        CUDA_TRY(cudaStreamSynchronize(M->sst[sl]));
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, M->ev[sl][0], M->ev[sl][1]);
-        kms += ms;
-        const Stage S = stage(sl);
-        const uint64_t *hk = S.key;
-        const int32_t *hst = S.st;
-        const uint8_t *hov = S.ov, *hnr = S.nr;
-        const int64_t len = C.p1 - C.p0;
-        par_for(len, [&](int64_t lo, int64_t hi) {
-            if (grouped) {
-                std::memcpy(key + C.p0 + lo, hk + lo, (hi - lo) * 8);
-                std::memcpy(st + C.p0 + lo, hst + lo, (hi - lo) * 4);
-                std::memcpy(ov + C.p0 + lo, hov + lo, hi - lo);
-                std::memcpy(nr + C.p0 + lo, hnr + lo, hi - lo);
-            } else {
-                for (int64_t j = lo; j < hi; ++j) {
-                    const int64_t i = order[C.p0 + j];
-                    key[i] = hk[j];
-                    st[i] = hst[j];
-                    ov[i] = hov[j];
-                    nr[i] = hnr[j];
-                }
-            }
-        });
-        return TCG_OK;
-    };
-    for (size_t c = 0; c < chunks.size() + 2; ++c) {
-        if (c >= 2) {
-            int rc = drain(c - 2);
-            if (rc) return rc;
-        }
-        if (c >= chunks.size()) continue;
-        const int sl = (int)(c & 1);
-        const Chunk &C = chunks[c];
-        const int64_t len = C.p1 - C.p0;
-        cudaStream_t s = M->sst[sl];
-        const Stage S = stage(sl);
-        uint64_t *hs = S.sig, *hk = S.key;
-        int32_t *hst = S.st;
-        uint8_t *hov = S.ov, *hnr = S.nr;
-        par_for(len, [&](int64_t lo, int64_t hi) { std::memcpy(hs + lo, gsig + C.p0 + lo, (hi - lo) * 8); });
-        CUDA_TRY(cudaMemcpyAsync(M->d_sig + C.p0, hs, len * 8, cudaMemcpyHostToDevice, s));
-        const int4 *it = M->d_items + C.ib;
-        void *args[] = {&M->d_kp, &it, &M->d_sig, &M->d_key, &M->d_ov, &M->d_nr, &M->d_st};
-        cudaEventRecord(M->ev[sl][0], s);
-        CUDA_TRY(cudaLaunchKernel(fn, dim3((unsigned)(C.ie - C.ib)), dim3(THREADS), args, M->smem, s));
-        cudaEventRecord(M->ev[sl][1], s);
-        M->launches++;
-        CUDA_TRY(cudaMemcpyAsync(hk, M->d_key + C.p0, len * 8, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(hst, M->d_st + C.p0, len * 4, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(hov, M->d_ov + C.p0, len, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaMemcpyAsync(hnr, M->d_nr + C.p0, len, cudaMemcpyDeviceToHost, s));
-    }
-    host_mark("multi done");
-    M->last_ms = kms;
-    return TCG_OK;
-}
-
-double tcg_multi_last_ms(const tcg_multi *M) { return M ? (double)M->last_ms : -1.0; }
-
-
-// ------------------------------------------------------------ any degree (host)
-struct tcg_large {
-    int device = 0;
-    LargeParams lp{};
-    int32_t *d_i32 = nullptr;  // eu, ev, src, apu, apv
-    uint8_t *d_u8 = nullptr;   // par, used
-    size_t smem = 0;
-    cudaStream_t stream = nullptr;
-    int blocks = 0;
-    int64_t cap = 0;  // persistent batch buffers
-    uint64_t *d_sig = nullptr;
-    int32_t *d_st = nullptr, *d_nr = nullptr, *d_par = nullptr;
-};
-
-int tcg_large_destroy(tcg_large *G) {
-    if (!G) return TCG_OK;
-    DeviceGuard guard(G->device);
-    if (G->stream) cudaStreamSynchronize(G->stream);
-    if (G->d_i32) cudaFree(G->d_i32);
-    if (G->d_u8) cudaFree(G->d_u8);
-    void *bufs[] = {G->d_sig, G->d_st, G->d_nr, G->d_par};
-    for (void *q : bufs)
-        if (q) cudaFree(q);
-    if (G->stream) cudaStreamDestroy(G->stream);
-    delete G;
-    return TCG_OK;
-}
-
-int tcg_large_create(const tcg_desc *D, int device, tcg_large **out) {
-    if (!D || !out) return fail(TCG_E_ARG, "null argument");
-    *out = nullptr;
-    const int d = D->degree;
-    if (d < 1 || D->nv != 2 * d * d + 2 * d + 1 || D->npts != (d + 1) * (d + 2) / 2)
-        return fail(TCG_E_ARG, "descriptor sizes do not match the degree");
-    if (D->maxreg < 1 || D->maxreg >= 65535) return fail(TCG_E_UNSUPPORTED, "maxreg out of range");
-    if (D->ne < 1) return fail(TCG_E_ARG, "empty edge list");
-    for (int e = 0; e < D->ne; ++e)
-        if (D->edge_u[e] < 0 || D->edge_u[e] >= D->nv || D->edge_v[e] < 0 || D->edge_v[e] >= D->nv)
-            return fail(TCG_E_ARG, "edge endpoint out of range");
-    for (int v = 0; v < D->nv; ++v)
-        if (D->src[v] < 0 || D->src[v] >= D->npts) return fail(TCG_E_ARG, "src out of range");
-    for (int a = 0; a < D->nap; ++a)
-        if (D->ap_u[a] < 0 || D->ap_u[a] >= D->nv || D->ap_v[a] < 0 || D->ap_v[a] >= D->nv)
-            return fail(TCG_E_ARG, "antipodal pair out of range");
-    if (device < 0 && cudaGetDevice(&device) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(TCG_E_CUDA, "no CUDA device");
-    }
-    tcg_large *G = new tcg_large();
-    G->device = device;
-    DeviceGuard guard(device);
-    auto bail = [&](cudaError_t e, const char *what) {
-        std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
-        tcg_large_destroy(G);
-        return fail(TCG_E_CUDA, msg);
-    };
-    cudaError_t e;
-    cudaDeviceProp prop;
-    if ((e = cudaGetDeviceProperties(&prop, device)) != cudaSuccess) return bail(e, "props");
-    if (prop.major < 10) {
-        tcg_large_destroy(G);
-        return fail(TCG_E_UNSUPPORTED, "libtcg is built for sm_100a (Blackwell B200)");
-    }
-    if ((e = cudaStreamCreateWithFlags(&G->stream, cudaStreamNonBlocking)) != cudaSuccess)
-        return bail(e, "stream");
-    const size_t ni = 2 * (size_t)D->ne + D->nv + 2 * (size_t)D->nap;
-    std::vector<int32_t> i32(ni);
-    std::copy(D->edge_u, D->edge_u + D->ne, i32.begin());
-    std::copy(D->edge_v, D->edge_v + D->ne, i32.begin() + D->ne);
-    std::copy(D->src, D->src + D->nv, i32.begin() + 2 * D->ne);
-    std::copy(D->ap_u, D->ap_u + D->nap, i32.begin() + 2 * D->ne + D->nv);
-    std::copy(D->ap_v, D->ap_v + D->nap, i32.begin() + 2 * D->ne + D->nv + D->nap);
-    std::vector<uint8_t> u8(2 * (size_t)D->nv);
-    std::copy(D->par, D->par + D->nv, u8.begin());
-    std::copy(D->used, D->used + D->nv, u8.begin() + D->nv);
-    if ((e = cudaMalloc(&G->d_i32, 4 * ni)) != cudaSuccess) return bail(e, "malloc");
-    if ((e = cudaMalloc(&G->d_u8, u8.size())) != cudaSuccess) return bail(e, "malloc");
-    cudaMemcpy(G->d_i32, i32.data(), 4 * ni, cudaMemcpyHostToDevice);
-    if ((e = cudaMemcpy(G->d_u8, u8.data(), u8.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
-        return bail(e, "upload");
-    LargeParams &L = G->lp;
-    L.d = d;
-    L.nv = D->nv;
-    L.ne = D->ne;
-    L.nap = D->nap;
-    L.npts = D->npts;
-    L.maxreg = D->maxreg;
-    L.words = (D->npts + 63) / 64;
-    L.eu = G->d_i32;
-    L.ev = G->d_i32 + D->ne;
-    L.src = G->d_i32 + 2 * D->ne;
-    L.apu = G->d_i32 + 2 * D->ne + D->nv;
-    L.apv = L.apu + D->nap;
-    L.par = G->d_u8;
-    L.used = G->d_u8 + D->nv;
-    G->smem = 3 * 4 * (size_t)D->nv + 4 * (size_t)LHASH + 4 * (size_t)(5 * D->maxreg + 1) +
-              3 * (size_t)D->nv + 16;
-    if (G->smem > 200 * 1024) {
-        tcg_large_destroy(G);
-        return fail(TCG_E_UNSUPPORTED, "degree too large for one CTA's shared memory");
-    }
-    cudaFuncSetAttribute((void *)k_large, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)G->smem);
-    int bps = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, (void *)k_large, THREADS, G->smem);
-    G->blocks = std::max(1, bps) * prop.multiProcessorCount;
-    *out = G;
-    return TCG_OK;
-}
-
-int tcg_large_classify(tcg_large *G, const uint64_t *sigma_rows, int64_t n, int32_t *status,
-                       int32_t *nreg, int32_t *parent) {
-    if (!G || (n > 0 && (!sigma_rows || !status || !nreg || !parent)))
-        return fail(TCG_E_ARG, "null argument");
-    if (n <= 0) return TCG_OK;
-    DeviceGuard guard(G->device);
-    const LargeParams &L = G->lp;
-    if (n > G->cap) {
-        void *bufs[] = {G->d_sig, G->d_st, G->d_nr, G->d_par};
-        for (void *q : bufs)
-            if (q) cudaFree(q);
-        G->d_sig = nullptr;
-        G->d_st = G->d_nr = G->d_par = nullptr;
-        G->cap = 0;
-        const int64_t cap = std::max<int64_t>(n, 256);
-        CUDA_TRY(cudaMalloc(&G->d_sig, 8 * (size_t)cap * L.words));
-        CUDA_TRY(cudaMalloc(&G->d_st, 4 * (size_t)cap));
-        CUDA_TRY(cudaMalloc(&G->d_nr, 4 * (size_t)cap));
-        CUDA_TRY(cudaMalloc(&G->d_par, 4 * (size_t)cap * L.maxreg));
-        G->cap = cap;
-    }
-    uint64_t *d_sig = G->d_sig;
-    int32_t *d_st = G->d_st, *d_nr = G->d_nr, *d_par = G->d_par;
-    CUDA_TRY(cudaMemcpyAsync(d_sig, sigma_rows, 8 * (size_t)n * L.words, cudaMemcpyHostToDevice,
-                             G->stream));
-    const unsigned blocks = (unsigned)std::min<int64_t>(G->blocks, n);
-    LargeParams lp = L;
-    void *args[] = {&lp, &d_sig, &n, &d_st, &d_nr, &d_par};
-    CUDA_TRY(cudaLaunchKernel((void *)k_large, dim3(blocks), dim3(THREADS), args, G->smem,
-                              G->stream));
-    CUDA_TRY(cudaMemcpyAsync(status, d_st, 4 * (size_t)n, cudaMemcpyDeviceToHost, G->stream));
-    CUDA_TRY(cudaMemcpyAsync(nreg, d_nr, 4 * (size_t)n, cudaMemcpyDeviceToHost, G->stream));
-    CUDA_TRY(cudaMemcpyAsync(parent, d_par, 4 * (size_t)n * L.maxreg, cudaMemcpyDeviceToHost,
-                             G->stream));
-    CUDA_TRY(cudaStreamSynchronize(G->stream));
-    return TCG_OK;
-}
+#include "api_large.cuh"
 
 }  // extern "C"
