@@ -81,18 +81,19 @@ def source_sha16():
     return h.hexdigest()[:16]
 
 
-def ncu_profile():
-    """Per-kernel counters of one C3 step (N = 1) from the committed ncu
-    capture, if it was taken from this very source (profiles/ncu_kernels.json)."""
+def ncu_profile(name="ncu_kernels.json"):
+    """Per-kernel counters of one bench step (N = 1; ncu_kernels.json: C3,
+    ncu_kernels_c5.json: 2^26 bowtie8 draws) from the committed ncu capture,
+    if it was taken from this very source (profiles/<name>)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "ncu_kernels.json")) as f:
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             prof = json.load(f)
     except (OSError, ValueError):
-        return None, "profiles/ncu_kernels.json missing"
+        return None, f"profiles/{name} missing"
     if prof.get("tcg_cu_sha16") != source_sha16():
-        return None, (f"profiles/ncu_kernels.json is from CUDA sources {prof.get('tcg_cu_sha16')}, "
+        return None, (f"profiles/{name} is from CUDA sources {prof.get('tcg_cu_sha16')}, "
                       f"this build is {source_sha16()}: not used")
-    return prof, "profiles/ncu_kernels.json (same CUDA sources)"
+    return prof, f"profiles/{name} (same CUDA sources)"
 
 
 def peaks():
@@ -420,7 +421,27 @@ def bench_c5(dev, steps, warmup):
                    "sample": f"tcurves.sample({name}, 2^20, seed {seed}, workers={threads}), "
                              f"{sec:.1f} s"}
         kern_ms = (kt["sample_split"][0] + kt["sample_list"][0] if split else kt["enumerate"][0]) / steps
+        roof = None
+        if split and name == "bowtie8":  # the captured configuration
+            prof, psrc = ncu_profile("ncu_kernels_c5.json")
+            mhz, _, _ = peaks()
+            p_issue = c.native.info["sms"] * 128 * mhz * 1e6
+            roof = {"bound": "issue", "unit": "thread-inst/s", "peak": p_issue,
+                    "kernel": "k_sample_split", "source": psrc, "achieved": None, "frac": None}
+            kp = (prof or {}).get("kernels", {}).get("k_sample_split")
+            if kp:
+                draws = prof.get("draws", 1 << 26)
+                per_draw = kp["thread_inst_per_step"] / draws
+                split_ms = kt["sample_split"][0] / steps
+                roof["achieved"] = per_draw * n / (split_ms / 1e3)
+                roof["frac"] = roof["achieved"] / p_issue
+                roof["thread_inst_per_draw"] = per_draw
+                roof["dram_bytes_per_draw"] = kp["dram_bytes_per_step"] / draws
+                roof["ncu"] = {k: v for k, v in kp.items()
+                               if k in ("issue_active_pct", "alu_pipe_pct", "threads_per_inst",
+                                        "local_sectors_per_step", "registers", "warps_active_pct")}
         out[f"c5_{name}"] = {
+            "roofline": roof,
             "metric": "draws classified/sec (degree-8 uniform sampling, one B200)",
             "value": n / (ms / 1e3), "unit": "draws/s", "ms_per_step": ms,
             "e2e": {"value": e2e, "unit": "draws/s", "h2d_bytes_per_step": 32,
@@ -740,6 +761,10 @@ def run_ours(args, rank, world, local_rank):
                 gbps = byts / (kms / 1e3) / 1e9
                 hbm[kind] = {"dram_bytes_per_step": byts, "GBps": round(gbps, 1),
                              "frac_of_hbm": round(gbps / hbm_peak, 3)}
+        roof["issue_per_kind"] = {
+            kind: round(sum(kp[n]["thread_inst_per_step"] for n in KIND_KERNELS.get(kind, [])
+                            if n in kp) / (kms / 1e3) / p_issue, 3)
+            for kind, kms in kms_step.items() if kms > 0}
         roof["hbm"] = {"peak_GBps": hbm_peak, "per_kind": hbm,
                        "dram_bytes_per_step": step_bytes,
                        "bytes_per_patchwork": step_bytes / units_per_step}

@@ -21,4 +21,6 @@ if [ -z "$SKIP_NCU" ]; then
   timeout 900 ncu --set full --metrics smsp__thread_inst_executed.sum,smsp__inst_executed.sum --clock-control none --import-source on --profile-from-start off -o gpurun_out/step_${TAG} -f python scripts/profile_step.py c3 > gpurun_out/ncu_step_${TAG}.log 2>&1; echo "ncu step rc=$?"
   tail -2 gpurun_out/ncu_step_${TAG}.log
   python scripts/ncu_kernels_json.py gpurun_out/step_${TAG}.ncu-rep gpurun_out/ncu_kernels_${TAG}.json "ncu --set full, one C3 step (scripts/profile_step.py c3), TAG=${TAG}" > /dev/null 2>&1; echo "parse rc=$?"
+  timeout 600 ncu --set full --metrics smsp__thread_inst_executed.sum,smsp__inst_executed.sum --clock-control none --import-source on --profile-from-start off -o gpurun_out/step_c5_${TAG} -f python scripts/profile_step.py c5 > gpurun_out/ncu_step_c5_${TAG}.log 2>&1; echo "ncu c5 rc=$?"
+  python scripts/ncu_kernels_json.py gpurun_out/step_c5_${TAG}.ncu-rep gpurun_out/ncu_kernels_c5_${TAG}.json "ncu --set full, one C5 launch (2^26 bowtie8 draws at 2^39, scripts/profile_step.py c5), TAG=${TAG}" > /dev/null 2>&1; echo "parse c5 rc=$?"
 fi
