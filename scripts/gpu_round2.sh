@@ -23,4 +23,9 @@ if [ -z "$SKIP_NCU" ]; then
   python scripts/ncu_kernels_json.py gpurun_out/step_${TAG}.ncu-rep gpurun_out/ncu_kernels_${TAG}.json "ncu --set full, one C3 step (scripts/profile_step.py c3), TAG=${TAG}" > /dev/null 2>&1; echo "parse rc=$?"
   timeout 600 ncu --set full --metrics smsp__thread_inst_executed.sum,smsp__inst_executed.sum --clock-control none --import-source on --profile-from-start off -o gpurun_out/step_c5_${TAG} -f python scripts/profile_step.py c5 > gpurun_out/ncu_step_c5_${TAG}.log 2>&1; echo "ncu c5 rc=$?"
   python scripts/ncu_kernels_json.py gpurun_out/step_c5_${TAG}.ncu-rep gpurun_out/ncu_kernels_c5_${TAG}.json "ncu --set full, one C5 launch (2^26 bowtie8 draws at 2^39, scripts/profile_step.py c5), TAG=${TAG}" > /dev/null 2>&1; echo "parse c5 rc=$?"
+  # keep the merged-back output under gpurun's 64 MiB: summaries instead of reports
+  python scripts/ncu_lines.py gpurun_out/step_${TAG}.ncu-rep k_l15_build 40 > gpurun_out/l15_lines_${TAG}.txt 2>&1
+  python scripts/ncu_summary.py gpurun_out/step_c5_${TAG}.ncu-rep > gpurun_out/c5_full_${TAG}.txt 2>&1
+  python scripts/ncu_lines.py gpurun_out/step_c5_${TAG}.ncu-rep k_sample_split 30 >> gpurun_out/c5_full_${TAG}.txt 2>&1
+  if [ -z "$KEEP_REP" ]; then rm -f gpurun_out/step_${TAG}.ncu-rep gpurun_out/step_c5_${TAG}.ncu-rep; fi
 fi

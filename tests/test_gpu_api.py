@@ -578,3 +578,45 @@ def test_pipeline_deterministic_across_grid_shapes():
         res.append(json.loads(p.stdout.strip().splitlines()[-1]))
     for r in res:
         assert r[0] == r[1] == res[0][0] and r[2] == r[3] == res[0][2]
+
+
+_MULTI_CHUNKED = r'''
+import sys, numpy as np
+sys.path.insert(0, ".")
+from paper_2604_09221_b200 import Classifier, MultiClassifier
+from paper_2604_09221_b200.lifting import random_unimodular
+import random
+rng = random.Random(0xC4)
+Ts = [random_unimodular(7, rng) for _ in range(24)]
+mc = MultiClassifier(Ts, device=0)
+g = np.random.default_rng(9)
+n = (1 << 20) + 12345
+words = g.integers(0, 1 << 36, size=n, dtype=np.uint64)
+tri_sorted = np.sort(g.integers(0, len(Ts), size=n)).astype(np.int32)   # grouped: no regrouping
+tri_random = g.permutation(tri_sorted).astype(np.int32)                 # regrouped + scattered
+for tri in (tri_sorted, tri_random):
+    keys, ov, nr, st = mc.classify_words(tri, words)
+    assert (st == 0).all()
+    for t in range(len(Ts)):
+        sel = np.nonzero(tri == t)[0]
+        k1, o1, r1, s1 = Classifier(Ts[t], device=0).classify_words(words[sel])
+        assert (keys[sel] == k1).all() and (ov[sel] == o1).all() and (nr[sel] == r1).all()
+print("ok")
+'''
+
+
+def test_multi_triangulation_pipeline_chunks(api, tmp_path):
+    """tcg_multi_classify's pinned-staging pipeline over many chunks (2^18
+    pairs each, ~4 per call), grouped and regrouped inputs, against the
+    single-triangulation batch path."""
+    import os
+    import subprocess
+    import sys
+
+    script = tmp_path / "chunked.py"
+    script.write_text(_MULTI_CHUNKED)
+    env = dict(os.environ, TCG_MULTI_CHUNK_LOG2="18")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, str(script)], cwd=root, env=env, capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
