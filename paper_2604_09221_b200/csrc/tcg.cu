@@ -222,6 +222,9 @@ struct tcg_plan {
     uint32_t *d_oldlist = nullptr;   // [chunk_cap + 1]: count, then tiles for the level-1 path
     uint32_t *d_ovf = nullptr;       // [chunk_cap + 1]: count, then tiles of fallback super-tiles
     SuperRec *d_super = nullptr;     // [super_cap]
+    uint32_t *d_srep = nullptr;      // [super_cap] super-tile twin (k_super_dedup)
+    unsigned long long *d_sslots = nullptr;  // [2 pow2(super_cap)] super dedup table
+    uint32_t *d_repof = nullptr;     // [chunk_cap] tile -> its dedup group's representative
     unsigned long long *d_hash = nullptr;   // [chunk_cap] record hashes (written by the builders)
     unsigned long long *d_slots = nullptr;  // [2 pow2(chunk_cap)] dedup table: tag << 32 | tile
     size_t super_cap = 0;
@@ -478,7 +481,7 @@ int tcg_plan_destroy(tcg_plan *P) {
     void *ptrs[] = {P->d_adj, P->d_edges, P->d_tiles, P->d_lut, P->d_recs, P->d_dedup, P->d_tstats, P->d_l2pool, P->d_l2hash, P->d_l2u32, P->d_l2slots, P->d_l15pool, P->d_l15hash, P->d_l15slots, P->d_l15u32, P->d_oldlist, P->d_ovf, P->d_super, P->d_hash, P->d_slots, P->agg.keys, P->agg.cnt, P->agg.wit, P->agg.hist,
                     P->agg.bad, P->agg.overflow, P->d_ckey, P->d_ccnt, P->d_cwit, P->d_cn,
                     P->d_sig, P->d_key, P->d_ov, P->d_nr, P->d_st, P->d_splitA, P->d_splitB,
-                    P->d_fbl, P->d_pext, P->d_splitstats};
+                    P->d_fbl, P->d_pext, P->d_splitstats, P->d_srep, P->d_sslots, P->d_repof};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 2; ++i) {
@@ -1047,6 +1050,16 @@ static int l2_tail(tcg_plan *P, const TileTables &T, const TileTables *tt, uint3
     return TCG_OK;
 }
 
+// TCG_NO_SUPER_DEDUP=1 builds and compares the tiles of twin super-tiles too
+// (A/B and debugging); results are identical.
+static bool super_dedup_enabled() {
+    static const bool on = [] {
+        const char *e = std::getenv("TCG_NO_SUPER_DEDUP");
+        return !(e && e[0] && e[0] != '0');
+    }();
+    return on;
+}
+
 // TCG_NO_DEDUP=1 classifies every tile (A/B and debugging); results are identical.
 static bool dedup_enabled() {
     static const bool on = [] {
@@ -1219,6 +1232,9 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 P->d_hash = nullptr;
                 P->d_slots = nullptr;
                 CUDA_TRY(cudaMalloc(&P->d_hash, sizeof(unsigned long long) * (size_t)chunk));
+                cudaFree(P->d_repof);
+                P->d_repof = nullptr;
+                CUDA_TRY(cudaMalloc(&P->d_repof, sizeof(uint32_t) * (size_t)chunk));
                 CUDA_TRY(cudaMalloc(&P->d_slots,
                                     sizeof(unsigned long long) * 2 * (size_t)next_pow2(chunk)));
                 P->chunk_cap = chunk;
@@ -1238,6 +1254,7 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
             const uint32_t *nolist = nullptr, *nocount = nullptr;
             cudaEvent_t e0 = timing_begin(P);
             const int sh = P->h_tiles[mode].sh;
+            const uint32_t *srep = nullptr;  // super-tile twins (sh > 0 with deduplication)
             if (sh > 0) {
                 // super-tiles: contract the shared part once per 2^sh tiles, then
                 // each tile from its super record; fallback super-tiles go to the
@@ -1251,6 +1268,13 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                     P->super_cap = 0;
                     const size_t cap = std::max<size_t>(nsup, (P->chunk_cap >> sh) + 2);
                     CUDA_TRY(cudaMalloc(&P->d_super, sizeof(SuperRec) * cap));
+                    cudaFree(P->d_srep);
+                    cudaFree(P->d_sslots);
+                    P->d_srep = nullptr;
+                    P->d_sslots = nullptr;
+                    CUDA_TRY(cudaMalloc(&P->d_srep, sizeof(uint32_t) * cap));
+                    CUDA_TRY(cudaMalloc(&P->d_sslots, sizeof(unsigned long long) * 2 *
+                                                          (size_t)next_pow2((uint32_t)cap)));
                     P->super_cap = cap;
                 }
                 SuperRec *sr = P->d_super;
@@ -1260,12 +1284,28 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 CUDA_TRY(cudaLaunchKernel(pick_super(P->K, mode),
                                           dim3((nsup + THREADS - 1) / THREADS), dim3(THREADS), as,
                                           P->smem_build, P->stream));
+                const SuperRec *csr = sr;
+                srep = nullptr;
+                if ((P->dedup < 0 ? dedup_enabled() : P->dedup != 0) && super_dedup_enabled()) {
+                    // twin super-tiles: their tiles are neither built nor compared
+                    const uint32_t np2s = next_pow2(nsup);
+                    CUDA_TRY(cudaMemsetAsync(P->d_sslots, 0xff, sizeof(unsigned long long) * 2 * np2s,
+                                             P->stream));
+                    uint32_t smask_s = 2 * np2s - 1;
+                    uint64_t lo_s = start, hi_s = end;
+                    uint32_t *srp = P->d_srep;
+                    unsigned long long *ssl = P->d_sslots;
+                    void *asd[] = {&tt, &csr, &nsv, &tile0, &nt, &lo_s, &hi_s, &ssl, &smask_s, &srp};
+                    CUDA_TRY(cudaLaunchKernel((void *)k_super_dedup, dim3((nsup + THREADS - 1) / THREADS),
+                                              dim3(THREADS), asd, 0, P->stream));
+                    srep = P->d_srep;
+                    P->launches++;
+                }
                 timing_end(P, TCG_KT_SUPER_BUILD, e0);
                 e0 = timing_begin(P);
                 uint32_t *ovf = P->d_ovf;
                 CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(uint32_t), P->stream));
-                const SuperRec *csr = sr;
-                void *af[] = {&tt, &csr, &tile0, &nt, &recs, &hashes, &ovf};
+                void *af[] = {&tt, &csr, &tile0, &nt, &recs, &hashes, &ovf, &srep};
                 CUDA_TRY(cudaLaunchKernel((void *)k_tile_from_super,
                                           dim3((nt + THREADS - 1) / THREADS), dim3(THREADS), af,
                                           from_super_smem(P->h_tiles[mode].nf), P->stream));
@@ -1294,12 +1334,22 @@ static int enqueue(tcg_plan *P, int mode, uint64_t start, uint64_t end, uint64_t
                 CUDA_TRY(cudaMemsetAsync(ct, 0, sizeof(uint32_t), P->stream));
                 uint32_t smask = (uint32_t)(2 * Cn - 1);
                 int ibits = bits;
-                void *ad[] = {&crecs, &chash, &nt, &tile0, &ibits, &lo, &hi, &slots, &smask, &dp,
-                              &mnt, &ls, &ct};
+                TileRec *wrecs = recs;  // twins of never-merged tiles get a copy of the record
+                int shv = sh;
+                uint32_t *repof = srep ? P->d_repof : nullptr;
+                void *ad[] = {&wrecs, &chash, &nt, &tile0, &ibits, &lo, &hi, &slots, &smask, &dp,
+                              &mnt, &ls, &ct, &srep, &shv, &repof};
                 const unsigned gd = (unsigned)((nt + THREADS - 1) / THREADS);
                 cudaEvent_t ed = timing_begin(P);
                 CUDA_TRY(cudaLaunchKernel((void *)k_tile_dedup, dim3(gd), dim3(THREADS), ad, 0,
                                           P->stream));
+                if (srep) {  // tiles of twin super-tiles join their twins' groups
+                    const uint32_t *crep = repof;
+                    void *ap[] = {&crecs, &nt, &tile0, &shv, &srep, &crep, &dp, &mnt};
+                    CUDA_TRY(cudaLaunchKernel((void *)k_super_prop, dim3(gd), dim3(THREADS), ap, 0,
+                                              P->stream));
+                    P->launches++;
+                }
                 timing_end(P, TCG_KT_TILE_DEDUP, ed);
                 list = ls;
                 cnt = ct;

@@ -622,12 +622,101 @@ __global__ void __launch_bounds__(THREADS) k_super_build(KParams p,
 constexpr size_t FROM_SUPER_SMEM = sizeof(TileTables) + (16 + MAXF) * 4 * THREADS;  // max
 inline size_t from_super_smem(int nf) { return sizeof(TileTables) + (size_t)(16 + nf) * 4 * THREADS; }
 
+// Super-tile deduplication.  Every tile record of a super-tile is a function
+// of the super record (its used part) and the tile's mid pattern alone, so
+// two super-tiles with equal super records have equal tile records at equal
+// mid offsets: the tiles of a duplicate super-tile are not built or compared
+// -- each joins the tile-dedup group of its twin in the representative
+// super-tile (k_super_prop).  Only super-tiles whose tiles are all full
+// (inside the chunk and the index range) and whose contraction fit take part.
+// C3: 131,072 super-tiles per step, ~74,000 distinct.
+__device__ __forceinline__ unsigned long long super_hash(const SuperRec *__restrict__ r, int nf, int nm) {
+    unsigned long long h = 0x9E3779B97F4A7C15ull ^ (unsigned long long)r->nsn;
+    for (int k = 0; k < r->nsn; ++k) {
+        h = mix64(h ^ r->adj[k]);
+        h = mix64(h ^ r->link[k] ^ ((unsigned long long)r->fadj[k] << 7));
+    }
+    for (int f = 0; f < nf; ++f) h = mix64(h ^ r->fsn[f]);
+    for (int j = 0; j < nm; ++j) h = mix64(h ^ ((unsigned long long)r->msn[j] << (8 * (j & 7))));
+    return mix64(h ^ r->sgn);
+}
+
+__device__ __forceinline__ bool super_equal(const SuperRec *__restrict__ a, const SuperRec *__restrict__ b,
+                                            int nf, int nm) {
+    if (a->nsn != b->nsn || a->sgn != b->sgn) return false;
+    unsigned long long d = 0;
+    for (int k = 0; k < a->nsn; ++k)
+        d |= (a->adj[k] ^ b->adj[k]) | (a->link[k] ^ b->link[k]) | (unsigned long long)(a->fadj[k] ^ b->fadj[k]);
+    for (int f = 0; f < nf; ++f) d |= a->fsn[f] ^ b->fsn[f];
+    for (int j = 0; j < nm; ++j) d |= (unsigned long long)(a->msn[j] ^ b->msn[j]);
+    return d == 0ull;
+}
+
+// srep[s] = s (a representative, or not eligible) or the representative's index.
+__global__ void __launch_bounds__(THREADS) k_super_dedup(const TileTables *__restrict__ tt_g,
+                                                         const SuperRec *__restrict__ srecs, uint32_t nsup,
+                                                         uint64_t tile0, uint32_t ntiles,
+                                                         uint64_t start, uint64_t end,
+                                                         unsigned long long *__restrict__ slots,
+                                                         uint32_t smask, uint32_t *__restrict__ srep) {
+    const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= nsup) return;
+    const int sh = tt_g->sh, bits = tt_g->bits, nf = tt_g->nf, nm = tt_g->nm;
+    const uint64_t g0 = (((tile0 >> sh) + s) << sh), g1 = g0 + (1ull << sh);  // global tiles
+    const SuperRec *r = srecs + s;
+    uint32_t out = s;
+    if (!r->fallback && g0 >= tile0 && g1 <= tile0 + ntiles && (g0 << bits) >= start &&
+        (g1 << bits) <= end) {
+        const unsigned long long h = super_hash(r, nf, nm);
+        const unsigned long long tag = (h >> 32) << 32;
+        uint32_t at = (uint32_t)h & smask;
+        while (true) {
+            unsigned long long cur = slots[at];
+            if (cur == ~0ull) {
+                const unsigned long long prev = atomicCAS(&slots[at], ~0ull, tag | s);
+                if (prev == ~0ull) break;  // representative
+                cur = prev;
+            }
+            if ((cur & 0xffffffff00000000ull) == tag && super_equal(r, srecs + (uint32_t)cur, nf, nm)) {
+                out = (uint32_t)cur;
+                break;
+            }
+            at = (at + 1) & smask;
+        }
+    }
+    srep[s] = out;
+}
+
+// The tiles of duplicate super-tiles join their twins' groups (after
+// k_tile_dedup has settled the groups in repof).  A twin whose contraction
+// did not fit is never merged; k_tile_dedup copied its record and listed the
+// tile on its own.
+__global__ void __launch_bounds__(THREADS) k_super_prop(const TileRec *__restrict__ recs,
+                                                        uint32_t ntiles, uint64_t tile0, int sh,
+                                                        const uint32_t *__restrict__ srep,
+                                                        const uint32_t *__restrict__ repof,
+                                                        uint32_t *__restrict__ dup,
+                                                        uint32_t *__restrict__ mint) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= ntiles) return;
+    const uint64_t gt = tile0 + t;
+    const uint32_t si = (uint32_t)((gt >> sh) - (tile0 >> sh));
+    const uint32_t rs = srep[si];
+    if (rs == si) return;
+    const uint32_t tw = (uint32_t)(((((tile0 >> sh) + rs) << sh) | (gt & ((1ull << sh) - 1ull))) - tile0);
+    if (recs[tw].fallback) return;
+    const uint32_t R = repof[tw];
+    atomicAdd(&dup[R], 1u);
+    atomicMin(&mint[R], t);
+}
+
 __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *__restrict__ tt_g,
                                                              const SuperRec *__restrict__ srecs,
                                                              uint64_t tile0, uint32_t ntiles,
                                                              TileRec *__restrict__ recs,
                                                              unsigned long long *__restrict__ hashes,
-                                                             uint32_t *__restrict__ ovf) {
+                                                             uint32_t *__restrict__ ovf,
+                                                             const uint32_t *__restrict__ srep) {
     extern __shared__ __align__(16) uint32_t smem[];
     TileTables *tt = reinterpret_cast<TileTables *>(smem);
     uint8_t *lb = reinterpret_cast<uint8_t *>(smem + sizeof(TileTables) / 4 + threadIdx.x);
@@ -651,6 +740,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_from_super(const TileTables *_
         const uint64_t gt = tile0 + t;
         const SuperRec *S = srecs + ((gt >> h) - sbase);
         TileRec *rec = recs + t;
+        if (srep && srep[(gt >> h) - sbase] != (uint32_t)((gt >> h) - sbase)) continue;  // twin built
         if (S->fallback) {
             ovf[1 + atomicAdd(ovf, 1u)] = t;
             continue;
@@ -792,7 +882,7 @@ __device__ __forceinline__ bool rec_equal(const TileRec *__restrict__ a,
     return diff == 0u;
 }
 
-__global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restrict__ recs,
+__global__ void __launch_bounds__(THREADS) k_tile_dedup(TileRec *__restrict__ recs,
                                                         const unsigned long long *__restrict__ hashes,
                                                         uint32_t ntiles, uint64_t tile0, int bits,
                                                         uint64_t start, uint64_t end,
@@ -800,15 +890,34 @@ __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restric
                                                         uint32_t smask, uint32_t *__restrict__ dup,
                                                         uint32_t *__restrict__ mint,
                                                         uint32_t *__restrict__ list,
-                                                        uint32_t *__restrict__ count) {
+                                                        uint32_t *__restrict__ count,
+                                                        const uint32_t *__restrict__ srep, int sh,
+                                                        uint32_t *__restrict__ repof) {
     const int lane = threadIdx.x & 31;
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     bool rep = false;
-    if (t < ntiles) {
+    bool twin = false;  // a tile of a duplicate super-tile (record not built)
+    if (t < ntiles && srep) {
+        const uint64_t gt = tile0 + t;
+        const uint32_t si = (uint32_t)((gt >> sh) - (tile0 >> sh)), rs = srep[si];
+        if (rs != si) {
+            twin = true;
+            const uint32_t tw = (uint32_t)(((((tile0 >> sh) + rs) << sh) | (gt & ((1ull << sh) - 1ull))) - tile0);
+            if (recs[tw].fallback) {  // never merged: the tile is its own representative
+                const uint4 *src = reinterpret_cast<const uint4 *>(recs + tw);
+                uint4 *dst = reinterpret_cast<uint4 *>(recs + t);
+                for (int i = 0; i < (int)(sizeof(TileRec) / 16); ++i) dst[i] = src[i];
+                rep = true;
+                repof[t] = t;
+            }
+        }
+    }
+    if (t < ntiles && !twin) {
         const TileRec *r = recs + t;
         const uint64_t b0 = (tile0 + t) << bits, b1 = (tile0 + t + 1) << bits;
         if (r->fallback || b0 < start || b1 > end) {
             rep = true;
+            if (repof) repof[t] = t;
         } else {
             const unsigned long long h = hashes[t];
             const unsigned long long tag = (h >> 32) << 32;
@@ -819,6 +928,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restric
                     const unsigned long long prev = atomicCAS(&slots[at], SLOT_EMPTY, tag | t);
                     if (prev == SLOT_EMPTY) {
                         rep = true;
+                        if (repof) repof[t] = t;
                         break;
                     }
                     cur = prev;
@@ -829,6 +939,7 @@ __global__ void __launch_bounds__(THREADS) k_tile_dedup(const TileRec *__restric
                     if (rec_equal(r, recs + o)) {
                         atomicAdd(&dup[o], 1u);
                         atomicMin(&mint[o], t);
+                        if (repof) repof[t] = o;
                         break;
                     }
                 }

@@ -10,6 +10,7 @@ from paper_2604_09221_b200.sweep import sample_slice  # noqa: E402
 
 T = builtin(sys.argv[1] if len(sys.argv) > 1 else "bowtie8")
 c = Classifier(T)
+c.native.set_split(True)  # the split path from the first slice on
 sample_slice(T, 20260810, 0, 1 << 20, classifier=c)
 r = sample_slice(T, 20260810, 1 << 39, (1 << 39) + (1 << 24), classifier=c)
 print(r.total_classified, c.native.split_stats())
