@@ -58,11 +58,14 @@ CLOCK_FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.a
                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 # kernel kinds timed by the library (tcg.h TCG_KT_*) -> kernel names in ncu
 KIND_KERNELS = {
-    "super_build": ["k_super_build"], "tile_build": ["k_tile_from_super", "k_tile_build_lanes"],
-    "tile_dedup": ["k_tile_dedup"], "l15_build": ["k_l15_build"],
+    "super_build": ["k_super_build", "k_super_dedup"],
+    "tile_build": ["k_tile_from_super", "k_tile_build_lanes"],
+    "tile_dedup": ["k_tile_dedup", "k_super_prop"], "l15_build": ["k_l15_build"],
     "l15_dedup": ["k_l2_dedup/stage1"], "l2_build": ["k_l2_from_l15", "k_l2_build"],
     "l2_dedup": ["k_l2_dedup/level2"], "l2_classify": ["k_l2_classify", "k_l2_classify_even"],
     "tile_classify": ["k_tile_classify"], "enumerate": ["k_enumerate"], "batch": ["k_batch"],
+    "split_build": ["k_split_build"], "sample_split": ["k_sample_split"],
+    "sample_list": ["k_sample_list"],
 }
 
 
