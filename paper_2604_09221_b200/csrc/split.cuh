@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(THREADS) k_split_build(KParams p, SplitPart sp
         // neighbourhoods are read through the labels (O(|X|), not O(nc^2))
         uint8_t lab[32 * K];
         uint32_t sgn = 0;
+        TCG_ASSERT(sp.nF <= SPL_MAXF && sp.bits <= SPL_MAXBITS);
         for (int c = 0; c < nc; ++c) {
             uint32_t s = 0;
 #pragma unroll
@@ -170,6 +171,7 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
     constexpr int NSTEP = V >= 3 ? 4 : (V == 2 ? 3 : 2);  // frontier nodes per step
     u64 xs[V ? MAXR : 1];
     auto adjacency = [&](int rr, u64 w) {
+        TCG_ASSERT(rr >= 0 && rr < MAXR);
         uint32_t A = 0;
         while (w) {
             const int n = __ffsll((long long)w) - 1;
@@ -212,7 +214,9 @@ __device__ __forceinline__ void split_pass(const uint32_t *__restrict__ fadj_s,
     // masks), components one uint4 of their entry; the loads are issued
     // without branches so two nodes' loads are in flight together
     auto load = [&](int v, uint4 &t1, uint4 &t2) {
+        TCG_ASSERT(v >= 0 && v < nn && nn <= 64);
         const bool isF = v < nF, inA = v < sB;
+        TCG_ASSERT(isF || (inA ? v - nF : v - sB) < SPL_CAPC);
         const uint4 *pc = inA ? ca + (v - nF) : cb + (v - sB);
         t1 = __ldg(isF ? fa + (v >> 2) : pc);
         t2 = isF ? __ldg(fb + (v >> 2)) : make_uint4(0u, 0u, 0u, 0u);
@@ -457,6 +461,7 @@ __global__ void __launch_bounds__(THREADS, 3) k_sample_split(KParams p, SplitPar
 #pragma unroll
         for (int j = 0; j < SPL_NBYTES; ++j)
             if (j < sp.nbytes) ix |= __ldg(pext + j * 256 + ((sigma >> (8 * j)) & 255u));
+        TCG_ASSERT((ix & 0xffffffull) < (1ull << 24) && ((ix >> 24) & 0xffffffull) < (1ull << 24));
         const uint32_t *ea = sp.tabA + (size_t)(ix & 0xffffffull) * sp.stride;
         const uint32_t *eb = sp.tabB + (size_t)((ix >> 24) & 0xffffffull) * sp.stride;
         const uint32_t fb = (uint32_t)(ix >> 48);

@@ -677,6 +677,7 @@ __global__ void __launch_bounds__(THREADS) k_super_dedup(const TileTables *__res
                 if (prev == ~0ull) break;  // representative
                 cur = prev;
             }
+            TCG_ASSERT((cur & 0xffffffffull) < nsup);
             if ((cur & 0xffffffff00000000ull) == tag && super_equal(r, srecs + (uint32_t)cur, nf, nm)) {
                 out = (uint32_t)cur;
                 break;
@@ -704,8 +705,10 @@ __global__ void __launch_bounds__(THREADS) k_super_prop(const TileRec *__restric
     const uint32_t rs = srep[si];
     if (rs == si) return;
     const uint32_t tw = (uint32_t)(((((tile0 >> sh) + rs) << sh) | (gt & ((1ull << sh) - 1ull))) - tile0);
+    TCG_ASSERT(tw < ntiles);  // the representative may sit before or after the twin
     if (recs[tw].fallback) return;
     const uint32_t R = repof[tw];
+    TCG_ASSERT(R < ntiles);
     atomicAdd(&dup[R], 1u);
     atomicMin(&mint[R], t);
 }

@@ -15,6 +15,8 @@ Families (kernels exercised):
   sweep6    d = 6 raw sweep (even, K = 4 tiles)
   multi     k_multi (many triangulations)
   large     k_large (d = 10, any-degree engine)
+  split     k_split_build, k_sample_split, k_sample_list (d = 8 sampling through
+            the separator-split tables, forced fallbacks)
 Each run checks its result against the reference fixtures it can reach
 (tests/golden), so a sanitizer pass also shows the launch computed the
 right answer under instrumentation.
@@ -74,6 +76,16 @@ elif fam == "sweep6":
     g = golden("c2_delaunay6_rep.json")
     r = sweep(builtin("delaunay-6"), SweepRange(0, 1 << 21))
     assert r.total_classified == 1 << 21 and set(r.scheme_map) <= set(g["schemes"])
+elif fam == "split":
+    os.environ["TCG_SPLIT_MAXNODES"] = "44"  # some draws take the flat list kernel
+    for s in [x for x in golden("c5_sample_slices.json")["slices"] if x["k0"] == 0]:
+        T = builtin(s["name"])
+        c = Classifier(T)
+        c.native.set_split(True)
+        r = sample_slice(T, s["seed"], s["k0"], s["k1"], classifier=c)
+        check(r, s)
+        st = c.native.split_stats()
+        assert st[0] == 1 and st[2] > 0, st
 elif fam == "multi":
     from paper_2604_09221_b200.lifting import random_unimodular
 
