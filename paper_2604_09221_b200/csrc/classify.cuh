@@ -347,6 +347,101 @@ __device__ __forceinline__ void region_pass(const uint32_t *__restrict__ rows,
     out.oddmask = oddmask;
 }
 
+// AHU key of the region tree rooted at `root` (the same code as tree_key:
+// children sorted by sentinel key, leaves first as one run) without per-region
+// arrays: the levels of the rooted tree are bit masks, and only the internal
+// non-root regions -- a handful in practice -- keep a code, in register slots.
+// Returns false (caller falls back to the flat kernel) when the tree is
+// disconnected, deeper than SPL_MAXD or has more than SPL_SLOTS internal
+// non-root regions.
+constexpr int SPL_MAXD = 8;
+constexpr int SPL_SLOTS = 8;
+__device__ __forceinline__ bool graph_key(const uint32_t (&radj)[MAXR], int nreg, int root,
+                                          uint64_t &key) {
+    uint32_t lev[SPL_MAXD + 1];
+    uint32_t vis = 1u << root, internal = 0u;
+    lev[0] = vis;
+    int depth = 0;
+#pragma unroll
+    for (int k = 0; k < SPL_MAXD; ++k) {
+        lev[k + 1] = 0u;
+        if (k == depth) {
+            uint32_t nxt = 0u;
+            for (uint32_t l = lev[k]; l; l &= l - 1u) {
+                const int v = __ffs(l) - 1;
+                const uint32_t ch = radj[v] & ~vis;
+                if (ch) internal |= 1u << v;
+                nxt |= ch;
+            }
+            vis |= nxt;
+            lev[k + 1] = nxt;
+            if (nxt) depth = k + 1;
+        }
+    }
+    if (__popc(vis) != nreg) return false;  // disconnected or deeper than SPL_MAXD
+    if (__popc(internal & ~(1u << root)) > SPL_SLOTS) return false;
+    int snode[SPL_SLOTS];
+    uint64_t scode[SPL_SLOTS];
+#pragma unroll
+    for (int i = 0; i < SPL_SLOTS; ++i) {
+        snode[i] = -1;
+        scode[i] = 0ull;
+    }
+    int nslot = 0;
+    uint64_t acc = 1ull;
+#pragma unroll
+    for (int k = SPL_MAXD - 1; k >= 0; --k) {
+        if (k >= depth) continue;
+        for (uint32_t l = lev[k] & internal; l; l &= l - 1u) {
+            const int v = __ffs(l) - 1;
+            const uint32_t ch = radj[v] & lev[k + 1];
+            const int nleaf = __popc(ch & ~internal);
+            // codes of the internal children, ascending (register insertion)
+            uint64_t buf[SPL_SLOTS];
+            int h = 0;
+#pragma unroll
+            for (int i = 0; i < SPL_SLOTS; ++i) buf[i] = ~0ull;
+            for (uint32_t c = ch & internal; c; c &= c - 1u) {
+                const int cv = __ffs(c) - 1;
+                uint64_t ck = 0ull;
+#pragma unroll
+                for (int i = 0; i < SPL_SLOTS; ++i) ck = snode[i] == cv ? scode[i] : ck;
+#pragma unroll
+                for (int i = SPL_SLOTS - 1; i >= 0; --i)  // shift the larger ones, place ck
+                    buf[i] = (i > 0 && buf[i > 0 ? i - 1 : 0] > ck) ? buf[i > 0 ? i - 1 : 0]
+                                                                    : (buf[i] > ck ? ck : buf[i]);
+                ++h;
+            }
+            acc = 1ull;
+            if (nleaf) {
+                const int nb2 = 2 * nleaf;
+                acc = (1ull << nb2) | (0xAAAAAAAAAAAAAAAAull & ((1ull << nb2) - 1ull));
+            }
+#pragma unroll
+            for (int i = 0; i < SPL_SLOTS; ++i) {
+                if (i < h) {
+                    const uint64_t c = buf[i];
+                    const int ln = 63 - __clzll(c);
+                    acc = (acc << ln) | (c ^ (1ull << ln));
+                }
+            }
+            if (k > 0) {
+                const int il = 63 - __clzll(acc);
+                const uint64_t code = (acc << 1) | (1ull << (il + 2));
+#pragma unroll
+                for (int i = 0; i < SPL_SLOTS; ++i)
+                    if (i == nslot) {
+                        snode[i] = v;
+                        scode[i] = code;
+                    }
+                ++nslot;
+            }
+        }
+    }
+    key = acc;
+    return true;
+}
+
 // Region graph -> status (reference precedence) -> rooted tree -> AHU key.
 // EXACT: replay the two order-dependent status collisions in edge order
 // (only meaningful for the flat diamond layout); otherwise report a failure
@@ -466,7 +561,9 @@ __device__ __forceinline__ Result finish(const KParams &p, const uint32_t (&SG)[
         res.key = nreg == 1 ? 1ull : (nreg == 2 ? 6ull : (__popc(radj[root]) == 2 ? 26ull : 28ull));
         return res;
     }
-    res.key = tree_key(radj, nreg, root, res.status);
+    // register-slot AHU key (graph_key); the array version for trees it declines
+    if (graph_key(radj, nreg, root, res.key)) res.status = TCG_OK;
+    else res.key = tree_key(radj, nreg, root, res.status);
     return res;
 }
 
