@@ -158,7 +158,9 @@ int tcg_level2_stats(tcg_plan *plan, int64_t *out);
  * components of that side's diamond vertices (device memory, once); each draw
  * is then classified on the graph of F's vertices plus the two sides'
  * components.  Draws whose graph exceeds 64 nodes, or whose status is not OK,
- * are re-classified by the flat kernel.  tcg_split_stats: out[0] = state
+ * are re-classified by the flat kernel.  If the tables would take more than
+ * half of the free device memory the plan samples with the flat kernel.
+ * tcg_split_stats: out[0] = state
  * (1 ready, -1 unavailable: flat sampling, 0 not built yet), out[1] = draws
  * sampled through the split kernel, out[2] = of those, draws the flat kernel
  * took, out[3] = separator vertices, out[4] = table bytes; counts since the

@@ -1112,6 +1112,14 @@ static int ensure_split(tcg_plan *P) {
     if (!split_design(&D, L, S)) return TCG_OK;
     const size_t na = (size_t)1 << S.pa.bits, nb = (size_t)1 << S.pb.bits;
     const size_t ew = S.sp.stride;
+    {  // the tables are an accelerator: without the memory, sample on the flat kernel
+        size_t fr = 0, tot = 0;
+        const size_t need = (na + nb) * ew * 4 + S.pext.size() * 8 + (SPL_LAUNCH + 1) * 4 + 8;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || need > fr / 2) {
+            cudaGetLastError();
+            return TCG_OK;
+        }
+    }
     CUDA_TRY(cudaMalloc(&P->d_splitA, na * ew * 4));
     CUDA_TRY(cudaMalloc(&P->d_splitB, nb * ew * 4));
     CUDA_TRY(cudaMalloc(&P->d_pext, S.pext.size() * 8));
