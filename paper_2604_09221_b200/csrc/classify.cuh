@@ -224,7 +224,14 @@ struct Regions {
 // rows: per node K words of adjacency (+ K words of partner links if ROWS).
 // COMPS: no antipodal jumps, so every "region" is one same-sign component and
 // X collects all of its neighbours (used to contract a tile's fixed part).
-template <int K, bool EVEN, bool ROWS, bool COMPS = false, int CAP = MAXR>
+#ifndef TCG_FLAT_BATCH
+#define TCG_FLAT_BATCH 4  // measured: 1 / 2 / 3 / 4 / 6 / 8 / 12 -> C4 1.88 / 1.96 / 2.02 / 2.05 / 1.98 / 1.95 / 1.77e9 pairs/s
+#endif
+// BATCH > 1 (the full-diamond classifier): a lane whose layer has emptied waits
+// for the next iteration that is a multiple of BATCH before running
+// layer_end, so the lanes of a warp run their (divergent) layer ends together
+// instead of in most iterations one by one; waiting lanes skip their pop.
+template <int K, bool EVEN, bool ROWS, bool COMPS = false, int CAP = MAXR, int BATCH = 1>
 __device__ __forceinline__ void region_pass(const uint32_t *__restrict__ rows,
                                             const uint32_t (&SG)[K], const uint32_t (&USED)[K],
                                             const uint32_t (&BD)[K], int nused,
@@ -326,8 +333,12 @@ __device__ __forceinline__ void region_pass(const uint32_t *__restrict__ rows,
     };
 
     seed(USED);
-    for (int it = 0; it < nused; ++it) {
-        if (!any<K>(F)) layer_end(true);
+    for (int it = 0, pops = 0; pops < nused; ++it) {
+        if (!any<K>(F)) {
+            if (BATCH > 1 && it % BATCH != 0) continue;  // wait for the warp's batch
+            layer_end(true);
+        }
+        ++pops;
         int w, b;
         lowest<K>(F, w, b);
         const int v = 32 * w + b;
@@ -579,7 +590,7 @@ __device__ __forceinline__ Result classify(const KParams &p, const uint32_t *__r
         bd[k] = p.bd[k];
     }
     Regions<K> rg;
-    region_pass<K, EVEN, false>(adj, SG, used, bd, p.nused, rg);
+    region_pass<K, EVEN, false, false, MAXR, TCG_FLAT_BATCH>(adj, SG, used, bd, p.nused, rg);
     return finish<K, EVEN, true>(p, SG, rg, p.maxreg);
 }
 
