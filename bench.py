@@ -466,6 +466,64 @@ def bench_c5(dev, steps, warmup):
     return out
 
 
+def bench_c2(dev, steps, warmup):
+    """Config C2: delaunay-6, the exhaustive raw 2^28 sign space per step
+    (tile pipeline, even degree); parity: the raw histogram and scheme counts
+    are 8x the reference's full representative sweep (tests/golden, the
+    (Z/2)^3 symmetry of SURVEY A16), and a representative 2^25 sweep equals it
+    bit for bit (witnesses included)."""
+    import torch
+
+    from paper_2604_09221_b200 import Classifier, SweepRange, builtin, sweep
+
+    with open(os.path.join(ROOT, "tests", "golden", "c2_delaunay6_rep.json")) as fh:
+        g = json.load(fh)
+    T = builtin("delaunay-6")
+    c = Classifier(T, device=dev.index)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    c.native.set_stream(stream.cuda_stream)
+    n = 1 << 28
+    for _ in range(warmup):
+        c.native.agg_reset()
+        c.native.sweep_async(True, 0, n)
+        c.native.agg_fetch()
+    torch.cuda.synchronize()
+    evs = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c.native.agg_reset()
+        a.record(stream)
+        c.native.sweep_async(True, 0, n)
+        b.record(stream)
+        rc, bad, agg = c.native.agg_fetch()
+        assert rc == 0, (rc, bad)
+        evs.append((a, b))
+    torch.cuda.synchronize()
+    ms = sum(x.elapsed_time(y) for x, y in evs) / steps
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        r = sweep(T, SweepRange(0, n), raw_space=True, classifier=c)
+    e2e = n * steps / (time.perf_counter() - t0)
+    raw_ok = (list(r.oval_histogram) == [8 * x for x in g["hist"]] and
+              {k: v[0] for k, v in r.scheme_map.items()} ==
+              {k: 8 * v[0] for k, v in g["schemes"].items()})
+    rep = sweep(T, SweepRange(0, 1 << 25), classifier=c)
+    rep_ok = (list(rep.oval_histogram) == g["hist"] and
+              rep.scheme_map == {k: tuple(v) for k, v in g["schemes"].items()})
+    return {"c2": {
+        "metric": "patchworks classified/sec, degree-6 full raw sign enumeration, one B200",
+        "value": n / (ms / 1e3), "unit": "patchworks/s", "ms_per_step": ms,
+        "e2e": {"value": e2e, "unit": "patchworks/s", "h2d_bytes_per_step": 16,
+                "path": "sweep(T, SweepRange(0, 2^28), raw_space=True)"},
+        "config": {"workload": "C2: delaunay-6 raw [0, 2^28) (the full 2^28 raw space)",
+                   "patchworks_per_step": n},
+        "parity": f"raw = 8 x the reference's full representative sweep: {raw_ok}; "
+                  f"representative 2^25 sweep bit-exact: {rep_ok}",
+        "parity_ok": raw_ok and rep_ok,
+    }}
+
+
 def bench_c4(dev, steps, warmup):
     """Config C4: 4,096 random regular unimodular degree-7 triangulations
     (reference generator, Random(0xB7)) x 2^16 sign words each,
@@ -699,6 +757,7 @@ def run_ours(args, rank, world, local_rank):
     if world == 1 and not args.no_extra:
         other.update(bench_c5(dev, 3, 2))
         other.update(bench_c4(dev, 3, 1))
+        other.update(bench_c2(dev, 5, 3))
 
     if rank != 0:
         return 0
@@ -825,12 +884,13 @@ def run_ours(args, rank, world, local_rank):
 
 
 def run_single_workload(args):
-    """--workload c4 | c5: one line for that config (N = 1, for profiling)."""
+    """--workload c2 | c4 | c5: one line for that config (N = 1, for profiling)."""
     import torch
 
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    res = bench_c5(dev, args.steps, args.warmup) if args.workload == "c5" else bench_c4(
+    res = bench_c5(dev, args.steps, args.warmup) if args.workload == "c5" else bench_c2(
+        dev, args.steps, args.warmup) if args.workload == "c2" else bench_c4(
         dev, args.steps, args.warmup)
     for k, v in res.items():
         print(json.dumps({"workload": k, **v}), flush=True)
@@ -843,7 +903,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c3", "c4", "c5"], default="c3")
+    ap.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c3")
     ap.add_argument("--weak", action="store_true", help="fixed work per GPU (see docstring)")
     ap.add_argument("--slice-log2", type=int, default=33, help="--weak: indices per GPU-step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
