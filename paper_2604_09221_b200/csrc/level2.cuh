@@ -307,9 +307,11 @@ __global__ void __launch_bounds__(THREADS) k_l2_build(const TileTables *__restri
 // Stage 1 (k_l15_build, one lane per (representative tile, A1 pattern)):
 // fix the A1 nodes (tile bits 5, 6) and merge components + A1 nodes into
 // super-nodes, keeping their relations to the F nodes (B and A2) by member
-// sign; records are two words per super-node,
-//   word0 = cs | self << 31,   word1 = plusF | minusF << nF | linkF << 2nF,
-// and are deduplicated like level-2 records.  Stage 2 (k_l2_from_l15, one
+// sign; a record is a bit stream (L15Bits) of, per super-node,
+//   F relations = plusF | minusF << nF | linkF << 2nF   (3 nF bits), then
+//   cs row (m bits) + self flag (1 bit),
+// 3 nF + m + 1 bits per super-node (~23 words at C3 against 41 for two
+// words per super-node), and records are deduplicated like level-2 records.  Stage 2 (k_l2_from_l15, one
 // lane per (distinct stage-1 record, A2 pattern)) fixes the A2 nodes and
 // merges again, emitting ordinary level-2 records (same format and hash as
 // k_l2_build, so the rest of the pipeline is unchanged).  Either stage sets
@@ -330,7 +332,37 @@ __device__ __forceinline__ unsigned long long l15_compress(const L15Lut &L, uint
                                 L.b[2][(fm >> 16) & 0xffu] | L.b[3][fm >> 24]);
 }
 
-template <typename MT, bool PACK>
+// Stage-1 record bit stream (words 1..): the m super-nodes' F relations
+// (3 nF bits each), then their cs rows (m bits) + self flag (1 bit) each;
+// word 0 = m | stream words << 16.  Unused high bits of the last word are 0,
+// so equal records are equal word for word.
+struct L15Bits {
+    unsigned long long acc = 0;
+    int nacc = 0, wi = 1;
+    __device__ __forceinline__ void put(unsigned long long *out, unsigned long long v, int nb) {
+        // v < 2^nb, 1 <= nb <= 63
+        acc |= v << nacc;
+        nacc += nb;
+        if (nacc >= 64) {
+            out[wi++] = acc;
+            nacc -= 64;
+            acc = nacc ? v >> (nb - nacc) : 0ull;
+        }
+    }
+    __device__ __forceinline__ int finish(unsigned long long *out) {
+        if (nacc) out[wi++] = acc;
+        return wi - 1;
+    }
+};
+
+__device__ __forceinline__ unsigned long long l15_bits(const unsigned long long *r1, int pos, int nb) {
+    const int w = pos >> 6, o = pos & 63;
+    unsigned long long v = __ldg(r1 + 1 + w) >> o;
+    if (o + nb > 64) v |= __ldg(r1 + 2 + w) << (64 - o);
+    return v & ((1ull << nb) - 1ull);
+}
+
+template <typename MT>
 __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut,
                                          const TileRec *__restrict__ rec,
                                          const uint4 *__restrict__ R4, uint32_t a1,
@@ -349,6 +381,7 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
     MT unv = G, done = 0;
     unsigned long long hh = 0x9E3779B97F4A7C15ull;
     int m = 0;
+    L15Bits bw;
     auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
     while (unv) {
         if (m == tt.l15max) return -1;
@@ -394,29 +427,20 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
         const unsigned long long w1 = l15_compress(lut, (uint32_t)(pb >> n)) |
                                       l15_compress(lut, (uint32_t)(mb >> n)) << nF |
                                       l15_compress(lut, (uint32_t)(lk >> n)) << (2 * nF);
-        if (PACK) {  // low half now; the high half (w1 >> 32, cs, self) at the end
-            reinterpret_cast<uint32_t *>(out)[2 * (1 + m)] = (uint32_t)w1;
-            cs[m * THREADS] |= (uint32_t)(w1 >> 32) << 24;  // <= 7 bits: 3 nF <= 39
-        } else {
-            out[2 + 2 * m] = w1;
-        }
+        bw.put(out, w1, 3 * nF);
         hh = mix64(hh ^ w1);
         done |= M;
         ++m;
     }
-    out[0] = (unsigned long long)m;
     uint32_t hl = 0xC2B2AE3Du;
     for (int k = 0; k < m; ++k) {
         const uint32_t c = cs[k * THREADS];
-        if (PACK)  // word bits 32..: w1 >> 32, then cs (24 bits) and self from bit 3 nF
-            reinterpret_cast<uint32_t *>(out)[2 * (1 + k) + 1] =
-                ((c >> 24) & 0x7fu) | ((c & 0xffffffu) << (3 * nF - 32)) |
-                ((c >> 31) << (3 * nF - 32 + 24));
-        else
-            out[1 + 2 * k] = c;
+        bw.put(out, (unsigned long long)(c & 0xffffffu) | (unsigned long long)(c >> 31) << m, m + 1);
         hl = (hl ^ c) * 0x9E3779B1u;
         hl ^= hl >> 15;
     }
+    const int nw = bw.finish(out);
+    out[0] = (unsigned long long)m | (unsigned long long)nw << 16;
     hout = mix64((hh ^ hl) + 0x51ED2701ull * (unsigned long long)(m + 1));
     return m;
 }
@@ -484,16 +508,9 @@ __global__ void __launch_bounds__(THREADS) k_l15_build(const TileTables *__restr
             } else {
                 unsigned long long *out = pool + (size_t)j * stride;
                 unsigned long long h = 0;
-                const int nF = tt.nB + tt.nA2;
-                const bool pk = nF >= 11 && nF <= 13;  // one word per super-node
-                const int m =
-                    nn <= 32
-                        ? (pk ? l15_build<uint32_t, true>(tt, luts, rec, slot, a1, out, h, mine)
-                              : l15_build<uint32_t, false>(tt, luts, rec, slot, a1, out, h, mine))
-                        : (pk ? l15_build<unsigned long long, true>(tt, luts, rec, nn <= slotq ? slot : rec->rows,
-                                                                    a1, out, h, mine)
-                              : l15_build<unsigned long long, false>(tt, luts, rec, nn <= slotq ? slot : rec->rows,
-                                                                     a1, out, h, mine));
+                const int m = nn <= 32 ? l15_build<uint32_t>(tt, luts, rec, slot, a1, out, h, mine)
+                                       : l15_build<unsigned long long>(tt, luts, rec, nn <= slotq ? slot : rec->rows,
+                                                                       a1, out, h, mine);
                 if (m < 0) {
                     atomicOr(fail, 1u);
                     wts[j] = 0u;
@@ -542,21 +559,20 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
     const int mmax = min(32 - nB, L2B_CS);
     const int la2 = tt.la2;
     const uint32_t nrec = *count15 << la2;
-    const bool pk = nF >= 11 && nF <= 13;  // stage-1 records packed one word per super-node
-    // stage-1 super-node s: w1 = F relations, w0 = cs | self << 31
+    // stage-1 super-node s of an m1-node record (L15Bits): w1 = F relations,
+    // w0 = cs | self << 31
     auto rw1 = [&](const unsigned long long *r1, int s2) -> unsigned long long {
-        return pk ? (r1[1 + s2] & ((1ull << (3 * nF)) - 1ull)) : r1[2 + 2 * s2];
+        return l15_bits(r1, 3 * nF * s2, 3 * nF);
     };
-    auto rw0 = [&](const unsigned long long *r1, int s2) -> uint32_t {
-        if (!pk) return (uint32_t)r1[1 + 2 * s2];
-        const uint32_t x = (uint32_t)(r1[1 + s2] >> (3 * nF));
-        return (x & 0xffffffu) | ((x >> 24) & 1u) << 31;
+    auto rw0 = [&](const unsigned long long *r1, int s2, int m1) -> uint32_t {
+        const uint32_t x = (uint32_t)l15_bits(r1, m1 * 3 * nF + s2 * (m1 + 1), m1 + 1);
+        return (x & ((1u << m1) - 1u)) | (x >> m1) << 31;
     };
     auto label = [&](int v) -> uint32_t { return lb[(v >> 2) * (4 * THREADS) + (v & 3)]; };
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < nrec; j += gridDim.x * blockDim.x) {
         const uint32_t j1 = list15[j >> la2], a2 = j & ((1u << la2) - 1u);
         const unsigned long long *r1 = pool1 + (size_t)j1 * stride1;
-        const int m1 = (int)r1[0];
+        const int m1 = (int)(r1[0] & 0xffffu);
         const uint32_t SA2 = tt.a2sign[a2];
         // A2 rows toward the stage-1 super-nodes (same-sign or linked / crossed)
         uint32_t sameA[NA], crossA[NA];
@@ -601,7 +617,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_from_l15(const TileTables *__res
                 lb[(v >> 2) * (4 * THREADS) + (v & 3)] = (uint8_t)m;
                 uint32_t same, cross;
                 if (v < m1) {
-                    const unsigned long long w0 = rw0(r1, v), w1 = rw1(r1, v);
+                    const unsigned long long w0 = rw0(r1, v, m1), w1 = rw1(r1, v);
                     const uint32_t pA = (uint32_t)(w1 >> nB) & a2m,
                                    mA = (uint32_t)(w1 >> (nF + nB)) & a2m,
                                    lA = (uint32_t)(w1 >> (2 * nF + nB)) & a2m;
@@ -726,7 +742,7 @@ __global__ void __launch_bounds__(THREADS) k_l2_dedup(const unsigned long long *
             unsigned long long pw[L2D_PRE];
 #pragma unroll
             for (int q = 0; q < L2D_PRE; ++q) pw[q] = q < npre ? mine[1 + q] : 0ull;
-            const int nw = wps * (int)m;
+            const int nw = wps ? wps * (int)m : (int)(m >> 16);  // wps 0: stage-1 (L15Bits)
             uint32_t at = (uint32_t)h & smask;
             while (true) {
                 unsigned long long cur = slots[at];

@@ -738,8 +738,9 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
                           uint32_t i0, uint32_t nb, uint64_t tile0, uint64_t lo, uint64_t hi,
                           size_t cap, uint32_t stride, int &rc) {
     const TileTables &T = P->h_tiles[mode];
-    const bool pk = T.nB + T.nA2 >= 11 && T.nB + T.nA2 <= 13;  // one word per super-node
-    const uint32_t stride1 = (uint32_t)(1 + (pk ? 1 : 2) * L15_MAXM);
+    // L15Bits stream: 3 nF + m + 1 bits per super-node, m <= L15_MAXM, nF <= 21;
+    // one stride for every mode, so the pool's record capacity holds for all
+    const uint32_t stride1 = (uint32_t)(1 + (L15_MAXM * (3 * 21 + L15_MAXM + 1) + 63) / 64);
     const uint32_t nrec1 = nb << T.la1;
     auto cuda_ok = [&](cudaError_t e, const char *what) {
         if (e != cudaSuccess) rc = fail(TCG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -844,7 +845,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
     timing_end(P, TCG_KT_L15_BUILD, e0);
     e0 = timing_begin(P);
     uint32_t smask1 = 2 * np2 - 1;
-    int wps2 = pk ? 1 : 2;
+    int wps2 = 0;  // stage-1 records carry their word count
     uint32_t nr1 = nrec1;
     void *ad[] = {&pool1, &s1, &nr1, &hash1, &wts1, &poss1, &slots1, &smask1, &w15, &pos15,
                   &list15, &count15, &wps2};
