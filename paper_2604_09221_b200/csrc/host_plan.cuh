@@ -231,19 +231,28 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
     int sbit[TILE_BITS_MAX];
     for (int i = 0; i < bits; ++i)
         sbit[i] = mode == MODE_RAW ? i : (i < d - 1 ? i + 2 : i - (d - 1) + d + 2);
-    std::vector<int> fnode(D->nv, -1);
-    int nf = 0;
+    std::vector<int> fnode(D->nv, -1), vbit(D->nv, -1);
     for (int v = 0; v < D->nv; ++v) {
         if (!D->used[v]) continue;
-        int bit = -1;
         for (int i = 0; i < bits; ++i)
-            if (sbit[i] == D->src[v]) bit = i;
-        const int pos = L.pos[v];
-        if (bit < 0) {
+            if (sbit[i] == D->src[v]) vbit[v] = i;
+        if (vbit[v] < 0) {
+            const int pos = L.pos[v];
             T.fixed[pos >> 5] |= 1u << (pos & 31);
             ++T.nfixed;
-            continue;
         }
+    }
+    // free nodes numbered by tile bit (then vertex): the B, A1 and A2 nodes of
+    // the two-stage level 2 are contiguous free-node ranges, so the stage-1
+    // F-space compression is a shift (TileTables::l15sh)
+    int nf = 0;
+    std::vector<int> vorder;
+    for (int i = 0; i < bits; ++i)
+        for (int v = 0; v < D->nv; ++v)
+            if (D->used[v] && vbit[v] == i) vorder.push_back(v);
+    for (const int v : vorder) {
+        const int bit = vbit[v];
+        const int pos = L.pos[v];
         if (nf >= MAXF) return false;
         fnode[v] = nf;
         T.fword[nf] = (uint32_t)(pos >> 5);
@@ -326,6 +335,12 @@ bool build_tiles_bits(const tcg_desc *D, const Layout &L, int mode, int bits, Ti
                 T.l15max = std::max(1, std::min(L15_MAXM, std::atoi(e)));
             T.fa1 = fa1;
             T.fa2 = fa2;
+            {
+                const int n1 = __builtin_popcount(fa1);
+                const bool contig = fb == (1u << nB) - 1u && fa1 == ((1u << n1) - 1u) << nB &&
+                                    fa2 == ((1u << nA2) - 1u) << (nB + n1);
+                T.l15sh = contig && !std::getenv("TCG_L15_LUT") ? n1 : -1;
+            }
             T.nA2 = nA2;
             int a2j[MAXF], a2f[16], k = 0;
             for (int f = 0; f < MAXF; ++f) { T.l15F[f] = -1; a2j[f] = -1; }

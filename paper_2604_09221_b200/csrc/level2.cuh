@@ -424,9 +424,17 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
         TCG_ASSERT(m < L2B_CS);
         cs[m * THREADS] = c | self << 31;
         for (uint32_t y = c; y; y &= y - 1u) cs[(__ffs(y) - 1) * THREADS] |= 1u << m;
-        const unsigned long long w1 = l15_compress(lut, (uint32_t)(pb >> n)) |
-                                      l15_compress(lut, (uint32_t)(mb >> n)) << nF |
-                                      l15_compress(lut, (uint32_t)(lk >> n)) << (2 * nF);
+        unsigned long long w1;
+        if (tt.l15sh >= 0) {  // contiguous B | A1 | A2 free nodes (A1 bits are 0 here)
+            const uint32_t bmk = (1u << tt.nB) - 1u, sh = (uint32_t)tt.l15sh;
+            const uint32_t xp = (uint32_t)(pb >> n), xm = (uint32_t)(mb >> n), xl = (uint32_t)(lk >> n);
+            w1 = (unsigned long long)((xp & bmk) | ((xp >> sh) & ~bmk)) |
+                 (unsigned long long)((xm & bmk) | ((xm >> sh) & ~bmk)) << nF |
+                 (unsigned long long)((xl & bmk) | ((xl >> sh) & ~bmk)) << (2 * nF);
+        } else {
+            w1 = l15_compress(lut, (uint32_t)(pb >> n)) | l15_compress(lut, (uint32_t)(mb >> n)) << nF |
+                 l15_compress(lut, (uint32_t)(lk >> n)) << (2 * nF);
+        }
         bw.put(out, w1, 3 * nF);
         hh = mix64(hh ^ w1);
         done |= M;

@@ -821,7 +821,7 @@ static bool run_two_stage(tcg_plan *P, int mode, const TileTables *tt, const Til
         cudaFuncGetAttributes(&fa, (const void *)k_l15_build);
         return (int)fa.sharedSizeBytes;
     }();
-    int slotq = slotq_env, lut_smem = !lutg_env;
+    int slotq = slotq_env, lut_smem = !lutg_env && T.l15sh < 0;  // tables unused with l15sh
     if (slotq == 0) {  // the widest slot that keeps 4 CTAs (= the register limit) per SM:
         // with the whole-grid launch 4 CTAs and 47-row slots beat 3 CTAs and 64 (profiles/README.md)
         const int tiles = (THREADS / 32) * (32 >> T.la1);

@@ -43,6 +43,7 @@ struct alignas(16) TileTables {  // per plan and domain (raw / representative), 
     // then A2 nodes nB..nB+nA2-1.
     int ts, nA2;
     uint32_t fa1, fa2;                      // free-node masks of A1 / A2 nodes
+    int32_t l15sh;                          // B | A1 | A2 contiguous: F index = f or f - l15sh (else -1: lookup tables)
     int8_t l15F[MAXF];                      // free node -> F index (or -1)
     uint32_t a2sign[16];                    // A2-node signs (A2 index space) per A2 pattern
     int la1, la2;                           // A1 = tile bits 5 .. 4+la1, A2 = the la2 = la - la1 above
