@@ -377,7 +377,7 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
     const MT one = 1;
     const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa1) << n);
     const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa1 << n);
-    const MT FBn = (MT)(tt.fbm | tt.fa2) << n;
+    const uint32_t fbm32 = tt.fbm | tt.fa2;
     MT unv = G, done = 0;
     unsigned long long hh = 0x9E3779B97F4A7C15ull;
     int m = 0;
@@ -387,7 +387,8 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
         if (m == tt.l15max) return -1;
         MT f = unv & ((MT)0 - unv);
         unv ^= f;
-        MT M = f, cg = 0, pb = 0, mb = 0, lk = 0;
+        MT M = f, cg = 0;
+        uint32_t pb = 0, mb = 0, lk = 0;  // F relations in free-node space
         while (f) {
             const int u = WIDE ? __ffsll((long long)f) - 1 : __ffs((uint32_t)f) - 1;
             f &= f - one;
@@ -410,10 +411,10 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
             f |= nw;
             M |= nw;
             cg |= rx & G & diff;
-            const MT bp = rx & FBn;
-            pb |= s ? bp : (MT)0;
-            mb |= s ? (MT)0 : bp;
-            lk |= ry & FBn;
+            const uint32_t bp = (uint32_t)(rx >> n) & fbm32;
+            pb |= s ? bp : 0u;
+            mb |= s ? 0u : bp;
+            lk |= (uint32_t)(ry >> n) & fbm32;
         }
         uint32_t c = 0;
         const MT x = cg & done;
@@ -427,13 +428,12 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
         unsigned long long w1;
         if (tt.l15sh >= 0) {  // contiguous B | A1 | A2 free nodes (A1 bits are 0 here)
             const uint32_t bmk = (1u << tt.nB) - 1u, sh = (uint32_t)tt.l15sh;
-            const uint32_t xp = (uint32_t)(pb >> n), xm = (uint32_t)(mb >> n), xl = (uint32_t)(lk >> n);
+            const uint32_t xp = pb, xm = mb, xl = lk;
             w1 = (unsigned long long)((xp & bmk) | ((xp >> sh) & ~bmk)) |
                  (unsigned long long)((xm & bmk) | ((xm >> sh) & ~bmk)) << nF |
                  (unsigned long long)((xl & bmk) | ((xl >> sh) & ~bmk)) << (2 * nF);
         } else {
-            w1 = l15_compress(lut, (uint32_t)(pb >> n)) | l15_compress(lut, (uint32_t)(mb >> n)) << nF |
-                 l15_compress(lut, (uint32_t)(lk >> n)) << (2 * nF);
+            w1 = l15_compress(lut, pb) | l15_compress(lut, mb) << nF | l15_compress(lut, lk) << (2 * nF);
         }
         bw.put(out, w1, 3 * nF);
         hh = mix64(hh ^ w1);
