@@ -377,6 +377,7 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
     const MT one = 1;
     const MT sg1 = (MT)rec->sgn_fixed | ((MT)((uint32_t)fsA & tt.fa1) << n);
     const MT G = (n >= 8 * (int)sizeof(MT) ? ~(MT)0 : ((one << n) - one)) | ((MT)tt.fa1 << n);
+    const MT nsg1 = ~sg1;
     const uint32_t fbm32 = tt.fbm | tt.fa2;
     MT unv = G, done = 0;
     unsigned long long hh = 0x9E3779B97F4A7C15ull;
@@ -405,12 +406,12 @@ __device__ __forceinline__ int l15_build(const TileTables &tt, const L15Lut &lut
                 ry = r.y;
             }
             const MT s = (sg1 >> u) & one;
-            const MT diff = sg1 ^ ((MT)0 - s);
+            const MT diff = s ? nsg1 : sg1;
             const MT nw = ((rx & ~diff) | ry) & unv;
             unv ^= nw;
             f |= nw;
             M |= nw;
-            cg |= rx & G & diff;
+            cg |= rx & diff;  // only read as cg & done / cg & M, both inside G
             const uint32_t bp = (uint32_t)(rx >> n) & fbm32;
             pb |= s ? bp : 0u;
             mb |= s ? 0u : bp;
